@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Virtual-node training-step benchmark (BASELINE.json metric: samples/sec at
+fixed global batch and V).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3]
+                    [--impl ours|reference] [--gemm-mode auto]
+
+A "step" is one Trainer::step of the hot path (runner.cpp:75-82): forward +
+backward of every virtual node, exact gradient reduction (NCCL all-reduce when
+N > 1), fused SGD.  Default workload = BASELINE config 3 (wide MLP
+[784,4096x4,10] relu/softmax-CE fp32, B = 8192, V = 64), the GEMM-bound
+configuration the north star's roofline target is stated on.  N > 1: launch
+with torch.distributed.run, one rank per GPU; virtual nodes are dealt
+round-robin (make_uniform_mapping) so per-GPU work is B/N (fixed global batch).
+
+One JSON line on rank 0.  `value` = samples/s with the batch resident in HBM;
+`e2e` = the same through the C-ABI with pinned host batches (H2D + loss D2H in
+the timed region).  `--impl reference` times the reference's own CPU
+implementation (oracle/_ref, else our C port) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: widths, act, loss, B, V, lr, capacity
+    "cfg1": dict(widths=[784, 16, 10], act="tanh", loss="softmax-cross-entropy", B=256, V=16,
+                 lr=0.05, capacity=1 << 20, config_index=1),
+    "cfg3": dict(widths=[784, 4096, 4096, 4096, 4096, 10], act="relu",
+                 loss="softmax-cross-entropy", B=8192, V=64, lr=0.01, capacity=1 << 20,
+                 config_index=2),
+    "cfg4": dict(widths=[784, 4096, 4096, 4096, 4096, 10], act="relu",
+                 loss="softmax-cross-entropy", B=65536, V=256, lr=0.01, capacity=256,
+                 config_index=3),
+}
+
+
+def gemm_flops_per_step(widths, B):
+    """B * 2 * (3*sum_ww - w0*w1) (fwd + bwd-data except layer 0 + dW)."""
+    sww = sum(widths[i] * widths[i + 1] for i in range(len(widths) - 1))
+    return B * 2 * (3 * sww - widths[0] * widths[1])
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference(work, steps, warmup):
+    """The reference's own CPU implementation (oracle/_ref), bounded sample.
+
+    cfg1: full Trainer::step (runner.cpp:75-82).  cfg3/cfg4: a full step needs
+    two 71-limb exact accumulators of 30 GB each and ~6 h; the sample is
+    Model::accumulate_example_grads over a few full-width examples plus one
+    ExactVectorAccumulator::rounded(), extrapolated linearly to B examples."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    ref = oracle_lib.ref()
+    kind = "reference" if ref is not None else "port"
+    o = ref if ref is not None else oracle_lib.port()
+    w, B, V = work["widths"], work["B"], work["V"]
+    cores = 1
+    if work["widths"][1] <= 256:
+        t = o.trainer(w, work["act"], work["loss"], 11, B, V, work["lr"], 11, 60000, 1)
+        for _ in range(warmup):
+            t.step()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            t.step()
+        dt = (time.perf_counter() - t0) / steps
+        return {"value": B / dt, "unit": "samples/s", "cores": cores, "kind": kind,
+                "sample": f"{steps} full Trainer::step of B={B}, V={V}, G=1 serial"}, dt
+    # wide model: bounded sample (needs ~31 GB host RAM for the exact accumulator)
+    avail = 0
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable"):
+                avail = int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    P = sum(w[i] * w[i + 1] + w[i + 1] for i in range(len(w) - 1))
+    need = P * 71 * 8 * 1.15
+    n_ex = 2
+    x, y = o.synth_batch(1, 65536, w[0], w[-1], 0, n_ex)
+    if ref is not None and avail > need:
+        import ctypes as C
+        f = ref.lib.vntref_accumulate_sample
+        acc_s, rnd_s = C.c_double(), C.c_double()
+        wa = (C.c_uint64 * len(w))(*w)
+        rc = f(wa, C.c_uint32(len(w)), C.c_int(0), C.c_int(1), C.c_uint64(1),
+               x.ctypes.data_as(C.POINTER(C.c_double)), y.ctypes.data_as(C.POINTER(C.c_double)),
+               C.c_uint64(n_ex), C.byref(acc_s), C.byref(rnd_s))
+        assert rc == 0
+        per_ex = acc_s.value / n_ex
+        step_s = B * per_ex + rnd_s.value * 2  # device buffer rounding + sync rounding
+        sample = (f"Model::accumulate_example_grads on {n_ex} full-width examples "
+                  f"({acc_s.value:.1f} s) + one ExactVectorAccumulator::rounded "
+                  f"({rnd_s.value:.1f} s), linearly extrapolated to B={B} (x2 rounding)")
+    else:
+        kind = "port"
+        t0 = time.perf_counter()
+        p = oracle_lib.port().init_params(w, 1)
+        oracle_lib.port().forward_backward(w, work["act"], work["loss"], p, x, y)
+        per = time.perf_counter() - t0
+        step_s = B * per / n_ex
+        sample = (f"C port forward_backward on {n_ex} full-width examples ({per:.1f} s, "
+                  f"MemAvailable {avail/2**30:.0f} GiB < exact-accumulator need), "
+                  f"extrapolated to B={B}")
+    return {"value": B / step_s, "unit": "samples/s", "cores": cores, "kind": kind,
+            "sample": sample}, step_s
+
+
+def run_reference(args, work):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    base, step_s = cpu_reference(work, max(1, min(args.steps, 3)), 1 if work["widths"][1] <= 256 else 0)
+    line = {
+        "metric": "samples/sec at fixed global batch & V", "impl": "reference",
+        "value": base["value"], "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "layer_widths": work["widths"],
+                   "global_batch": work["B"], "virtual_nodes": work["V"]},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------ our arm
+def run_ours(args, work):
+    import torch
+    import torch.distributed as dist
+    import paper_2009_09523_b200 as vnt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nccl_id = None
+    if world > 1:
+        obj = [vnt.Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    os.environ.setdefault("VNT_PROFILE_KERNELS", "1")
+    w, B, V, lr = work["widths"], work["B"], work["V"], work["lr"]
+    eng = vnt.Engine(w, work["act"], work["loss"], cuda_device=local, rank=rank,
+                     world_size=world, nccl_id=nccl_id, gemm_mode=args.gemm_mode,
+                     resident_rows=args.resident_rows)
+    eng.add_device(work["capacity"])
+    g = np.random.default_rng(1)
+    params = []
+    for i in range(len(w) - 1):
+        params.append(g.standard_normal(w[i] * w[i + 1]) / np.sqrt(w[i]))
+        params.append(np.zeros(w[i + 1]))
+    eng.set_params(np.concatenate(params))
+    sizes, dev_of = vnt.uniform_mapping(B, V, world, work["capacity"])
+    node_device = np.where(dev_of == rank, 0, -1).astype(np.int32)
+
+    # Synthetic batches of the named shape (SynthDataset semantics, data.cpp:50-105:
+    # x ~ N(0,1), soft labels softmax(x T)), resident in HBM, fp64 like vnt::Batch.
+    nb = 4
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    T = torch.randn(w[0], w[-1], device="cuda", dtype=torch.float64, generator=gen) / w[0] ** 0.5
+    xs, ys = [], []
+    for _ in range(nb):
+        x = torch.randn(B, w[0], device="cuda", dtype=torch.float64, generator=gen)
+        xs.append(x)
+        ys.append(torch.softmax(x @ T, dim=1))
+    stream = torch.cuda.ExternalStream(eng.stream_ptr())
+
+    def step(i, resident=True, host=None):
+        if resident:
+            return eng.train_step_ptr(xs[i % nb].data_ptr(), ys[i % nb].data_ptr(), B, sizes,
+                                      node_device, lr, resident=True)
+        hx, hy = host
+        return eng.train_step_ptr(hx[i % nb].data_ptr(), hy[i % nb].data_ptr(), B, sizes,
+                                  node_device, lr, resident=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    gemm_ms, gemm_fl, gemm_n, launches = 0.0, 0.0, 0, 0
+    with ClockSampler(local) as clocks:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        losses = []
+        for i in range(args.steps):
+            losses.append(step(i))
+            t = eng.timings()
+            gemm_ms += t["gemm_ms"]
+            gemm_fl += t["gemm_flops"]
+            gemm_n += t["gemm_launches"]
+            launches += t["kernel_launches"]
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    value = B / (ms_per_step / 1e3)
+
+    # e2e: through the C-ABI with pinned host batches (H2D of the rank's rows +
+    # loss/flag D2H inside the timed region).
+    hx = [x.cpu().pin_memory() for x in xs]
+    hy = [y.cpu().pin_memory() for y in ys]
+    step(0, resident=False, host=(hx, hy))
+    barrier()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i, resident=False, host=(hx, hy))
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = B / (e2e_ms / args.steps / 1e3)
+    local_rows = int(sizes[node_device >= 0].sum())
+    h2d = local_rows * (w[0] + w[-1]) * 8
+    d2h = (3 + 2 * (len(w) - 1)) * 8 + 2 * (len(w) - 1) * 8
+
+    peaks, peak_src = measured_peaks()
+    flops_step = gemm_flops_per_step(w, B)
+    line = {
+        "metric": "samples/sec at fixed global batch & V", "value": value, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "baseline_config_index": work["config_index"],
+                   "layer_widths": w, "activation": work["act"], "loss": work["loss"],
+                   "global_batch": B, "virtual_nodes": V, "lr": lr,
+                   "parallelism": f"vn-dp{world}", "gemm_mode": args.gemm_mode,
+                   "l2": "per-step working set (fp64+fp32 params, activations) >> 126 MB L2; "
+                         "4 resident batches rotate"},
+        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "final_loss": losses[-1],
+        "clocks": clocks.summary(),
+    }
+    if gemm_n:
+        achieved = gemm_fl / (gemm_ms / 1e3) / 1e12
+        # TF32 tensor peak is not in MEASURED_PEAKS.json: half the measured bf16 dense rate
+        # (tf32 kind runs at 1/2 the f16 rate; 1.1 vs 2.25 PF nominal).
+        mode = args.gemm_mode
+        if mode == "ffma":
+            peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+            peak_note = "fp32 FFMA peak 148 SM x 128 FMA/clk x 2 x sm_max_mhz"
+        else:
+            peak = peaks["bf16_tflops"] / 2
+            if mode in ("auto", "3xtf32"):
+                peak /= 3
+                peak_note = f"TF32 = bf16/2 ({peak_src}), /3 for 3xTF32 passes"
+            else:
+                peak_note = f"TF32 = bf16/2 ({peak_src})"
+        line["roofline"] = {
+            "bound": "tensor", "kernel": "dense-layer GEMMs (fwd, bwd-data, per-node dW)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "peak_source": peak_note,
+            "gemm_share_of_step": (gemm_ms / args.steps) / ms_per_step,
+            "algorithmic_flops_per_step": flops_step,
+            "gemm_launches_per_step": gemm_n / args.steps,
+        }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base, _ = cpu_reference(work, 1, 0)
+        line["cpu_baseline"] = base
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gemm-mode", default="auto", choices=["auto", "ffma", "tf32", "3xtf32"])
+    ap.add_argument("--resident-rows", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    work = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, work)
+    else:
+        run_ours(args, work)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+/* vnt_engine.h — the thin C-ABI between the reference-compatible C++ host
+ * layer (include/vnt/*.hpp, the `vnt::` drop-in) and the B200 CUDA engine
+ * (paper_2009_09523_b200/csrc/).  Plain pointers and sizes only; all CUDA /
+ * NCCL state lives behind the opaque `vnt_engine`.  There is no CPU fallback:
+ * every compute entry point fails with VNT_ERR_CUDA when no sm_100 device is
+ * usable.
+ *
+ * Each entry point names the reference interface it replaces (paths relative
+ * to /root/reference/proj/core):
+ *
+ *   vnt_engine_create        Model::Model + make_world          model.hpp:98-106, virtual_exec.cpp:194-205
+ *   vnt_engine_set_params    World replica assignment / init    model.cpp:170-183
+ *   vnt_engine_add_device    WorkerState{DeviceSpec,...}        virtual_exec.hpp:100-104
+ *   vnt_engine_device_step   device_step                        virtual_exec.hpp:89-92, .cpp:120-144
+ *   vnt_engine_sync          sync_gradients                     virtual_exec.hpp:97-98, .cpp:146-168
+ *   vnt_engine_sgd_apply     sgd_apply on every replica         model.hpp:130, model.cpp:364-374
+ *   vnt_engine_train_step    train_step                         virtual_exec.hpp:130-132, .cpp:207-282
+ *   vnt_engine_{get,set}_input_stats  StatefulKernelState       model.hpp:65-93, elastic.cpp:50-88
+ *
+ * Numerical contract: per-virtual-node fp32 gradients are
+ * quantised to int64 fixed point (power-of-two scale per tensor) and summed
+ * exactly, so the reduced gradient — and the whole trajectory — is a function
+ * of the virtual-node partition only, never of the device mapping or count.
+ */
+#ifndef VNT_ENGINE_H
+#define VNT_ENGINE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror the reference exception classes (errors.hpp:13-58);
+ * the CLI exit-code mapping is vnt.cpp:395-413. */
+#define VNT_OK 0
+#define VNT_ERR_INTERNAL 1        /* vnt::Error (generic)                */
+#define VNT_ERR_CONFIG 2          /* vnt::ConfigError                    */
+#define VNT_ERR_CAPACITY 3        /* vnt::CapacityError                  */
+#define VNT_ERR_SHAPE 6           /* vnt::ShapeError                     */
+#define VNT_ERR_CONSISTENCY 7     /* vnt::ConsistencyError               */
+#define VNT_ERR_MIGRATION 8       /* vnt::MigrationError                 */
+#define VNT_ERR_CUDA 9            /* no usable sm_100 GPU / CUDA failure */
+#define VNT_ERR_NCCL 10           /* collective failure                  */
+#define VNT_ERR_NONFINITE 11      /* non-finite gradient (exact_sum.cpp:17-19) */
+#define VNT_ERR_RESCALE 12        /* fixed-point range exceeded; scale lowered, redo the step */
+
+/* model.hpp:20-21 enum order */
+#define VNT_ACT_RELU 0
+#define VNT_ACT_TANH 1
+#define VNT_ACT_IDENTITY 2
+#define VNT_LOSS_MSE 0
+#define VNT_LOSS_SOFTMAX_CE 1
+
+/* GEMM arithmetic for the dense layers.  Selection depends on layer widths
+ * only (never on rows), so it is identical on every rank. */
+#define VNT_GEMM_AUTO 0        /* tcgen05 3xTF32 for wide layers, FFMA fp32 otherwise */
+#define VNT_GEMM_FFMA 1        /* fp32 FFMA everywhere (exact fp32 products)          */
+#define VNT_GEMM_TF32 2        /* tcgen05 kind::tf32, 1 pass                         */
+#define VNT_GEMM_3XTF32 3      /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi          */
+
+typedef struct vnt_engine vnt_engine;
+
+typedef struct vnt_model_desc {
+  const uint64_t* layer_widths; /* ModelSpec::layer_widths (model.hpp:27-37) */
+  uint32_t num_widths;
+  int32_t activation;           /* VNT_ACT_*  */
+  int32_t loss;                 /* VNT_LOSS_* */
+} vnt_model_desc;
+
+typedef struct vnt_engine_options {
+  int32_t cuda_device;     /* CUDA ordinal driven by this process                  */
+  int32_t rank;            /* NCCL rank of this process                            */
+  int32_t world_size;      /* processes in the NCCL group (1: no collective)       */
+  const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from rank 0, NULL if world 1   */
+  int32_t gemm_mode;       /* VNT_GEMM_*                                           */
+  double momentum;         /* 0: plain SGD exactly as the reference                */
+  uint64_t resident_rows;  /* rows kept resident per pass on the GPU (0: all)      */
+} vnt_engine_options;
+
+typedef struct vnt_device_metrics { /* DeviceStepMetrics, virtual_exec.hpp:72-78 */
+  uint64_t waves;
+  uint64_t examples;
+  uint64_t peak_resident;
+  uint64_t buffer_bytes;   /* modeled: 8 * |params| (acceptance criterion 10) */
+} vnt_device_metrics;
+
+typedef struct vnt_step_timings { /* device time of the last train step, ms (CUDA events) */
+  float total_ms;
+  float forward_ms;
+  float backward_ms;
+  float sync_ms;
+  float update_ms;
+  uint32_t kernel_launches;
+  uint32_t rescale_retries;
+  /* Dense-layer GEMM launches only, filled when VNT_PROFILE_KERNELS=1 (events
+   * around each launch on the engine stream): summed device time, algorithmic
+   * flops (2*M*N*K per launch) and launch count. */
+  float gemm_ms;
+  uint32_t gemm_launches;
+  double gemm_flops;
+} vnt_step_timings;
+
+const char* vnt_last_error(void);
+const char* vnt_build_info(void);
+
+/* 128-byte NCCL unique id for vnt_engine_options::nccl_id (rank 0 creates it). */
+int vnt_nccl_unique_id(uint8_t out[128]);
+
+int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* options,
+                      vnt_engine** out);
+void vnt_engine_destroy(vnt_engine* e);
+uint64_t vnt_engine_param_count(const vnt_engine* e);
+
+/* Replica parameters, reference layout (model.cpp:62-77), fp64 master copy. */
+int vnt_engine_set_params(vnt_engine* e, const double* params, uint64_t n);
+int vnt_engine_get_params(vnt_engine* e, double* params, uint64_t n);
+
+/* Adds a logical device (a World worker) hosted by this process. */
+int vnt_engine_add_device(vnt_engine* e, uint64_t memory_capacity, int32_t* out_index);
+int vnt_engine_device_count(const vnt_engine* e);
+
+/* device_step: the device's node micro-batches, ascending node id, rows
+ * concatenated (x: rows x in, y: rows x out, fp64 host).  Accumulates the
+ * example-weighted gradient sum into the process gradient buffer and updates
+ * the device's input statistics. */
+int vnt_engine_device_step(vnt_engine* e, int32_t device, const double* x, const double* y,
+                           const uint64_t* node_sizes, uint32_t num_nodes,
+                           vnt_device_metrics* metrics);
+
+/* sync_gradients: exact sum of every device buffer (and, world_size > 1, every
+ * process) divided by the examples accumulated.  mean_grad (nullable, P
+ * doubles) receives the reduced mean; loss_sum receives the exact loss sum. */
+int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum,
+                    uint64_t* examples);
+
+/* sgd_apply with the synced gradient on this replica (plus momentum if set). */
+int vnt_engine_sgd_apply(vnt_engine* e, double lr);
+
+/* train_step: the whole global batch (x: batch_rows x in, y: batch_rows x out,
+ * fp64 host).  node_sizes[total_nodes] partitions the rows contiguously by node
+ * id; node_device[n] is the local device index running node n, or -1 if node n
+ * runs in another process.  per_device (nullable) receives one entry per local
+ * device. */
+int vnt_engine_train_step(vnt_engine* e, const double* x, const double* y,
+                          uint64_t batch_rows, const uint64_t* node_sizes,
+                          const int32_t* node_device, uint32_t total_nodes, double lr,
+                          double* loss, vnt_device_metrics* per_device);
+
+/* Same, with the fp64 batch already resident in device memory (bench `value`). */
+int vnt_engine_train_step_resident(vnt_engine* e, const double* x_dev, const double* y_dev,
+                                   uint64_t batch_rows, const uint64_t* node_sizes,
+                                   const int32_t* node_device, uint32_t total_nodes,
+                                   double lr, double* loss, vnt_device_metrics* per_device);
+
+/* LayerStats "input" of a local device (model.hpp:65-76): count, mean[in], m2[in]. */
+int vnt_engine_get_input_stats(vnt_engine* e, int32_t device, double* count, double* mean,
+                               double* m2);
+int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count,
+                               const double* mean, const double* m2);
+
+/* Fixed-point scale state (part of the numerical state: migrated on resize). */
+int vnt_engine_get_scales(vnt_engine* e, int32_t* scales, uint32_t n);
+int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n);
+uint32_t vnt_engine_tensor_count(const vnt_engine* e);
+
+int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out);
+/* The CUDA stream the engine launches on (cudaStream_t as void*). */
+void* vnt_engine_stream(vnt_engine* e);
+/* Scratch device allocation owned by the engine (bench/test staging). */
+int vnt_engine_device_alloc(vnt_engine* e, uint64_t bytes, void** out);
+int vnt_engine_device_free(vnt_engine* e, void* p);
+int vnt_engine_memcpy_h2d(vnt_engine* e, void* dst, const void* src, uint64_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VNT_ENGINE_H */

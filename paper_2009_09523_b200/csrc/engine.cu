@@ -1,0 +1,1062 @@
+// B200 virtual-node training engine: the implementation behind the C-ABI in
+// include/vnt_engine.h.  One process drives one GPU; the process hosts one or
+// more logical devices (World workers, virtual_exec.hpp:100-114) and joins an
+// NCCL group when world_size > 1.
+//
+// Step structure (train_step, virtual_exec.cpp:207-282):
+//   passes of resident virtual nodes -> ingest + input stats -> forward layers
+//   -> loss/delta -> backward (per-node dW/db quantised into the exact int64
+//   sum, bwd-data) -> [ncclAllReduce int64] -> fused rescale + SGD.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/vnt_engine.h"
+#include "common.cuh"
+#include "kernels_simt.cuh"
+
+using namespace vntb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+constexpr int kScaleTargetBits = 40;   // |sum| of the largest element ~ 2^40 after scaling
+constexpr int kLimBits = 50;           // per-node partial bound (2^12 nodes x 2^50 < 2^62)
+constexpr int kRescaleStep = 12;
+
+struct PassNode {
+  int node;          // global node id
+  int dev;           // local device index
+  uint64_t rows;     // node size
+  uint64_t src_row;  // first row in the source batch
+  uint64_t prow;     // first row in the pass
+  uint64_t pcol;     // first column in the padded feature-major buffers
+};
+
+struct Pass {
+  std::vector<PassNode> nodes;
+  uint64_t rows = 0;
+  uint64_t ldT = 0;
+  int* d_meta = nullptr;   // [tcol(rows) | row0(n) | rows(n) | col0(n)]
+};
+
+}  // namespace
+
+struct vnt_engine {
+  // model (ModelSpec, model.hpp:27-37; Layout, model.cpp:62-77)
+  std::vector<uint64_t> widths;
+  int L = 0;
+  int act = 1, loss = 0;
+  uint64_t P = 0;
+  std::vector<uint64_t> woff, boff, wtoff;
+  std::vector<int> tc_layer;   // 1: layer runs on tcgen05 tiles
+  vnt_engine_options opt{};
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+
+  // replica state
+  double* w64 = nullptr;
+  double* v64 = nullptr;
+  float* w32 = nullptr;
+  float* wt32 = nullptr;
+  long long* G = nullptr;   // P + ntail
+  size_t ntail = 0;
+  unsigned long long* gmax = nullptr;
+  double* gout = nullptr;
+  std::vector<int> scales;
+  bool scales_init = false;
+
+  // pass buffers
+  uint64_t cap_rows = 0, cap_ldT = 0, cap_vns = 0;
+  double* xin = nullptr;
+  double* yin = nullptr;
+  std::vector<float*> X, XT, D, DT;
+  float* logits = nullptr;
+  double* vn_mean = nullptr;
+  double* vn_m2 = nullptr;
+  CombineStep* d_combine = nullptr;
+  CombineStep* h_combine = nullptr;
+  size_t combine_cap = 0;
+  long long* h_tail = nullptr;
+  unsigned long long* h_gmax = nullptr;
+
+  struct LDev {
+    uint64_t capacity = 0;
+    double count = 0;
+    double* mean = nullptr;
+    double* m2 = nullptr;
+    double count_bak = 0;          // snapshot at round start (restored on rescale)
+    double* mean_bak = nullptr;
+    double* m2_bak = nullptr;
+  };
+  std::vector<LDev> devs;
+
+  // plan cache (mapping -> passes with device-resident metadata)
+  std::map<std::vector<int64_t>, std::vector<Pass>> plans;
+
+  // accumulation state
+  bool round_open = false;
+  bool acc_started = false;
+  uint64_t acc_examples = 0;
+  bool synced = false;
+  uint64_t total_nodes_hint = 0;
+
+  vnt_step_timings timings{};
+  cudaEvent_t ev[6] = {};
+  // Per-GEMM-launch device timing (CUDA events on the engine stream).
+  bool profile = false;
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<double> prof_flops;
+  size_t prof_n = 0;
+  uint32_t launches = 0;
+  std::vector<void*> scratch;
+};
+
+#include "gemm_tc.cuh"
+
+namespace {
+
+void prof_begin(vnt_engine* e) {
+  if (!e->profile) return;
+  if (e->prof_n + 2 > e->prof_ev.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t ev;
+      VNT_CUDA(cudaEventCreate(&ev));
+      e->prof_ev.push_back(ev);
+    }
+  }
+  VNT_CUDA(cudaEventRecord(e->prof_ev[e->prof_n], e->stream));
+}
+
+void prof_end(vnt_engine* e, double flops) {
+  if (!e->profile) return;
+  VNT_CUDA(cudaEventRecord(e->prof_ev[e->prof_n + 1], e->stream));
+  e->prof_n += 2;
+  e->prof_flops.push_back(flops);
+}
+
+// After the step's final synchronisation: fold the GEMM launch times in.
+void prof_collect(vnt_engine* e) {
+  if (!e->profile) return;
+  double ms_total = 0.0, fl = 0.0;
+  for (size_t i = 0; i + 1 < e->prof_n; i += 2) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->prof_ev[i], e->prof_ev[i + 1]);
+    ms_total += ms;
+  }
+  for (double f : e->prof_flops) fl += f;
+  e->timings.gemm_ms = (float)ms_total;
+  e->timings.gemm_flops = fl;
+  e->timings.gemm_launches = (uint32_t)(e->prof_n / 2);
+  e->prof_n = 0;
+  e->prof_flops.clear();
+}
+
+void* dalloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  VNT_CUDA(cudaMalloc(&p, bytes));
+  return p;
+}
+
+void bind(vnt_engine* e) { VNT_CUDA(cudaSetDevice(e->opt.cuda_device)); }
+
+uint32_t ntensors(const vnt_engine* e) { return 2u * e->L; }
+
+float pow2f(int s) { return std::ldexp(1.0f, s); }
+
+int initial_scale(uint64_t batch) {
+  // No gradient history: assume max |mean grad| ~ 1.
+  return kScaleTargetBits - (int)std::ceil(std::log2((double)std::max<uint64_t>(batch, 1)));
+}
+
+void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
+  const int L = e->L;
+  if (rows <= e->cap_rows && ldT <= e->cap_ldT && vns <= e->cap_vns) return;
+  rows = std::max(rows, e->cap_rows);
+  ldT = std::max(ldT, e->cap_ldT);
+  vns = std::max(vns, e->cap_vns);
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  auto fre = [](auto*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  };
+  fre(e->xin);
+  fre(e->yin);
+  fre(e->logits);
+  fre(e->vn_mean);
+  fre(e->vn_m2);
+  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT})
+    for (auto*& p : *v) fre(p);
+  const uint64_t in = e->widths[0], out = e->widths[L];
+  e->xin = (double*)dalloc(rows * in * sizeof(double));
+  e->yin = (double*)dalloc(rows * out * sizeof(double));
+  e->logits = (float*)dalloc(rows * out * sizeof(float));
+  e->vn_mean = (double*)dalloc(vns * in * sizeof(double));
+  e->vn_m2 = (double*)dalloc(vns * in * sizeof(double));
+  e->X.assign(L + 1, nullptr);
+  e->XT.assign(L + 1, nullptr);
+  e->D.assign(L + 1, nullptr);
+  e->DT.assign(L + 1, nullptr);
+  for (int l = 0; l <= L; ++l) {
+    const uint64_t w = e->widths[l];
+    if (l < L) {
+      e->X[l] = (float*)dalloc(rows * w * sizeof(float));
+      e->XT[l] = (float*)dalloc(w * ldT * sizeof(float));
+      VNT_CUDA(cudaMemset(e->XT[l], 0, w * ldT * sizeof(float)));   // padding stays zero
+    }
+    if (l > 0) {
+      e->D[l] = (float*)dalloc(rows * w * sizeof(float));
+      e->DT[l] = (float*)dalloc(w * ldT * sizeof(float));
+      VNT_CUDA(cudaMemset(e->DT[l], 0, w * ldT * sizeof(float)));
+    }
+  }
+  e->cap_rows = rows;
+  e->cap_ldT = ldT;
+  e->cap_vns = vns;
+}
+
+void ensure_combine(vnt_engine* e, size_t n) {
+  if (n <= e->combine_cap) return;
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->d_combine) cudaFree(e->d_combine);
+  if (e->h_combine) cudaFreeHost(e->h_combine);
+  n = std::max<size_t>(n, 64);
+  e->d_combine = (CombineStep*)dalloc(n * sizeof(CombineStep));
+  VNT_CUDA(cudaMallocHost(&e->h_combine, n * sizeof(CombineStep)));
+  e->combine_cap = n;
+}
+
+// Group local nodes (ascending id) into passes that fit resident_rows.
+std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
+  std::vector<int64_t> key;
+  key.reserve(local.size() * 4 + 1);
+  key.push_back((int64_t)e->opt.resident_rows);
+  for (const auto& n : local) {
+    key.push_back(n.node);
+    key.push_back(n.dev);
+    key.push_back((int64_t)n.rows);
+    key.push_back((int64_t)n.src_row);
+  }
+  auto it = e->plans.find(key);
+  if (it != e->plans.end()) return it->second;
+  std::vector<Pass> passes;
+  const uint64_t budget = e->opt.resident_rows ? e->opt.resident_rows : ~0ull;
+  Pass cur;
+  for (const auto& n : local) {
+    if (!cur.nodes.empty() && cur.rows + n.rows > budget) {
+      passes.push_back(cur);
+      cur = Pass{};
+    }
+    PassNode pn = n;
+    pn.prow = cur.rows;
+    pn.pcol = cur.ldT;
+    cur.rows += n.rows;
+    cur.ldT += round_up(n.rows, 32);
+    cur.nodes.push_back(pn);
+  }
+  if (!cur.nodes.empty()) passes.push_back(cur);
+  for (auto& p : passes) {
+    const size_t nn = p.nodes.size();
+    std::vector<int> meta(p.rows + 3 * nn);
+    for (size_t k = 0; k < nn; ++k) {
+      const auto& pn = p.nodes[k];
+      for (uint64_t r = 0; r < pn.rows; ++r) meta[pn.prow + r] = (int)(pn.pcol + r);
+      meta[p.rows + k] = (int)pn.prow;
+      meta[p.rows + nn + k] = (int)pn.rows;
+      meta[p.rows + 2 * nn + k] = (int)pn.pcol;
+    }
+    p.d_meta = (int*)dalloc(meta.size() * sizeof(int));
+    VNT_CUDA(cudaMemcpy(p.d_meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  return e->plans.emplace(key, std::move(passes)).first->second;
+}
+
+void tail_reset(vnt_engine* e) {
+  VNT_CUDA(cudaMemsetAsync(e->G + e->P, 0, e->ntail * sizeof(long long), e->stream));
+}
+
+// ---------------------------------------------------------------- one pass
+void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bool x_on_device,
+              bool do_stats, bool first_write) {
+  const int L = e->L;
+  const uint64_t in = e->widths[0], out = e->widths[L];
+  const size_t nn = p.nodes.size();
+  ensure_capacity(e, p.rows, p.ldT, nn);
+  cudaStream_t s = e->stream;
+  const cudaMemcpyKind kind = x_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  // Batch::slice copies (data.cpp:36-48): each node's contiguous rows.
+  for (const auto& pn : p.nodes) {
+    VNT_CUDA(cudaMemcpyAsync(e->xin + pn.prow * in, x + pn.src_row * in,
+                             pn.rows * in * sizeof(double), kind, s));
+    VNT_CUDA(cudaMemcpyAsync(e->yin + pn.prow * out, y + pn.src_row * out,
+                             pn.rows * out * sizeof(double), kind, s));
+  }
+  const int* tcol = p.d_meta;
+  const int* row0 = p.d_meta + p.rows;
+  const int* nrows = row0 + nn;
+  const int* col0 = nrows + nn;
+  const int rows = (int)p.rows, ldT = (int)p.ldT;
+  {
+    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(p.rows, 32)), block(32, 8);
+    k_ingest<<<grid, block, 0, s>>>(e->xin, e->X[0], e->XT[0], tcol, rows, (int)in, ldT);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+  }
+  if (do_stats) {
+    // observe_batch per node then Chan-combine into the node's device lineage
+    // in ascending node id (virtual_exec.cpp:137-138, model.cpp:152-154).
+    dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
+    k_vn_stats<<<grid, 128, 0, s>>>(e->xin, (int)in, row0, nrows, e->vn_mean, e->vn_m2);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+    std::vector<std::vector<CombineStep>> per_dev(e->devs.size());
+    for (size_t k = 0; k < nn; ++k) {
+      auto& d = e->devs[p.nodes[k].dev];
+      const double other = (double)p.nodes[k].rows;
+      CombineStep st{(int)k, 0, 0.0, 0.0};
+      if (d.count == 0) {
+        st.copy = 1;
+        d.count = other;
+      } else {
+        const double n = d.count + other;
+        st.f1 = d.count * other / n;
+        st.f2 = other / n;
+        d.count = n;
+      }
+      per_dev[p.nodes[k].dev].push_back(st);
+    }
+    size_t total = 0;
+    for (auto& v : per_dev) total += v.size();
+    ensure_combine(e, total);
+    size_t off = 0;
+    for (size_t dv = 0; dv < per_dev.size(); ++dv) {
+      if (per_dev[dv].empty()) continue;
+      // The pinned staging is reused only after the step's final sync.
+      std::memcpy(e->h_combine + off, per_dev[dv].data(), per_dev[dv].size() * sizeof(CombineStep));
+      VNT_CUDA(cudaMemcpyAsync(e->d_combine + off, e->h_combine + off,
+                               per_dev[dv].size() * sizeof(CombineStep), cudaMemcpyHostToDevice, s));
+      k_stats_combine<<<(unsigned)ceil_div(in, 128), 128, 0, s>>>(
+          e->devs[dv].mean, e->devs[dv].m2, (int)in, e->vn_mean, e->vn_m2, e->d_combine + off,
+          (int)per_dev[dv].size());
+      VNT_LAUNCH_CHECK();
+      e->launches++;
+      off += per_dev[dv].size();
+    }
+  }
+  // Forward (model.cpp:275-287).
+  for (int l = 0; l < L; ++l) {
+    const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
+    const bool last = (l == L - 1);
+    const float* W = e->w32 + e->woff[l];
+    const float* b = e->w32 + e->boff[l];
+    prof_begin(e);
+    if (e->tc_layer[l]) {
+      tc_forward(e, l, rows, ldT, tcol, last);
+    } else {
+      dim3 grid((unsigned)ceil_div(N, 64), (unsigned)ceil_div(p.rows, 64));
+      if (last) {
+        k_gemm_ffma<kEpiLogits><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
+                                                     e->logits, N, nullptr, 0, nullptr, nullptr, 0);
+      } else {
+        k_gemm_ffma<kEpiHidden><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
+                                                     e->X[l + 1], N, e->XT[l + 1], ldT, tcol,
+                                                     nullptr, 0);
+      }
+      VNT_LAUNCH_CHECK();
+      e->launches++;
+    }
+    prof_end(e, 2.0 * rows * (double)K * N);
+  }
+  cudaEventRecord(e->ev[1], s);
+  // Loss + output delta (model.cpp:289-315).
+  {
+    const unsigned warps_per_block = 8;
+    k_loss<<<(unsigned)ceil_div(p.rows, warps_per_block), warps_per_block * 32, 0, s>>>(
+        e->logits, e->yin, rows, (int)out, e->loss, e->D[L], e->DT[L], ldT, tcol, e->G + e->P);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+  }
+  // Backward (model.cpp:317-338): dW/db per node into the exact sum, then delta.
+  const float lim = pow2f(kLimBits);
+  for (int l = L - 1; l >= 0; --l) {
+    const int in_l = (int)e->widths[l], out_l = (int)e->widths[l + 1];
+    const int tw = 2 * l, tb = 2 * l + 1;
+    prof_begin(e);
+    if (e->tc_layer[l]) {
+      tc_weight_grad(e, l, p, col0, nrows, pow2f(e->scales[tw]), lim, first_write, tw);
+    } else {
+      dim3 grid((unsigned)ceil_div(out_l, 64), (unsigned)ceil_div(in_l, 64));
+      k_dw_ffma<<<grid, 256, 0, s>>>(e->XT[l], e->DT[l + 1], ldT, in_l, out_l, col0, nrows,
+                                     (int)nn, pow2f(e->scales[tw]), lim, e->G + e->woff[l],
+                                     first_write ? 1 : 0, e->G + e->P, tw);
+      VNT_LAUNCH_CHECK();
+      e->launches++;
+    }
+    prof_end(e, 2.0 * rows * (double)in_l * out_l);
+    k_db<<<(unsigned)ceil_div(out_l, 128), 128, 0, s>>>(
+        e->D[l + 1], out_l, row0, nrows, (int)nn, pow2f(e->scales[tb]), lim, e->G + e->boff[l],
+        first_write ? 1 : 0, e->G + e->P, tb);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+    if (l > 0) {
+      prof_begin(e);
+      if (e->tc_layer[l]) {
+        tc_backward_data(e, l, rows, ldT, tcol);
+      } else {
+        const float* WT = e->wt32 + e->wtoff[l];
+        dim3 grid((unsigned)ceil_div(in_l, 64), (unsigned)ceil_div(p.rows, 64));
+        k_gemm_ffma<kEpiBwd><<<grid, 256, 0, s>>>(e->D[l + 1], out_l, WT, in_l, rows, in_l, out_l,
+                                                  nullptr, e->act, e->D[l], in_l, e->DT[l], ldT,
+                                                  tcol, e->X[l], in_l);
+        VNT_LAUNCH_CHECK();
+        e->launches++;
+      }
+      prof_end(e, 2.0 * rows * (double)in_l * out_l);
+    }
+  }
+}
+
+void begin_round(vnt_engine* e, uint64_t batch_hint) {
+  if (e->round_open) return;
+  tail_reset(e);
+  e->acc_examples = 0;
+  e->acc_started = false;
+  e->round_open = true;
+  if (!e->scales_init) {
+    std::fill(e->scales.begin(), e->scales.end(), initial_scale(batch_hint));
+    e->scales_init = true;
+  }
+  const uint64_t in = e->widths[0];
+  for (auto& d : e->devs) {
+    d.count_bak = d.count;
+    VNT_CUDA(cudaMemcpyAsync(d.mean_bak, d.mean, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    VNT_CUDA(cudaMemcpyAsync(d.m2_bak, d.m2, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+  }
+}
+
+// Undo the round's input-statistics updates (a rescaled redo observes again).
+void restore_stats(vnt_engine* e) {
+  const uint64_t in = e->widths[0];
+  for (auto& d : e->devs) {
+    d.count = d.count_bak;
+    VNT_CUDA(cudaMemcpyAsync(d.mean, d.mean_bak, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    VNT_CUDA(cudaMemcpyAsync(d.m2, d.m2_bak, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+  }
+}
+
+void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, const double* y,
+                bool on_device, bool do_stats) {
+  auto& passes = plan_for(e, local);
+  for (const auto& p : passes) {
+    run_pass(e, p, x, y, on_device, do_stats, !e->acc_started);
+    e->acc_started = true;
+    e->acc_examples += p.rows;
+  }
+}
+
+void collective(vnt_engine* e) {
+  // Exact int64 sum over processes; associative, so any NCCL algorithm or
+  // topology gives the same bits.
+  if (e->opt.world_size > 1) {
+    const ncclResult_t r = ncclAllReduce(e->G, e->G, e->P + e->ntail, ncclInt64, ncclSum,
+                                         e->comm, e->stream);
+    if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+  }
+}
+
+void launch_sgd(vnt_engine* e, double lr, uint64_t examples) {
+  cudaStream_t s = e->stream;
+  VNT_CUDA(cudaMemsetAsync(e->gmax, 0, ntensors(e) * sizeof(unsigned long long), s));
+  const double inv_b = 1.0 / (double)examples;   // virtual_exec.cpp:165
+  for (int l = 0; l < e->L; ++l) {
+    for (int part = 0; part < 2; ++part) {
+      const int t = 2 * l + part;
+      SgdArgs a{};
+      const uint64_t off = part ? e->boff[l] : e->woff[l];
+      a.w64 = e->w64 + off;
+      a.v64 = e->v64 ? e->v64 + off : nullptr;
+      a.G = e->G + off;
+      a.w32 = e->w32 + off;
+      a.wt32 = part ? nullptr : e->wt32 + e->wtoff[l];
+      a.gout = e->gout ? e->gout + off : nullptr;
+      a.gmax = e->gmax + t;
+      a.tail = e->G + e->P;
+      a.ntail_flags = (int)ntensors(e);
+      a.inv_scale = std::ldexp(1.0, -e->scales[t]);
+      a.inv_b = inv_b;
+      a.lr = lr;
+      a.mu = e->opt.momentum;
+      if (part == 0) {
+        a.rows = (int)e->widths[l];
+        a.cols = (int)e->widths[l + 1];
+        dim3 grid((unsigned)ceil_div(a.cols, 32), (unsigned)ceil_div(a.rows, 32)), block(32, 8);
+        k_sgd_weight<<<grid, block, 0, s>>>(a);
+      } else {
+        a.rows = 1;
+        a.cols = (int)e->widths[l + 1];
+        k_sgd_vec<<<(unsigned)std::min<uint64_t>(ceil_div(a.cols, 256), 1024), 256, 0, s>>>(a);
+      }
+      VNT_LAUNCH_CHECK();
+      e->launches++;
+    }
+  }
+}
+
+struct Readback {
+  double loss_sum;
+  uint64_t examples;
+  bool nonfinite;
+  std::vector<int> overflow;   // tensor ids
+};
+
+Readback read_tail(vnt_engine* e, bool with_gmax) {
+  cudaStream_t s = e->stream;
+  VNT_CUDA(cudaMemcpyAsync(e->h_tail, e->G + e->P, e->ntail * sizeof(long long),
+                           cudaMemcpyDeviceToHost, s));
+  if (with_gmax)
+    VNT_CUDA(cudaMemcpyAsync(e->h_gmax, e->gmax, ntensors(e) * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+  VNT_CUDA(cudaStreamSynchronize(s));
+  Readback r;
+  r.loss_sum = std::ldexp((double)e->h_tail[kTailLoss], -kLossScaleBits);
+  r.examples = (uint64_t)e->h_tail[kTailExamples];
+  r.nonfinite = e->h_tail[kTailNonfinite] != 0;
+  for (uint32_t t = 0; t < ntensors(e); ++t)
+    if (e->h_tail[kTailOverflow + t]) r.overflow.push_back((int)t);
+  return r;
+}
+
+void update_scales(vnt_engine* e, uint64_t batch) {
+  for (uint32_t t = 0; t < ntensors(e); ++t) {
+    double g;
+    std::memcpy(&g, &e->h_gmax[t], sizeof g);
+    if (!(g > 0.0) || !std::isfinite(g)) continue;
+    const int s = kScaleTargetBits - (int)std::ceil(std::log2(g * (double)batch));
+    e->scales[t] = std::clamp(s, -100, 100);
+  }
+}
+
+// Adds the examples count into the exact tail (so it is summed by the collective).
+__global__ void k_tail_add(long long* tail, int slot, long long v) { tail[slot] += v; }
+
+void reset_acc(vnt_engine* e) {
+  e->round_open = false;
+  e->acc_started = false;
+  e->acc_examples = 0;
+  e->synced = false;
+}
+
+std::vector<PassNode> local_nodes(vnt_engine* e, const uint64_t* node_sizes,
+                                  const int32_t* node_device, uint32_t total_nodes,
+                                  uint64_t batch_rows) {
+  std::vector<PassNode> local;
+  uint64_t off = 0;
+  for (uint32_t n = 0; n < total_nodes; ++n) {
+    if (node_sizes[n] == 0) throw EngineError(VNT_ERR_CONFIG, "virtual node with zero examples");
+    const int32_t d = node_device[n];
+    if (d >= (int32_t)e->devs.size())
+      throw EngineError(VNT_ERR_CONFIG, "node_device references unknown local device");
+    if (d >= 0) {
+      if (node_sizes[n] > e->devs[d].capacity)
+        throw EngineError(VNT_ERR_CAPACITY, "virtual node " + std::to_string(n) + " (" +
+                                                std::to_string(node_sizes[n]) +
+                                                " examples) exceeds memory capacity of device");
+      local.push_back(PassNode{(int)n, d, node_sizes[n], off, 0, 0});
+    }
+    off += node_sizes[n];
+  }
+  if (off != batch_rows)
+    throw EngineError(VNT_ERR_CONFIG, "node sizes cover " + std::to_string(off) +
+                                          " examples but batch has " + std::to_string(batch_rows));
+  return local;
+}
+
+int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t batch_rows,
+                    const uint64_t* node_sizes, const int32_t* node_device,
+                    uint32_t total_nodes, double lr, double* loss, vnt_device_metrics* per_dev,
+                    bool on_device) {
+  bind(e);
+  if (!(lr > 0.0)) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: learning rate must be positive");
+  auto local = local_nodes(e, node_sizes, node_device, total_nodes, batch_rows);
+  reset_acc(e);
+  e->launches = 0;
+  uint32_t retries = 0;
+  for (int attempt = 0;; ++attempt) {
+    cudaEventRecord(e->ev[0], e->stream);
+    begin_round(e, batch_rows);
+    if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0);
+    k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
+    e->launches++;
+    if (local.empty()) {
+      // This process hosts no node this step: contribute zeros.
+      VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
+    }
+    cudaEventRecord(e->ev[2], e->stream);
+    collective(e);
+    cudaEventRecord(e->ev[3], e->stream);
+    launch_sgd(e, lr, batch_rows);
+    cudaEventRecord(e->ev[4], e->stream);
+    Readback rb = read_tail(e, true);
+    if (rb.nonfinite || !rb.overflow.empty()) {
+      e->prof_n = 0;
+      e->prof_flops.clear();
+    }
+    if (rb.nonfinite) {
+      reset_acc(e);
+      throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
+    }
+    if (!rb.overflow.empty()) {
+      for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
+      ++retries;
+      reset_acc(e);
+      if (retries > 8) throw EngineError(VNT_ERR_RESCALE, "fixed-point range could not be found");
+      continue;
+    }
+    update_scales(e, batch_rows);
+    if (loss) *loss = rb.loss_sum / (double)batch_rows;   // virtual_exec.cpp:275
+    break;
+  }
+  float ms[4] = {};
+  cudaEventElapsedTime(&ms[0], e->ev[0], e->ev[1]);
+  cudaEventElapsedTime(&ms[1], e->ev[1], e->ev[2]);
+  cudaEventElapsedTime(&ms[2], e->ev[2], e->ev[3]);
+  cudaEventElapsedTime(&ms[3], e->ev[3], e->ev[4]);
+  e->timings.forward_ms = ms[0];
+  e->timings.backward_ms = ms[1];
+  e->timings.sync_ms = ms[2];
+  e->timings.update_ms = ms[3];
+  cudaEventElapsedTime(&e->timings.total_ms, e->ev[0], e->ev[4]);
+  e->timings.kernel_launches = e->launches;
+  e->timings.rescale_retries = retries;
+  prof_collect(e);
+  if (per_dev) {
+    for (size_t d = 0; d < e->devs.size(); ++d) {
+      vnt_device_metrics m{};
+      for (const auto& pn : local) {
+        if (pn.dev != (int)d) continue;
+        m.waves += 1;
+        m.examples += pn.rows;
+        m.peak_resident = std::max<uint64_t>(m.peak_resident, pn.rows);
+      }
+      m.buffer_bytes = e->P * sizeof(double);
+      per_dev[d] = m;
+    }
+  }
+  reset_acc(e);
+  return VNT_OK;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const EngineError& err) {
+    return set_error(err.code, err.what());
+  } catch (const std::exception& err) {
+    return set_error(VNT_ERR_INTERNAL, err.what());
+  }
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* vnt_last_error(void) { return g_last_error.c_str(); }
+
+const char* vnt_build_info(void) {
+  return "vnt-b200 engine: sm_100a, FFMA + tcgen05 kind::tf32, int64 exact gradient sum, NCCL";
+}
+
+int vnt_nccl_unique_id(uint8_t out[128]) {
+  return guarded([&] {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* options,
+                      vnt_engine** out) {
+  return guarded([&] {
+    if (!model || !options || !out) throw EngineError(VNT_ERR_CONFIG, "null argument");
+    if (model->num_widths < 2)
+      throw EngineError(VNT_ERR_CONFIG, "ModelSpec: need at least input and output widths");
+    for (uint32_t i = 0; i < model->num_widths; ++i)
+      if (model->layer_widths[i] == 0)
+        throw EngineError(VNT_ERR_CONFIG, "ModelSpec: layer widths must be positive");
+    if (model->activation < 0 || model->activation > 2 || model->loss < 0 || model->loss > 1)
+      throw EngineError(VNT_ERR_CONFIG, "unknown activation or loss");
+    if (options->world_size < 1 || options->rank < 0 || options->rank >= options->world_size)
+      throw EngineError(VNT_ERR_CONFIG, "bad rank/world_size");
+    if (options->momentum < 0.0 || options->momentum >= 1.0)
+      throw EngineError(VNT_ERR_CONFIG, "momentum must lie in [0, 1)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw EngineError(VNT_ERR_CUDA, "no CUDA device visible: the B200 engine has no CPU fallback");
+    if (options->cuda_device < 0 || options->cuda_device >= ndev)
+      throw EngineError(VNT_ERR_CUDA, "cuda_device out of range");
+    cudaDeviceProp prop;
+    VNT_CUDA(cudaGetDeviceProperties(&prop, options->cuda_device));
+    if (prop.major != 10)
+      throw EngineError(VNT_ERR_CUDA, std::string("engine is built for sm_100a (B200); found ") +
+                                          prop.name);
+    auto e = std::make_unique<vnt_engine>();
+    e->opt = *options;
+    e->opt.nccl_id = nullptr;
+    e->profile = getenv("VNT_PROFILE_KERNELS") && getenv("VNT_PROFILE_KERNELS")[0] == '1';
+    e->widths.assign(model->layer_widths, model->layer_widths + model->num_widths);
+    e->L = (int)model->num_widths - 1;
+    e->act = model->activation;
+    e->loss = model->loss;
+    e->sm_count = prop.multiProcessorCount;
+    uint64_t off = 0, toff = 0;
+    for (int l = 0; l < e->L; ++l) {
+      e->woff.push_back(off);
+      off += e->widths[l] * e->widths[l + 1];
+      e->boff.push_back(off);
+      off += e->widths[l + 1];
+      e->wtoff.push_back(toff);
+      toff += e->widths[l] * e->widths[l + 1];
+      e->tc_layer.push_back(tc_layer_eligible(e->opt.gemm_mode, e->widths[l], e->widths[l + 1]));
+    }
+    e->P = off;
+    bind(e.get());
+    VNT_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    for (auto& ev : e->ev) VNT_CUDA(cudaEventCreate(&ev));
+    e->w64 = (double*)dalloc(e->P * sizeof(double));
+    VNT_CUDA(cudaMemset(e->w64, 0, e->P * sizeof(double)));
+    if (e->opt.momentum > 0.0) {
+      e->v64 = (double*)dalloc(e->P * sizeof(double));
+      VNT_CUDA(cudaMemset(e->v64, 0, e->P * sizeof(double)));
+    }
+    e->w32 = (float*)dalloc(e->P * sizeof(float));
+    VNT_CUDA(cudaMemset(e->w32, 0, e->P * sizeof(float)));
+    e->wt32 = (float*)dalloc(toff * sizeof(float));
+    VNT_CUDA(cudaMemset(e->wt32, 0, toff * sizeof(float)));
+    e->ntail = kTailOverflow + ntensors(e.get());
+    e->G = (long long*)dalloc((e->P + e->ntail) * sizeof(long long));
+    e->gmax = (unsigned long long*)dalloc(ntensors(e.get()) * sizeof(unsigned long long));
+    VNT_CUDA(cudaMallocHost(&e->h_tail, e->ntail * sizeof(long long)));
+    VNT_CUDA(cudaMallocHost(&e->h_gmax, ntensors(e.get()) * sizeof(unsigned long long)));
+    e->scales.assign(ntensors(e.get()), 0);
+    tc_init(e.get());
+    if (e->opt.world_size > 1) {
+      if (!options->nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
+      ncclUniqueId id;
+      std::memcpy(&id, options->nccl_id, sizeof id);
+      const ncclResult_t r = ncclCommInitRank(&e->comm, e->opt.world_size, id, e->opt.rank);
+      if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+    }
+    *out = e.release();
+    return VNT_OK;
+  });
+}
+
+void vnt_engine_destroy(vnt_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->opt.cuda_device);
+  cudaStreamSynchronize(e->stream);
+  if (e->comm) ncclCommDestroy(e->comm);
+  tc_destroy(e);
+  for (auto& kv : e->plans)
+    for (auto& p : kv.second) cudaFree(p.d_meta);
+  for (auto* p : e->scratch) cudaFree(p);
+  for (void* p : {(void*)e->w64, (void*)e->v64, (void*)e->w32, (void*)e->wt32, (void*)e->G,
+                  (void*)e->gmax, (void*)e->gout, (void*)e->xin, (void*)e->yin, (void*)e->logits,
+                  (void*)e->vn_mean, (void*)e->vn_m2, (void*)e->d_combine})
+    if (p) cudaFree(p);
+  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT})
+    for (auto* p : *v)
+      if (p) cudaFree(p);
+  for (auto& d : e->devs) {
+    cudaFree(d.mean);
+    cudaFree(d.m2);
+    cudaFree(d.mean_bak);
+    cudaFree(d.m2_bak);
+  }
+  if (e->h_combine) cudaFreeHost(e->h_combine);
+  if (e->h_tail) cudaFreeHost(e->h_tail);
+  if (e->h_gmax) cudaFreeHost(e->h_gmax);
+  for (auto& ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : e->prof_ev) cudaEventDestroy(ev);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+uint64_t vnt_engine_param_count(const vnt_engine* e) { return e ? e->P : 0; }
+uint32_t vnt_engine_tensor_count(const vnt_engine* e) { return e ? ntensors(e) : 0; }
+
+int vnt_engine_set_params(vnt_engine* e, const double* params, uint64_t n) {
+  return guarded([&] {
+    if (n != e->P) throw EngineError(VNT_ERR_SHAPE, "params layout does not match model layout");
+    bind(e);
+    VNT_CUDA(cudaMemcpyAsync(e->w64, params, n * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    for (int l = 0; l < e->L; ++l) {
+      const int rows = (int)e->widths[l], cols = (int)e->widths[l + 1];
+      dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+      k_refresh_weight<<<grid, block, 0, e->stream>>>(e->w64 + e->woff[l], e->w32 + e->woff[l],
+                                                      e->wt32 + e->wtoff[l], rows, cols);
+      VNT_LAUNCH_CHECK();
+      k_refresh_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, e->stream>>>(
+          e->w64 + e->boff[l], e->w32 + e->boff[l], (size_t)cols);
+      VNT_LAUNCH_CHECK();
+    }
+    if (e->v64) VNT_CUDA(cudaMemsetAsync(e->v64, 0, e->P * sizeof(double), e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_get_params(vnt_engine* e, double* params, uint64_t n) {
+  return guarded([&] {
+    if (n != e->P) throw EngineError(VNT_ERR_SHAPE, "params layout does not match model layout");
+    bind(e);
+    VNT_CUDA(cudaMemcpyAsync(params, e->w64, n * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_add_device(vnt_engine* e, uint64_t capacity, int32_t* out_index) {
+  return guarded([&] {
+    bind(e);
+    vnt_engine::LDev d;
+    d.capacity = capacity;
+    const uint64_t in = e->widths[0];
+    d.mean = (double*)dalloc(in * sizeof(double));
+    d.m2 = (double*)dalloc(in * sizeof(double));
+    d.mean_bak = (double*)dalloc(in * sizeof(double));
+    d.m2_bak = (double*)dalloc(in * sizeof(double));
+    VNT_CUDA(cudaMemset(d.mean, 0, in * sizeof(double)));
+    VNT_CUDA(cudaMemset(d.m2, 0, in * sizeof(double)));
+    e->devs.push_back(d);
+    if (out_index) *out_index = (int32_t)e->devs.size() - 1;
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_device_count(const vnt_engine* e) { return e ? (int)e->devs.size() : 0; }
+
+int vnt_engine_device_step(vnt_engine* e, int32_t device, const double* x, const double* y,
+                           const uint64_t* node_sizes, uint32_t num_nodes,
+                           vnt_device_metrics* metrics) {
+  return guarded([&] {
+    bind(e);
+    if (device < 0 || device >= (int32_t)e->devs.size())
+      throw EngineError(VNT_ERR_CONFIG, "unknown device");
+    if (num_nodes == 0)
+      throw EngineError(VNT_ERR_CONFIG, "device_step: device has no virtual nodes to run");
+    std::vector<PassNode> local;
+    uint64_t off = 0;
+    vnt_device_metrics m{};
+    for (uint32_t k = 0; k < num_nodes; ++k) {
+      if (node_sizes[k] == 0) throw EngineError(VNT_ERR_CONFIG, "Batch: count must be >= 1");
+      if (node_sizes[k] > e->devs[device].capacity)
+        throw EngineError(VNT_ERR_CAPACITY, "micro-batch of " + std::to_string(node_sizes[k]) +
+                                                " examples exceeds memory capacity of device");
+      local.push_back(PassNode{(int)k, device, node_sizes[k], off, 0, 0});
+      off += node_sizes[k];
+      m.waves += 1;
+      m.examples += node_sizes[k];
+      m.peak_resident = std::max<uint64_t>(m.peak_resident, node_sizes[k]);
+    }
+    m.buffer_bytes = e->P * sizeof(double);
+    if (e->synced) reset_acc(e);
+    if (!e->round_open) e->launches = 0;
+    begin_round(e, off * std::max<uint64_t>(1, e->devs.size()) * (uint64_t)e->opt.world_size);
+    accumulate(e, local, x, y, false, true);
+    if (metrics) *metrics = m;
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum, uint64_t* examples) {
+  return guarded([&] {
+    bind(e);
+    if (!e->acc_started) {
+      // This process accumulated nothing: contribute zeros to the collective.
+      begin_round(e, 1);
+      VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
+      e->acc_started = true;
+    }
+    k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
+    e->acc_examples = 0;
+    collective(e);
+    Readback rb = read_tail(e, false);
+    if (rb.nonfinite) {
+      reset_acc(e);
+      throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
+    }
+    if (!rb.overflow.empty()) {
+      for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
+      restore_stats(e);
+      reset_acc(e);
+      throw EngineError(VNT_ERR_RESCALE, "fixed-point range exceeded; scale lowered, redo the step");
+    }
+    if (rb.examples == 0) throw EngineError(VNT_ERR_CONFIG, "sync_gradients: zero examples accumulated");
+    e->synced = true;
+    e->timings.rescale_retries = 0;
+    if (loss_sum) *loss_sum = rb.loss_sum;
+    if (examples) *examples = rb.examples;
+    e->h_tail[kTailExamples] = (long long)rb.examples;
+    if (mean_grad) {
+      if (!e->gout) e->gout = (double*)dalloc(e->P * sizeof(double));
+      for (int l = 0; l < e->L; ++l) {
+        for (int part = 0; part < 2; ++part) {
+          const uint64_t off = part ? e->boff[l] : e->woff[l];
+          const uint64_t n = part ? e->widths[l + 1] : e->widths[l] * e->widths[l + 1];
+          k_mean_grad<<<(unsigned)std::min<uint64_t>(ceil_div(n, 256), 4096), 256, 0, e->stream>>>(
+              e->G + off, e->gout + off, n, std::ldexp(1.0, -e->scales[2 * l + part]),
+              1.0 / (double)rb.examples);
+          VNT_LAUNCH_CHECK();
+        }
+      }
+      VNT_CUDA(cudaMemcpyAsync(mean_grad, e->gout, e->P * sizeof(double), cudaMemcpyDeviceToHost,
+                               e->stream));
+      VNT_CUDA(cudaStreamSynchronize(e->stream));
+    }
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_sgd_apply(vnt_engine* e, double lr) {
+  return guarded([&] {
+    bind(e);
+    if (!(lr > 0.0)) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: learning rate must be positive");
+    if (!e->synced) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: call vnt_engine_sync first");
+    const uint64_t examples = (uint64_t)e->h_tail[kTailExamples];
+    launch_sgd(e, lr, examples);
+    read_tail(e, true);
+    update_scales(e, examples);
+    reset_acc(e);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_train_step(vnt_engine* e, const double* x, const double* y, uint64_t batch_rows,
+                          const uint64_t* node_sizes, const int32_t* node_device,
+                          uint32_t total_nodes, double lr, double* loss,
+                          vnt_device_metrics* per_device) {
+  return guarded([&] {
+    return train_step_impl(e, x, y, batch_rows, node_sizes, node_device, total_nodes, lr, loss,
+                           per_device, false);
+  });
+}
+
+int vnt_engine_train_step_resident(vnt_engine* e, const double* x, const double* y,
+                                   uint64_t batch_rows, const uint64_t* node_sizes,
+                                   const int32_t* node_device, uint32_t total_nodes, double lr,
+                                   double* loss, vnt_device_metrics* per_device) {
+  return guarded([&] {
+    return train_step_impl(e, x, y, batch_rows, node_sizes, node_device, total_nodes, lr, loss,
+                           per_device, true);
+  });
+}
+
+int vnt_engine_get_input_stats(vnt_engine* e, int32_t device, double* count, double* mean,
+                               double* m2) {
+  return guarded([&] {
+    bind(e);
+    if (device < 0 || device >= (int32_t)e->devs.size())
+      throw EngineError(VNT_ERR_CONFIG, "unknown device");
+    const auto& d = e->devs[device];
+    const uint64_t in = e->widths[0];
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    if (count) *count = d.count;
+    if (mean) VNT_CUDA(cudaMemcpy(mean, d.mean, in * sizeof(double), cudaMemcpyDeviceToHost));
+    if (m2) VNT_CUDA(cudaMemcpy(m2, d.m2, in * sizeof(double), cudaMemcpyDeviceToHost));
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count, const double* mean,
+                               const double* m2) {
+  return guarded([&] {
+    bind(e);
+    if (device < 0 || device >= (int32_t)e->devs.size())
+      throw EngineError(VNT_ERR_CONFIG, "unknown device");
+    auto& d = e->devs[device];
+    const uint64_t in = e->widths[0];
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    d.count = count;
+    VNT_CUDA(cudaMemcpy(d.mean, mean, in * sizeof(double), cudaMemcpyHostToDevice));
+    VNT_CUDA(cudaMemcpy(d.m2, m2, in * sizeof(double), cudaMemcpyHostToDevice));
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_get_scales(vnt_engine* e, int32_t* scales, uint32_t n) {
+  return guarded([&] {
+    if (n != ntensors(e)) throw EngineError(VNT_ERR_SHAPE, "scale count mismatch");
+    std::copy(e->scales.begin(), e->scales.end(), scales);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n) {
+  return guarded([&] {
+    if (n != ntensors(e)) throw EngineError(VNT_ERR_SHAPE, "scale count mismatch");
+    e->scales.assign(scales, scales + n);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out) {
+  if (!e || !out) return VNT_ERR_CONFIG;
+  *out = e->timings;
+  return VNT_OK;
+}
+
+void* vnt_engine_stream(vnt_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+int vnt_engine_device_alloc(vnt_engine* e, uint64_t bytes, void** out) {
+  return guarded([&] {
+    bind(e);
+    *out = dalloc(bytes);
+    e->scratch.push_back(*out);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_device_free(vnt_engine* e, void* p) {
+  return guarded([&] {
+    bind(e);
+    auto it = std::find(e->scratch.begin(), e->scratch.end(), p);
+    if (it == e->scratch.end()) throw EngineError(VNT_ERR_CONFIG, "not an engine allocation");
+    e->scratch.erase(it);
+    VNT_CUDA(cudaFree(p));
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_memcpy_h2d(vnt_engine* e, void* dst, const void* src, uint64_t bytes) {
+  return guarded([&] {
+    bind(e);
+    VNT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    return VNT_OK;
+  });
+}
+
+}  // extern "C"

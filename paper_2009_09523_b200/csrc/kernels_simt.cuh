@@ -1,0 +1,468 @@
+// FFMA / memory-bound kernels of the virtual-node step (sm_100a).
+//
+// Layout in HBM: for a pass of `rows` examples (virtual nodes
+// concatenated in ascending node id, exactly the contiguous slices of
+// virtual_exec.cpp:221-238):
+//   X[l]  fp32 [rows][w_l]      activations (X[0] = input), row-major
+//   XT[l] fp32 [w_l][ldT]       the same, feature-major; node k occupies columns
+//                               [col0_k, col0_k + rows_k), padded to 32 with zeros
+//   D[l]  fp32 [rows][w_l]      dLoss/dZ_l (l = 1..L); DT[l] feature-major
+//   G     int64 [P + tail]      fixed-point gradient sum (exact, order-free)
+#pragma once
+
+#include "common.cuh"
+
+namespace vntb {
+
+// Tail slots of the int64 accumulator (all summed exactly by the collective).
+enum : int { kTailLoss = 0, kTailExamples = 1, kTailNonfinite = 2, kTailOverflow = 3 };
+
+// ---------------------------------------------------------------- ingest
+// fp64 rows (reference Batch layout, data.hpp:14-31) -> fp32 X0 and XT0.
+__global__ void k_ingest(const double* __restrict__ x, float* __restrict__ X0,
+                         float* __restrict__ XT0, const int* __restrict__ tcol, int rows,
+                         int in, int ldT) {
+  __shared__ float tile[32][33];
+  const int r0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, j = j0 + tx;
+    float v = 0.f;
+    if (r < rows && j < in) {
+      v = __double2float_rn(x[(size_t)r * in + j]);
+      X0[(size_t)r * in + j] = v;
+    }
+    tile[k][tx] = v;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int j = j0 + k, r = r0 + tx;
+    if (r < rows && j < in) XT0[(size_t)j * ldT + tcol[r]] = tile[tx][k];
+  }
+}
+
+// ------------------------------------------------------------ input stats
+// LayerStats::observe batch part (model.cpp:101-121): per node, per feature,
+// sequential fp64 sums in row order; __d*_rn forbid FMA contraction so the
+// result is bit-identical to the reference's x86-64 build.
+__global__ void k_vn_stats(const double* __restrict__ x, int in, const int* __restrict__ vn_row0,
+                           const int* __restrict__ vn_rows, double* __restrict__ vn_mean,
+                           double* __restrict__ vn_m2) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (j >= in) return;
+  const int r0 = vn_row0[k], n = vn_rows[k];
+  double m = 0.0;
+  for (int r = 0; r < n; ++r) m = __dadd_rn(m, x[(size_t)(r0 + r) * in + j]);
+  m = __ddiv_rn(m, (double)n);
+  double s = 0.0;
+  for (int r = 0; r < n; ++r) {
+    const double d = __dsub_rn(x[(size_t)(r0 + r) * in + j], m);
+    s = __dadd_rn(s, __dmul_rn(d, d));
+  }
+  vn_mean[(size_t)k * in + j] = m;
+  vn_m2[(size_t)k * in + j] = s;
+}
+
+// LayerStats::combine (model.cpp:123-139) of a device's nodes, ascending id.
+// The count arithmetic is done on the host with the same double ops; f1 =
+// count*other.count/n and f2 = other.count/n arrive precomputed.
+struct CombineStep {
+  int vn;        // index into the pass's node table
+  int copy;      // lineage empty: *this = other
+  double f1, f2;
+};
+
+__global__ void k_stats_combine(double* __restrict__ mean, double* __restrict__ m2, int in,
+                                const double* __restrict__ vn_mean,
+                                const double* __restrict__ vn_m2,
+                                const CombineStep* __restrict__ steps, int nsteps) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= in) return;
+  double mu = mean[j], s = m2[j];
+  for (int t = 0; t < nsteps; ++t) {
+    const CombineStep st = steps[t];
+    const double om = vn_mean[(size_t)st.vn * in + j], os = vn_m2[(size_t)st.vn * in + j];
+    if (st.copy) {
+      mu = om;
+      s = os;
+    } else {
+      const double delta = __dsub_rn(om, mu);
+      s = __dadd_rn(s, __dadd_rn(os, __dmul_rn(__dmul_rn(delta, delta), st.f1)));
+      mu = __dadd_rn(mu, __dmul_rn(delta, st.f2));
+    }
+  }
+  mean[j] = mu;
+  m2[j] = s;
+}
+
+// ------------------------------------------------------ FFMA dense layer
+// C[r][n] = init[n] + sum_k A[r][k] * B[k][n] with k strictly ascending in a
+// single fmaf chain per output (model.cpp:280-283: z = b; z += a_i * w_io), so
+// each output depends only on its row and the weights — never on how many
+// rows (virtual nodes) share the launch.  Epilogues:
+//   kEpiHidden: a = f(z) -> X[l+1], XT[l+1]
+//   kEpiLogits: z -> logits
+//   kEpiBwd:    d = z * f'(X[l]) -> D[l], DT[l]   (model.cpp:328-337)
+enum : int { kEpiHidden = 0, kEpiLogits = 1, kEpiBwd = 2 };
+
+template <int EPI>
+__global__ void __launch_bounds__(256) k_gemm_ffma(
+    const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb, int M, int N,
+    int K, const float* __restrict__ bias, int act, float* __restrict__ out, int ldo,
+    float* __restrict__ outT, int ldT, const int* __restrict__ tcol,
+    const float* __restrict__ Xprev, int ldx) {
+  __shared__ __align__(16) float As[16][64 + 4];
+  __shared__ __align__(16) float Bs[16][64 + 4];
+  const int t = threadIdx.x;
+  const int tx = t % 16, ty = t / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int n = n0 + tx * 4 + j;
+    const float b0 = (EPI != kEpiBwd && n < N) ? bias[n] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][j] = b0;
+  }
+  for (int k0 = 0; k0 < K; k0 += 16) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = t + e * 256;
+      const int mm = idx / 16, kk = idx % 16;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? A[(size_t)gm * lda + gk] : 0.f;
+      const int kb = idx / 64, nn = idx % 64;
+      const int gn = n0 + nn, gkb = k0 + kb;
+      Bs[kb][nn] = (gn < N && gkb < K) ? B[(size_t)gkb * ldb + gn] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + ty * 4 + i;
+    if (r >= M) continue;
+    const int tc = (EPI != kEpiLogits) ? tcol[r] : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (EPI == kEpiHidden) {
+        v = act_fwd(act, v);
+      } else if (EPI == kEpiBwd) {
+        v = v * act_grad_from_out(act, Xprev[(size_t)r * ldx + n]);
+      }
+      out[(size_t)r * ldo + n] = v;
+      if (EPI != kEpiLogits) outT[(size_t)n * ldT + tc] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------- loss/delta
+// model.cpp:289-315, one warp per row, fp64 from fp32 logits.  Row loss is
+// quantised at 2^-32 and summed exactly (int64 atomics: order-free).
+__global__ void k_loss(const float* __restrict__ logits, const double* __restrict__ y, int rows,
+                       int outw, int loss_kind, float* __restrict__ D, float* __restrict__ DT,
+                       int ldT, const int* __restrict__ tcol, long long* __restrict__ tail) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int r = warp;
+  const float* z = logits + (size_t)r * outw;
+  const double* yr = y + (size_t)r * outw;
+  const int tc = tcol[r];
+  double loss = 0.0;
+  if (loss_kind == 0) {
+    for (int o = lane; o < outw; o += 32) {
+      const double d = (double)z[o] - yr[o];
+      loss += d * d;
+      const float dl = (float)(2.0 * d / (double)outw);
+      D[(size_t)r * outw + o] = dl;
+      DT[(size_t)o * ldT + tc] = dl;
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
+    loss /= (double)outw;
+  } else {
+    double mx = -1e300;
+    for (int o = lane; o < outw; o += 32) mx = fmax(mx, (double)z[o]);
+#pragma unroll
+    for (int s = 16; s; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    double norm = 0.0;
+    for (int o = lane; o < outw; o += 32) norm += exp((double)z[o] - mx);
+#pragma unroll
+    for (int s = 16; s; s >>= 1) norm += __shfl_xor_sync(0xffffffffu, norm, s);
+    const double lognorm = log(norm);
+    for (int o = lane; o < outw; o += 32) {
+      const double zm = (double)z[o] - mx;
+      loss -= yr[o] * (zm - lognorm);
+      const float dl = (float)(exp(zm) / norm - yr[o]);
+      D[(size_t)r * outw + o] = dl;
+      DT[(size_t)o * ldT + tc] = dl;
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
+  }
+  if (lane == 0) {
+    if (!isfinite(loss)) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
+    } else {
+      const long long q = __double2ll_rn(ldexp(loss, kLossScaleBits));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailLoss]), (unsigned long long)q);
+    }
+  }
+}
+
+// Fixed-point quantisation of one per-node partial:
+// q = rint(g * 2^s).  |g * 2^s| must stay below lim = 2^62 / V so that any sum
+// of V partials fits int64; violations are counted and force a re-scaled redo.
+__device__ __forceinline__ long long quantise(float g, float scale, float lim,
+                                              long long* __restrict__ tail, int tensor) {
+  const float v = g * scale;
+  if (!isfinite(v)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
+    return 0;
+  }
+  if (fabsf(v) >= lim) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailOverflow + tensor]), 1ull);
+    return 0;
+  }
+  return __float2ll_rn(v);
+}
+
+// ------------------------------------------------ per-node dW, FFMA path
+// g_k[i][o] = sum_{r in node k} X[r][i] * D[r][o] (one fmaf chain, rows
+// ascending), quantised per node and accumulated in int64 registers across
+// every node of the pass; one read-modify-write of G per pass.
+__global__ void __launch_bounds__(256) k_dw_ffma(
+    const float* __restrict__ XT, const float* __restrict__ DT, int ldT, int in, int out,
+    const int* __restrict__ vn_col0, const int* __restrict__ vn_rows, int nvn, float scale,
+    float lim, long long* __restrict__ G, int first, long long* __restrict__ tail, int tensor) {
+  __shared__ __align__(16) float As[16][64 + 4];
+  __shared__ __align__(16) float Bs[16][64 + 4];
+  const int t = threadIdx.x;
+  const int tx = t % 16, ty = t / 16;
+  const int i0 = blockIdx.y * 64, o0 = blockIdx.x * 64;
+  long long acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+  for (int v = 0; v < nvn; ++v) {
+    const int c0 = vn_col0[v], n = vn_rows[v];
+    float g[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) g[i][j] = 0.f;
+    for (int k0 = 0; k0 < n; k0 += 16) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int idx = t + e * 256;
+        const int mm = idx / 16, kk = idx % 16;
+        const bool kin = (k0 + kk) < n;
+        As[kk][mm] = (kin && i0 + mm < in) ? XT[(size_t)(i0 + mm) * ldT + c0 + k0 + kk] : 0.f;
+        Bs[kk][mm] = (kin && o0 + mm < out) ? DT[(size_t)(o0 + mm) * ldT + c0 + k0 + kk] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+        const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+        const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+        const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) g[i][j] = fmaf(a[i], b[j], g[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] += quantise(g[i][j], scale, lim, tail, tensor);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gi = i0 + ty * 4 + i;
+    if (gi >= in) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int go = o0 + tx * 4 + j;
+      if (go >= out) continue;
+      long long* p = G + (size_t)gi * out + go;
+      *p = first ? acc[i][j] : *p + acc[i][j];
+    }
+  }
+}
+
+// Per-node bias gradient (model.cpp:322: gb = delta): column sums of D over
+// the node's rows, fp32 in row order, quantised per node.
+__global__ void k_db(const float* __restrict__ D, int out, const int* __restrict__ vn_row0,
+                     const int* __restrict__ vn_rows, int nvn, float scale, float lim,
+                     long long* __restrict__ G, int first, long long* __restrict__ tail,
+                     int tensor) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= out) return;
+  long long acc = 0;
+  for (int v = 0; v < nvn; ++v) {
+    const int r0 = vn_row0[v], n = vn_rows[v];
+    float g = 0.f;
+    for (int r = 0; r < n; ++r) g += D[(size_t)(r0 + r) * out + o];
+    acc += quantise(g, scale, lim, tail, tensor);
+  }
+  G[o] = first ? acc : G[o] + acc;
+}
+
+// -------------------------------------------------------------------- SGD
+// sync_gradients' rounding + x(1/B) (virtual_exec.cpp:169-174) and
+// sgd_apply (model.cpp:364-374) fused: g = double(S) * 2^-s * (1/B);
+// [v = mu*v + g]; w = w - lr*g in fp64 (no contraction), then refresh the
+// fp32 copies W32 [in][out] and WT32 [out][in].  Skipped wholesale when the
+// step hit a fixed-point overflow (the host lowers the scale and redoes it).
+struct SgdArgs {
+  double* w64;
+  double* v64;          // momentum buffer or nullptr
+  const long long* G;   // exact gradient sum (same layout as params)
+  float* w32;
+  float* wt32;          // transposed copy (weights only) or nullptr
+  double* gout;         // optional mean-gradient export
+  unsigned long long* gmax;  // max |g| of this tensor (bit pattern of a positive double)
+  const long long* tail;
+  int ntail_flags;
+  double inv_scale;     // 2^-s
+  double inv_b;         // 1.0 / B  (virtual_exec.cpp:165)
+  double lr, mu;
+  int rows, cols;       // tensor shape (bias: rows = 1)
+};
+
+__device__ __forceinline__ bool step_poisoned(const long long* tail, int nflags) {
+  if (tail[kTailNonfinite]) return true;
+  for (int t = 0; t < nflags; ++t)
+    if (tail[kTailOverflow + t]) return true;
+  return false;
+}
+
+__device__ __forceinline__ double sgd_one(const SgdArgs& a, size_t k, float& w32) {
+  const double g = __dmul_rn(__ll2double_rn(a.G[k]) * a.inv_scale, a.inv_b);
+  double u = g;
+  if (a.v64) {
+    u = __dadd_rn(__dmul_rn(a.mu, a.v64[k]), g);
+    a.v64[k] = u;
+  }
+  const double w = __dsub_rn(a.w64[k], __dmul_rn(a.lr, u));
+  a.w64[k] = w;
+  w32 = __double2float_rn(w);
+  if (a.gout) a.gout[k] = g;
+  return fabs(g);
+}
+
+__device__ __forceinline__ void block_max_to(unsigned long long* dst, double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+#pragma unroll
+  for (int s = 16; s; s >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, b, s);
+    b = o > b ? o : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(dst, b);
+}
+
+// Weight tensor: 32x32 tiles, 32x8 threads; transposed fp32 copy via smem.
+__global__ void k_sgd_weight(SgdArgs a) {
+  __shared__ float tile[32][33];
+  __shared__ int poisoned;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  if (tx == 0 && ty == 0) poisoned = step_poisoned(a.tail, a.ntail_flags);
+  __syncthreads();
+  if (poisoned) return;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  double mx = 0.0;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, c = c0 + tx;
+    float w32 = 0.f;
+    if (r < a.rows && c < a.cols) {
+      const size_t idx = (size_t)r * a.cols + c;
+      mx = fmax(mx, sgd_one(a, idx, w32));
+      a.w32[idx] = w32;
+    }
+    tile[k][tx] = w32;
+  }
+  block_max_to(a.gmax, mx);
+  if (!a.wt32) return;
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int c = c0 + k, r = r0 + tx;
+    if (r < a.rows && c < a.cols) a.wt32[(size_t)c * a.rows + r] = tile[tx][k];
+  }
+}
+
+__global__ void k_sgd_vec(SgdArgs a) {
+  __shared__ int poisoned;
+  if (threadIdx.x == 0) poisoned = step_poisoned(a.tail, a.ntail_flags);
+  __syncthreads();
+  if (poisoned) return;
+  const size_t n = (size_t)a.rows * a.cols;
+  double mx = 0.0;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+       k += (size_t)gridDim.x * blockDim.x) {
+    float w32;
+    mx = fmax(mx, sgd_one(a, k, w32));
+    a.w32[k] = w32;
+  }
+  block_max_to(a.gmax, mx);
+}
+
+// fp64 master -> fp32 working copies (set_params / resize seeding).
+__global__ void k_refresh_weight(const double* __restrict__ w64, float* __restrict__ w32,
+                                 float* __restrict__ wt32, int rows, int cols) {
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, c = c0 + tx;
+    float v = 0.f;
+    if (r < rows && c < cols) {
+      v = __double2float_rn(w64[(size_t)r * cols + c]);
+      w32[(size_t)r * cols + c] = v;
+    }
+    tile[k][tx] = v;
+  }
+  __syncthreads();
+  if (!wt32) return;
+  for (int k = ty; k < 32; k += 8) {
+    const int c = c0 + k, r = r0 + tx;
+    if (r < rows && c < cols) wt32[(size_t)c * rows + r] = tile[tx][k];
+  }
+}
+
+__global__ void k_refresh_vec(const double* __restrict__ w64, float* __restrict__ w32, size_t n) {
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+       k += (size_t)gridDim.x * blockDim.x)
+    w32[k] = __double2float_rn(w64[k]);
+}
+
+}  // namespace vntb
+
+namespace vntb {
+// sync_gradients export: mean = double(S) * 2^-s * (1/B) (virtual_exec.cpp:162-166).
+__global__ void k_mean_grad(const long long* __restrict__ G, double* __restrict__ out, size_t n,
+                            double inv_scale, double inv_b) {
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+       k += (size_t)gridDim.x * blockDim.x)
+    out[k] = __dmul_rn(__ll2double_rn(G[k]) * inv_scale, inv_b);
+}
+}  // namespace vntb
