@@ -307,6 +307,17 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     VNT_CUDA(cudaMemcpyAsync(e->yin + pn.prow * out, y + pn.src_row * out,
                              pn.rows * out * sizeof(double), kind, s));
   }
+  // The tcgen05 dW reads each node's columns padded to 32: keep the padding zero
+  // (a previous pass with another layout may have written there).
+  bool padded = false;
+  for (const auto& pn : p.nodes) padded |= (pn.rows % 32) != 0;
+  if (padded) {
+    for (int l = 0; l < L; ++l) {
+      if (!e->tc_layer[l]) continue;
+      VNT_CUDA(cudaMemsetAsync(e->XT[l], 0, e->widths[l] * p.ldT * sizeof(float), s));
+      VNT_CUDA(cudaMemsetAsync(e->DT[l + 1], 0, e->widths[l + 1] * p.ldT * sizeof(float), s));
+    }
+  }
   const int* tcol = p.d_meta;
   const int* row0 = p.d_meta + p.rows;
   const int* nrows = row0 + nn;

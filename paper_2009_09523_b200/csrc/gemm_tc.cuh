@@ -1,17 +1,446 @@
-// tcgen05 / TMA tensor-core path (filled in below the FFMA baseline).
+// tcgen05 / TMA tensor-core GEMMs for the wide dense layers (sm_100a).
+//
+// One kernel, three epilogues, all "TN" (both operands K-major in HBM):
+//   forward    Z[r][n]  = X[l][r][:] . WT[l][n][:]        -> bias + f -> X[l+1], XT[l+1]
+//   bwd-data   Dl[r][i] = D[l+1][r][:] . W[l][i][:]        -> * f'(X[l]) -> D[l], DT[l]
+//   dW         per node k: g_k[i][o] = XT[l][i][cols_k] . DT[l+1][o][cols_k]
+//              -> quantised to int64 and summed over the pass's nodes in
+//                 registers, one store per tile (the virtual-node gradient
+//                 accumulation fused into the GEMM epilogue).
+// CTA = 128x128 output tile.  Warp roles: w0 TMA producer (one elected lane),
+// w1 MMA issuer (one lane, tcgen05.mma.cta_group::1.kind::tf32, accumulators
+// in TMEM), w2 TMEM allocator, w4..w11 epilogue (tcgen05.ld, 32x32b).  Smem
+// operand tiles are 128B-swizzled K-major (TMA SWIZZLE_128B <-> UMMA
+// SWIZZLE_128B descriptors); a 4-stage mbarrier ring feeds the MMA warp; two
+// TMEM accumulators let the epilogue of segment s overlap the MMAs of s+1.
+//
+// Every output element is one K-chain over the same k-blocks in the same
+// order whatever the row count or tile position, so results are independent
+// of how many virtual nodes share a launch (the mapping-invariance contract).
 #pragma once
 
+#include <cuda.h>
+
+#include <unordered_map>
+
+namespace vntb {
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int STAGES = 4;
+constexpr int kBytesA = BM * BK * 4;
+constexpr int kBytesB = BN * BK * 4;
+constexpr int kThreads = 384;
+constexpr int kTmemCols = 256;
+constexpr int kSmemBytes = STAGES * (kBytesA + kBytesB) + 1024 /*align*/ + 256 /*barriers*/;
+
+enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
+
+struct EpiArgs {
+  int M, N;
+  // forward / bwd-data
+  const float* bias;
+  int act;
+  float* out;
+  int ldo;
+  float* outT;
+  int ldT;
+  const int* tcol;
+  const float* Xprev;
+  int ldx;
+  // dW
+  long long* G;
+  int ldg;
+  int first;
+  float scale, lim;
+  long long* tail;
+  int tensor;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"((uint64_t)tm), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: 8-row core groups
+// 1024 B apart (SBO), version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, D fp32, A/B tf32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// nseg == 0: one segment covering K.  Otherwise segment s covers K columns
+// [seg_k0[s], seg_k0[s] + round_up(seg_rows[s], 32)) — one virtual node.
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              int K, int nseg, const int* __restrict__ seg_k0, const int* __restrict__ seg_rows,
+              EpiArgs ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kBytesA;
+  uint64_t* full = (uint64_t*)(sB + STAGES * kBytesB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int segs = nseg > 0 ? nseg : 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int s = 0; s < segs; ++s) {
+        const int kb = nseg > 0 ? seg_k0[s] : 0;
+        const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
+        for (int k = 0; k < kl; k += BK) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], kBytesA + kBytesB);
+          tma_load_2d(sA + stage * kBytesA, &tmA, &full[stage], kb + k, m0);
+          tma_load_2d(sB + stage * kBytesB, &tmB, &full[stage], kb + k, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int s = 0; s < segs; ++s) {
+        const int b = s & 1;
+        mbar_wait(&tempty[b], ((s >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
+        for (int k = 0; k < kl; k += BK) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(su32(sA + stage * kBytesA));
+          const uint64_t bd = sdesc_sw128(su32(sB + stage * kBytesB));
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                     (k > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[b]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int h = (warp - 4) >> 2;       // column half
+    const int row = q * 32 + lane;       // tile row == TMEM lane
+    const int r = m0 + row;
+    long long acc[EPI == kTcDw ? 64 : 1];
+    if (EPI == kTcDw) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] = 0;
+    }
+    for (int s = 0; s < segs; ++s) {
+      const int b = s & 1;
+      mbar_wait(&tfull[b], (s >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        const int col = h * 64 + c * 32;
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
+        const int nb = n0 + col;
+        if (EPI == kTcDw) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            acc[c * 32 + j] += quantise(v[j], ep.scale, ep.lim, ep.tail, ep.tensor);
+        } else if (r < ep.M) {
+          const int tc = ep.tcol[r];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = nb + j;
+            if (n < ep.N) {
+              float x = v[j];
+              if (EPI == kTcFwd) {
+                x = act_fwd(ep.act, x + ep.bias[n]);
+              } else {
+                x = x * act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
+              }
+              v[j] = x;
+              ep.outT[(size_t)n * ep.ldT + tc] = x;
+            }
+          }
+          float* orow = ep.out + (size_t)r * ep.ldo + nb;
+          if (nb + 32 <= ep.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+            for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+    if (EPI == kTcDw && r < ep.M) {
+      long long* g = ep.G + (size_t)r * ep.ldg + n0 + h * 64;
+      const int nvalid = ep.N - (n0 + h * 64);
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (j < nvalid) g[j] = ep.first ? acc[j] : g[j] + acc[j];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    VNT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess)
+      throw EngineError(9, "cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// K-major fp32 operand [rows][K] with leading dimension ld (elements); box
+// 32 (K, 128 B) x box_rows, 128B swizzle, zero fill out of bounds.
+inline CUtensorMap make_map(const float* base, uint64_t rows, uint64_t K, uint64_t ld,
+                            uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {K, rows};
+  const cuuint64_t strides[1] = {ld * sizeof(float)};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw EngineError(9, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+template <int EPI>
+inline void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, int nseg,
+                        const int* seg_k0, const int* seg_rows, const EpiArgs& ep,
+                        cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    VNT_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemBytes));
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM));
+  k_gemm_tc<EPI><<<grid, kThreads, kSmemBytes, s>>>(a, b, K, nseg, seg_k0, seg_rows, ep);
+  VNT_LAUNCH_CHECK();
+}
+
+}  // namespace tc
+}  // namespace vntb
+
+// ---------------------------------------------- engine glue (needs vnt_engine)
 namespace {
-bool tc_layer_eligible(int, uint64_t, uint64_t) { return false; }
+
+bool tc_layer_eligible(int mode, uint64_t in, uint64_t out) {
+  if (mode == VNT_GEMM_FFMA) return false;
+  return in >= 64 && out >= 64 && in % 4 == 0 && out % 4 == 0;
+}
+
 void tc_init(vnt_engine*) {}
 void tc_destroy(vnt_engine*) {}
-void tc_forward(vnt_engine*, int, int, int, const int*, bool) {
-  throw vntb::EngineError(1, "tcgen05 path not built");
+
+void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool last) {
+  using namespace vntb::tc;
+  const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
+  if (last) throw vntb::EngineError(1, "tcgen05 path does not produce logits");
+  const CUtensorMap a = make_map(e->X[l], rows, K, K, BM);
+  const CUtensorMap b = make_map(e->wt32 + e->wtoff[l], N, K, K, BN);
+  EpiArgs ep{};
+  ep.M = rows;
+  ep.N = N;
+  ep.bias = e->w32 + e->boff[l];
+  ep.act = e->act;
+  ep.out = e->X[l + 1];
+  ep.ldo = N;
+  ep.outT = e->XT[l + 1];
+  ep.ldT = ldT;
+  ep.tcol = tcol;
+  launch_gemm<kTcFwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->stream);
+  e->launches++;
 }
-void tc_weight_grad(vnt_engine*, int, const Pass&, const int*, const int*, float, float, bool, int) {
-  throw vntb::EngineError(1, "tcgen05 path not built");
+
+void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol) {
+  using namespace vntb::tc;
+  const int N = (int)e->widths[l], K = (int)e->widths[l + 1];
+  const CUtensorMap a = make_map(e->D[l + 1], rows, K, K, BM);
+  const CUtensorMap b = make_map(e->w32 + e->woff[l], N, K, K, BN);
+  EpiArgs ep{};
+  ep.M = rows;
+  ep.N = N;
+  ep.act = e->act;
+  ep.out = e->D[l];
+  ep.ldo = N;
+  ep.outT = e->DT[l];
+  ep.ldT = ldT;
+  ep.tcol = tcol;
+  ep.Xprev = e->X[l];
+  ep.ldx = N;
+  launch_gemm<kTcBwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->stream);
+  e->launches++;
 }
-void tc_backward_data(vnt_engine*, int, int, int, const int*) {
-  throw vntb::EngineError(1, "tcgen05 path not built");
+
+void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const int* nrows,
+                    float scale, float lim, bool first, int tensor) {
+  using namespace vntb::tc;
+  const int M = (int)e->widths[l], N = (int)e->widths[l + 1];
+  const uint64_t ldT = p.ldT;
+  const CUtensorMap a = make_map(e->XT[l], M, ldT, ldT, BM);
+  const CUtensorMap b = make_map(e->DT[l + 1], N, ldT, ldT, BN);
+  EpiArgs ep{};
+  ep.M = M;
+  ep.N = N;
+  ep.G = e->G + e->woff[l];
+  ep.ldg = N;
+  ep.first = first ? 1 : 0;
+  ep.scale = scale;
+  ep.lim = lim;
+  ep.tail = e->G + e->P;
+  ep.tensor = tensor;
+  launch_gemm<kTcDw>(a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep, e->stream);
+  e->launches++;
 }
+
 }  // namespace

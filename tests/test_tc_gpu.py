@@ -1,0 +1,92 @@
+"""tcgen05 (kind::tf32) path: correctness against the FFMA path and the fp64
+oracle, and the mapping-invariance contract (bits independent of how rows
+are grouped into launches).  Tolerances: 1xTF32 per-GEMM
+relative error ~2^-11, so the synced mean gradient must agree with the FFMA
+path within 1e-2 of its max magnitude; trajectories within 1e-3 relative
+loss and 1e-4 absolute weights of the fp64 reference."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def vnt():
+    import paper_2009_09523_b200 as m
+    return m
+
+
+def engine(widths, act, loss, port, seed=1, n_devices=1, **kw):
+    e = vnt().Engine(widths, act, loss, **kw)
+    for _ in range(n_devices):
+        e.add_device(1 << 30)
+    e.set_params(port.init_params(widths, seed))
+    return e
+
+
+def synced_grad(e, x, y, sizes):
+    off = 0
+    for k, s in enumerate(sizes):
+        pass
+    e.device_step(0, x, y, sizes)
+    g, loss_sum, ex = e.sync()
+    return g, loss_sum / ex
+
+
+@pytest.mark.parametrize("sizes", [[64, 64, 64, 64], [24, 40, 7, 57, 128]])
+def test_tc_gradient_matches_ffma_and_oracle(port, sizes):
+    w = [256, 512, 384, 10]
+    B = sum(sizes)
+    x, y = port.synth_batch(3, 4096, w[0], w[-1], 0, B)
+    p0 = port.init_params(w, 1)
+    want, want_loss = port.forward_backward(w, "relu", "softmax-cross-entropy", p0, x, y)
+    res = {}
+    for mode in ("ffma", "tf32"):
+        e = engine(w, "relu", "softmax-cross-entropy", port, gemm_mode=mode)
+        res[mode] = synced_grad(e, x, y, sizes)
+    gmax = np.abs(want).max()
+    err_ffma = np.abs(res["ffma"][0] - want).max() / gmax
+    err_tc = np.abs(res["tf32"][0] - want).max() / gmax
+    print(f"sizes {sizes}: rel grad err ffma {err_ffma:.2e}, tf32 {err_tc:.2e}; "
+          f"loss {res['tf32'][1]:.9f} vs {want_loss:.9f}")
+    assert err_ffma < 1e-5
+    assert err_tc < 1e-2
+    assert abs(res["tf32"][1] - want_loss) < 1e-3 * abs(want_loss)
+
+
+def test_tc_bitwise_across_pass_grouping_and_devices(port):
+    w = [128, 256, 256, 10]
+    outs = []
+    for rr, G in ((0, 1), (64, 1), (96, 2), (0, 4), (32, 3)):
+        e = engine(w, "relu", "softmax-cross-entropy", port, n_devices=G, gemm_mode="tf32",
+                   resident_rows=rr)
+        sizes, dev = vnt().uniform_mapping(256, 8, G)
+        losses = []
+        for s in range(3):
+            x, y = port.synth_batch(4, 2048, w[0], w[-1], s * 256, 256)
+            losses.append(e.train_step(x, y, sizes, dev, 0.02)[0])
+        outs.append((e.get_params(), np.array(losses)))
+    for p, l in outs[1:]:
+        assert np.array_equal(p, outs[0][0])
+        assert np.array_equal(l, outs[0][1])
+
+
+def test_tc_trajectory_vs_reference(port):
+    z = np.load(GOLDEN / "ref_wide_small.npz")
+    c = json.loads(str(z["config"]))
+    e = engine(c["widths"], c["act"], c["loss"], port, seed=c["seed"], gemm_mode="tf32")
+    sizes, dev = vnt().uniform_mapping(c["B"], c["V"], 1)
+    losses = []
+    for s in range(c["steps"]):
+        x, y = port.synth_batch(c["data_seed"], c["dataset_size"], c["widths"][0],
+                                c["widths"][-1], s * c["B"], c["B"])
+        losses.append(e.train_step(x, y, sizes, dev, c["lr"])[0])
+    rel = np.abs(np.array(losses) - z["losses"]) / np.abs(z["losses"])
+    dw = np.abs(e.get_params() - z["params"]).max()
+    print(f"tf32 wide_small: max rel loss dev {rel.max():.2e}, max |dw| {dw:.2e}")
+    assert rel.max() < 1e-3
+    assert dw < 1e-4
