@@ -291,6 +291,41 @@ void tail_reset(vnt_engine* e) {
   VNT_CUDA(cudaMemsetAsync(e->G + e->P, 0, e->ntail * sizeof(long long), e->stream));
 }
 
+// Skinny-layer (out <= 32) kernels: NO is the compile-time bound.
+template <template <int> class F, class... A>
+void dispatch_skinny(int no, A&&... a) {
+  if (no <= 4) F<4>::run(a...);
+  else if (no <= 8) F<8>::run(a...);
+  else if (no <= 16) F<16>::run(a...);
+  else F<32>::run(a...);
+}
+
+template <int NO>
+struct FwdSkinny {
+  static void run(cudaStream_t s, const float* X, int K, const float* W, int no, const float* b,
+                  int rows, int act, int last, float* out, float* outT, int ldT, const int* tcol) {
+    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
+                                                                 out, outT, ldT, tcol);
+  }
+};
+template <int NO>
+struct BwdSkinny {
+  static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
+                  int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol) {
+    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+    k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol);
+  }
+};
+template <int NO>
+struct DwSkinny {
+  static void run(cudaStream_t s, const float* X, int in, const float* Dn, int no, const int* row0,
+                  const int* nrows, int nn, float scale, float lim, long long* G, long long* tail,
+                  int tensor) {
+    dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
+    k_dw_skinny<NO><<<grid, 128, 0, s>>>(X, in, Dn, no, row0, nrows, scale, lim, G, tail, tensor);
+  }
+};
+
 // ---------------------------------------------------------------- one pass
 void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bool x_on_device,
               bool do_stats, bool first_write) {
@@ -379,6 +414,12 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     prof_begin(e);
     if (e->tc_layer[l]) {
       tc_forward(e, l, rows, ldT, tcol, last);
+    } else if (N <= 32) {
+      dispatch_skinny<FwdSkinny>(N, s, e->X[l], K, W, N, b, rows, e->act, last ? 1 : 0,
+                                 last ? e->logits : e->X[l + 1], last ? nullptr : e->XT[l + 1],
+                                 ldT, tcol);
+      VNT_LAUNCH_CHECK();
+      e->launches++;
     } else {
       dim3 grid((unsigned)ceil_div(N, 64), (unsigned)ceil_div(p.rows, 64));
       if (last) {
@@ -411,24 +452,35 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     prof_begin(e);
     if (e->tc_layer[l]) {
       tc_weight_grad(e, l, p, col0, nrows, pow2f(e->scales[tw]), lim, first_write, tw);
+    } else if (out_l <= 32) {
+      dispatch_skinny<DwSkinny>(out_l, s, e->X[l], in_l, e->D[l + 1], out_l, row0, nrows, (int)nn,
+                                pow2f(e->scales[tw]), lim, e->G + e->woff[l], e->G + e->P, tw);
+      VNT_LAUNCH_CHECK();
+      e->launches++;
     } else {
-      dim3 grid((unsigned)ceil_div(out_l, 64), (unsigned)ceil_div(in_l, 64));
+      dim3 grid((unsigned)ceil_div(out_l, 64), (unsigned)ceil_div(in_l, 64), (unsigned)nn);
       k_dw_ffma<<<grid, 256, 0, s>>>(e->XT[l], e->DT[l + 1], ldT, in_l, out_l, col0, nrows,
-                                     (int)nn, pow2f(e->scales[tw]), lim, e->G + e->woff[l],
-                                     first_write ? 1 : 0, e->G + e->P, tw);
+                                     pow2f(e->scales[tw]), lim, e->G + e->woff[l], e->G + e->P, tw);
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
     prof_end(e, 2.0 * rows * (double)in_l * out_l);
-    k_db<<<(unsigned)ceil_div(out_l, 128), 128, 0, s>>>(
-        e->D[l + 1], out_l, row0, nrows, (int)nn, pow2f(e->scales[tb]), lim, e->G + e->boff[l],
-        first_write ? 1 : 0, e->G + e->P, tb);
-    VNT_LAUNCH_CHECK();
-    e->launches++;
+    {
+      dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
+      k_db<<<grid, 128, 0, s>>>(e->D[l + 1], out_l, row0, nrows, pow2f(e->scales[tb]), lim,
+                                e->G + e->boff[l], e->G + e->P, tb);
+      VNT_LAUNCH_CHECK();
+      e->launches++;
+    }
     if (l > 0) {
       prof_begin(e);
       if (e->tc_layer[l]) {
         tc_backward_data(e, l, rows, ldT, tcol);
+      } else if (out_l <= 32) {
+        dispatch_skinny<BwdSkinny>(out_l, s, e->D[l + 1], e->w32 + e->woff[l], out_l, in_l, rows,
+                                   e->act, e->X[l], e->D[l], e->DT[l], ldT, tcol);
+        VNT_LAUNCH_CHECK();
+        e->launches++;
       } else {
         const float* WT = e->wt32 + e->wtoff[l];
         dim3 grid((unsigned)ceil_div(in_l, 64), (unsigned)ceil_div(p.rows, 64));
@@ -446,6 +498,14 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
 void begin_round(vnt_engine* e, uint64_t batch_hint) {
   if (e->round_open) return;
   tail_reset(e);
+  // Slices filled by exact int64 atomics start from zero (bias always, weights
+  // of non-tcgen05 layers); tcgen05 dW tiles store on the first pass.
+  for (int l = 0; l < e->L; ++l) {
+    VNT_CUDA(cudaMemsetAsync(e->G + e->boff[l], 0, e->widths[l + 1] * sizeof(long long), e->stream));
+    if (!e->tc_layer[l])
+      VNT_CUDA(cudaMemsetAsync(e->G + e->woff[l], 0, e->widths[l] * e->widths[l + 1] * sizeof(long long),
+                               e->stream));
+  }
   e->acc_examples = 0;
   e->acc_started = false;
   e->round_open = true;
@@ -516,7 +576,7 @@ void launch_sgd(vnt_engine* e, double lr, uint64_t examples) {
       if (part == 0) {
         a.rows = (int)e->widths[l];
         a.cols = (int)e->widths[l + 1];
-        dim3 grid((unsigned)ceil_div(a.cols, 32), (unsigned)ceil_div(a.rows, 32)), block(32, 8);
+        dim3 grid((unsigned)ceil_div(a.cols, 32), (unsigned)ceil_div(a.rows, 64)), block(32, 8);
         k_sgd_weight<<<grid, block, 0, s>>>(a);
       } else {
         a.rows = 1;

@@ -245,56 +245,46 @@ __device__ __forceinline__ long long quantise(float g, float scale, float lim,
 
 // ------------------------------------------------ per-node dW, FFMA path
 // g_k[i][o] = sum_{r in node k} X[r][i] * D[r][o] (one fmaf chain, rows
-// ascending), quantised per node and accumulated in int64 registers across
-// every node of the pass; one read-modify-write of G per pass.
+// ascending); blockIdx.z = node.  Quantised per node and added with exact
+// int64 atomics into the zeroed weight slice of G (order-free).
 __global__ void __launch_bounds__(256) k_dw_ffma(
     const float* __restrict__ XT, const float* __restrict__ DT, int ldT, int in, int out,
-    const int* __restrict__ vn_col0, const int* __restrict__ vn_rows, int nvn, float scale,
-    float lim, long long* __restrict__ G, int first, long long* __restrict__ tail, int tensor) {
+    const int* __restrict__ vn_col0, const int* __restrict__ vn_rows, float scale, float lim,
+    long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
   __shared__ __align__(16) float As[16][64 + 4];
   __shared__ __align__(16) float Bs[16][64 + 4];
   const int t = threadIdx.x;
   const int tx = t % 16, ty = t / 16;
   const int i0 = blockIdx.y * 64, o0 = blockIdx.x * 64;
-  long long acc[4][4];
+  const int v = blockIdx.z;
+  const int c0 = vn_col0[v], n = vn_rows[v];
+  float g[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
-  for (int v = 0; v < nvn; ++v) {
-    const int c0 = vn_col0[v], n = vn_rows[v];
-    float g[4][4];
+    for (int j = 0; j < 4; ++j) g[i][j] = 0.f;
+  for (int k0 = 0; k0 < n; k0 += 16) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) g[i][j] = 0.f;
-    for (int k0 = 0; k0 < n; k0 += 16) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int idx = t + e * 256;
-        const int mm = idx / 16, kk = idx % 16;
-        const bool kin = (k0 + kk) < n;
-        As[kk][mm] = (kin && i0 + mm < in) ? XT[(size_t)(i0 + mm) * ldT + c0 + k0 + kk] : 0.f;
-        Bs[kk][mm] = (kin && o0 + mm < out) ? DT[(size_t)(o0 + mm) * ldT + c0 + k0 + kk] : 0.f;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
-        const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
-        const float a[4] = {a4.x, a4.y, a4.z, a4.w};
-        const float b[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) g[i][j] = fmaf(a[i], b[j], g[i][j]);
-      }
-      __syncthreads();
+    for (int e = 0; e < 4; ++e) {
+      const int idx = t + e * 256;
+      const int mm = idx / 16, kk = idx % 16;
+      const bool kin = (k0 + kk) < n;
+      As[kk][mm] = (kin && i0 + mm < in) ? XT[(size_t)(i0 + mm) * ldT + c0 + k0 + kk] : 0.f;
+      Bs[kk][mm] = (kin && o0 + mm < out) ? DT[(size_t)(o0 + mm) * ldT + c0 + k0 + kk] : 0.f;
     }
+    __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int kk = 0; kk < 16; ++kk) {
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] += quantise(g[i][j], scale, lim, tail, tensor);
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) g[i][j] = fmaf(a[i], b[j], g[i][j]);
+    }
+    __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -304,28 +294,146 @@ __global__ void __launch_bounds__(256) k_dw_ffma(
     for (int j = 0; j < 4; ++j) {
       const int go = o0 + tx * 4 + j;
       if (go >= out) continue;
-      long long* p = G + (size_t)gi * out + go;
-      *p = first ? acc[i][j] : *p + acc[i][j];
+      const long long q = quantise(g[i][j], scale, lim, tail, tensor);
+      if (q) atomicAdd(reinterpret_cast<unsigned long long*>(G + (size_t)gi * out + go),
+                       (unsigned long long)q);
     }
   }
 }
 
 // Per-node bias gradient (model.cpp:322: gb = delta): column sums of D over
-// the node's rows, fp32 in row order, quantised per node.
+// the node's rows, fp32 in row order, quantised per node; one CTA column per
+// node, exact int64 atomics (order-free) into the zeroed bias slice of G.
 __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict__ vn_row0,
-                     const int* __restrict__ vn_rows, int nvn, float scale, float lim,
-                     long long* __restrict__ G, int first, long long* __restrict__ tail,
-                     int tensor) {
+                     const int* __restrict__ vn_rows, float scale, float lim,
+                     long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
   if (o >= out) return;
-  long long acc = 0;
-  for (int v = 0; v < nvn; ++v) {
-    const int r0 = vn_row0[v], n = vn_rows[v];
-    float g = 0.f;
-    for (int r = 0; r < n; ++r) g += D[(size_t)(r0 + r) * out + o];
-    acc += quantise(g, scale, lim, tail, tensor);
+  const int r0 = vn_row0[v], n = vn_rows[v];
+  float g = 0.f;
+  for (int r = 0; r < n; ++r) g += D[(size_t)(r0 + r) * out + o];
+  const long long q = quantise(g, scale, lim, tail, tensor);
+  if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&G[o]), (unsigned long long)q);
+}
+
+// ---------------------------------------------- skinny layers (out <= 32)
+// Forward with few outputs (the 4096 -> 10 classifier): one warp per row,
+// lane-strided partial dot products over k then a fixed xor tree, so every
+// output depends only on its row.
+template <int NO>
+__global__ void k_fwd_skinny(const float* __restrict__ X, int K, const float* __restrict__ W,
+                             int no, const float* __restrict__ bias, int rows, int act, int last,
+                             float* __restrict__ out, float* __restrict__ outT, int ldT,
+                             const int* __restrict__ tcol) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float* x = X + (size_t)warp * K;
+  float acc[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+  for (int k = lane; k < K; k += 32) {
+    const float a = x[k];
+    const float* w = W + (size_t)k * no;
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+      if (o < no) acc[o] = fmaf(a, __ldg(w + o), acc[o]);
   }
-  G[o] = first ? acc : G[o] + acc;
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+#pragma unroll
+    for (int s = 16; s; s >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], s);
+  }
+  if (lane < no) {
+    float v = 0.f;
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+      if (o == lane) v = acc[o];
+    v += bias[lane];
+    if (!last) v = act_fwd(act, v);
+    out[(size_t)warp * no + lane] = v;
+    if (!last) outT[(size_t)lane * ldT + tcol[warp]] = v;
+  }
+}
+
+// bwd-data through a skinny layer: D[r][i] = (sum_o Dn[r][o] W[i][o]) f'(X[r][i]),
+// o ascending; 32x32 (row, i) tiles, transposed copy through smem.
+template <int NO>
+__global__ void k_bwd_skinny(const float* __restrict__ Dn, const float* __restrict__ W, int no,
+                             int in, int rows, int act, const float* __restrict__ Xprev,
+                             float* __restrict__ Dout, float* __restrict__ DT, int ldT,
+                             const int* __restrict__ tcol) {
+  __shared__ float tile[32][33];
+  __shared__ float dn[32][NO];
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  const int r0 = blockIdx.y * 32, i0 = blockIdx.x * 32;
+  for (int k = ty * 32 + tx; k < 32 * NO; k += 256) {
+    const int rr = k / NO, o = k % NO;
+    dn[rr][o] = (r0 + rr < rows && o < no) ? Dn[(size_t)(r0 + rr) * no + o] : 0.f;
+  }
+  __syncthreads();
+  const int i = i0 + tx;
+  float w[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) w[o] = (i < in && o < no) ? W[(size_t)i * no + o] : 0.f;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k;
+    float acc = 0.f;
+#pragma unroll
+    for (int o = 0; o < NO; ++o) acc = fmaf(dn[k][o], w[o], acc);
+    float v = 0.f;
+    if (r < rows && i < in) {
+      v = acc * act_grad_from_out(act, Xprev[(size_t)r * in + i]);
+      Dout[(size_t)r * in + i] = v;
+    }
+    tile[k][tx] = v;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int ii = i0 + k, r = r0 + tx;
+    if (r < rows && ii < in) DT[(size_t)ii * ldT + tcol[r]] = tile[tx][k];
+  }
+}
+
+// Per-node dW of a skinny layer: thread per input feature i, NO accumulators,
+// rows of the node in order; node partials quantised and added with int64
+// atomics (exact) into the zeroed weight slice of G.
+template <int NO>
+__global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __restrict__ Dn,
+                            int no,
+                            const int* __restrict__ vn_row0, const int* __restrict__ vn_rows,
+                            float scale, float lim, long long* __restrict__ G,
+                            long long* __restrict__ tail, int tensor) {
+  __shared__ float dn[64][NO];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  const int r0 = vn_row0[v], n = vn_rows[v];
+  float g[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) g[o] = 0.f;
+  for (int c = 0; c < n; c += 64) {
+    const int cn = min(64, n - c);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cn * NO; k += blockDim.x)
+      dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
+    __syncthreads();
+    if (i < in) {
+      for (int rr = 0; rr < cn; ++rr) {
+        const float a = X[(size_t)(r0 + c + rr) * in + i];
+#pragma unroll
+        for (int o = 0; o < NO; ++o) g[o] = fmaf(a, dn[rr][o], g[o]);
+      }
+    }
+  }
+  if (i >= in) return;
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    if (o >= no) break;
+    const long long q = quantise(g[o], scale, lim, tail, tensor);
+    if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&G[(size_t)i * no + o]),
+                     (unsigned long long)q);
+  }
 }
 
 // -------------------------------------------------------------------- SGD
@@ -381,32 +489,64 @@ __device__ __forceinline__ void block_max_to(unsigned long long* dst, double v) 
   if ((threadIdx.x & 31) == 0 && b) atomicMax(dst, b);
 }
 
-// Weight tensor: 32x32 tiles, 32x8 threads; transposed fp32 copy via smem.
-__global__ void k_sgd_weight(SgdArgs a) {
-  __shared__ float tile[32][33];
+// Weight tensor: 64x32 (rows x cols) tiles, 32x8 threads, 8 elements per
+// thread with all loads issued before the dependent math; transposed fp32 copy
+// via smem.
+__global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
+  constexpr int TR = 64, TC = 32, PER = TR / 8;
+  __shared__ float tile[TR][TC + 1];
   __shared__ int poisoned;
   const int tx = threadIdx.x, ty = threadIdx.y;
   if (tx == 0 && ty == 0) poisoned = step_poisoned(a.tail, a.ntail_flags);
   __syncthreads();
   if (poisoned) return;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
+  const int c = c0 + tx;
+  long long S[PER];
+  double w[PER], v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int r = r0 + ty + 8 * k;
+    const bool ok = r < a.rows && c < a.cols;
+    const size_t idx = (size_t)r * a.cols + c;
+    S[k] = ok ? __ldg(a.G + idx) : 0;
+    w[k] = ok ? a.w64[idx] : 0.0;
+    v[k] = (ok && a.v64) ? a.v64[idx] : 0.0;
+  }
   double mx = 0.0;
-  for (int k = ty; k < 32; k += 8) {
-    const int r = r0 + k, c = c0 + tx;
-    float w32 = 0.f;
-    if (r < a.rows && c < a.cols) {
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int r = r0 + ty + 8 * k;
+    const bool ok = r < a.rows && c < a.cols;
+    const double g = __dmul_rn(__ll2double_rn(S[k]) * a.inv_scale, a.inv_b);
+    double u = g;
+    if (a.v64) u = __dadd_rn(__dmul_rn(a.mu, v[k]), g);
+    const double wn = __dsub_rn(w[k], __dmul_rn(a.lr, u));
+    const float w32 = __double2float_rn(wn);
+    tile[ty + 8 * k][tx] = ok ? w32 : 0.f;
+    if (ok) {
       const size_t idx = (size_t)r * a.cols + c;
-      mx = fmax(mx, sgd_one(a, idx, w32));
+      a.w64[idx] = wn;
+      if (a.v64) a.v64[idx] = u;
       a.w32[idx] = w32;
+      if (a.gout) a.gout[idx] = g;
+      mx = fmax(mx, fabs(g));
     }
-    tile[k][tx] = w32;
   }
   block_max_to(a.gmax, mx);
   if (!a.wt32) return;
   __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int c = c0 + k, r = r0 + tx;
-    if (r < a.rows && c < a.cols) a.wt32[(size_t)c * a.rows + r] = tile[tx][k];
+  // transposed: WT[c][r], 32 columns x 64 rows -> each warp row writes 64 contiguous rows
+#pragma unroll
+  for (int k = 0; k < TC / 8; ++k) {
+    const int cc = ty + 8 * k;
+    const int col = c0 + cc;
+    if (col >= a.cols) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + h * 32 + tx;
+      if (r < a.rows) a.wt32[(size_t)col * a.rows + r] = tile[h * 32 + tx][cc];
+    }
   }
 }
 
