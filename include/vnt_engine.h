@@ -135,6 +135,14 @@ int vnt_engine_device_step(vnt_engine* e, int32_t device, const double* x, const
 int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum,
                     uint64_t* examples);
 
+/* The process-local example-summed gradient (no collective), as the
+ * reference GradientBuffer::rounded_sum() of one device (virtual_exec.cpp:
+ * 102-118): sum[P] = double(S) * 2^-s per tensor, exact while |S| < 2^53.
+ * Closes the accumulation round. */
+int vnt_engine_take_gradient_sum(vnt_engine* e, double* sum, double* loss_sum,
+                                 uint64_t* examples);
+int vnt_engine_set_device_capacity(vnt_engine* e, int32_t device, uint64_t capacity);
+
 /* sgd_apply with the synced gradient on this replica (plus momentum if set). */
 int vnt_engine_sgd_apply(vnt_engine* e, double lr);
 

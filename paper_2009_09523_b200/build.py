@@ -68,7 +68,7 @@ def build_host(force=False) -> Path | None:
         return None
     deps = srcs + list(INC.glob("vnt/*.hpp")) + [INC / "vnt_trainer.h", PKG / "libvnt_engine.so"]
     if force or _stale(out, deps):
-        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{INC}",
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", f"-I{INC}",
               f"-I/usr/local/cuda/include", "-o", out, *srcs,
               f"-L{PKG}", "-lvnt_engine", f"-Wl,-rpath,{PKG}", f"-Wl,-rpath,$ORIGIN",
               "-lpthread"])

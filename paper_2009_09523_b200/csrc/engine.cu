@@ -1011,6 +1011,53 @@ int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum, uint64_t
   });
 }
 
+int vnt_engine_take_gradient_sum(vnt_engine* e, double* sum, double* loss_sum,
+                                 uint64_t* examples) {
+  return guarded([&] {
+    bind(e);
+    if (!e->acc_started) throw EngineError(VNT_ERR_CONFIG, "no gradients accumulated");
+    k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
+    Readback rb = read_tail(e, false);
+    if (rb.nonfinite) {
+      restore_stats(e);
+      reset_acc(e);
+      throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
+    }
+    if (!rb.overflow.empty()) {
+      for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
+      restore_stats(e);
+      reset_acc(e);
+      throw EngineError(VNT_ERR_RESCALE, "fixed-point range exceeded; scale lowered, redo the step");
+    }
+    if (!e->gout) e->gout = (double*)dalloc(e->P * sizeof(double));
+    for (int l = 0; l < e->L; ++l) {
+      for (int part = 0; part < 2; ++part) {
+        const uint64_t off = part ? e->boff[l] : e->woff[l];
+        const uint64_t n = part ? e->widths[l + 1] : e->widths[l] * e->widths[l + 1];
+        // double(S) * 2^-s: exact while |S| < 2^53 (the scale keeps sums near 2^40).
+        k_mean_grad<<<(unsigned)std::min<uint64_t>(ceil_div(n, 256), 4096), 256, 0, e->stream>>>(
+            e->G + off, e->gout + off, n, std::ldexp(1.0, -e->scales[2 * l + part]), 1.0);
+        VNT_LAUNCH_CHECK();
+      }
+    }
+    VNT_CUDA(cudaMemcpyAsync(sum, e->gout, e->P * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    if (loss_sum) *loss_sum = rb.loss_sum;
+    if (examples) *examples = rb.examples;
+    reset_acc(e);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_set_device_capacity(vnt_engine* e, int32_t device, uint64_t capacity) {
+  return guarded([&] {
+    if (device < 0 || device >= (int32_t)e->devs.size())
+      throw EngineError(VNT_ERR_CONFIG, "unknown device");
+    e->devs[device].capacity = capacity;
+    return VNT_OK;
+  });
+}
+
 int vnt_engine_sgd_apply(vnt_engine* e, double lr) {
   return guarded([&] {
     bind(e);

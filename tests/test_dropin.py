@@ -1,0 +1,133 @@
+"""The C++ drop-in `vnt::` API (include/vnt/*.hpp, libvnt.so).
+
+CPU: C++ host tests (tests/cpp/test_host.cpp) and the host-only C-ABI
+(SynthDataset, init) bit-identical to the reference oracle.
+GPU: C++ drop-in tests mirroring the reference suites
+(tests/cpp/test_dropin_gpu.cpp) and the drop-in Trainer, through
+include/vnt_trainer.h, against the reference Trainer (oracle/_ref or port)."""
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+BUILD = ROOT / "build" / "tests"
+
+
+def _bin(name):
+    p = BUILD / name
+    if not p.exists():
+        from paper_2009_09523_b200 import build as b
+        b.build_host()
+        b.build_cpp_tests()
+    return p
+
+
+def _host():
+    import paper_2009_09523_b200 as vnt
+    if not vnt.HOST_SO.exists():
+        from paper_2009_09523_b200 import build as b
+        b.build_host()
+    vnt.load_engine()
+    lib = C.CDLL(str(vnt.HOST_SO))
+    lib.vnt_host_last_error.restype = C.c_char_p
+    return lib
+
+
+def test_cpp_host_suite():
+    r = subprocess.run([str(_bin("test_host"))], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_host_data_and_init_bit_identical_to_reference(port):
+    lib = _host()
+    f64p = C.POINTER(C.c_double)
+    for (seed, n, i, o, start, cnt) in [(11, 64, 4, 4, 5, 20), (11, 60000, 784, 10, 59990, 16)]:
+        x = np.empty((cnt, i))
+        y = np.empty((cnt, o))
+        assert lib.vnt_synth_batch(C.c_uint64(seed), C.c_uint64(n), C.c_uint64(i), C.c_uint64(o),
+                                   C.c_uint64(start), C.c_uint64(cnt), x.ctypes.data_as(f64p),
+                                   y.ctypes.data_as(f64p)) == 0
+        x2, y2 = port.synth_batch(seed, n, i, o, start, cnt)
+        assert np.array_equal(x, x2) and np.array_equal(y, y2)
+    w = [784, 16, 10]
+    wa = (C.c_uint64 * 3)(*w)
+    p = np.empty(port.param_count(w))
+    assert lib.vnt_init_params(wa, 3, C.c_uint64(11), p.ctypes.data_as(f64p)) == 0
+    assert np.array_equal(p, port.init_params(w, 11))
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_suite_on_gpu():
+    r = subprocess.run([str(_bin("test_dropin_gpu"))], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+class _Dev(C.Structure):
+    _fields_ = [("device_id", C.c_char_p), ("device_type", C.c_char_p), ("memory_capacity", C.c_uint64)]
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("layer_widths", C.POINTER(C.c_uint64)), ("num_widths", C.c_uint32),
+                ("activation", C.c_int32), ("loss", C.c_int32), ("seed", C.c_uint64),
+                ("global_batch", C.c_uint64), ("virtual_nodes", C.c_uint64), ("lr", C.c_double),
+                ("data_seed", C.c_uint64), ("dataset_size", C.c_uint64),
+                ("shuffle_epochs", C.c_int32), ("shuffle_seed", C.c_uint64),
+                ("devices", C.POINTER(_Dev)), ("num_devices", C.c_uint32),
+                ("parallel_devices", C.c_int32), ("prefetch", C.c_int32), ("gemm_mode", C.c_int32),
+                ("momentum", C.c_double)]
+
+
+def _devs(n):
+    arr = (_Dev * n)()
+    for i in range(n):
+        arr[i] = _Dev(f"gpu{i}".encode(), b"B200", 1 << 20)
+    return arr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["headline", "cfg1"])
+def test_dropin_trainer_matches_reference_trainer(port, ref, case):
+    """Trainer::step through the drop-in vs the reference's Trainer, same config,
+    including a resize 8 -> 4 -> 8 (cfg5 shape) for the headline case."""
+    lib = _host()
+    o = ref if ref is not None else port
+    if case == "headline":
+        w, act, loss, seed, B, V, lr, ds, n, G, steps = [4, 16, 4], 1, 0, 11, 64, 8, 0.05, 11, 256, 8, 30
+    else:
+        w, act, loss, seed, B, V, lr, ds, n, G, steps = [784, 16, 10], 1, 1, 11, 256, 16, 0.05, 11, 60000, 1, 10
+    wa = (C.c_uint64 * len(w))(*w)
+    devs = _devs(G)
+    cfg = _Cfg(wa, len(w), act, loss, seed, B, V, lr, ds, n, 0, 0, devs, G, 0, 0, 1, 0.0)
+    h = C.c_void_p()
+    assert lib.vnt_trainer_create(C.byref(cfg), C.byref(h)) == 0, lib.vnt_host_last_error()
+    t = o.trainer(w, ["relu", "tanh", "identity"][act], ["mse", "softmax-cross-entropy"][loss], seed,
+                  B, V, lr, ds, n, G)
+    lo = C.c_double()
+    for s in range(steps):
+        if case == "headline" and s in (10, 20):
+            k = 4 if s == 10 else 8
+            assert lib.vnt_trainer_resize(h, _devs(k), k) == 0, lib.vnt_host_last_error()
+            t.resize(k)
+        assert lib.vnt_trainer_step(h, C.byref(lo), None, 0) == 0, lib.vnt_host_last_error()
+        want = t.step()
+        assert abs(lo.value - want) <= 2e-5 * abs(want), (s, lo.value, want)
+    P = port.param_count(w)
+    p = np.empty(P)
+    assert lib.vnt_trainer_params(h, p.ctypes.data_as(C.POINTER(C.c_double)), P) == 0
+    assert np.abs(p - t.params()).max() <= 2e-5
+    # Input statistics are fp64 in the reference's op order: bit-identical,
+    # including lineages merged/seeded by the resizes.
+    for i in range(G):
+        cnt = C.c_double()
+        mean = np.empty(w[0])
+        m2 = np.empty(w[0])
+        assert lib.vnt_trainer_input_stats(h, i, C.byref(cnt), mean.ctypes.data_as(C.POINTER(C.c_double)),
+                                           m2.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        c2, mean2, m22 = t.input_stats(i)
+        assert cnt.value == c2 and np.array_equal(mean, mean2) and np.array_equal(m2, m22)
+    lib.vnt_trainer_destroy(h)
