@@ -21,20 +21,27 @@
 
 #include <cuda.h>
 
-#include <unordered_map>
+#include <algorithm>
 
 namespace vntb {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 32;
-constexpr int STAGES = 4;
-constexpr int kBytesA = BM * BK * 4;
-constexpr int kBytesB = BN * BK * 4;
+constexpr int BM = 128, BK = 32;
 constexpr int kThreads = 384;
-constexpr int kTmemCols = 256;
-constexpr int kSmemBytes = STAGES * (kBytesA + kBytesB) + 1024 /*align*/ + 256 /*barriers*/;
 
 enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
+
+// fwd / bwd-data: 128x256 tiles (A 4 KB + B 8 KB of smem per 128-cycle MMA);
+// dW: 128x128 (the int64 per-node accumulators live in registers).
+template <int EPI>
+struct TileCfg {
+  static constexpr int BN = EPI == kTcDw ? 128 : 256;
+  static constexpr int STAGES = EPI == kTcDw ? 6 : 4;
+  static constexpr int kBytesA = BM * BK * 4;
+  static constexpr int kBytesB = BN * BK * 4;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmemBytes = STAGES * (kBytesA + kBytesB) + 1024 + 256;
+};
 
 struct EpiArgs {
   int M, N;
@@ -151,26 +158,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// nseg == 0: one segment covering K.  Otherwise segment s covers K columns
-// [seg_k0[s], seg_k0[s] + round_up(seg_rows[s], 32)) — one virtual node.
+// Persistent: CTA b processes tiles b, b + gridDim.x, ... (n fastest).  Per
+// tile, nseg == 0 means one segment covering K; otherwise segment s covers K
+// columns [seg_k0[s], seg_k0[s] + round_up(seg_rows[s], 32)) — one virtual node.
+// Accumulator buffers alternate over the global (tile, segment) sequence, so the
+// epilogue of one segment overlaps the MMAs of the next, across tiles too.
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               int K, int nseg, const int* __restrict__ seg_k0, const int* __restrict__ seg_rows,
               EpiArgs ep) {
+  using C = TileCfg<EPI>;
+  constexpr int BN = C::BN, STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * kBytesA;
-  uint64_t* full = (uint64_t*)(sB + STAGES * kBytesB);
+  uint8_t* sB = smem + STAGES * C::kBytesA;
+  uint64_t* full = (uint64_t*)(sB + STAGES * C::kBytesB);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int segs = nseg > 0 ? nseg : 1;
+  const int tiles_n = (int)ceil_div(ep.N, BN);
+  const int tiles = (int)ceil_div(ep.M, BM) * tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -186,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(kTmemCols)
+                 "r"(C::kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -201,17 +214,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int s = 0; s < segs; ++s) {
-        const int kb = nseg > 0 ? seg_k0[s] : 0;
-        const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
-        for (int k = 0; k < kl; k += BK) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], kBytesA + kBytesB);
-          tma_load_2d(sA + stage * kBytesA, &tmA, &full[stage], kb + k, m0);
-          tma_load_2d(sB + stage * kBytesB, &tmB, &full[stage], kb + k, n0);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+        for (int s = 0; s < segs; ++s) {
+          const int kb = nseg > 0 ? seg_k0[s] : 0;
+          const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
+          for (int k = 0; k < kl; k += BK) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], C::kBytesA + C::kBytesB);
+            tma_load_2d(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
+            tma_load_2d(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -221,90 +237,133 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = idesc_tf32(BM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      for (int s = 0; s < segs; ++s) {
-        const int b = s & 1;
-        mbar_wait(&tempty[b], ((s >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(b * BN);
-        const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
-        for (int k = 0; k < kl; k += BK) {
-          mbar_wait(&full[stage], phase);
+      uint32_t it = 0;  // global (tile, segment) counter
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int s = 0; s < segs; ++s, ++it) {
+          const int b = it & 1;
+          mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint64_t ad = sdesc_sw128(su32(sA + stage * kBytesA));
-          const uint64_t bd = sdesc_sw128(su32(sB + stage * kBytesB));
+          const uint32_t d = tmem + (uint32_t)(b * BN);
+          const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
+          for (int k = 0; k < kl; k += BK) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
+            const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
-                     (k > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+            for (int kk = 0; kk < BK / 8; ++kk)
+              mma_tf32(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                       (k > 0 || kk > 0) ? 1u : 0u);
+            mma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
+          mma_commit(&tfull[b]);
         }
-        mma_commit(&tfull[b]);
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int h = (warp - 4) >> 2;       // column half
-    const int row = q * 32 + lane;       // tile row == TMEM lane
-    const int r = m0 + row;
-    long long acc[EPI == kTcDw ? 64 : 1];
-    if (EPI == kTcDw) {
+    constexpr int COLS = BN / 2;          // columns per epilogue thread
+    const int q = warp & 3;               // TMEM lane quarter this warp may access
+    const int h = (warp - 4) >> 2;        // column half
+    const int row = q * 32 + lane;        // tile row == TMEM lane
+    uint32_t it = 0;
+    bool bad = false, nonfin = false;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      const int r = m0 + row;
+      long long acc[EPI == kTcDw ? COLS : 1];
+      if (EPI == kTcDw) {
 #pragma unroll
-      for (int j = 0; j < 64; ++j) acc[j] = 0;
-    }
-    for (int s = 0; s < segs; ++s) {
-      const int b = s & 1;
-      mbar_wait(&tfull[b], (s >> 1) & 1);
-      tc_fence_after();
+        for (int j = 0; j < COLS; ++j) acc[j] = 0;
+      }
+      for (int s = 0; s < segs; ++s, ++it) {
+        const int b = it & 1;
+        mbar_wait(&tfull[b], (it >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float v[32];
-        const int col = h * 64 + c * 32;
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
-        const int nb = n0 + col;
-        if (EPI == kTcDw) {
+        for (int c = 0; c < COLS / 32; ++c) {
+          float v[32];
+          const int col = h * COLS + c * 32;
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
+          const int nb = n0 + col;
+          if (EPI == kTcDw) {
+            // Branch-free per-node quantisation: out-of-range or
+            // non-finite partials are flagged once per tile, never summed.
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            acc[c * 32 + j] += quantise(v[j], ep.scale, ep.lim, ep.tail, ep.tensor);
-        } else if (r < ep.M) {
-          const int tc = ep.tcol[r];
+            for (int j = 0; j < 32; ++j) {
+              const float x = v[j] * ep.scale;
+              const float ax = fabsf(x);
+              const bool ok = ax < ep.lim;
+              bad |= !ok;
+              nonfin |= !(ax <= 3.4028234663852886e38f);
+              acc[c * 32 + j] += __float2ll_rn(ok ? x : 0.f);
+            }
+          } else if (r < ep.M) {
+            const int tc = ep.tcol[r];
+            if (EPI == kTcBwd && nb + 32 <= ep.N) {
+              const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = nb + j;
-            if (n < ep.N) {
-              float x = v[j];
-              if (EPI == kTcFwd) {
-                x = act_fwd(ep.act, x + ep.bias[n]);
-              } else {
-                x = x * act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
+              for (int j = 0; j < 32; j += 4) {
+                const float4 xv = __ldg(xp + j / 4);
+                v[j] *= act_grad_from_out(ep.act, xv.x);
+                v[j + 1] *= act_grad_from_out(ep.act, xv.y);
+                v[j + 2] *= act_grad_from_out(ep.act, xv.z);
+                v[j + 3] *= act_grad_from_out(ep.act, xv.w);
               }
-              v[j] = x;
-              ep.outT[(size_t)n * ep.ldT + tc] = x;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int n = nb + j;
+                if (n < ep.N) {
+                  if (EPI == kTcFwd)
+                    v[j] = act_fwd(ep.act, v[j] + __ldg(ep.bias + n));
+                  else
+                    v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nb + j < ep.N) ep.outT[(size_t)(nb + j) * ep.ldT + tc] = v[j];
+            float* orow = ep.out + (size_t)r * ep.ldo + nb;
+            if (nb + 32 <= ep.N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+              for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
             }
           }
-          float* orow = ep.out + (size_t)r * ep.ldo + nb;
-          if (nb + 32 <= ep.N) {
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+      }
+      if (EPI == kTcDw && r < ep.M) {
+        long long* g = ep.G + (size_t)r * ep.ldg + n0 + h * COLS;
+        const int nvalid = ep.N - (n0 + h * COLS);
+        if (nvalid >= COLS) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
-            for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+          for (int j = 0; j < COLS; j += 2) {
+            longlong2* gp = reinterpret_cast<longlong2*>(g + j);
+            longlong2 o = ep.first ? make_longlong2(0, 0) : *gp;
+            o.x += acc[j];
+            o.y += acc[j + 1];
+            *gp = o;
           }
+        } else {
+#pragma unroll
+          for (int j = 0; j < COLS; ++j)
+            if (j < nvalid) g[j] = ep.first ? acc[j] : g[j] + acc[j];
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
     }
-    if (EPI == kTcDw && r < ep.M) {
-      long long* g = ep.G + (size_t)r * ep.ldg + n0 + h * 64;
-      const int nvalid = ep.N - (n0 + h * 64);
-#pragma unroll
-      for (int j = 0; j < 64; ++j)
-        if (j < nvalid) g[j] = ep.first ? acc[j] : g[j] + acc[j];
+    if (EPI == kTcDw) {
+      if (nonfin) atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
+      else if (bad) atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);
     }
   }
   tc_fence_before();
@@ -312,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols)
+                 "r"(C::kTmemCols)
                  : "memory");
   }
 }
@@ -355,16 +414,18 @@ inline CUtensorMap make_map(const float* base, uint64_t rows, uint64_t K, uint64
 
 template <int EPI>
 inline void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, int nseg,
-                        const int* seg_k0, const int* seg_rows, const EpiArgs& ep,
+                        const int* seg_k0, const int* seg_rows, const EpiArgs& ep, int sms,
                         cudaStream_t s) {
+  using C = TileCfg<EPI>;
   static bool attr = false;
   if (!attr) {
     VNT_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBytes));
+                                  C::kSmemBytes));
     attr = true;
   }
-  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM));
-  k_gemm_tc<EPI><<<grid, kThreads, kSmemBytes, s>>>(a, b, K, nseg, seg_k0, seg_rows, ep);
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, C::BN));
+  const int grid = std::min(tiles, sms);
+  k_gemm_tc<EPI><<<grid, kThreads, C::kSmemBytes, s>>>(a, b, K, nseg, seg_k0, seg_rows, ep);
   VNT_LAUNCH_CHECK();
 }
 
@@ -387,7 +448,7 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
   if (last) throw vntb::EngineError(1, "tcgen05 path does not produce logits");
   const CUtensorMap a = make_map(e->X[l], rows, K, K, BM);
-  const CUtensorMap b = make_map(e->wt32 + e->wtoff[l], N, K, K, BN);
+  const CUtensorMap b = make_map(e->wt32 + e->wtoff[l], N, K, K, TileCfg<kTcFwd>::BN);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
@@ -398,7 +459,7 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   ep.outT = e->XT[l + 1];
   ep.ldT = ldT;
   ep.tcol = tcol;
-  launch_gemm<kTcFwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->stream);
+  launch_gemm<kTcFwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
   e->launches++;
 }
 
@@ -406,7 +467,7 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol) 
   using namespace vntb::tc;
   const int N = (int)e->widths[l], K = (int)e->widths[l + 1];
   const CUtensorMap a = make_map(e->D[l + 1], rows, K, K, BM);
-  const CUtensorMap b = make_map(e->w32 + e->woff[l], N, K, K, BN);
+  const CUtensorMap b = make_map(e->w32 + e->woff[l], N, K, K, TileCfg<kTcBwd>::BN);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
@@ -418,7 +479,7 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol) 
   ep.tcol = tcol;
   ep.Xprev = e->X[l];
   ep.ldx = N;
-  launch_gemm<kTcBwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->stream);
+  launch_gemm<kTcBwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
   e->launches++;
 }
 
@@ -428,7 +489,7 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   const int M = (int)e->widths[l], N = (int)e->widths[l + 1];
   const uint64_t ldT = p.ldT;
   const CUtensorMap a = make_map(e->XT[l], M, ldT, ldT, BM);
-  const CUtensorMap b = make_map(e->DT[l + 1], N, ldT, ldT, BN);
+  const CUtensorMap b = make_map(e->DT[l + 1], N, ldT, ldT, TileCfg<kTcDw>::BN);
   EpiArgs ep{};
   ep.M = M;
   ep.N = N;
@@ -439,7 +500,8 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   ep.lim = lim;
   ep.tail = e->G + e->P;
   ep.tensor = tensor;
-  launch_gemm<kTcDw>(a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep, e->stream);
+  launch_gemm<kTcDw>(a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep, e->sm_count,
+                     e->stream);
   e->launches++;
 }
 
