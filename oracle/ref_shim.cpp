@@ -17,6 +17,7 @@
 //                               model.cpp:364-374)
 
 #include <chrono>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -211,6 +212,42 @@ int vntref_accumulate_sample(const uint64_t* widths, uint32_t nw, int act, int l
     auto t2 = std::chrono::steady_clock::now();
     *accumulate_s = std::chrono::duration<double>(t1 - t0).count();
     *round_s = std::chrono::duration<double>(t2 - t1).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Multi-threaded bounded sample: `threads` workers, each with its own exact
+// accumulator (as each simulated device has its own GradientBuffer), each
+// accumulating `per_thread` examples.  Returns the wall time of the parallel
+// accumulate phase (examples / wall = throughput on this many host cores).
+int vntref_accumulate_sample_mt(const uint64_t* widths, uint32_t nw, int act, int loss,
+                                uint64_t seed, const double* x, const double* y,
+                                uint64_t per_thread, uint32_t threads, double* wall_s) {
+  try {
+    Model m(spec_of(widths, nw, act, loss, seed));
+    const ParamVector p = m.init_params();
+    std::vector<std::unique_ptr<ExactVectorAccumulator>> accs;
+    for (uint32_t t = 0; t < threads; ++t)
+      accs.push_back(std::make_unique<ExactVectorAccumulator>(m.param_count()));
+    Batch b;
+    b.count = per_thread;
+    b.input_width = widths[0];
+    b.output_width = widths[nw - 1];
+    b.examples.assign(x, x + per_thread * widths[0]);
+    b.labels.assign(y, y + per_thread * widths[nw - 1]);
+    b.ids.resize(per_thread);
+    for (uint64_t i = 0; i < per_thread; ++i) b.ids[i] = i;
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < threads; ++t)
+      pool.emplace_back([&, t] {
+        ExactAccumulator ls;
+        m.accumulate_example_grads(p, b, *accs[t], ls);
+      });
+    for (auto& th : pool) th.join();
+    *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

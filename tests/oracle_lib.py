@@ -116,7 +116,7 @@ class Oracle:
         return g, lo.value
 
     def trainer(self, widths, act, loss, seed, global_batch, virtual_nodes, lr,
-                data_seed, dataset_size, n_devices, capacity=1 << 20):
+                data_seed, dataset_size, n_devices, capacity=1 << 20, parallel=False):
         w, n = _widths(widths)
         if self.kind == "port":
             h = self._tc(w, C.c_uint32(n), C.c_int(ACT[act]), C.c_int(LOSS[loss]),
@@ -127,7 +127,7 @@ class Oracle:
             h = self._tc(w, C.c_uint32(n), C.c_int(ACT[act]), C.c_int(LOSS[loss]),
                          C.c_uint64(seed), C.c_uint64(global_batch), C.c_uint64(virtual_nodes),
                          C.c_double(lr), C.c_uint64(data_seed), C.c_uint64(dataset_size),
-                         C.c_uint32(n_devices), C.c_uint64(capacity), C.c_int(0))
+                         C.c_uint32(n_devices), C.c_uint64(capacity), C.c_int(1 if parallel else 0))
         assert h, "trainer_create failed"
         return _Trainer(self, h, self.param_count(widths), widths[0])
 
