@@ -34,8 +34,8 @@ int set_error(int code, const std::string& msg) {
   return code;
 }
 
-constexpr int kScaleTargetBits = 40;   // |sum| of the largest element ~ 2^40 after scaling
-constexpr int kLimBits = 50;           // per-node partial bound (2^12 nodes x 2^50 < 2^62)
+constexpr int kScaleTargetBits = 36;   // |sum| of the largest element ~ 2^36 after scaling
+constexpr int kLimBits = 44;           // per-node partial bound (exact FP-add split; 2^18 nodes x 2^44 < 2^62)
 constexpr int kRescaleStep = 12;
 
 struct PassNode {
@@ -259,7 +259,7 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
   const uint64_t budget = e->opt.resident_rows ? e->opt.resident_rows : ~0ull;
   Pass cur;
   for (const auto& n : local) {
-    if (!cur.nodes.empty() && cur.rows + n.rows > budget) {
+    if (!cur.nodes.empty() && (cur.rows + n.rows > budget || cur.nodes.size() >= 512)) {
       passes.push_back(cur);
       cur = Pass{};
     }
@@ -311,9 +311,11 @@ struct FwdSkinny {
 template <int NO>
 struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
-                  int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol) {
+                  int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
+                  float tscale) {
     dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
-    k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol);
+    k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
+                                            tscale);
   }
 };
 template <int NO>
@@ -424,11 +426,12 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
       dim3 grid((unsigned)ceil_div(N, 64), (unsigned)ceil_div(p.rows, 64));
       if (last) {
         k_gemm_ffma<kEpiLogits><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
-                                                     e->logits, N, nullptr, 0, nullptr, nullptr, 0);
+                                                     e->logits, N, nullptr, 0, nullptr, nullptr, 0,
+                                                     1.f);
       } else {
         k_gemm_ffma<kEpiHidden><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
                                                      e->X[l + 1], N, e->XT[l + 1], ldT, tcol,
-                                                     nullptr, 0);
+                                                     nullptr, 0, 1.f);
       }
       VNT_LAUNCH_CHECK();
       e->launches++;
@@ -436,11 +439,15 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     prof_end(e, 2.0 * rows * (double)K * N);
   }
   cudaEventRecord(e->ev[1], s);
+  // Feature-major delta copies DT[l] feed the dW of layer l-1; for tcgen05
+  // layers they carry that dW's 2^s quantisation scale (exact power of two).
+  auto dts = [&](int l) { return e->tc_layer[l - 1] ? pow2f(e->scales[2 * (l - 1)]) : 1.f; };
   // Loss + output delta (model.cpp:289-315).
   {
     const unsigned warps_per_block = 8;
     k_loss<<<(unsigned)ceil_div(p.rows, warps_per_block), warps_per_block * 32, 0, s>>>(
-        e->logits, e->yin, rows, (int)out, e->loss, e->D[L], e->DT[L], ldT, tcol, e->G + e->P);
+        e->logits, e->yin, rows, (int)out, e->loss, e->D[L], e->DT[L], ldT, tcol, e->G + e->P,
+        dts(L));
     VNT_LAUNCH_CHECK();
     e->launches++;
   }
@@ -451,7 +458,7 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     const int tw = 2 * l, tb = 2 * l + 1;
     prof_begin(e);
     if (e->tc_layer[l]) {
-      tc_weight_grad(e, l, p, col0, nrows, pow2f(e->scales[tw]), lim, first_write, tw);
+      tc_weight_grad(e, l, p, col0, nrows, 1.f, lim, first_write, tw);
     } else if (out_l <= 32) {
       dispatch_skinny<DwSkinny>(out_l, s, e->X[l], in_l, e->D[l + 1], out_l, row0, nrows, (int)nn,
                                 pow2f(e->scales[tw]), lim, e->G + e->woff[l], e->G + e->P, tw);
@@ -475,10 +482,10 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     if (l > 0) {
       prof_begin(e);
       if (e->tc_layer[l]) {
-        tc_backward_data(e, l, rows, ldT, tcol);
+        tc_backward_data(e, l, rows, ldT, tcol, dts(l));
       } else if (out_l <= 32) {
         dispatch_skinny<BwdSkinny>(out_l, s, e->D[l + 1], e->w32 + e->woff[l], out_l, in_l, rows,
-                                   e->act, e->X[l], e->D[l], e->DT[l], ldT, tcol);
+                                   e->act, e->X[l], e->D[l], e->DT[l], ldT, tcol, dts(l));
         VNT_LAUNCH_CHECK();
         e->launches++;
       } else {
@@ -486,7 +493,7 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
         dim3 grid((unsigned)ceil_div(in_l, 64), (unsigned)ceil_div(p.rows, 64));
         k_gemm_ffma<kEpiBwd><<<grid, 256, 0, s>>>(e->D[l + 1], out_l, WT, in_l, rows, in_l, out_l,
                                                   nullptr, e->act, e->D[l], in_l, e->DT[l], ldT,
-                                                  tcol, e->X[l], in_l);
+                                                  tcol, e->X[l], in_l, dts(l));
         VNT_LAUNCH_CHECK();
         e->launches++;
       }

@@ -55,6 +55,7 @@ struct EpiArgs {
   const int* tcol;
   const float* Xprev;
   int ldx;
+  float tscale;        // scale applied to the feature-major copy (DT: 2^s of the next dW)
   // dW
   long long* G;
   int ldg;
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int h = (warp - 4) >> 2;        // column half
     const int row = q * 32 + lane;        // tile row == TMEM lane
     uint32_t it = 0;
-    bool bad = false, nonfin = false;
+    float amax = 0.f, canary = 0.f;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
       const int r = m0 + row;
@@ -290,16 +291,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
           const int nb = n0 + col;
           if (EPI == kTcDw) {
-            // Branch-free per-node quantisation: out-of-range or
-            // non-finite partials are flagged once per tile, never summed.
+            // Per-node quantisation.  The 2^s scale is already in
+            // the DT operand (exact power-of-two scaling), so TMEM holds g*2^s:
+            // track max|x| and a NaN/inf canary, convert, accumulate.
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const float x = v[j] * ep.scale;
-              const float ax = fabsf(x);
-              const bool ok = ax < ep.lim;
-              bad |= !ok;
-              nonfin |= !(ax <= 3.4028234663852886e38f);
-              acc[c * 32 + j] += __float2ll_rn(ok ? x : 0.f);
+              const float x = v[j];
+              amax = fmaxf(amax, fabsf(x));
+              canary = fmaf(x, 0.f, canary);
+              acc[c * 32 + j] += __float2ll_rn(x);
             }
           } else if (r < ep.M) {
             const int tc = ep.tcol[r];
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (nb + j < ep.N) ep.outT[(size_t)(nb + j) * ep.ldT + tc] = v[j];
+              if (nb + j < ep.N) ep.outT[(size_t)(nb + j) * ep.ldT + tc] = v[j] * ep.tscale;
             float* orow = ep.out + (size_t)r * ep.ldo + nb;
             if (nb + 32 <= ep.N) {
 #pragma unroll
@@ -362,8 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (EPI == kTcDw) {
-      if (nonfin) atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
-      else if (bad) atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);
+      if (canary != 0.f)   // NaN: some partial was NaN or inf
+        atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
+      else if (!(amax < ep.lim))
+        atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);
     }
   }
   tc_fence_before();
@@ -432,8 +434,16 @@ inline void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int M, int N
 }  // namespace tc
 }  // namespace vntb
 
+#include "gemm_tc_pair.cuh"
+
 // ---------------------------------------------- engine glue (needs vnt_engine)
 namespace {
+
+// CTA pairs for forward / bwd-data (VNT_TC_PAIR=0 selects the single-CTA kernel).
+bool tc_use_pair() {
+  static const bool on = !(getenv("VNT_TC_PAIR") && getenv("VNT_TC_PAIR")[0] == '0');
+  return on;
+}
 
 bool tc_layer_eligible(int mode, uint64_t in, uint64_t out) {
   if (mode == VNT_GEMM_FFMA) return false;
@@ -447,8 +457,10 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   using namespace vntb::tc;
   const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
   if (last) throw vntb::EngineError(1, "tcgen05 path does not produce logits");
+  const bool pair = tc_use_pair();
   const CUtensorMap a = make_map(e->X[l], rows, K, K, BM);
-  const CUtensorMap b = make_map(e->wt32 + e->wtoff[l], N, K, K, TileCfg<kTcFwd>::BN);
+  const CUtensorMap b = make_map(e->wt32 + e->wtoff[l], N, K, K,
+                                 pair ? PairCfg<kTcFwd>::BNH : TileCfg<kTcFwd>::BN);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
@@ -459,15 +471,21 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   ep.outT = e->XT[l + 1];
   ep.ldT = ldT;
   ep.tcol = tcol;
-  launch_gemm<kTcFwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
+  ep.tscale = 1.f;
+  if (pair)
+    launch_gemm_pair<kTcFwd>(a, b, rows, N, K, ep, e->sm_count, e->stream);
+  else
+    launch_gemm<kTcFwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
   e->launches++;
 }
 
-void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol) {
+void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol, float tscale) {
   using namespace vntb::tc;
   const int N = (int)e->widths[l], K = (int)e->widths[l + 1];
+  const bool pair = tc_use_pair();
   const CUtensorMap a = make_map(e->D[l + 1], rows, K, K, BM);
-  const CUtensorMap b = make_map(e->w32 + e->woff[l], N, K, K, TileCfg<kTcBwd>::BN);
+  const CUtensorMap b = make_map(e->w32 + e->woff[l], N, K, K,
+                                 pair ? PairCfg<kTcBwd>::BNH : TileCfg<kTcBwd>::BN);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
@@ -479,7 +497,11 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol) 
   ep.tcol = tcol;
   ep.Xprev = e->X[l];
   ep.ldx = N;
-  launch_gemm<kTcBwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
+  ep.tscale = tscale;
+  if (pair)
+    launch_gemm_pair<kTcBwd>(a, b, rows, N, K, ep, e->sm_count, e->stream);
+  else
+    launch_gemm<kTcBwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
   e->launches++;
 }
 

@@ -1,0 +1,267 @@
+// CTA-pair (cta_group::2) variant of the tcgen05 GEMM, used for the forward
+// and bwd-data layers.  A cluster of two CTAs (the two SMs of a TPC) computes
+// a 256 x BN tile: CTA r owns A rows [m0 + 128 r, +128) and B rows
+// [n0 + r BN/2, +BN/2) in its own smem; the leader (r = 0) issues
+// tcgen05.mma.cta_group::2 on the pair's operands and each CTA receives its
+// 128 accumulator rows in its own TMEM.  Per SM this cuts the TMA bytes
+// written into smem per MAC by a third (B loaded once per pair), which is the
+// shared-memory bound of the single-CTA kernel.
+#pragma once
+
+namespace vntb {
+namespace tc {
+
+template <int EPI>
+struct PairCfg {
+  static constexpr int BN = 256;
+  static constexpr int BNH = BN / 2;
+  static constexpr int kBytesA = BM * BK * 4;
+  static constexpr int kBytesB = BNH * BK * 4;
+  static constexpr int STAGES = 192 * 1024 / (kBytesA + kBytesB);
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmemBytes = STAGES * (kBytesA + kBytesB) + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Arrive on the leader CTA's copy of `bar` (same smem offset).
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(su32(bar))
+      : "memory");
+}
+
+// TMA load into this CTA's smem; completion counted on the leader's barrier
+// (peer bit 24 of the shared::cluster address cleared).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* tm, uint64_t* bar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"((uint64_t)tm), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm_tc_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int K, EpiArgs ep) {
+  static_assert(EPI != kTcDw, "pair kernel: forward / bwd-data epilogues only");
+  using C = PairCfg<EPI>;
+  constexpr int BN = C::BN, BNH = C::BNH, STAGES = C::STAGES, PM = 2 * BM;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::kBytesA;
+  uint64_t* full = (uint64_t*)(sB + STAGES * C::kBytesB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int tiles_n = (int)ceil_div(ep.N, BN);
+  const int tiles = (int)ceil_div(ep.M, PM) * tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 16);   // 8 epilogue warps x 2 CTAs (leader copy used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(C::kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < tiles; tile += npairs) {
+        const int m0 = (tile / tiles_n) * PM + (int)rank * BM;
+        const int n0 = (tile % tiles_n) * BN + (int)rank * BNH;
+        for (int k = 0; k < K; k += BK) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (C::kBytesA + C::kBytesB));
+          tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], k, m0);
+          tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], k, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_tf32(PM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t it = 0;
+      for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+        const int b = it & 1;
+        mbar_wait_cluster(&tempty[b], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int k = 0; k < K; k += BK) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
+          const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32_pair(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                          (k > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_pair(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[b]);
+      }
+    }
+  } else if (warp >= 4) {
+    constexpr int COLS = BN / 2;
+    const int q = warp & 3;
+    const int h = (warp - 4) >> 2;
+    const int row = q * 32 + lane;
+    uint32_t it = 0;
+    for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+      const int m0 = (tile / tiles_n) * PM + (int)rank * BM, n0 = (tile % tiles_n) * BN;
+      const int r = m0 + row;
+      const int b = it & 1;
+      mbar_wait(&tfull[b], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < COLS / 32; ++c) {
+        float v[32];
+        const int col = h * COLS + c * 32;
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
+        const int nb = n0 + col;
+        if (r < ep.M) {
+          const int tc = ep.tcol[r];
+          if (EPI == kTcBwd && nb + 32 <= ep.N) {
+            const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 xv = __ldg(xp + j / 4);
+              v[j] *= act_grad_from_out(ep.act, xv.x);
+              v[j + 1] *= act_grad_from_out(ep.act, xv.y);
+              v[j + 2] *= act_grad_from_out(ep.act, xv.z);
+              v[j + 3] *= act_grad_from_out(ep.act, xv.w);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = nb + j;
+              if (n < ep.N) {
+                if (EPI == kTcFwd)
+                  v[j] = act_fwd(ep.act, v[j] + __ldg(ep.bias + n));
+                else
+                  v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < ep.N) ep.outT[(size_t)(nb + j) * ep.ldT + tc] = v[j] * ep.tscale;
+          float* orow = ep.out + (size_t)r * ep.ldo + nb;
+          if (nb + 32 <= ep.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+            for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[b]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::kTmemCols)
+                 : "memory");
+  }
+}
+
+template <int EPI>
+inline void launch_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
+                             const EpiArgs& ep, int sms, cudaStream_t s) {
+  using C = PairCfg<EPI>;
+  static bool attr = false;
+  if (!attr) {
+    VNT_CUDA(cudaFuncSetAttribute(k_gemm_tc_pair<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  C::kSmemBytes));
+    attr = true;
+  }
+  const int tiles = (int)(ceil_div(M, 2 * BM) * ceil_div(N, C::BN));
+  const int pairs = std::max(1, std::min(tiles, sms / 2));
+  k_gemm_tc_pair<EPI><<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a, b, K, ep);
+  VNT_LAUNCH_CHECK();
+}
+
+}  // namespace tc
+}  // namespace vntb

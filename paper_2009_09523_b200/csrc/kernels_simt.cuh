@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
     const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb, int M, int N,
     int K, const float* __restrict__ bias, int act, float* __restrict__ out, int ldo,
     float* __restrict__ outT, int ldT, const int* __restrict__ tcol,
-    const float* __restrict__ Xprev, int ldx) {
+    const float* __restrict__ Xprev, int ldx, float tscale) {
   __shared__ __align__(16) float As[16][64 + 4];
   __shared__ __align__(16) float Bs[16][64 + 4];
   const int t = threadIdx.x;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
         v = v * act_grad_from_out(act, Xprev[(size_t)r * ldx + n]);
       }
       out[(size_t)r * ldo + n] = v;
-      if (EPI != kEpiLogits) outT[(size_t)n * ldT + tc] = v;
+      if (EPI != kEpiLogits) outT[(size_t)n * ldT + tc] = v * tscale;
     }
   }
 }
@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
 // quantised at 2^-32 and summed exactly (int64 atomics: order-free).
 __global__ void k_loss(const float* __restrict__ logits, const double* __restrict__ y, int rows,
                        int outw, int loss_kind, float* __restrict__ D, float* __restrict__ DT,
-                       int ldT, const int* __restrict__ tcol, long long* __restrict__ tail) {
+                       int ldT, const int* __restrict__ tcol, long long* __restrict__ tail,
+                       float tscale) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -191,7 +192,7 @@ __global__ void k_loss(const float* __restrict__ logits, const double* __restric
       loss += d * d;
       const float dl = (float)(2.0 * d / (double)outw);
       D[(size_t)r * outw + o] = dl;
-      DT[(size_t)o * ldT + tc] = dl;
+      DT[(size_t)o * ldT + tc] = dl * tscale;
     }
 #pragma unroll
     for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
@@ -211,7 +212,7 @@ __global__ void k_loss(const float* __restrict__ logits, const double* __restric
       loss -= yr[o] * (zm - lognorm);
       const float dl = (float)(exp(zm) / norm - yr[o]);
       D[(size_t)r * outw + o] = dl;
-      DT[(size_t)o * ldT + tc] = dl;
+      DT[(size_t)o * ldT + tc] = dl * tscale;
     }
 #pragma unroll
     for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
@@ -363,7 +364,7 @@ template <int NO>
 __global__ void k_bwd_skinny(const float* __restrict__ Dn, const float* __restrict__ W, int no,
                              int in, int rows, int act, const float* __restrict__ Xprev,
                              float* __restrict__ Dout, float* __restrict__ DT, int ldT,
-                             const int* __restrict__ tcol) {
+                             const int* __restrict__ tcol, float tscale) {
   __shared__ float tile[32][33];
   __shared__ float dn[32][NO];
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
@@ -392,7 +393,7 @@ __global__ void k_bwd_skinny(const float* __restrict__ Dn, const float* __restri
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
     const int ii = i0 + k, r = r0 + tx;
-    if (r < rows && ii < in) DT[(size_t)ii * ldT + tcol[r]] = tile[tx][k];
+    if (r < rows && ii < in) DT[(size_t)ii * ldT + tcol[r]] = tile[tx][k] * tscale;
   }
 }
 
