@@ -172,6 +172,9 @@ int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count,
 int vnt_engine_get_scales(vnt_engine* e, int32_t* scales, uint32_t n);
 int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n);
 uint32_t vnt_engine_tensor_count(const vnt_engine* e);
+/* Forget the scale history: the next step uses the deterministic initial scale
+ * 40 - ceil(log2 B) (stateless callers, e.g. vnt::train_step on a World). */
+int vnt_engine_reset_scales(vnt_engine* e);
 
 int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out);
 /* The CUDA stream the engine launches on (cudaStream_t as void*). */

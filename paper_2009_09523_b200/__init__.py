@@ -108,6 +108,7 @@ def load_engine() -> C.CDLL:
         "vnt_engine_get_scales": (C.c_int, [_vp, _i32p, C.c_uint32]),
         "vnt_engine_set_scales": (C.c_int, [_vp, _i32p, C.c_uint32]),
         "vnt_engine_last_timings": (C.c_int, [_vp, C.POINTER(StepTimings)]),
+        "vnt_engine_reset_scales": (C.c_int, [_vp]),
         "vnt_engine_stream": (_vp, [_vp]),
         "vnt_engine_device_alloc": (C.c_int, [_vp, C.c_uint64, C.POINTER(_vp)]),
         "vnt_engine_device_free": (C.c_int, [_vp, _vp]),

@@ -34,8 +34,8 @@ int set_error(int code, const std::string& msg) {
   return code;
 }
 
-constexpr int kScaleTargetBits = 36;   // |sum| of the largest element ~ 2^36 after scaling
-constexpr int kLimBits = 44;           // per-node partial bound (exact FP-add split; 2^18 nodes x 2^44 < 2^62)
+constexpr int kScaleTargetBits = 40;   // |sum| of the largest element ~ 2^40 after scaling
+constexpr int kLimBits = 50;           // per-node partial bound (2^12 nodes x 2^50 < 2^62)
 constexpr int kRescaleStep = 12;
 
 struct PassNode {
@@ -259,7 +259,7 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
   const uint64_t budget = e->opt.resident_rows ? e->opt.resident_rows : ~0ull;
   Pass cur;
   for (const auto& n : local) {
-    if (!cur.nodes.empty() && (cur.rows + n.rows > budget || cur.nodes.size() >= 512)) {
+    if (!cur.nodes.empty() && cur.rows + n.rows > budget) {
       passes.push_back(cur);
       cur = Pass{};
     }
@@ -304,8 +304,8 @@ template <int NO>
 struct FwdSkinny {
   static void run(cudaStream_t s, const float* X, int K, const float* W, int no, const float* b,
                   int rows, int act, int last, float* out, float* outT, int ldT, const int* tcol) {
-    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
-                                                                 out, outT, ldT, tcol);
+    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 64), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
+                                                                  out, outT, ldT, tcol);
   }
 };
 template <int NO>
@@ -313,7 +313,7 @@ struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
                   int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
                   float tscale) {
-    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 128)), block(32, 8);
     k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
                                             tscale);
   }
@@ -1145,6 +1145,12 @@ int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n) {
     e->scales.assign(scales, scales + n);
     return VNT_OK;
   });
+}
+
+int vnt_engine_reset_scales(vnt_engine* e) {
+  if (!e) return VNT_ERR_CONFIG;
+  e->scales_init = false;
+  return VNT_OK;
 }
 
 int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out) {

@@ -323,77 +323,101 @@ __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict
 // lane-strided partial dot products over k then a fixed xor tree, so every
 // output depends only on its row.
 template <int NO>
-__global__ void k_fwd_skinny(const float* __restrict__ X, int K, const float* __restrict__ W,
-                             int no, const float* __restrict__ bias, int rows, int act, int last,
-                             float* __restrict__ out, float* __restrict__ outT, int ldT,
-                             const int* __restrict__ tcol) {
+__global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X, int K,
+                                                    const float* __restrict__ W, int no,
+                                                    const float* __restrict__ bias, int rows,
+                                                    int act, int last, float* __restrict__ out,
+                                                    float* __restrict__ outT, int ldT,
+                                                    const int* __restrict__ tcol) {
+  // One warp per 8 rows: every weight row W[k][:] fetched once serves 8 rows.
+  constexpr int R = 8;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const float* x = X + (size_t)warp * K;
-  float acc[NO];
+  const int r0 = warp * R;
+  if (r0 >= rows) return;
+  float acc[R][NO];
 #pragma unroll
-  for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int o = 0; o < NO; ++o) acc[i][o] = 0.f;
   for (int k = lane; k < K; k += 32) {
-    const float a = x[k];
-    const float* w = W + (size_t)k * no;
+    float w[NO];
 #pragma unroll
-    for (int o = 0; o < NO; ++o)
-      if (o < no) acc[o] = fmaf(a, __ldg(w + o), acc[o]);
+    for (int o = 0; o < NO; ++o) w[o] = (o < no) ? __ldg(W + (size_t)k * no + o) : 0.f;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const float a = (r0 + i < rows) ? __ldg(X + (size_t)(r0 + i) * K + k) : 0.f;
+#pragma unroll
+      for (int o = 0; o < NO; ++o) acc[i][o] = fmaf(a, w[o], acc[i][o]);
+    }
   }
 #pragma unroll
-  for (int o = 0; o < NO; ++o) {
+  for (int i = 0; i < R; ++i) {
 #pragma unroll
-    for (int s = 16; s; s >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], s);
-  }
-  if (lane < no) {
-    float v = 0.f;
+    for (int o = 0; o < NO; ++o) {
 #pragma unroll
-    for (int o = 0; o < NO; ++o)
-      if (o == lane) v = acc[o];
-    v += bias[lane];
-    if (!last) v = act_fwd(act, v);
-    out[(size_t)warp * no + lane] = v;
-    if (!last) outT[(size_t)lane * ldT + tcol[warp]] = v;
+      for (int s = 16; s; s >>= 1) acc[i][o] += __shfl_xor_sync(0xffffffffu, acc[i][o], s);
+    }
+    const int r = r0 + i;
+    if (r < rows && lane < no) {
+      float v = 0.f;
+#pragma unroll
+      for (int o = 0; o < NO; ++o)
+        if (o == lane) v = acc[i][o];
+      v += bias[lane];
+      if (!last) v = act_fwd(act, v);
+      out[(size_t)r * no + lane] = v;
+      if (!last) outT[(size_t)lane * ldT + tcol[r]] = v;
+    }
   }
 }
 
 // bwd-data through a skinny layer: D[r][i] = (sum_o Dn[r][o] W[i][o]) f'(X[r][i]),
 // o ascending; 32x32 (row, i) tiles, transposed copy through smem.
 template <int NO>
-__global__ void k_bwd_skinny(const float* __restrict__ Dn, const float* __restrict__ W, int no,
-                             int in, int rows, int act, const float* __restrict__ Xprev,
-                             float* __restrict__ Dout, float* __restrict__ DT, int ldT,
-                             const int* __restrict__ tcol, float tscale) {
+__global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn,
+                                                    const float* __restrict__ W, int no, int in,
+                                                    int rows, int act,
+                                                    const float* __restrict__ Xprev,
+                                                    float* __restrict__ Dout,
+                                                    float* __restrict__ DT, int ldT,
+                                                    const int* __restrict__ tcol, float tscale) {
+  // 32 features x 128 rows per block (4 chunks of 32 rows), o ascending per
+  // output; transposed copy through smem.
   __shared__ float tile[32][33];
   __shared__ float dn[32][NO];
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
-  const int r0 = blockIdx.y * 32, i0 = blockIdx.x * 32;
-  for (int k = ty * 32 + tx; k < 32 * NO; k += 256) {
-    const int rr = k / NO, o = k % NO;
-    dn[rr][o] = (r0 + rr < rows && o < no) ? Dn[(size_t)(r0 + rr) * no + o] : 0.f;
-  }
-  __syncthreads();
+  const int i0 = blockIdx.x * 32;
   const int i = i0 + tx;
   float w[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) w[o] = (i < in && o < no) ? W[(size_t)i * no + o] : 0.f;
-  for (int k = ty; k < 32; k += 8) {
-    const int r = r0 + k;
-    float acc = 0.f;
-#pragma unroll
-    for (int o = 0; o < NO; ++o) acc = fmaf(dn[k][o], w[o], acc);
-    float v = 0.f;
-    if (r < rows && i < in) {
-      v = acc * act_grad_from_out(act, Xprev[(size_t)r * in + i]);
-      Dout[(size_t)r * in + i] = v;
+  for (int chunk = 0; chunk < 4; ++chunk) {
+    const int r0 = (blockIdx.y * 4 + chunk) * 32;
+    if (r0 >= rows) break;
+    __syncthreads();
+    for (int k = ty * 32 + tx; k < 32 * NO; k += 256) {
+      const int rr = k / NO, o = k % NO;
+      dn[rr][o] = (r0 + rr < rows && o < no) ? Dn[(size_t)(r0 + rr) * no + o] : 0.f;
     }
-    tile[k][tx] = v;
-  }
-  __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int ii = i0 + k, r = r0 + tx;
-    if (r < rows && ii < in) DT[(size_t)ii * ldT + tcol[r]] = tile[tx][k] * tscale;
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int r = r0 + k;
+      float acc = 0.f;
+#pragma unroll
+      for (int o = 0; o < NO; ++o) acc = fmaf(dn[k][o], w[o], acc);
+      float v = 0.f;
+      if (r < rows && i < in) {
+        v = acc * act_grad_from_out(act, Xprev[(size_t)r * in + i]);
+        Dout[(size_t)r * in + i] = v;
+      }
+      tile[k][tx] = v;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int ii = i0 + k, r = r0 + tx;
+      if (r < rows && ii < in) DT[(size_t)ii * ldT + tcol[r]] = tile[tx][k] * tscale;
+    }
   }
 }
 
