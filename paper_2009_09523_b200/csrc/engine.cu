@@ -86,6 +86,10 @@ struct vnt_engine {
   double* xin = nullptr;
   double* yin = nullptr;
   std::vector<float*> X, XT, D, DT;
+  // 3xTF32 operand twins (hi = rna_tf32(x), lo = x - hi), only when split.
+  bool split = false;
+  std::vector<float*> Xh, Xl, XTh, XTl, Dh, Dl, DTh, DTl;
+  float *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
   float* logits = nullptr;
   double* vn_mean = nullptr;
   double* vn_m2 = nullptr;
@@ -201,7 +205,8 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
   fre(e->logits);
   fre(e->vn_mean);
   fre(e->vn_m2);
-  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT})
+  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT, &e->Xh, &e->Xl, &e->XTh, &e->XTl, &e->Dh, &e->Dl,
+                  &e->DTh, &e->DTl})
     for (auto*& p : *v) fre(p);
   const uint64_t in = e->widths[0], out = e->widths[L];
   e->xin = (double*)dalloc(rows * in * sizeof(double));
@@ -209,10 +214,9 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
   e->logits = (float*)dalloc(rows * out * sizeof(float));
   e->vn_mean = (double*)dalloc(vns * in * sizeof(double));
   e->vn_m2 = (double*)dalloc(vns * in * sizeof(double));
-  e->X.assign(L + 1, nullptr);
-  e->XT.assign(L + 1, nullptr);
-  e->D.assign(L + 1, nullptr);
-  e->DT.assign(L + 1, nullptr);
+  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT, &e->Xh, &e->Xl, &e->XTh, &e->XTl, &e->Dh, &e->Dl,
+                  &e->DTh, &e->DTl})
+    v->assign(L + 1, nullptr);
   for (int l = 0; l <= L; ++l) {
     const uint64_t w = e->widths[l];
     if (l < L) {
@@ -224,6 +228,20 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
       e->D[l] = (float*)dalloc(rows * w * sizeof(float));
       e->DT[l] = (float*)dalloc(w * ldT * sizeof(float));
       VNT_CUDA(cudaMemset(e->DT[l], 0, w * ldT * sizeof(float)));
+    }
+    if (e->split) {
+      if (l < L && e->tc_layer[l]) {   // operands of layer l: X[l] (fwd), XT[l] (dW)
+        e->Xh[l] = (float*)dalloc(rows * w * sizeof(float));
+        e->Xl[l] = (float*)dalloc(rows * w * sizeof(float));
+        e->XTh[l] = (float*)dalloc(w * ldT * sizeof(float));
+        e->XTl[l] = (float*)dalloc(w * ldT * sizeof(float));
+      }
+      if (l > 0 && e->tc_layer[l - 1]) {   // D[l] (bwd-data of l-1), DT[l] (dW of l-1)
+        e->Dh[l] = (float*)dalloc(rows * w * sizeof(float));
+        e->Dl[l] = (float*)dalloc(rows * w * sizeof(float));
+        e->DTh[l] = (float*)dalloc(w * ldT * sizeof(float));
+        e->DTl[l] = (float*)dalloc(w * ldT * sizeof(float));
+      }
     }
   }
   e->cap_rows = rows;
@@ -291,6 +309,22 @@ void tail_reset(vnt_engine* e) {
   VNT_CUDA(cudaMemsetAsync(e->G + e->P, 0, e->ntail * sizeof(long long), e->stream));
 }
 
+void split_into(vnt_engine* e, const float* x, float* hi, float* lo, size_t n) {
+  if (!e->split || !hi) return;
+  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(n / 4 + 1, 256), 148 * 16);
+  k_split<<<blocks, 256, 0, e->stream>>>(x, hi, lo, n);
+  VNT_LAUNCH_CHECK();
+  e->launches++;
+}
+
+void split_weights(vnt_engine* e) {
+  if (!e->split) return;
+  split_into(e, e->w32, e->w32h, e->w32l, e->P);
+  uint64_t tot = 0;
+  for (int l = 0; l < e->L; ++l) tot += e->widths[l] * e->widths[l + 1];
+  split_into(e, e->wt32, e->wt32h, e->wt32l, tot);
+}
+
 // Skinny-layer (out <= 32) kernels: NO is the compile-time bound.
 template <template <int> class F, class... A>
 void dispatch_skinny(int no, A&&... a) {
@@ -304,8 +338,8 @@ template <int NO>
 struct FwdSkinny {
   static void run(cudaStream_t s, const float* X, int K, const float* W, int no, const float* b,
                   int rows, int act, int last, float* out, float* outT, int ldT, const int* tcol) {
-    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 64), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
-                                                                  out, outT, ldT, tcol);
+    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
+                                                                 out, outT, ldT, tcol);
   }
 };
 template <int NO>
@@ -313,7 +347,7 @@ struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
                   int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
                   float tscale) {
-    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 128)), block(32, 8);
+    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
     k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
                                             tscale);
   }
@@ -365,6 +399,8 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     k_ingest<<<grid, block, 0, s>>>(e->xin, e->X[0], e->XT[0], tcol, rows, (int)in, ldT);
     VNT_LAUNCH_CHECK();
     e->launches++;
+    split_into(e, e->X[0], e->Xh[0], e->Xl[0], p.rows * in);
+    split_into(e, e->XT[0], e->XTh[0], e->XTl[0], in * p.ldT);
   }
   if (do_stats) {
     // observe_batch per node then Chan-combine into the node's device lineage
@@ -437,6 +473,10 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
       e->launches++;
     }
     prof_end(e, 2.0 * rows * (double)K * N);
+    if (!last) {
+      split_into(e, e->X[l + 1], e->Xh[l + 1], e->Xl[l + 1], p.rows * (uint64_t)N);
+      split_into(e, e->XT[l + 1], e->XTh[l + 1], e->XTl[l + 1], (uint64_t)N * p.ldT);
+    }
   }
   cudaEventRecord(e->ev[1], s);
   // Feature-major delta copies DT[l] feed the dW of layer l-1; for tcgen05
@@ -450,6 +490,8 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
         dts(L));
     VNT_LAUNCH_CHECK();
     e->launches++;
+    split_into(e, e->D[L], e->Dh[L], e->Dl[L], p.rows * out);
+    split_into(e, e->DT[L], e->DTh[L], e->DTl[L], out * p.ldT);
   }
   // Backward (model.cpp:317-338): dW/db per node into the exact sum, then delta.
   const float lim = pow2f(kLimBits);
@@ -498,6 +540,8 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
         e->launches++;
       }
       prof_end(e, 2.0 * rows * (double)in_l * out_l);
+      split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l);
+      split_into(e, e->DT[l], e->DTh[l], e->DTl[l], (uint64_t)in_l * p.ldT);
     }
   }
 }
@@ -594,6 +638,7 @@ void launch_sgd(vnt_engine* e, double lr, uint64_t examples) {
       e->launches++;
     }
   }
+  split_weights(e);
 }
 
 struct Readback {
@@ -831,6 +876,13 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     VNT_CUDA(cudaMemset(e->w32, 0, e->P * sizeof(float)));
     e->wt32 = (float*)dalloc(toff * sizeof(float));
     VNT_CUDA(cudaMemset(e->wt32, 0, toff * sizeof(float)));
+    e->split = e->opt.gemm_mode == VNT_GEMM_3XTF32;
+    if (e->split) {
+      e->w32h = (float*)dalloc(e->P * sizeof(float));
+      e->w32l = (float*)dalloc(e->P * sizeof(float));
+      e->wt32h = (float*)dalloc(toff * sizeof(float));
+      e->wt32l = (float*)dalloc(toff * sizeof(float));
+    }
     e->ntail = kTailOverflow + ntensors(e.get());
     e->G = (long long*)dalloc((e->P + e->ntail) * sizeof(long long));
     e->gmax = (unsigned long long*)dalloc(ntensors(e.get()) * sizeof(unsigned long long));
@@ -859,6 +911,11 @@ void vnt_engine_destroy(vnt_engine* e) {
   for (auto& kv : e->plans)
     for (auto& p : kv.second) cudaFree(p.d_meta);
   for (auto* p : e->scratch) cudaFree(p);
+  for (void* p : {(void*)e->w32h, (void*)e->w32l, (void*)e->wt32h, (void*)e->wt32l})
+    if (p) cudaFree(p);
+  for (auto* v : {&e->Xh, &e->Xl, &e->XTh, &e->XTl, &e->Dh, &e->Dl, &e->DTh, &e->DTl})
+    for (auto* p : *v)
+      if (p) cudaFree(p);
   for (void* p : {(void*)e->w64, (void*)e->v64, (void*)e->w32, (void*)e->wt32, (void*)e->G,
                   (void*)e->gmax, (void*)e->gout, (void*)e->xin, (void*)e->yin, (void*)e->logits,
                   (void*)e->vn_mean, (void*)e->vn_m2, (void*)e->d_combine})
@@ -901,6 +958,7 @@ int vnt_engine_set_params(vnt_engine* e, const double* params, uint64_t n) {
       VNT_LAUNCH_CHECK();
     }
     if (e->v64) VNT_CUDA(cudaMemsetAsync(e->v64, 0, e->P * sizeof(double), e->stream));
+    split_weights(e);
     VNT_CUDA(cudaStreamSynchronize(e->stream));
     return VNT_OK;
   });

@@ -33,15 +33,21 @@ enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
 
 // fwd / bwd-data: 128x256 tiles (A 4 KB + B 8 KB of smem per 128-cycle MMA);
 // dW: 128x128 (the int64 per-node accumulators live in registers).
-template <int EPI>
+template <int EPI, int SPLIT = 1>
 struct TileCfg {
   static constexpr int BN = EPI == kTcDw ? 128 : 256;
-  static constexpr int STAGES = EPI == kTcDw ? 6 : 4;
   static constexpr int kBytesA = BM * BK * 4;
   static constexpr int kBytesB = BN * BK * 4;
+  static constexpr int kStageBytes = (SPLIT == 3 ? 2 : 1) * (kBytesA + kBytesB);
+  static constexpr int STAGES_MAX = EPI == kTcDw ? 6 : 4;
+  static constexpr int STAGES = (192 * 1024 / kStageBytes) < STAGES_MAX ? (192 * 1024 / kStageBytes)
+                                                                         : STAGES_MAX;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = STAGES * (kBytesA + kBytesB) + 1024 + 256;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256;
 };
+
+// 3xTF32: x = hi + lo with hi = rna_tf32(x) (cvt.rna.tf32.f32) and lo = x - hi
+// (exact); per k-step hi*hi + hi*lo + lo*hi accumulate into one TMEM tile.
 
 struct EpiArgs {
   int M, N;
@@ -164,18 +170,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // columns [seg_k0[s], seg_k0[s] + round_up(seg_rows[s], 32)) — one virtual node.
 // Accumulator buffers alternate over the global (tile, segment) sequence, so the
 // epilogue of one segment overlaps the MMAs of the next, across tiles too.
-template <int EPI>
+template <int EPI, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmBl,
               int K, int nseg, const int* __restrict__ seg_k0, const int* __restrict__ seg_rows,
               EpiArgs ep) {
-  using C = TileCfg<EPI>;
+  using C = TileCfg<EPI, SPLIT>;
   constexpr int BN = C::BN, STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::kBytesA;
-  uint64_t* full = (uint64_t*)(sB + STAGES * C::kBytesB);
+  uint8_t* sAl = sB + STAGES * C::kBytesB;                       // SPLIT == 3 only
+  uint8_t* sBl = sAl + (SPLIT == 3 ? STAGES * C::kBytesA : 0);
+  uint64_t* full = (uint64_t*)(smem + STAGES * C::kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -222,9 +231,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
           for (int k = 0; k < kl; k += BK) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], C::kBytesA + C::kBytesB);
+            mbar_expect_tx(&full[stage], C::kStageBytes);
             tma_load_2d(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
             tma_load_2d(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
+            if (SPLIT == 3) {
+              tma_load_2d(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
+              tma_load_2d(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
+            }
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -251,10 +264,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
             const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
+            const uint64_t ald = sdesc_sw128(su32(sAl + stage * C::kBytesA));
+            const uint64_t bld = sdesc_sw128(su32(sBl + stage * C::kBytesB));
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk)
-              mma_tf32(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
-                       (k > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t o = (uint64_t)(kk * 2);
+              mma_tf32(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+              if (SPLIT == 3) {
+                mma_tf32(d, ad + o, bld + o, idesc, 1u);
+                mma_tf32(d, ald + o, bd + o, idesc, 1u);
+              }
+            }
             mma_commit(&empty[stage]);
             if (++stage == STAGES) {
               stage = 0;
@@ -414,20 +434,21 @@ inline CUtensorMap make_map(const float* base, uint64_t rows, uint64_t K, uint64
   return m;
 }
 
-template <int EPI>
-inline void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, int nseg,
-                        const int* seg_k0, const int* seg_rows, const EpiArgs& ep, int sms,
-                        cudaStream_t s) {
-  using C = TileCfg<EPI>;
+template <int EPI, int SPLIT>
+inline void launch_gemm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& al,
+                        const CUtensorMap& bl, int M, int N, int K, int nseg, const int* seg_k0,
+                        const int* seg_rows, const EpiArgs& ep, int sms, cudaStream_t s) {
+  using C = TileCfg<EPI, SPLIT>;
   static bool attr = false;
   if (!attr) {
-    VNT_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  C::kSmemBytes));
+    VNT_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI, SPLIT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     attr = true;
   }
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, C::BN));
   const int grid = std::min(tiles, sms);
-  k_gemm_tc<EPI><<<grid, kThreads, C::kSmemBytes, s>>>(a, b, K, nseg, seg_k0, seg_rows, ep);
+  k_gemm_tc<EPI, SPLIT><<<grid, kThreads, C::kSmemBytes, s>>>(a, b, al, bl, K, nseg, seg_k0,
+                                                              seg_rows, ep);
   VNT_LAUNCH_CHECK();
 }
 
@@ -453,14 +474,57 @@ bool tc_layer_eligible(int mode, uint64_t in, uint64_t out) {
 void tc_init(vnt_engine*) {}
 void tc_destroy(vnt_engine*) {}
 
+// Operand maps: the fp32 tensor itself (1 pass) or its tf32 hi / lo twins (3 passes).
+struct OpMaps {
+  CUtensorMap hi, lo;
+};
+
+OpMaps op_maps(const vnt_engine* e, const float* full, const float* hi, const float* lo,
+               uint64_t rows, uint64_t K, uint64_t ld, uint32_t box) {
+  using namespace vntb::tc;
+  OpMaps m;
+  if (e->split) {
+    m.hi = make_map(hi, rows, K, ld, box);
+    m.lo = make_map(lo, rows, K, ld, box);
+  } else {
+    m.hi = make_map(full, rows, K, ld, box);
+    m.lo = m.hi;
+  }
+  return m;
+}
+
+template <int EPI>
+void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M, int N, int K,
+               int nseg, const int* seg_k0, const int* seg_rows, const vntb::tc::EpiArgs& ep) {
+  using namespace vntb::tc;
+  if constexpr (EPI != kTcDw) {
+    if (pair) {
+      if (e->split)
+        launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, ep, e->sm_count, e->stream);
+      else
+        launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, ep, e->sm_count, e->stream);
+      e->launches++;
+      return;
+    }
+  }
+  if (e->split)
+    launch_gemm<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->sm_count,
+                        e->stream);
+  else
+    launch_gemm<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->sm_count,
+                        e->stream);
+  e->launches++;
+}
+
 void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool last) {
   using namespace vntb::tc;
   const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
   if (last) throw vntb::EngineError(1, "tcgen05 path does not produce logits");
   const bool pair = tc_use_pair();
-  const CUtensorMap a = make_map(e->X[l], rows, K, K, BM);
-  const CUtensorMap b = make_map(e->wt32 + e->wtoff[l], N, K, K,
-                                 pair ? PairCfg<kTcFwd>::BNH : TileCfg<kTcFwd>::BN);
+  const uint32_t bn = pair ? PairCfg<kTcFwd>::BNH : TileCfg<kTcFwd>::BN;
+  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, K, K, BM);
+  const uint64_t wo = e->wtoff[l];
+  const OpMaps b = op_maps(e, e->wt32 + wo, e->wt32h + wo, e->wt32l + wo, N, K, K, bn);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
@@ -472,20 +536,17 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   ep.ldT = ldT;
   ep.tcol = tcol;
   ep.tscale = 1.f;
-  if (pair)
-    launch_gemm_pair<kTcFwd>(a, b, rows, N, K, ep, e->sm_count, e->stream);
-  else
-    launch_gemm<kTcFwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
-  e->launches++;
+  tc_launch<kTcFwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
 void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol, float tscale) {
   using namespace vntb::tc;
   const int N = (int)e->widths[l], K = (int)e->widths[l + 1];
   const bool pair = tc_use_pair();
-  const CUtensorMap a = make_map(e->D[l + 1], rows, K, K, BM);
-  const CUtensorMap b = make_map(e->w32 + e->woff[l], N, K, K,
-                                 pair ? PairCfg<kTcBwd>::BNH : TileCfg<kTcBwd>::BN);
+  const uint32_t bn = pair ? PairCfg<kTcBwd>::BNH : TileCfg<kTcBwd>::BN;
+  const OpMaps a = op_maps(e, e->D[l + 1], e->Dh[l + 1], e->Dl[l + 1], rows, K, K, BM);
+  const uint64_t wo = e->woff[l];
+  const OpMaps b = op_maps(e, e->w32 + wo, e->w32h + wo, e->w32l + wo, N, K, K, bn);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
@@ -498,11 +559,7 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol, 
   ep.Xprev = e->X[l];
   ep.ldx = N;
   ep.tscale = tscale;
-  if (pair)
-    launch_gemm_pair<kTcBwd>(a, b, rows, N, K, ep, e->sm_count, e->stream);
-  else
-    launch_gemm<kTcBwd>(a, b, rows, N, K, 0, nullptr, nullptr, ep, e->sm_count, e->stream);
-  e->launches++;
+  tc_launch<kTcBwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
 void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const int* nrows,
@@ -510,8 +567,11 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   using namespace vntb::tc;
   const int M = (int)e->widths[l], N = (int)e->widths[l + 1];
   const uint64_t ldT = p.ldT;
-  const CUtensorMap a = make_map(e->XT[l], M, ldT, ldT, BM);
-  const CUtensorMap b = make_map(e->DT[l + 1], N, ldT, ldT, TileCfg<kTcDw>::BN);
+  // dW stays on the single-CTA kernel: its per-node epilogue, not operand
+  // traffic, bounds it once tiles are paired (measured).
+  const OpMaps a = op_maps(e, e->XT[l], e->XTh[l], e->XTl[l], M, ldT, ldT, BM);
+  const OpMaps b = op_maps(e, e->DT[l + 1], e->DTh[l + 1], e->DTl[l + 1], N, ldT, ldT,
+                           TileCfg<kTcDw>::BN);
   EpiArgs ep{};
   ep.M = M;
   ep.N = N;
@@ -522,9 +582,7 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   ep.lim = lim;
   ep.tail = e->G + e->P;
   ep.tensor = tensor;
-  launch_gemm<kTcDw>(a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep, e->sm_count,
-                     e->stream);
-  e->launches++;
+  tc_launch<kTcDw>(e, false, a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep);
 }
 
 }  // namespace

@@ -11,15 +11,16 @@
 namespace vntb {
 namespace tc {
 
-template <int EPI>
+template <int EPI, int SPLIT = 1>
 struct PairCfg {
   static constexpr int BN = 256;
   static constexpr int BNH = BN / 2;
   static constexpr int kBytesA = BM * BK * 4;
   static constexpr int kBytesB = BNH * BK * 4;
-  static constexpr int STAGES = 192 * 1024 / (kBytesA + kBytesB);
+  static constexpr int kStageBytes = (SPLIT == 3 ? 2 : 1) * (kBytesA + kBytesB);
+  static constexpr int STAGES = 192 * 1024 / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = STAGES * (kBytesA + kBytesB) + 1024 + 256;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -81,18 +82,21 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int EPI>
+template <int EPI, int SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int K, EpiArgs ep) {
+                   const __grid_constant__ CUtensorMap tmAl,
+                   const __grid_constant__ CUtensorMap tmBl, int K, EpiArgs ep) {
   static_assert(EPI != kTcDw, "pair kernel: forward / bwd-data epilogues only");
-  using C = PairCfg<EPI>;
+  using C = PairCfg<EPI, SPLIT>;
   constexpr int BN = C::BN, BNH = C::BNH, STAGES = C::STAGES, PM = 2 * BM;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::kBytesA;
-  uint64_t* full = (uint64_t*)(sB + STAGES * C::kBytesB);
+  uint8_t* sAl = sB + STAGES * C::kBytesB;
+  uint8_t* sBl = sAl + (SPLIT == 3 ? STAGES * C::kBytesA : 0);
+  uint64_t* full = (uint64_t*)(smem + STAGES * C::kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -138,9 +142,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int n0 = (tile % tiles_n) * BN + (int)rank * BNH;
         for (int k = 0; k < K; k += BK) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (C::kBytesA + C::kBytesB));
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
           tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], k, m0);
           tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], k, n0);
+          if (SPLIT == 3) {
+            tma_load_2d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], k, m0);
+            tma_load_2d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], k, n0);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -164,10 +172,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
           const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
+          const uint64_t ald = sdesc_sw128(su32(sAl + stage * C::kBytesA));
+          const uint64_t bld = sdesc_sw128(su32(sBl + stage * C::kBytesB));
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32_pair(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
-                          (k > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t o = (uint64_t)(kk * 2);
+            mma_tf32_pair(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            if (SPLIT == 3) {
+              mma_tf32_pair(d, ad + o, bld + o, idesc, 1u);
+              mma_tf32_pair(d, ald + o, bd + o, idesc, 1u);
+            }
+          }
           mma_commit_pair(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -247,19 +262,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int EPI>
-inline void launch_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
-                             const EpiArgs& ep, int sms, cudaStream_t s) {
-  using C = PairCfg<EPI>;
+template <int EPI, int SPLIT>
+inline void launch_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& al,
+                             const CUtensorMap& bl, int M, int N, int K, const EpiArgs& ep,
+                             int sms, cudaStream_t s) {
+  using C = PairCfg<EPI, SPLIT>;
   static bool attr = false;
   if (!attr) {
-    VNT_CUDA(cudaFuncSetAttribute(k_gemm_tc_pair<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  C::kSmemBytes));
+    VNT_CUDA(cudaFuncSetAttribute(k_gemm_tc_pair<EPI, SPLIT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     attr = true;
   }
   const int tiles = (int)(ceil_div(M, 2 * BM) * ceil_div(N, C::BN));
   const int pairs = std::max(1, std::min(tiles, sms / 2));
-  k_gemm_tc_pair<EPI><<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a, b, K, ep);
+  k_gemm_tc_pair<EPI, SPLIT><<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a, b, al, bl, K, ep);
   VNT_LAUNCH_CHECK();
 }
 

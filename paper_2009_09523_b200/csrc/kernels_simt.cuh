@@ -329,46 +329,48 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
                                                     int act, int last, float* __restrict__ out,
                                                     float* __restrict__ outT, int ldT,
                                                     const int* __restrict__ tcol) {
-  // One warp per 8 rows: every weight row W[k][:] fetched once serves 8 rows.
-  constexpr int R = 8;
+  // One warp per row; lane l owns k in {4l + 128i, ..., 4l + 128i + 3} (float4
+  // loads), then a fixed xor tree: each output depends only on its row.
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int r0 = warp * R;
-  if (r0 >= rows) return;
-  float acc[R][NO];
+  if (warp >= rows) return;
+  const float* x = X + (size_t)warp * K;
+  float acc[NO];
 #pragma unroll
-  for (int i = 0; i < R; ++i)
+  for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+  const bool vec = (K % 4) == 0;
+  for (int k0 = 4 * lane; k0 < K; k0 += 128) {
+    float a[4];
+    if (vec && k0 + 3 < K) {
+      const float4 a4 = __ldg(reinterpret_cast<const float4*>(x + k0));
+      a[0] = a4.x; a[1] = a4.y; a[2] = a4.z; a[3] = a4.w;
+    } else {
 #pragma unroll
-    for (int o = 0; o < NO; ++o) acc[i][o] = 0.f;
-  for (int k = lane; k < K; k += 32) {
-    float w[NO];
+      for (int u = 0; u < 4; ++u) a[u] = (k0 + u < K) ? x[k0 + u] : 0.f;
+    }
 #pragma unroll
-    for (int o = 0; o < NO; ++o) w[o] = (o < no) ? __ldg(W + (size_t)k * no + o) : 0.f;
+    for (int u = 0; u < 4; ++u) {
+      if (k0 + u >= K) break;
+      const float* w = W + (size_t)(k0 + u) * no;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const float a = (r0 + i < rows) ? __ldg(X + (size_t)(r0 + i) * K + k) : 0.f;
-#pragma unroll
-      for (int o = 0; o < NO; ++o) acc[i][o] = fmaf(a, w[o], acc[i][o]);
+      for (int o = 0; o < NO; ++o)
+        if (o < no) acc[o] = fmaf(a[u], __ldg(w + o), acc[o]);
     }
   }
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
+  for (int o = 0; o < NO; ++o) {
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
+    for (int s = 16; s; s >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], s);
+  }
+  if (lane < no) {
+    float v = 0.f;
 #pragma unroll
-      for (int s = 16; s; s >>= 1) acc[i][o] += __shfl_xor_sync(0xffffffffu, acc[i][o], s);
-    }
-    const int r = r0 + i;
-    if (r < rows && lane < no) {
-      float v = 0.f;
-#pragma unroll
-      for (int o = 0; o < NO; ++o)
-        if (o == lane) v = acc[i][o];
-      v += bias[lane];
-      if (!last) v = act_fwd(act, v);
-      out[(size_t)r * no + lane] = v;
-      if (!last) outT[(size_t)lane * ldT + tcol[r]] = v;
-    }
+    for (int o = 0; o < NO; ++o)
+      if (o == lane) v = acc[o];
+    v += bias[lane];
+    if (!last) v = act_fwd(act, v);
+    out[(size_t)warp * no + lane] = v;
+    if (!last) outT[(size_t)lane * ldT + tcol[warp]] = v;
   }
 }
 
@@ -392,8 +394,8 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
   float w[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) w[o] = (i < in && o < no) ? W[(size_t)i * no + o] : 0.f;
-  for (int chunk = 0; chunk < 4; ++chunk) {
-    const int r0 = (blockIdx.y * 4 + chunk) * 32;
+  for (int chunk = 0; chunk < 1; ++chunk) {
+    const int r0 = (blockIdx.y + chunk) * 32;
     if (r0 >= rows) break;
     __syncthreads();
     for (int k = ty * 32 + tx; k < 32 * NO; k += 256) {
@@ -623,6 +625,35 @@ __global__ void k_refresh_vec(const double* __restrict__ w64, float* __restrict_
 }  // namespace vntb
 
 namespace vntb {
+// 3xTF32 operand split: hi = rna_tf32(x) (cvt.rna.tf32.f32), lo = x - hi (exact).
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void k_split(const float* __restrict__ x, float* __restrict__ hi,
+                        float* __restrict__ lo, size_t n) {
+  const size_t n4 = n / 4;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n4;
+       k += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(x)[k];
+    float4 h, l;
+    h.x = tf32_rna(v.x); l.x = v.x - h.x;
+    h.y = tf32_rna(v.y); l.y = v.y - h.y;
+    h.z = tf32_rna(v.z); l.z = v.z - h.z;
+    h.w = tf32_rna(v.w); l.w = v.w - h.w;
+    reinterpret_cast<float4*>(hi)[k] = h;
+    reinterpret_cast<float4*>(lo)[k] = l;
+  }
+  for (size_t k = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+       k += (size_t)gridDim.x * blockDim.x) {
+    const float h = tf32_rna(x[k]);
+    hi[k] = h;
+    lo[k] = x[k] - h;
+  }
+}
+
 // sync_gradients export: mean = double(S) * 2^-s * (1/B) (virtual_exec.cpp:162-166).
 __global__ void k_mean_grad(const long long* __restrict__ G, double* __restrict__ out, size_t n,
                             double inv_scale, double inv_b) {

@@ -90,3 +90,42 @@ def test_tc_trajectory_vs_reference(port):
     print(f"tf32 wide_small: max rel loss dev {rel.max():.2e}, max |dw| {dw:.2e}")
     assert rel.max() < 1e-3
     assert dw < 1e-4
+
+
+@pytest.mark.parametrize("sizes", [[64, 64, 64, 64], [24, 40, 7, 57, 128]])
+def test_3xtf32_gradient_is_fp32_grade(port, sizes):
+    """3xTF32 (hi*hi + hi*lo + lo*hi): the tensor-core path meets the fp32 tier."""
+    w = [256, 512, 384, 10]
+    B = sum(sizes)
+    x, y = port.synth_batch(3, 4096, w[0], w[-1], 0, B)
+    p0 = port.init_params(w, 1)
+    want, want_loss = port.forward_backward(w, "relu", "softmax-cross-entropy", p0, x, y)
+    e = engine(w, "relu", "softmax-cross-entropy", port, gemm_mode="3xtf32")
+    g, loss = synced_grad(e, x, y, sizes)
+    err = np.abs(g - want).max() / np.abs(want).max()
+    print(f"3xtf32 sizes {sizes}: rel grad err {err:.2e}, loss {loss:.9f} vs {want_loss:.9f}")
+    assert err < 2e-5
+    assert abs(loss - want_loss) < 2e-6 * abs(want_loss)
+
+
+def test_3xtf32_trajectory_and_bitwise(port):
+    z = np.load(GOLDEN / "ref_wide_small.npz")
+    c = json.loads(str(z["config"]))
+    finals = []
+    for rr, G in ((0, 1), (192, 2), (64, 3)):
+        e = engine(c["widths"], c["act"], c["loss"], port, seed=c["seed"], gemm_mode="3xtf32",
+                   n_devices=G, resident_rows=rr)
+        sizes, dev = vnt().uniform_mapping(c["B"], c["V"], G)
+        losses = []
+        for s in range(c["steps"]):
+            x, y = port.synth_batch(c["data_seed"], c["dataset_size"], c["widths"][0],
+                                    c["widths"][-1], s * c["B"], c["B"])
+            losses.append(e.train_step(x, y, sizes, dev, c["lr"])[0])
+        finals.append((e.get_params(), np.array(losses)))
+    rel = np.abs(finals[0][1] - z["losses"]) / np.abs(z["losses"])
+    dw = np.abs(finals[0][0] - z["params"]).max()
+    print(f"3xtf32 wide_small: max rel loss dev {rel.max():.2e}, max |dw| {dw:.2e}")
+    assert rel.max() < 2e-5
+    assert dw < 2e-5
+    for p, l in finals[1:]:
+        assert np.array_equal(p, finals[0][0]) and np.array_equal(l, finals[0][1])
