@@ -55,7 +55,7 @@ extern "C" {
 
 /* GEMM arithmetic for the dense layers.  Selection depends on layer widths
  * only (never on rows), so it is identical on every rank. */
-#define VNT_GEMM_AUTO 0        /* tcgen05 kind::tf32 for wide layers, FFMA fp32 otherwise */
+#define VNT_GEMM_AUTO 0        /* = VNT_GEMM_3XTF32 for wide layers, FFMA fp32 otherwise    */
 #define VNT_GEMM_FFMA 1        /* fp32 FFMA everywhere (exact fp32 products)          */
 #define VNT_GEMM_TF32 2        /* tcgen05 kind::tf32, 1 pass                         */
 #define VNT_GEMM_3XTF32 3      /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi          */

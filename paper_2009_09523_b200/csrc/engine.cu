@@ -876,7 +876,7 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     VNT_CUDA(cudaMemset(e->w32, 0, e->P * sizeof(float)));
     e->wt32 = (float*)dalloc(toff * sizeof(float));
     VNT_CUDA(cudaMemset(e->wt32, 0, toff * sizeof(float)));
-    e->split = e->opt.gemm_mode == VNT_GEMM_3XTF32;
+    e->split = e->opt.gemm_mode == VNT_GEMM_3XTF32 || e->opt.gemm_mode == VNT_GEMM_AUTO;
     if (e->split) {
       e->w32h = (float*)dalloc(e->P * sizeof(float));
       e->w32l = (float*)dalloc(e->P * sizeof(float));
