@@ -473,7 +473,7 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
       e->launches++;
     }
     prof_end(e, 2.0 * rows * (double)K * N);
-    if (!last) {
+    if (!last && !e->tc_layer[l]) {   // tcgen05 epilogues write the twins themselves
       split_into(e, e->X[l + 1], e->Xh[l + 1], e->Xl[l + 1], p.rows * (uint64_t)N);
       split_into(e, e->XT[l + 1], e->XTh[l + 1], e->XTl[l + 1], (uint64_t)N * p.ldT);
     }
@@ -540,8 +540,10 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
         e->launches++;
       }
       prof_end(e, 2.0 * rows * (double)in_l * out_l);
-      split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l);
-      split_into(e, e->DT[l], e->DTh[l], e->DTl[l], (uint64_t)in_l * p.ldT);
+      if (!e->tc_layer[l]) {
+        split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l);
+        split_into(e, e->DT[l], e->DTh[l], e->DTl[l], (uint64_t)in_l * p.ldT);
+      }
     }
   }
 }
@@ -616,6 +618,12 @@ void launch_sgd(vnt_engine* e, double lr, uint64_t examples) {
       a.G = e->G + off;
       a.w32 = e->w32 + off;
       a.wt32 = part ? nullptr : e->wt32 + e->wtoff[l];
+      if (e->split) {
+        a.w32h = e->w32h + off;
+        a.w32l = e->w32l + off;
+        a.wt32h = part ? nullptr : e->wt32h + e->wtoff[l];
+        a.wt32l = part ? nullptr : e->wt32l + e->wtoff[l];
+      }
       a.gout = e->gout ? e->gout + off : nullptr;
       a.gmax = e->gmax + t;
       a.tail = e->G + e->P;
@@ -638,7 +646,6 @@ void launch_sgd(vnt_engine* e, double lr, uint64_t examples) {
       e->launches++;
     }
   }
-  split_weights(e);
 }
 
 struct Readback {

@@ -62,6 +62,8 @@ struct EpiArgs {
   const float* Xprev;
   int ldx;
   float tscale;        // scale applied to the feature-major copy (DT: 2^s of the next dW)
+  // 3xTF32 operand twins of out / outT for the next tcgen05 consumer (or nullptr)
+  float *outh, *outl, *outTh, *outTl;
   // dW
   long long* G;
   int ldg;
@@ -347,7 +349,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (nb + j < ep.N) ep.outT[(size_t)(nb + j) * ep.ldT + tc] = v[j] * ep.tscale;
+              if (nb + j < ep.N) {
+                const size_t o = (size_t)(nb + j) * ep.ldT + tc;
+                const float t = v[j] * ep.tscale;
+                ep.outT[o] = t;
+                if (ep.outTh) {
+                  const float th = tf32_rna(t);
+                  ep.outTh[o] = th;
+                  ep.outTl[o] = t - th;
+                }
+              }
             float* orow = ep.out + (size_t)r * ep.ldo + nb;
             if (nb + 32 <= ep.N) {
 #pragma unroll
@@ -355,6 +366,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             } else {
               for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+            }
+            if (ep.outh) {
+              const size_t o = (size_t)r * ep.ldo + nb;
+              for (int j = 0; j < 32 && nb + j < ep.N; j += 4) {
+                float4 hv, lv;
+                hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
+                hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
+                hv.z = tf32_rna(v[j + 2]); lv.z = v[j + 2] - hv.z;
+                hv.w = tf32_rna(v[j + 3]); lv.w = v[j + 3] - hv.w;
+                *reinterpret_cast<float4*>(ep.outh + o + j) = hv;
+                *reinterpret_cast<float4*>(ep.outl + o + j) = lv;
+              }
             }
           }
         }
@@ -536,6 +559,11 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   ep.ldT = ldT;
   ep.tcol = tcol;
   ep.tscale = 1.f;
+  // twins are allocated only when the consuming layer l+1 runs on tcgen05 in 3xTF32
+  ep.outh = e->Xh[l + 1];
+  ep.outl = e->Xl[l + 1];
+  ep.outTh = e->XTh[l + 1];
+  ep.outTl = e->XTl[l + 1];
   tc_launch<kTcFwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
@@ -559,6 +587,10 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol, 
   ep.Xprev = e->X[l];
   ep.ldx = N;
   ep.tscale = tscale;
+  ep.outh = e->Dh[l];
+  ep.outl = e->Dl[l];
+  ep.outTh = e->DTh[l];
+  ep.outTl = e->DTl[l];
   tc_launch<kTcBwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 

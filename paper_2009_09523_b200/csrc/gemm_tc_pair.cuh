@@ -236,7 +236,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (nb + j < ep.N) ep.outT[(size_t)(nb + j) * ep.ldT + tc] = v[j] * ep.tscale;
+            if (nb + j < ep.N) {
+              const size_t o = (size_t)(nb + j) * ep.ldT + tc;
+              const float t = v[j] * ep.tscale;
+              ep.outT[o] = t;
+              if (ep.outTh) {
+                const float th = tf32_rna(t);
+                ep.outTh[o] = th;
+                ep.outTl[o] = t - th;
+              }
+            }
           float* orow = ep.out + (size_t)r * ep.ldo + nb;
           if (nb + 32 <= ep.N) {
 #pragma unroll
@@ -244,6 +253,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
             for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+          }
+          if (ep.outh) {
+            const size_t o = (size_t)r * ep.ldo + nb;
+            for (int j = 0; j < 32 && nb + j < ep.N; j += 4) {
+              float4 hv, lv;
+              hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
+              hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
+              hv.z = tf32_rna(v[j + 2]); lv.z = v[j + 2] - hv.z;
+              hv.w = tf32_rna(v[j + 3]); lv.w = v[j + 3] - hv.w;
+              *reinterpret_cast<float4*>(ep.outh + o + j) = hv;
+              *reinterpret_cast<float4*>(ep.outl + o + j) = lv;
+            }
           }
         }
       }

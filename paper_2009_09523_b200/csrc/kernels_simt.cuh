@@ -14,6 +14,13 @@
 
 namespace vntb {
 
+// 3xTF32 operand split: hi = rna_tf32(x) (cvt.rna.tf32.f32), lo = x - hi (exact).
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 // Tail slots of the int64 accumulator (all summed exactly by the collective).
 enum : int { kTailLoss = 0, kTailExamples = 1, kTailNonfinite = 2, kTailOverflow = 3 };
 
@@ -329,8 +336,8 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
                                                     int act, int last, float* __restrict__ out,
                                                     float* __restrict__ outT, int ldT,
                                                     const int* __restrict__ tcol) {
-  // One warp per row; lane l owns k in {4l + 128i, ..., 4l + 128i + 3} (float4
-  // loads), then a fixed xor tree: each output depends only on its row.
+  // One warp per row, lane-strided k, then a fixed xor tree: each output
+  // depends only on its row.
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -338,24 +345,12 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
   float acc[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) acc[o] = 0.f;
-  const bool vec = (K % 4) == 0;
-  for (int k0 = 4 * lane; k0 < K; k0 += 128) {
-    float a[4];
-    if (vec && k0 + 3 < K) {
-      const float4 a4 = __ldg(reinterpret_cast<const float4*>(x + k0));
-      a[0] = a4.x; a[1] = a4.y; a[2] = a4.z; a[3] = a4.w;
-    } else {
+  for (int k = lane; k < K; k += 32) {
+    const float a = x[k];
+    const float* w = W + (size_t)k * no;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = (k0 + u < K) ? x[k0 + u] : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (k0 + u >= K) break;
-      const float* w = W + (size_t)(k0 + u) * no;
-#pragma unroll
-      for (int o = 0; o < NO; ++o)
-        if (o < no) acc[o] = fmaf(a[u], __ldg(w + o), acc[o]);
-    }
+    for (int o = 0; o < NO; ++o)
+      if (o < no) acc[o] = fmaf(a, __ldg(w + o), acc[o]);
   }
 #pragma unroll
   for (int o = 0; o < NO; ++o) {
@@ -475,6 +470,8 @@ struct SgdArgs {
   const long long* G;   // exact gradient sum (same layout as params)
   float* w32;
   float* wt32;          // transposed copy (weights only) or nullptr
+  float *w32h, *w32l;   // 3xTF32 twins of w32 (or nullptr)
+  float *wt32h, *wt32l; // 3xTF32 twins of wt32 (or nullptr)
   double* gout;         // optional mean-gradient export
   unsigned long long* gmax;  // max |g| of this tensor (bit pattern of a positive double)
   const long long* tail;
@@ -556,6 +553,11 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
       a.w64[idx] = wn;
       if (a.v64) a.v64[idx] = u;
       a.w32[idx] = w32;
+      if (a.w32h) {
+        const float h = tf32_rna(w32);
+        a.w32h[idx] = h;
+        a.w32l[idx] = w32 - h;
+      }
       if (a.gout) a.gout[idx] = g;
       mx = fmax(mx, fabs(g));
     }
@@ -572,7 +574,16 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int r = r0 + h * 32 + tx;
-      if (r < a.rows) a.wt32[(size_t)col * a.rows + r] = tile[h * 32 + tx][cc];
+      if (r < a.rows) {
+        const float v = tile[h * 32 + tx][cc];
+        const size_t o = (size_t)col * a.rows + r;
+        a.wt32[o] = v;
+        if (a.wt32h) {
+          const float hv = tf32_rna(v);
+          a.wt32h[o] = hv;
+          a.wt32l[o] = v - hv;
+        }
+      }
     }
   }
 }
@@ -589,6 +600,11 @@ __global__ void k_sgd_vec(SgdArgs a) {
     float w32;
     mx = fmax(mx, sgd_one(a, k, w32));
     a.w32[k] = w32;
+    if (a.w32h) {
+      const float h = tf32_rna(w32);
+      a.w32h[k] = h;
+      a.w32l[k] = w32 - h;
+    }
   }
   block_max_to(a.gmax, mx);
 }
@@ -625,13 +641,6 @@ __global__ void k_refresh_vec(const double* __restrict__ w64, float* __restrict_
 }  // namespace vntb
 
 namespace vntb {
-// 3xTF32 operand split: hi = rna_tf32(x) (cvt.rna.tf32.f32), lo = x - hi (exact).
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
 __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi,
                         float* __restrict__ lo, size_t n) {
   const size_t n4 = n / 4;
