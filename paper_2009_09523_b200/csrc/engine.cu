@@ -371,12 +371,22 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
   ensure_capacity(e, p.rows, p.ldT, nn);
   cudaStream_t s = e->stream;
   const cudaMemcpyKind kind = x_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  // Batch::slice copies (data.cpp:36-48): each node's contiguous rows.
-  for (const auto& pn : p.nodes) {
-    VNT_CUDA(cudaMemcpyAsync(e->xin + pn.prow * in, x + pn.src_row * in,
-                             pn.rows * in * sizeof(double), kind, s));
-    VNT_CUDA(cudaMemcpyAsync(e->yin + pn.prow * out, y + pn.src_row * out,
-                             pn.rows * out * sizeof(double), kind, s));
+  // Batch::slice copies (data.cpp:36-48): each node's contiguous rows; runs of
+  // nodes adjacent both in the source batch and in the pass move as one copy.
+  for (size_t k = 0; k < p.nodes.size();) {
+    const auto& first = p.nodes[k];
+    uint64_t nrow = first.rows;
+    size_t j = k + 1;
+    while (j < p.nodes.size() && p.nodes[j].src_row == first.src_row + nrow &&
+           p.nodes[j].prow == first.prow + nrow) {
+      nrow += p.nodes[j].rows;
+      ++j;
+    }
+    VNT_CUDA(cudaMemcpyAsync(e->xin + first.prow * in, x + first.src_row * in,
+                             nrow * in * sizeof(double), kind, s));
+    VNT_CUDA(cudaMemcpyAsync(e->yin + first.prow * out, y + first.src_row * out,
+                             nrow * out * sizeof(double), kind, s));
+    k = j;
   }
   // The tcgen05 dW reads each node's columns padded to 32: keep the padding zero
   // (a previous pass with another layout may have written there).
