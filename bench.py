@@ -377,6 +377,14 @@ def run_ours(args, work):
             "algorithmic_flops_per_step": flops_step,
             "gemm_launches_per_step": gemm_n / args.steps,
         }
+        # DRAM bytes per GEMM launch from the committed `ncu --set full` capture of
+        # this workload and mode (profiles/), next to the algorithmic operand bytes.
+        prof = ROOT / "profiles" / "r01_ncu_gemm_3xtf32.json"
+        if prof.exists() and args.workload == "cfg3" and args.gemm_mode in ("auto", "3xtf32"):
+            pj = json.loads(prof.read_text())
+            line["roofline"]["traffic"] = pj["mean_dram_bytes_per_gemm_launch"]
+            line["roofline"]["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write)"
+            line["roofline"]["traffic_source"] = str(prof.relative_to(ROOT))
     eng.close()
     if args.gemm_mode == "auto" and not args.no_extra and "roofline" in line:
         # Secondary: the same step with 1-pass TF32 GEMMs (TF32-grade tolerance,
