@@ -1,0 +1,113 @@
+"""BASELINE.json configurations at full size, checked through size-independent
+properties (the fp64 oracle cannot run them: its exact accumulator alone needs
+30 GB per device at cfg3):
+
+* mapping invariance — bit-identical parameters and losses for any logical
+  device count and any resident-row budget (pass grouping) at cfg3 and cfg4;
+* sanity of the trajectory — finite loss starting near ln(10) and decreasing;
+* cfg5 — elastic resize 8 -> 4 -> 8 through the drop-in Trainer leaves the
+  trajectory bitwise unchanged at the cfg2 shape.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+WIDE = [784, 4096, 4096, 4096, 4096, 10]
+
+
+def _batches(B, n, seed=11):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    T = torch.randn(784, 10, device="cuda", dtype=torch.float64, generator=g) / 28.0
+    out = []
+    for _ in range(n):
+        x = torch.randn(B, 784, device="cuda", dtype=torch.float64, generator=g)
+        out.append((x, torch.softmax(x @ T, dim=1)))
+    return out
+
+
+def _params(seed=1):
+    r = np.random.default_rng(seed)
+    ps = []
+    for i in range(len(WIDE) - 1):
+        ps.append(r.standard_normal(WIDE[i] * WIDE[i + 1]) / np.sqrt(WIDE[i]))
+        ps.append(np.zeros(WIDE[i + 1]))
+    return np.concatenate(ps)
+
+
+def _run(B, V, G, rr, steps, batches, mode="auto", capacity=1 << 20):
+    import paper_2009_09523_b200 as vnt
+    e = vnt.Engine(WIDE, "relu", "softmax-cross-entropy", gemm_mode=mode, resident_rows=rr)
+    for _ in range(G):
+        e.add_device(capacity)
+    e.set_params(_params())
+    sizes, dev = vnt.uniform_mapping(B, V, G, capacity)
+    losses = []
+    for s in range(steps):
+        x, y = batches[s % len(batches)]
+        losses.append(e.train_step_ptr(x.data_ptr(), y.data_ptr(), B, sizes, dev, 0.01,
+                                       resident=True))
+    p = e.get_params()
+    e.close()
+    return p, np.array(losses)
+
+
+@pytest.mark.parametrize("mode", ["auto", "tf32"])
+def test_cfg3_fullsize_invariance(mode):
+    B, V = 8192, 64
+    batches = _batches(B, 2)
+    ref_p, ref_l = _run(B, V, 1, 0, 3, batches, mode)
+    assert np.all(np.isfinite(ref_l)) and abs(ref_l[0] - np.log(10)) < 0.5
+    assert ref_l[-1] < ref_l[0]
+    for G, rr in ((8, 0), (4, 2048), (3, 1280)):
+        p, l = _run(B, V, G, rr, 3, batches, mode)
+        assert np.array_equal(l, ref_l), (G, rr)
+        assert np.array_equal(p, ref_p), (G, rr)
+
+
+def test_cfg4_fullsize_memory_bounded_passes():
+    """cfg4: B = 65536, V = 256, memory_capacity 256 per node; one pass per 16 nodes
+    vs all nodes resident — identical bits."""
+    B, V = 65536, 256
+    batches = _batches(B, 1)
+    a_p, a_l = _run(B, V, 1, 0, 1, batches, capacity=256)
+    b_p, b_l = _run(B, V, 8, 4096, 1, batches, capacity=256)
+    assert np.array_equal(a_l, b_l) and np.array_equal(a_p, b_p)
+    assert np.isfinite(a_l).all()
+
+
+def test_cfg5_resize_8_4_8_transparent():
+    """config 5 shape: cfg2 ([784,16,10], B=256, V=16) with resize 8->4 at step 10 and
+    4->8 at step 20 over 30 steps, through the drop-in Trainer (vnt_trainer.h)."""
+    import paper_2009_09523_b200 as vnt
+    from test_dropin import _Cfg, _devs, _host
+    lib = _host()
+    w = [784, 16, 10]
+    wa = (C.c_uint64 * 3)(*w)
+
+    def run(schedule):
+        devs = _devs(8)
+        cfg = _Cfg(wa, 3, 1, 1, 11, 256, 16, 0.05, 11, 60000, 0, 0, devs, 8, 0, 0, 0, 0.0)
+        h = C.c_void_p()
+        assert lib.vnt_trainer_create(C.byref(cfg), C.byref(h)) == 0
+        lo = C.c_double()
+        losses = []
+        for s in range(30):
+            if s in schedule:
+                k = schedule[s]
+                assert lib.vnt_trainer_resize(h, _devs(k), k) == 0
+            assert lib.vnt_trainer_step(h, C.byref(lo), None, 0) == 0
+            losses.append(lo.value)
+        P = vnt.param_count(w)
+        p = np.empty(P)
+        assert lib.vnt_trainer_params(h, p.ctypes.data_as(C.POINTER(C.c_double)), P) == 0
+        lib.vnt_trainer_destroy(h)
+        return p, losses
+
+    p0, l0 = run({})
+    p1, l1 = run({10: 4, 20: 8})
+    assert l0 == l1
+    assert np.array_equal(p0, p1)
