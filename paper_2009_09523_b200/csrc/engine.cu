@@ -120,6 +120,20 @@ struct vnt_engine {
   bool synced = false;
   uint64_t total_nodes_hint = 0;
 
+  // per-step kernel parameters (device copy read by kernels, pinned staging)
+  StepParams* d_sp = nullptr;
+  StepParams* h_sp = nullptr;
+  // CUDA-graph replay of single-pass steps (VNT_GRAPHS=0 disables)
+  struct GraphEntry {
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+    uint32_t launches = 0;
+    size_t prof_n = 0;
+    std::vector<double> prof_flops;
+  };
+  bool graphs = true;
+  std::map<std::vector<int64_t>, GraphEntry> graph_cache;
+
   vnt_step_timings timings{};
   cudaEvent_t ev[6] = {};
   // Per-GEMM-launch device timing (CUDA events on the engine stream).
@@ -184,6 +198,32 @@ uint32_t ntensors(const vnt_engine* e) { return 2u * e->L; }
 
 float pow2f(int s) { return std::ldexp(1.0f, s); }
 
+const float* sp_scale(vnt_engine* e, int t) { return &e->d_sp->scale[t]; }
+// DT[l] is consumed by the dW of layer l-1; tcgen05 dW expects it pre-scaled by 2^s.
+const float* dts_ptr(vnt_engine* e, int l) {
+  return e->tc_layer[l - 1] ? &e->d_sp->dts[l] : nullptr;
+}
+
+void drop_graphs(vnt_engine* e) {
+  for (auto& kv : e->graph_cache)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  e->graph_cache.clear();
+}
+
+// Stage this step's kernel parameters (scales, 1/B, lr, momentum) for the device.
+void upload_step_params(vnt_engine* e, double lr, double inv_b) {
+  StepParams& h = *e->h_sp;
+  for (uint32_t t = 0; t < ntensors(e); ++t) {
+    h.scale[t] = pow2f(e->scales[t]);
+    h.inv_scale[t] = std::ldexp(1.0, -e->scales[t]);
+  }
+  for (int l = 1; l <= e->L; ++l) h.dts[l] = e->tc_layer[l - 1] ? pow2f(e->scales[2 * (l - 1)]) : 1.f;
+  h.lr = lr;
+  h.mu = e->opt.momentum;
+  h.inv_b = inv_b;
+  VNT_CUDA(cudaMemcpyAsync(e->d_sp, e->h_sp, sizeof(StepParams), cudaMemcpyHostToDevice, e->stream));
+}
+
 int initial_scale(uint64_t batch) {
   // No gradient history: assume max |mean grad| ~ 1.
   return kScaleTargetBits - (int)std::ceil(std::log2((double)std::max<uint64_t>(batch, 1)));
@@ -196,6 +236,7 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
   ldT = std::max(ldT, e->cap_ldT);
   vns = std::max(vns, e->cap_vns);
   VNT_CUDA(cudaStreamSynchronize(e->stream));
+  drop_graphs(e);
   auto fre = [](auto*& p) {
     if (p) cudaFree(p);
     p = nullptr;
@@ -252,6 +293,7 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
 void ensure_combine(vnt_engine* e, size_t n) {
   if (n <= e->combine_cap) return;
   VNT_CUDA(cudaStreamSynchronize(e->stream));
+  drop_graphs(e);
   if (e->d_combine) cudaFree(e->d_combine);
   if (e->h_combine) cudaFreeHost(e->h_combine);
   n = std::max<size_t>(n, 64);
@@ -346,7 +388,7 @@ template <int NO>
 struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
                   int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
-                  float tscale) {
+                  const float* tscale) {
     dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
     k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
                                             tscale);
@@ -355,20 +397,52 @@ struct BwdSkinny {
 template <int NO>
 struct DwSkinny {
   static void run(cudaStream_t s, const float* X, int in, const float* Dn, int no, const int* row0,
-                  const int* nrows, int nn, float scale, float lim, long long* G, long long* tail,
-                  int tensor) {
+                  const int* nrows, int nn, const float* scale, float lim, long long* G,
+                  long long* tail, int tensor) {
     dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
     k_dw_skinny<NO><<<grid, 128, 0, s>>>(X, in, Dn, no, row0, nrows, scale, lim, G, tail, tensor);
   }
 };
 
 // ---------------------------------------------------------------- one pass
-void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bool x_on_device,
-              bool do_stats, bool first_write) {
-  const int L = e->L;
-  const uint64_t in = e->widths[0], out = e->widths[L];
-  const size_t nn = p.nodes.size();
-  ensure_capacity(e, p.rows, p.ldT, nn);
+// Host side of observe_batch/combine for one pass: advances the device counts
+// (double ops of model.cpp:123-139) and stages the per-node combine factors in
+// pinned memory at `off`; the launches read them through a memcpy node.
+struct StatsLaunch {
+  int dev;
+  size_t off;
+  int n;
+};
+
+std::vector<StatsLaunch> prep_stats(vnt_engine* e, const Pass& p, size_t& off) {
+  std::vector<std::vector<CombineStep>> per_dev(e->devs.size());
+  for (size_t k = 0; k < p.nodes.size(); ++k) {
+    auto& d = e->devs[p.nodes[k].dev];
+    const double other = (double)p.nodes[k].rows;
+    CombineStep st{(int)k, 0, 0.0, 0.0};
+    if (d.count == 0) {
+      st.copy = 1;
+      d.count = other;
+    } else {
+      const double n = d.count + other;
+      st.f1 = d.count * other / n;
+      st.f2 = other / n;
+      d.count = n;
+    }
+    per_dev[p.nodes[k].dev].push_back(st);
+  }
+  std::vector<StatsLaunch> out;
+  for (size_t dv = 0; dv < per_dev.size(); ++dv) {
+    if (per_dev[dv].empty()) continue;
+    std::memcpy(e->h_combine + off, per_dev[dv].data(), per_dev[dv].size() * sizeof(CombineStep));
+    out.push_back({(int)dv, off, (int)per_dev[dv].size()});
+    off += per_dev[dv].size();
+  }
+  return out;
+}
+
+void stage_inputs(vnt_engine* e, const Pass& p, const double* x, const double* y, bool x_on_device) {
+  const uint64_t in = e->widths[0], out = e->widths[e->L];
   cudaStream_t s = e->stream;
   const cudaMemcpyKind kind = x_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   // Batch::slice copies (data.cpp:36-48): each node's contiguous rows; runs of
@@ -388,6 +462,15 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
                              nrow * out * sizeof(double), kind, s));
     k = j;
   }
+}
+
+// Device work of one pass (inputs already staged in xin/yin).
+void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats,
+              bool first_write) {
+  const int L = e->L;
+  const uint64_t in = e->widths[0], out = e->widths[L];
+  const size_t nn = p.nodes.size();
+  cudaStream_t s = e->stream;
   // The tcgen05 dW reads each node's columns padded to 32: keep the padding zero
   // (a previous pass with another layout may have written there).
   bool padded = false;
@@ -412,45 +495,21 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
     split_into(e, e->X[0], e->Xh[0], e->Xl[0], p.rows * in);
     split_into(e, e->XT[0], e->XTh[0], e->XTl[0], in * p.ldT);
   }
-  if (do_stats) {
+  if (stats) {
     // observe_batch per node then Chan-combine into the node's device lineage
     // in ascending node id (virtual_exec.cpp:137-138, model.cpp:152-154).
     dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
     k_vn_stats<<<grid, 128, 0, s>>>(e->xin, (int)in, row0, nrows, e->vn_mean, e->vn_m2);
     VNT_LAUNCH_CHECK();
     e->launches++;
-    std::vector<std::vector<CombineStep>> per_dev(e->devs.size());
-    for (size_t k = 0; k < nn; ++k) {
-      auto& d = e->devs[p.nodes[k].dev];
-      const double other = (double)p.nodes[k].rows;
-      CombineStep st{(int)k, 0, 0.0, 0.0};
-      if (d.count == 0) {
-        st.copy = 1;
-        d.count = other;
-      } else {
-        const double n = d.count + other;
-        st.f1 = d.count * other / n;
-        st.f2 = other / n;
-        d.count = n;
-      }
-      per_dev[p.nodes[k].dev].push_back(st);
-    }
-    size_t total = 0;
-    for (auto& v : per_dev) total += v.size();
-    ensure_combine(e, total);
-    size_t off = 0;
-    for (size_t dv = 0; dv < per_dev.size(); ++dv) {
-      if (per_dev[dv].empty()) continue;
-      // The pinned staging is reused only after the step's final sync.
-      std::memcpy(e->h_combine + off, per_dev[dv].data(), per_dev[dv].size() * sizeof(CombineStep));
-      VNT_CUDA(cudaMemcpyAsync(e->d_combine + off, e->h_combine + off,
-                               per_dev[dv].size() * sizeof(CombineStep), cudaMemcpyHostToDevice, s));
+    for (const auto& sl : *stats) {
+      VNT_CUDA(cudaMemcpyAsync(e->d_combine + sl.off, e->h_combine + sl.off,
+                               sl.n * sizeof(CombineStep), cudaMemcpyHostToDevice, s));
       k_stats_combine<<<(unsigned)ceil_div(in, 128), 128, 0, s>>>(
-          e->devs[dv].mean, e->devs[dv].m2, (int)in, e->vn_mean, e->vn_m2, e->d_combine + off,
-          (int)per_dev[dv].size());
+          e->devs[sl.dev].mean, e->devs[sl.dev].m2, (int)in, e->vn_mean, e->vn_m2,
+          e->d_combine + sl.off, sl.n);
       VNT_LAUNCH_CHECK();
       e->launches++;
-      off += per_dev[dv].size();
     }
   }
   // Forward (model.cpp:275-287).
@@ -473,11 +532,11 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
       if (last) {
         k_gemm_ffma<kEpiLogits><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
                                                      e->logits, N, nullptr, 0, nullptr, nullptr, 0,
-                                                     1.f);
+                                                     nullptr);
       } else {
         k_gemm_ffma<kEpiHidden><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
                                                      e->X[l + 1], N, e->XT[l + 1], ldT, tcol,
-                                                     nullptr, 0, 1.f);
+                                                     nullptr, 0, nullptr);
       }
       VNT_LAUNCH_CHECK();
       e->launches++;
@@ -491,7 +550,7 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
   cudaEventRecord(e->ev[1], s);
   // Feature-major delta copies DT[l] feed the dW of layer l-1; for tcgen05
   // layers they carry that dW's 2^s quantisation scale (exact power of two).
-  auto dts = [&](int l) { return e->tc_layer[l - 1] ? pow2f(e->scales[2 * (l - 1)]) : 1.f; };
+  auto dts = [&](int l) { return dts_ptr(e, l); };
   // Loss + output delta (model.cpp:289-315).
   {
     const unsigned warps_per_block = 8;
@@ -513,20 +572,20 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
       tc_weight_grad(e, l, p, col0, nrows, 1.f, lim, first_write, tw);
     } else if (out_l <= 32) {
       dispatch_skinny<DwSkinny>(out_l, s, e->X[l], in_l, e->D[l + 1], out_l, row0, nrows, (int)nn,
-                                pow2f(e->scales[tw]), lim, e->G + e->woff[l], e->G + e->P, tw);
+                                sp_scale(e, tw), lim, e->G + e->woff[l], e->G + e->P, tw);
       VNT_LAUNCH_CHECK();
       e->launches++;
     } else {
       dim3 grid((unsigned)ceil_div(out_l, 64), (unsigned)ceil_div(in_l, 64), (unsigned)nn);
       k_dw_ffma<<<grid, 256, 0, s>>>(e->XT[l], e->DT[l + 1], ldT, in_l, out_l, col0, nrows,
-                                     pow2f(e->scales[tw]), lim, e->G + e->woff[l], e->G + e->P, tw);
+                                     sp_scale(e, tw), lim, e->G + e->woff[l], e->G + e->P, tw);
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
     prof_end(e, 2.0 * rows * (double)in_l * out_l);
     {
       dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
-      k_db<<<grid, 128, 0, s>>>(e->D[l + 1], out_l, row0, nrows, pow2f(e->scales[tb]), lim,
+      k_db<<<grid, 128, 0, s>>>(e->D[l + 1], out_l, row0, nrows, sp_scale(e, tb), lim,
                                 e->G + e->boff[l], e->G + e->P, tb);
       VNT_LAUNCH_CHECK();
       e->launches++;
@@ -558,8 +617,18 @@ void run_pass(vnt_engine* e, const Pass& p, const double* x, const double* y, bo
   }
 }
 
-void begin_round(vnt_engine* e, uint64_t batch_hint) {
-  if (e->round_open) return;
+void begin_round_host(vnt_engine* e, uint64_t batch_hint) {
+  e->acc_examples = 0;
+  e->acc_started = false;
+  e->round_open = true;
+  if (!e->scales_init) {
+    std::fill(e->scales.begin(), e->scales.end(), initial_scale(batch_hint));
+    e->scales_init = true;
+  }
+  for (auto& d : e->devs) d.count_bak = d.count;
+}
+
+void begin_round_device(vnt_engine* e) {
   tail_reset(e);
   // Slices filled by exact int64 atomics start from zero (bias always, weights
   // of non-tcgen05 layers); tcgen05 dW tiles store on the first pass.
@@ -569,19 +638,18 @@ void begin_round(vnt_engine* e, uint64_t batch_hint) {
       VNT_CUDA(cudaMemsetAsync(e->G + e->woff[l], 0, e->widths[l] * e->widths[l + 1] * sizeof(long long),
                                e->stream));
   }
-  e->acc_examples = 0;
-  e->acc_started = false;
-  e->round_open = true;
-  if (!e->scales_init) {
-    std::fill(e->scales.begin(), e->scales.end(), initial_scale(batch_hint));
-    e->scales_init = true;
-  }
   const uint64_t in = e->widths[0];
   for (auto& d : e->devs) {
-    d.count_bak = d.count;
     VNT_CUDA(cudaMemcpyAsync(d.mean_bak, d.mean, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
     VNT_CUDA(cudaMemcpyAsync(d.m2_bak, d.m2, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
   }
+}
+
+void begin_round(vnt_engine* e, uint64_t batch_hint) {
+  if (e->round_open) return;
+  begin_round_host(e, batch_hint);
+  upload_step_params(e, 0.0, 0.0);
+  begin_round_device(e);
 }
 
 // Undo the round's input-statistics updates (a rescaled redo observes again).
@@ -597,8 +665,19 @@ void restore_stats(vnt_engine* e) {
 void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, const double* y,
                 bool on_device, bool do_stats) {
   auto& passes = plan_for(e, local);
-  for (const auto& p : passes) {
-    run_pass(e, p, x, y, on_device, do_stats, !e->acc_started);
+  std::vector<std::vector<StatsLaunch>> stats(passes.size());
+  if (do_stats) {
+    size_t total = 0;
+    for (const auto& p : passes) total += p.nodes.size();
+    ensure_combine(e, total);
+    size_t off = 0;
+    for (size_t i = 0; i < passes.size(); ++i) stats[i] = prep_stats(e, passes[i], off);
+  }
+  for (size_t i = 0; i < passes.size(); ++i) {
+    const auto& p = passes[i];
+    ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
+    stage_inputs(e, p, x, y, on_device);
+    run_pass(e, p, do_stats ? &stats[i] : nullptr, !e->acc_started);
     e->acc_started = true;
     e->acc_examples += p.rows;
   }
@@ -614,10 +693,10 @@ void collective(vnt_engine* e) {
   }
 }
 
-void launch_sgd(vnt_engine* e, double lr, uint64_t examples) {
+// lr, 1/B (virtual_exec.cpp:165), momentum and 2^-s come from the step params.
+void launch_sgd(vnt_engine* e) {
   cudaStream_t s = e->stream;
   VNT_CUDA(cudaMemsetAsync(e->gmax, 0, ntensors(e) * sizeof(unsigned long long), s));
-  const double inv_b = 1.0 / (double)examples;   // virtual_exec.cpp:165
   for (int l = 0; l < e->L; ++l) {
     for (int part = 0; part < 2; ++part) {
       const int t = 2 * l + part;
@@ -638,10 +717,8 @@ void launch_sgd(vnt_engine* e, double lr, uint64_t examples) {
       a.gmax = e->gmax + t;
       a.tail = e->G + e->P;
       a.ntail_flags = (int)ntensors(e);
-      a.inv_scale = std::ldexp(1.0, -e->scales[t]);
-      a.inv_b = inv_b;
-      a.lr = lr;
-      a.mu = e->opt.momentum;
+      a.sp = e->d_sp;
+      a.tensor = t;
       if (part == 0) {
         a.rows = (int)e->widths[l];
         a.cols = (int)e->widths[l + 1];
@@ -665,14 +742,16 @@ struct Readback {
   std::vector<int> overflow;   // tensor ids
 };
 
-Readback read_tail(vnt_engine* e, bool with_gmax) {
+void enqueue_readback(vnt_engine* e, bool with_gmax) {
   cudaStream_t s = e->stream;
   VNT_CUDA(cudaMemcpyAsync(e->h_tail, e->G + e->P, e->ntail * sizeof(long long),
                            cudaMemcpyDeviceToHost, s));
   if (with_gmax)
     VNT_CUDA(cudaMemcpyAsync(e->h_gmax, e->gmax, ntensors(e) * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
-  VNT_CUDA(cudaStreamSynchronize(s));
+}
+
+Readback parse_readback(vnt_engine* e) {
   Readback r;
   r.loss_sum = std::ldexp((double)e->h_tail[kTailLoss], -kLossScaleBits);
   r.examples = (uint64_t)e->h_tail[kTailExamples];
@@ -680,6 +759,12 @@ Readback read_tail(vnt_engine* e, bool with_gmax) {
   for (uint32_t t = 0; t < ntensors(e); ++t)
     if (e->h_tail[kTailOverflow + t]) r.overflow.push_back((int)t);
   return r;
+}
+
+Readback read_tail(vnt_engine* e, bool with_gmax) {
+  enqueue_readback(e, with_gmax);
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  return parse_readback(e);
 }
 
 void update_scales(vnt_engine* e, uint64_t batch) {
@@ -737,27 +822,103 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
   reset_acc(e);
   e->launches = 0;
   uint32_t retries = 0;
+  const double inv_b = 1.0 / (double)batch_rows;   // virtual_exec.cpp:165
   for (int attempt = 0;; ++attempt) {
-    cudaEventRecord(e->ev[0], e->stream);
-    begin_round(e, batch_rows);
-    if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0);
-    k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
-    e->launches++;
-    if (local.empty()) {
-      // This process hosts no node this step: contribute zeros.
-      VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
+    // Device work of the step, in order; recorded once per plan as a CUDA graph.
+    auto enqueue_step = [&](const std::vector<StatsLaunch>* stats) {
+      cudaEventRecord(e->ev[0], e->stream);
+      begin_round_device(e);
+      auto& passes = plan_for(e, local);
+      if (passes.size() == 1) {
+        run_pass(e, passes[0], stats, true);
+        e->acc_started = true;
+        e->acc_examples += passes[0].rows;
+      }
+      k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
+      e->launches++;
+      cudaEventRecord(e->ev[2], e->stream);
+      collective(e);
+      cudaEventRecord(e->ev[3], e->stream);
+      launch_sgd(e);
+      cudaEventRecord(e->ev[4], e->stream);
+      enqueue_readback(e, true);
+    };
+    begin_round_host(e, batch_rows);
+    upload_step_params(e, lr, inv_b);
+    Readback rb;
+    const std::vector<Pass>* passes = local.empty() ? nullptr : &plan_for(e, local);
+    const bool single = passes && passes->size() == 1;
+    if (single && attempt == 0 && e->graphs && e->opt.world_size == 1) {
+      // Graph path: host prep outside, the whole device step as one graph launch.
+      const Pass& p = (*passes)[0];
+      ensure_combine(e, p.nodes.size());
+      ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
+      size_t off = 0;
+      const std::vector<StatsLaunch> stats = prep_stats(e, p, off);
+      stage_inputs(e, p, x, y, on_device);
+      std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1};
+      for (const auto& n : local) {
+        key.push_back(n.node);
+        key.push_back(n.dev);
+        key.push_back((int64_t)n.rows);
+        key.push_back((int64_t)n.src_row);
+      }
+      auto& ge = e->graph_cache[key];
+      if (ge.exec == nullptr && ge.seen == 0) {
+        ge.seen = 1;   // first encounter runs eagerly (allocations, attributes)
+        enqueue_step(&stats);
+      } else {
+        if (ge.exec == nullptr) {
+          const uint32_t l0 = e->launches;
+          const size_t p0 = e->prof_n;
+          cudaGraph_t g;
+          VNT_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+          try {
+            enqueue_step(&stats);
+          } catch (...) {
+            cudaStreamEndCapture(e->stream, &g);
+            throw;
+          }
+          VNT_CUDA(cudaStreamEndCapture(e->stream, &g));
+          VNT_CUDA(cudaGraphInstantiate(&ge.exec, g, 0));
+          cudaGraphDestroy(g);
+          ge.launches = e->launches - l0;
+          ge.prof_n = e->prof_n - p0;
+          ge.prof_flops.assign(e->prof_flops.end() - (long)(ge.prof_n / 2), e->prof_flops.end());
+        } else {
+          e->acc_started = true;
+          e->acc_examples = p.rows;
+          e->launches += ge.launches;
+          e->prof_n = ge.prof_n;
+          e->prof_flops = ge.prof_flops;
+        }
+        VNT_CUDA(cudaGraphLaunch(ge.exec, e->stream));
+      }
+      VNT_CUDA(cudaStreamSynchronize(e->stream));
+      rb = parse_readback(e);
+    } else {
+      cudaEventRecord(e->ev[0], e->stream);
+      begin_round_device(e);
+      if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0);
+      k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
+      e->launches++;
+      if (local.empty()) {
+        // This process hosts no node this step: contribute zeros.
+        VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
+      }
+      cudaEventRecord(e->ev[2], e->stream);
+      collective(e);
+      cudaEventRecord(e->ev[3], e->stream);
+      launch_sgd(e);
+      cudaEventRecord(e->ev[4], e->stream);
+      rb = read_tail(e, true);
     }
-    cudaEventRecord(e->ev[2], e->stream);
-    collective(e);
-    cudaEventRecord(e->ev[3], e->stream);
-    launch_sgd(e, lr, batch_rows);
-    cudaEventRecord(e->ev[4], e->stream);
-    Readback rb = read_tail(e, true);
     if (rb.nonfinite || !rb.overflow.empty()) {
       e->prof_n = 0;
       e->prof_flops.clear();
     }
     if (rb.nonfinite) {
+      restore_stats(e);
       reset_acc(e);
       throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
     }
@@ -906,6 +1067,11 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     VNT_CUDA(cudaMallocHost(&e->h_tail, e->ntail * sizeof(long long)));
     VNT_CUDA(cudaMallocHost(&e->h_gmax, ntensors(e.get()) * sizeof(unsigned long long)));
     e->scales.assign(ntensors(e.get()), 0);
+    if (e->L > vntb::kMaxLayers) throw EngineError(VNT_ERR_CONFIG, "too many layers (max 64)");
+    e->d_sp = (StepParams*)dalloc(sizeof(StepParams));
+    VNT_CUDA(cudaMallocHost(&e->h_sp, sizeof(StepParams)));
+    std::memset(e->h_sp, 0, sizeof(StepParams));
+    e->graphs = !(getenv("VNT_GRAPHS") && getenv("VNT_GRAPHS")[0] == '0');
     tc_init(e.get());
     if (e->opt.world_size > 1) {
       if (!options->nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
@@ -948,6 +1114,9 @@ void vnt_engine_destroy(vnt_engine* e) {
   }
   if (e->h_combine) cudaFreeHost(e->h_combine);
   if (e->h_tail) cudaFreeHost(e->h_tail);
+  if (e->h_sp) cudaFreeHost(e->h_sp);
+  if (e->d_sp) cudaFree(e->d_sp);
+  drop_graphs(e);
   if (e->h_gmax) cudaFreeHost(e->h_gmax);
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
@@ -1004,6 +1173,7 @@ int vnt_engine_add_device(vnt_engine* e, uint64_t capacity, int32_t* out_index) 
     VNT_CUDA(cudaMemset(d.mean, 0, in * sizeof(double)));
     VNT_CUDA(cudaMemset(d.m2, 0, in * sizeof(double)));
     e->devs.push_back(d);
+    drop_graphs(e);
     if (out_index) *out_index = (int32_t)e->devs.size() - 1;
     return VNT_OK;
   });
@@ -1146,7 +1316,8 @@ int vnt_engine_sgd_apply(vnt_engine* e, double lr) {
     if (!(lr > 0.0)) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: learning rate must be positive");
     if (!e->synced) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: call vnt_engine_sync first");
     const uint64_t examples = (uint64_t)e->h_tail[kTailExamples];
-    launch_sgd(e, lr, examples);
+    upload_step_params(e, lr, 1.0 / (double)examples);
+    launch_sgd(e);
     read_tail(e, true);
     update_scales(e, examples);
     reset_acc(e);

@@ -61,7 +61,7 @@ struct EpiArgs {
   const int* tcol;
   const float* Xprev;
   int ldx;
-  float tscale;        // scale applied to the feature-major copy (DT: 2^s of the next dW)
+  const float* tscale_p;  // scale of the feature-major copy (DT: 2^s of the next dW); null = 1
   // 3xTF32 operand twins of out / outT for the next tcgen05 consumer (or nullptr)
   float *outh, *outl, *outTh, *outTl;
   // dW
@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;               // TMEM lane quarter this warp may access
     const int h = (warp - 4) >> 2;        // column half
     const int row = q * 32 + lane;        // tile row == TMEM lane
+    const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
     float amax = 0.f, canary = 0.f;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j)
               if (nb + j < ep.N) {
                 const size_t o = (size_t)(nb + j) * ep.ldT + tc;
-                const float t = v[j] * ep.tscale;
+                const float t = v[j] * tscale;
                 ep.outT[o] = t;
                 if (ep.outTh) {
                   const float th = tf32_rna(t);
@@ -558,7 +559,7 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   ep.outT = e->XT[l + 1];
   ep.ldT = ldT;
   ep.tcol = tcol;
-  ep.tscale = 1.f;
+  ep.tscale_p = nullptr;
   // twins are allocated only when the consuming layer l+1 runs on tcgen05 in 3xTF32
   ep.outh = e->Xh[l + 1];
   ep.outl = e->Xl[l + 1];
@@ -567,7 +568,8 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   tc_launch<kTcFwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
-void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol, float tscale) {
+void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol,
+                      const float* tscale) {
   using namespace vntb::tc;
   const int N = (int)e->widths[l], K = (int)e->widths[l + 1];
   const bool pair = tc_use_pair();
@@ -586,7 +588,7 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol, 
   ep.tcol = tcol;
   ep.Xprev = e->X[l];
   ep.ldx = N;
-  ep.tscale = tscale;
+  ep.tscale_p = tscale;
   ep.outh = e->Dh[l];
   ep.outl = e->Dl[l];
   ep.outTh = e->DTh[l];

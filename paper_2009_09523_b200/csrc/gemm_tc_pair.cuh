@@ -197,6 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int h = (warp - 4) >> 2;
     const int row = q * 32 + lane;
+    const float tscale = ep.tscale_p ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++it) {
       const int m0 = (tile / tiles_n) * PM + (int)rank * BM, n0 = (tile % tiles_n) * BN;
@@ -238,7 +239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j)
             if (nb + j < ep.N) {
               const size_t o = (size_t)(nb + j) * ep.ldT + tc;
-              const float t = v[j] * ep.tscale;
+              const float t = v[j] * tscale;
               ep.outT[o] = t;
               if (ep.outTh) {
                 const float th = tf32_rna(t);

@@ -24,6 +24,17 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // Tail slots of the int64 accumulator (all summed exactly by the collective).
 enum : int { kTailLoss = 0, kTailExamples = 1, kTailNonfinite = 2, kTailOverflow = 3 };
 
+// Per-step values the kernels read from device memory (one small H2D copy per
+// step), so the launch sequence of a step is static and can be replayed as a
+// CUDA graph while the fixed-point scales adapt.
+constexpr int kMaxLayers = 64;
+struct StepParams {
+  float scale[2 * kMaxLayers];       // 2^s_t: per-node partial quantisation multiplier
+  float dts[kMaxLayers + 1];         // DT[l] copy scale (2^s of the dW consuming it, or 1)
+  double inv_scale[2 * kMaxLayers];  // 2^-s_t
+  double lr, mu, inv_b;
+};
+
 // ---------------------------------------------------------------- ingest
 // fp64 rows (reference Batch layout, data.hpp:14-31) -> fp32 X0 and XT0.
 __global__ void k_ingest(const double* __restrict__ x, float* __restrict__ X0,
@@ -118,8 +129,9 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
     const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb, int M, int N,
     int K, const float* __restrict__ bias, int act, float* __restrict__ out, int ldo,
     float* __restrict__ outT, int ldT, const int* __restrict__ tcol,
-    const float* __restrict__ Xprev, int ldx, float tscale) {
+    const float* __restrict__ Xprev, int ldx, const float* __restrict__ tscale_p) {
   __shared__ __align__(16) float As[16][64 + 4];
+  const float tscale = tscale_p ? *tscale_p : 1.f;
   __shared__ __align__(16) float Bs[16][64 + 4];
   const int t = threadIdx.x;
   const int tx = t % 16, ty = t / 16;
@@ -184,7 +196,8 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
 __global__ void k_loss(const float* __restrict__ logits, const double* __restrict__ y, int rows,
                        int outw, int loss_kind, float* __restrict__ D, float* __restrict__ DT,
                        int ldT, const int* __restrict__ tcol, long long* __restrict__ tail,
-                       float tscale) {
+                       const float* __restrict__ tscale_p) {
+  const float tscale = tscale_p ? *tscale_p : 1.f;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -257,9 +270,11 @@ __device__ __forceinline__ long long quantise(float g, float scale, float lim,
 // int64 atomics into the zeroed weight slice of G (order-free).
 __global__ void __launch_bounds__(256) k_dw_ffma(
     const float* __restrict__ XT, const float* __restrict__ DT, int ldT, int in, int out,
-    const int* __restrict__ vn_col0, const int* __restrict__ vn_rows, float scale, float lim,
-    long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
+    const int* __restrict__ vn_col0, const int* __restrict__ vn_rows,
+    const float* __restrict__ scale_p, float lim, long long* __restrict__ G,
+    long long* __restrict__ tail, int tensor) {
   __shared__ __align__(16) float As[16][64 + 4];
+  const float scale = *scale_p;
   __shared__ __align__(16) float Bs[16][64 + 4];
   const int t = threadIdx.x;
   const int tx = t % 16, ty = t / 16;
@@ -313,12 +328,13 @@ __global__ void __launch_bounds__(256) k_dw_ffma(
 // the node's rows, fp32 in row order, quantised per node; one CTA column per
 // node, exact int64 atomics (order-free) into the zeroed bias slice of G.
 __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict__ vn_row0,
-                     const int* __restrict__ vn_rows, float scale, float lim,
+                     const int* __restrict__ vn_rows, const float* __restrict__ scale_p, float lim,
                      long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
   if (o >= out) return;
   const int r0 = vn_row0[v], n = vn_rows[v];
+  const float scale = *scale_p;
   float g = 0.f;
   for (int r = 0; r < n; ++r) g += D[(size_t)(r0 + r) * out + o];
   const long long q = quantise(g, scale, lim, tail, tensor);
@@ -378,8 +394,10 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
                                                     const float* __restrict__ Xprev,
                                                     float* __restrict__ Dout,
                                                     float* __restrict__ DT, int ldT,
-                                                    const int* __restrict__ tcol, float tscale) {
-  // 32 features x 128 rows per block (4 chunks of 32 rows), o ascending per
+                                                    const int* __restrict__ tcol,
+                                                    const float* __restrict__ tscale_p) {
+  const float tscale = tscale_p ? *tscale_p : 1.f;
+  // 32 features x 32 rows per block (4 chunks of 32 rows), o ascending per
   // output; transposed copy through smem.
   __shared__ float tile[32][33];
   __shared__ float dn[32][NO];
@@ -425,9 +443,10 @@ template <int NO>
 __global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __restrict__ Dn,
                             int no,
                             const int* __restrict__ vn_row0, const int* __restrict__ vn_rows,
-                            float scale, float lim, long long* __restrict__ G,
-                            long long* __restrict__ tail, int tensor) {
+                            const float* __restrict__ scale_p, float lim,
+                            long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
   __shared__ float dn[64][NO];
+  const float scale = *scale_p;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
   const int r0 = vn_row0[v], n = vn_rows[v];
@@ -476,9 +495,8 @@ struct SgdArgs {
   unsigned long long* gmax;  // max |g| of this tensor (bit pattern of a positive double)
   const long long* tail;
   int ntail_flags;
-  double inv_scale;     // 2^-s
-  double inv_b;         // 1.0 / B  (virtual_exec.cpp:165)
-  double lr, mu;
+  const StepParams* sp; // 2^-s per tensor, 1/B (virtual_exec.cpp:165), lr, mu
+  int tensor;
   int rows, cols;       // tensor shape (bias: rows = 1)
 };
 
@@ -490,13 +508,13 @@ __device__ __forceinline__ bool step_poisoned(const long long* tail, int nflags)
 }
 
 __device__ __forceinline__ double sgd_one(const SgdArgs& a, size_t k, float& w32) {
-  const double g = __dmul_rn(__ll2double_rn(a.G[k]) * a.inv_scale, a.inv_b);
+  const double g = __dmul_rn(__ll2double_rn(a.G[k]) * a.sp->inv_scale[a.tensor], a.sp->inv_b);
   double u = g;
   if (a.v64) {
-    u = __dadd_rn(__dmul_rn(a.mu, a.v64[k]), g);
+    u = __dadd_rn(__dmul_rn(a.sp->mu, a.v64[k]), g);
     a.v64[k] = u;
   }
-  const double w = __dsub_rn(a.w64[k], __dmul_rn(a.lr, u));
+  const double w = __dsub_rn(a.w64[k], __dmul_rn(a.sp->lr, u));
   a.w64[k] = w;
   w32 = __double2float_rn(w);
   if (a.gout) a.gout[k] = g;
@@ -528,6 +546,8 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
   const int c = c0 + tx;
   long long S[PER];
   double w[PER], v[PER];
+  const double inv_scale = a.sp->inv_scale[a.tensor], inv_b = a.sp->inv_b;
+  const double lr = a.sp->lr, mu = a.sp->mu;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int r = r0 + ty + 8 * k;
@@ -542,10 +562,10 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
   for (int k = 0; k < PER; ++k) {
     const int r = r0 + ty + 8 * k;
     const bool ok = r < a.rows && c < a.cols;
-    const double g = __dmul_rn(__ll2double_rn(S[k]) * a.inv_scale, a.inv_b);
+    const double g = __dmul_rn(__ll2double_rn(S[k]) * inv_scale, inv_b);
     double u = g;
-    if (a.v64) u = __dadd_rn(__dmul_rn(a.mu, v[k]), g);
-    const double wn = __dsub_rn(w[k], __dmul_rn(a.lr, u));
+    if (a.v64) u = __dadd_rn(__dmul_rn(mu, v[k]), g);
+    const double wn = __dsub_rn(w[k], __dmul_rn(lr, u));
     const float w32 = __double2float_rn(wn);
     tile[ty + 8 * k][tx] = ok ? w32 : 0.f;
     if (ok) {
