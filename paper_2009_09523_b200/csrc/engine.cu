@@ -132,6 +132,7 @@ struct vnt_engine {
     std::vector<double> prof_flops;
   };
   bool graphs = true;
+  bool timings_graphed = false;   // last step replayed a graph: only total_ms is timed
   std::map<std::vector<int64_t>, GraphEntry> graph_cache;
 
   vnt_step_timings timings{};
@@ -158,7 +159,7 @@ void prof_begin(vnt_engine* e) {
       e->prof_ev.push_back(ev);
     }
   }
-  VNT_CUDA(cudaEventRecord(e->prof_ev[e->prof_n], e->stream));
+  VNT_CUDA(cudaEventRecord(e->prof_ev[e->prof_n], e->stream));  // prof_begin
 }
 
 void prof_end(vnt_engine* e, double flops) {
@@ -174,7 +175,10 @@ void prof_collect(vnt_engine* e) {
   double ms_total = 0.0, fl = 0.0;
   for (size_t i = 0; i + 1 < e->prof_n; i += 2) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e->prof_ev[i], e->prof_ev[i + 1]);
+    if (cudaEventElapsedTime(&ms, e->prof_ev[i], e->prof_ev[i + 1]) != cudaSuccess) {
+      (void)cudaGetLastError();   // timing unavailable: not an engine error
+      ms = 0.f;
+    }
     ms_total += ms;
   }
   for (double f : e->prof_flops) fl += f;
@@ -547,7 +551,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       split_into(e, e->XT[l + 1], e->XTh[l + 1], e->XTl[l + 1], (uint64_t)N * p.ldT);
     }
   }
-  cudaEventRecord(e->ev[1], s);
+  VNT_CUDA(cudaEventRecord(e->ev[1], s));
   // Feature-major delta copies DT[l] feed the dW of layer l-1; for tcgen05
   // layers they carry that dW's 2^s quantisation scale (exact power of two).
   auto dts = [&](int l) { return dts_ptr(e, l); };
@@ -825,8 +829,8 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
   const double inv_b = 1.0 / (double)batch_rows;   // virtual_exec.cpp:165
   for (int attempt = 0;; ++attempt) {
     // Device work of the step, in order; recorded once per plan as a CUDA graph.
-    auto enqueue_step = [&](const std::vector<StatsLaunch>* stats) {
-      cudaEventRecord(e->ev[0], e->stream);
+    auto enqueue_step = [&](const std::vector<StatsLaunch>* stats, bool events) {
+      if (events) VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
       begin_round_device(e);
       auto& passes = plan_for(e, local);
       if (passes.size() == 1) {
@@ -836,13 +840,14 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       }
       k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
       e->launches++;
-      cudaEventRecord(e->ev[2], e->stream);
+      if (events) VNT_CUDA(cudaEventRecord(e->ev[2], e->stream));
       collective(e);
-      cudaEventRecord(e->ev[3], e->stream);
+      if (events) VNT_CUDA(cudaEventRecord(e->ev[3], e->stream));
       launch_sgd(e);
-      cudaEventRecord(e->ev[4], e->stream);
+      if (events) VNT_CUDA(cudaEventRecord(e->ev[4], e->stream));
       enqueue_readback(e, true);
     };
+    bool graphed = false;
     begin_round_host(e, batch_rows);
     upload_step_params(e, lr, inv_b);
     Readback rb;
@@ -866,7 +871,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       auto& ge = e->graph_cache[key];
       if (ge.exec == nullptr && ge.seen == 0) {
         ge.seen = 1;   // first encounter runs eagerly (allocations, attributes)
-        enqueue_step(&stats);
+        enqueue_step(&stats, true);
       } else {
         if (ge.exec == nullptr) {
           const uint32_t l0 = e->launches;
@@ -874,7 +879,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
           cudaGraph_t g;
           VNT_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
           try {
-            enqueue_step(&stats);
+            enqueue_step(&stats, false);
           } catch (...) {
             cudaStreamEndCapture(e->stream, &g);
             throw;
@@ -892,12 +897,15 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
           e->prof_n = ge.prof_n;
           e->prof_flops = ge.prof_flops;
         }
+        VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
         VNT_CUDA(cudaGraphLaunch(ge.exec, e->stream));
+        VNT_CUDA(cudaEventRecord(e->ev[4], e->stream));
+        graphed = true;
       }
       VNT_CUDA(cudaStreamSynchronize(e->stream));
       rb = parse_readback(e);
     } else {
-      cudaEventRecord(e->ev[0], e->stream);
+      VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
       begin_round_device(e);
       if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0);
       k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
@@ -906,11 +914,11 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
         // This process hosts no node this step: contribute zeros.
         VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
       }
-      cudaEventRecord(e->ev[2], e->stream);
+      VNT_CUDA(cudaEventRecord(e->ev[2], e->stream));
       collective(e);
-      cudaEventRecord(e->ev[3], e->stream);
+      VNT_CUDA(cudaEventRecord(e->ev[3], e->stream));
       launch_sgd(e);
-      cudaEventRecord(e->ev[4], e->stream);
+      VNT_CUDA(cudaEventRecord(e->ev[4], e->stream));
       rb = read_tail(e, true);
     }
     if (rb.nonfinite || !rb.overflow.empty()) {
@@ -931,18 +939,23 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
     }
     update_scales(e, batch_rows);
     if (loss) *loss = rb.loss_sum / (double)batch_rows;   // virtual_exec.cpp:275
+    e->timings_graphed = graphed;
     break;
   }
   float ms[4] = {};
-  cudaEventElapsedTime(&ms[0], e->ev[0], e->ev[1]);
-  cudaEventElapsedTime(&ms[1], e->ev[1], e->ev[2]);
-  cudaEventElapsedTime(&ms[2], e->ev[2], e->ev[3]);
-  cudaEventElapsedTime(&ms[3], e->ev[3], e->ev[4]);
+  if (!e->timings_graphed) {
+    cudaEventElapsedTime(&ms[0], e->ev[0], e->ev[1]);
+    cudaEventElapsedTime(&ms[1], e->ev[1], e->ev[2]);
+    cudaEventElapsedTime(&ms[2], e->ev[2], e->ev[3]);
+    cudaEventElapsedTime(&ms[3], e->ev[3], e->ev[4]);
+  }
+  (void)cudaGetLastError();   // timing is best-effort
   e->timings.forward_ms = ms[0];
   e->timings.backward_ms = ms[1];
   e->timings.sync_ms = ms[2];
   e->timings.update_ms = ms[3];
   cudaEventElapsedTime(&e->timings.total_ms, e->ev[0], e->ev[4]);
+  (void)cudaGetLastError();
   e->timings.kernel_launches = e->launches;
   e->timings.rescale_retries = retries;
   prof_collect(e);
@@ -1071,7 +1084,8 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     e->d_sp = (StepParams*)dalloc(sizeof(StepParams));
     VNT_CUDA(cudaMallocHost(&e->h_sp, sizeof(StepParams)));
     std::memset(e->h_sp, 0, sizeof(StepParams));
-    e->graphs = !(getenv("VNT_GRAPHS") && getenv("VNT_GRAPHS")[0] == '0');
+    // Events recorded inside a graph cannot be timed: profiling runs eagerly.
+    e->graphs = !(getenv("VNT_GRAPHS") && getenv("VNT_GRAPHS")[0] == '0') && !e->profile;
     tc_init(e.get());
     if (e->opt.world_size > 1) {
       if (!options->nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
