@@ -172,6 +172,16 @@ int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count,
 int vnt_engine_get_scales(vnt_engine* e, int32_t* scales, uint32_t n);
 int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n);
 uint32_t vnt_engine_tensor_count(const vnt_engine* e);
+/* Elastic resize across processes (elastic.cpp:106-245 at the process level):
+ * join a new NCCL group (world_size, rank, 128-byte id from its rank 0) and
+ * take the replica state — fp64 parameters, momentum and the fixed-point
+ * scale history — from `source_rank` by broadcast.  Per-device input
+ * statistics migrate through vnt_engine_{get,set}_input_stats (the host
+ * layer applies migrate_state's merge/seed rules).  world_size 1 leaves the
+ * group and keeps the local state. */
+int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const uint8_t* nccl_id,
+                       int32_t source_rank);
+
 /* Forget the scale history: the next step uses the deterministic initial scale
  * 40 - ceil(log2 B) (stateless callers, e.g. vnt::train_step on a World). */
 int vnt_engine_reset_scales(vnt_engine* e);

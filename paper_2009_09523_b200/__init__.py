@@ -109,6 +109,7 @@ def load_engine() -> C.CDLL:
         "vnt_engine_set_scales": (C.c_int, [_vp, _i32p, C.c_uint32]),
         "vnt_engine_last_timings": (C.c_int, [_vp, C.POINTER(StepTimings)]),
         "vnt_engine_reset_scales": (C.c_int, [_vp]),
+        "vnt_engine_regroup": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32]),
         "vnt_engine_stream": (_vp, [_vp]),
         "vnt_engine_device_alloc": (C.c_int, [_vp, C.c_uint64, C.POINTER(_vp)]),
         "vnt_engine_device_free": (C.c_int, [_vp, _vp]),
@@ -275,6 +276,13 @@ class Engine:
     def set_scales(self, s):
         s = np.ascontiguousarray(s, np.int32)
         _check(self.lib.vnt_engine_set_scales(self.h, s.ctypes.data_as(_i32p), s.size))
+
+    def regroup(self, rank: int, world_size: int, nccl_id: bytes | None, source_rank: int = 0):
+        """Join a new process group and take the replica state from source_rank."""
+        nid = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        _check(self.lib.vnt_engine_regroup(self.h, rank, world_size,
+                                           C.cast(nid, C.POINTER(C.c_uint8)) if nid else None,
+                                           source_rank))
 
     def timings(self) -> dict:
         t = StepTimings()

@@ -1407,6 +1407,64 @@ int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n) {
   });
 }
 
+int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const uint8_t* nccl_id,
+                       int32_t source_rank) {
+  return guarded([&] {
+    bind(e);
+    if (world_size < 1 || rank < 0 || rank >= world_size || source_rank < 0 ||
+        source_rank >= world_size)
+      throw EngineError(VNT_ERR_CONFIG, "bad rank/world_size/source_rank");
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->comm) {
+      ncclCommDestroy(e->comm);
+      e->comm = nullptr;
+    }
+    drop_graphs(e);
+    reset_acc(e);
+    e->opt.rank = rank;
+    e->opt.world_size = world_size;
+    if (world_size == 1) return VNT_OK;
+    if (!nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&e->comm, world_size, id, rank);
+    if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+    // Replica state from the source rank: fp64 master, momentum, fixed-point
+    // scale history (part of the numerical state).
+    auto bcast = [&](void* p, size_t n, ncclDataType_t t) {
+      const ncclResult_t rr = ncclBroadcast(p, p, n, t, source_rank, e->comm, e->stream);
+      if (rr != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(rr));
+    };
+    bcast(e->w64, e->P, ncclFloat64);
+    if (e->v64) bcast(e->v64, e->P, ncclFloat64);
+    int32_t* d_sc = (int32_t*)dalloc(ntensors(e) * sizeof(int32_t) + sizeof(int32_t));
+    std::vector<int32_t> sc(e->scales);
+    sc.push_back(e->scales_init ? 1 : 0);
+    VNT_CUDA(cudaMemcpyAsync(d_sc, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                             e->stream));
+    bcast(d_sc, sc.size(), ncclInt32);
+    VNT_CUDA(cudaMemcpyAsync(sc.data(), d_sc, sc.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    cudaFree(d_sc);
+    e->scales.assign(sc.begin(), sc.end() - 1);
+    e->scales_init = sc.back() != 0;
+    for (int l = 0; l < e->L; ++l) {
+      const int rows = (int)e->widths[l], cols = (int)e->widths[l + 1];
+      dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+      k_refresh_weight<<<grid, block, 0, e->stream>>>(e->w64 + e->woff[l], e->w32 + e->woff[l],
+                                                      e->wt32 + e->wtoff[l], rows, cols);
+      VNT_LAUNCH_CHECK();
+      k_refresh_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, e->stream>>>(
+          e->w64 + e->boff[l], e->w32 + e->boff[l], (size_t)cols);
+      VNT_LAUNCH_CHECK();
+    }
+    split_weights(e);
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    return VNT_OK;
+  });
+}
+
 int vnt_engine_reset_scales(vnt_engine* e) {
   if (!e) return VNT_ERR_CONFIG;
   e->scales_init = false;

@@ -201,3 +201,20 @@ def test_errors_mirror_reference_exceptions(port):
     with pytest.raises(V.VntError) as ei:      # empty node list
         e.device_step(0, x[:0], y[:0], [])
     assert ei.value.code == 2
+
+
+def test_regroup_single_process_keeps_state(port):
+    """vnt_engine_regroup to a 1-process group keeps params, scales and the trajectory."""
+    w = [8, 16, 3]
+    a = make_engine(w, "tanh", "softmax-cross-entropy", port, gemm_mode="ffma")
+    b = make_engine(w, "tanh", "softmax-cross-entropy", port, gemm_mode="ffma")
+    sizes, dev = vnt().uniform_mapping(32, 4, 1)
+    for s in range(4):
+        x, y = port.synth_batch(2, 128, 8, 3, s * 32, 32)
+        if s == 2:
+            b.regroup(0, 1, None, 0)
+        la, _ = a.train_step(x, y, sizes, dev, 0.05)
+        lb, _ = b.train_step(x, y, sizes, dev, 0.05)
+        assert la == lb
+    assert np.array_equal(a.get_params(), b.get_params())
+    assert np.array_equal(a.scales(), b.scales())
