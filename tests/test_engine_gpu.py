@@ -206,8 +206,8 @@ def test_errors_mirror_reference_exceptions(port):
 def test_regroup_single_process_keeps_state(port):
     """vnt_engine_regroup to a 1-process group keeps params, scales and the trajectory."""
     w = [8, 16, 3]
-    a = make_engine(w, "tanh", "softmax-cross-entropy", port, gemm_mode="ffma")
-    b = make_engine(w, "tanh", "softmax-cross-entropy", port, gemm_mode="ffma")
+    a = make_engine(w, "tanh", "softmax-cross-entropy", 5, port, gemm_mode="ffma")
+    b = make_engine(w, "tanh", "softmax-cross-entropy", 5, port, gemm_mode="ffma")
     sizes, dev = vnt().uniform_mapping(32, 4, 1)
     for s in range(4):
         x, y = port.synth_batch(2, 128, 8, 3, s * 32, 32)
