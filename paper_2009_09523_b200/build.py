@@ -89,6 +89,23 @@ def build_cpp_tests(force=False):
     return outs
 
 
+NLOHMANN = Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty")
+
+
+def build_tools(force=False):
+    """`vnt_train` — the reference CLI's train command over the drop-in Trainer."""
+    src = PKG / "tools" / "vnt_train.cpp"
+    out = ROOT / "build" / "bin" / "vnt_train"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    if not (NLOHMANN / "nlohmann" / "json.hpp").exists():
+        print("nlohmann/json.hpp not found; skipping vnt_train")
+        return None
+    if force or _stale(out, [src, PKG / "libvnt.so"]):
+        _run(["g++", "-std=c++20", "-O2", f"-I{INC}", f"-I{NLOHMANN}", "-o", out, src,
+              f"-L{PKG}", "-lvnt", "-lvnt_engine", f"-Wl,-rpath,{PKG}", "-lpthread"])
+    return out
+
+
 def build_oracle():
     """Test-only: our C restatement always; the reference itself when present."""
     _run(["make", "-s", "-C", ROOT / "oracle", "oracle"])
@@ -100,6 +117,7 @@ def build_all(force=False):
     build_engine(force)
     if build_host(force):
         build_cpp_tests(force)
+        build_tools(force)
     build_oracle()
 
 
