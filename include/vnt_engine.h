@@ -162,6 +162,18 @@ int vnt_engine_train_step_resident(vnt_engine* e, const double* x_dev, const dou
                                    const int32_t* node_device, uint32_t total_nodes,
                                    double lr, double* loss, vnt_device_metrics* per_device);
 
+/* Prefetch (runner.cpp:64-73 on the device): stage the rows this process
+ * needs from a future step's batch on a copy stream, into the spare input
+ * buffer.  One batch is in flight at a time: called while none is, the copy
+ * starts now; otherwise the request is queued and the next train_step starts
+ * it right after launching its own work, so the H2D overlaps that step's
+ * compute.  A train_step with the same (x, y) pointers consumes the staged
+ * batch and skips its own copy; any other step discards it.  The caller keeps
+ * (x, y) unchanged until that step.  Multi-pass plans ignore prefetch. */
+int vnt_engine_prefetch(vnt_engine* e, const double* x, const double* y, uint64_t batch_rows,
+                        const uint64_t* node_sizes, const int32_t* node_device,
+                        uint32_t total_nodes, int32_t x_on_device);
+
 /* LayerStats "input" of a local device (model.hpp:65-76): count, mean[in], m2[in]. */
 int vnt_engine_get_input_stats(vnt_engine* e, int32_t device, double* count, double* mean,
                                double* m2);

@@ -109,6 +109,8 @@ def load_engine() -> C.CDLL:
         "vnt_engine_set_scales": (C.c_int, [_vp, _i32p, C.c_uint32]),
         "vnt_engine_last_timings": (C.c_int, [_vp, C.POINTER(StepTimings)]),
         "vnt_engine_reset_scales": (C.c_int, [_vp]),
+        "vnt_engine_prefetch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _u64p, _i32p, C.c_uint32,
+                                          C.c_int32]),
         "vnt_engine_regroup": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32]),
         "vnt_engine_stream": (_vp, [_vp]),
         "vnt_engine_device_alloc": (C.c_int, [_vp, C.c_uint64, C.POINTER(_vp)]),
@@ -255,6 +257,15 @@ class Engine:
                     C.byref(loss), pm)
         _check(rc)
         return loss.value
+
+    def prefetch_ptr(self, x_ptr: int, y_ptr: int, rows: int, node_sizes, node_device,
+                     resident: bool):
+        """Stage a future step's rows on the copy stream (vnt_engine_prefetch):
+        call prefetch(i) once, then before each step(i) queue prefetch(i+1)."""
+        ns, nd, _ = self._mapping_args(node_sizes, node_device)
+        _check(self.lib.vnt_engine_prefetch(self.h, _vp(x_ptr), _vp(y_ptr), rows,
+                                            ns.ctypes.data_as(_u64p), nd.ctypes.data_as(_i32p),
+                                            ns.size, 1 if resident else 0))
 
     # ---- kernel state / scales / timings
     def input_stats(self, device):

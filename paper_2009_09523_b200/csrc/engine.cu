@@ -83,8 +83,31 @@ struct vnt_engine {
 
   // pass buffers
   uint64_t cap_rows = 0, cap_ldT = 0, cap_vns = 0;
-  double* xin = nullptr;
+  double* xin = nullptr;   // = xbuf[cur]: the staged batch the kernels read
   double* yin = nullptr;
+  double* xbuf[2] = {nullptr, nullptr};   // double-buffered input staging
+  double* ybuf[2] = {nullptr, nullptr};
+  int cur = 0;
+  // next-step input prefetch (Trainer prefetch, runner.cpp:64-73, on the device)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t pf_event = nullptr;
+  struct {
+    const double* x = nullptr;
+    const double* y = nullptr;
+    int buf = -1;
+    bool valid = false;
+  } pf;
+  // a second request waits until the in-flight one is consumed, then starts
+  // right after the consuming step has launched its own work
+  struct {
+    const double* x = nullptr;
+    const double* y = nullptr;
+    uint64_t rows = 0;
+    std::vector<uint64_t> sizes;
+    std::vector<int32_t> devs;
+    bool on_device = false;
+    bool valid = false;
+  } pf_next;
   std::vector<float*> X, XT, D, DT;
   // 3xTF32 operand twins (hi = rna_tf32(x), lo = x - hi), only when split.
   bool split = false;
@@ -240,13 +263,18 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
   ldT = std::max(ldT, e->cap_ldT);
   vns = std::max(vns, e->cap_vns);
   VNT_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->copy_stream) VNT_CUDA(cudaStreamSynchronize(e->copy_stream));
+  e->pf.valid = false;
   drop_graphs(e);
   auto fre = [](auto*& p) {
     if (p) cudaFree(p);
     p = nullptr;
   };
-  fre(e->xin);
-  fre(e->yin);
+  for (int b = 0; b < 2; ++b) {
+    fre(e->xbuf[b]);
+    fre(e->ybuf[b]);
+  }
+  e->xin = e->yin = nullptr;
   fre(e->logits);
   fre(e->vn_mean);
   fre(e->vn_m2);
@@ -254,8 +282,12 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
                   &e->DTh, &e->DTl})
     for (auto*& p : *v) fre(p);
   const uint64_t in = e->widths[0], out = e->widths[L];
-  e->xin = (double*)dalloc(rows * in * sizeof(double));
-  e->yin = (double*)dalloc(rows * out * sizeof(double));
+  for (int b = 0; b < 2; ++b) {
+    e->xbuf[b] = (double*)dalloc(rows * in * sizeof(double));
+    e->ybuf[b] = (double*)dalloc(rows * out * sizeof(double));
+  }
+  e->xin = e->xbuf[e->cur];
+  e->yin = e->ybuf[e->cur];
   e->logits = (float*)dalloc(rows * out * sizeof(float));
   e->vn_mean = (double*)dalloc(vns * in * sizeof(double));
   e->vn_m2 = (double*)dalloc(vns * in * sizeof(double));
@@ -445,9 +477,9 @@ std::vector<StatsLaunch> prep_stats(vnt_engine* e, const Pass& p, size_t& off) {
   return out;
 }
 
-void stage_inputs(vnt_engine* e, const Pass& p, const double* x, const double* y, bool x_on_device) {
+void stage_inputs_to(vnt_engine* e, const Pass& p, const double* x, const double* y,
+                     bool x_on_device, double* xdst, double* ydst, cudaStream_t s) {
   const uint64_t in = e->widths[0], out = e->widths[e->L];
-  cudaStream_t s = e->stream;
   const cudaMemcpyKind kind = x_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   // Batch::slice copies (data.cpp:36-48): each node's contiguous rows; runs of
   // nodes adjacent both in the source batch and in the pass move as one copy.
@@ -460,12 +492,66 @@ void stage_inputs(vnt_engine* e, const Pass& p, const double* x, const double* y
       nrow += p.nodes[j].rows;
       ++j;
     }
-    VNT_CUDA(cudaMemcpyAsync(e->xin + first.prow * in, x + first.src_row * in,
+    VNT_CUDA(cudaMemcpyAsync(xdst + first.prow * in, x + first.src_row * in,
                              nrow * in * sizeof(double), kind, s));
-    VNT_CUDA(cudaMemcpyAsync(e->yin + first.prow * out, y + first.src_row * out,
+    VNT_CUDA(cudaMemcpyAsync(ydst + first.prow * out, y + first.src_row * out,
                              nrow * out * sizeof(double), kind, s));
     k = j;
   }
+}
+
+void stage_inputs(vnt_engine* e, const Pass& p, const double* x, const double* y, bool x_on_device) {
+  stage_inputs_to(e, p, x, y, x_on_device, e->xin, e->yin, e->stream);
+}
+
+std::vector<PassNode> local_nodes(vnt_engine* e, const uint64_t* node_sizes,
+                                  const int32_t* node_device, uint32_t total_nodes,
+                                  uint64_t batch_rows);
+std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local);
+
+// Copy the rows this process needs from (x, y) into the spare input buffer on
+// the copy stream (single-pass plans only: multi-pass steps stage per pass).
+void start_prefetch(vnt_engine* e, const double* x, const double* y, uint64_t batch_rows,
+                    const uint64_t* node_sizes, const int32_t* node_device, uint32_t total_nodes,
+                    bool on_device, bool may_grow) {
+  e->pf.valid = false;
+  auto local = local_nodes(e, node_sizes, node_device, total_nodes, batch_rows);
+  if (local.empty()) return;
+  auto& passes = plan_for(e, local);
+  if (passes.size() != 1) return;
+  const Pass& p = passes[0];
+  const bool fits = p.rows <= e->cap_rows && p.ldT <= e->cap_ldT && p.nodes.size() <= e->cap_vns;
+  if (!fits && !may_grow) return;   // never reallocate under a running step
+  ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
+  const int b = 1 - e->cur;
+  stage_inputs_to(e, p, x, y, on_device, e->xbuf[b], e->ybuf[b], e->copy_stream);
+  VNT_CUDA(cudaEventRecord(e->pf_event, e->copy_stream));
+  e->pf.x = x;
+  e->pf.y = y;
+  e->pf.buf = b;
+  e->pf.valid = true;
+}
+
+// After a step has launched its work: start the queued next batch's copy.
+void start_queued_prefetch(vnt_engine* e) {
+  auto& q = e->pf_next;
+  if (!q.valid || e->pf.valid) return;
+  q.valid = false;
+  start_prefetch(e, q.x, q.y, q.rows, q.sizes.data(), q.devs.data(), (uint32_t)q.sizes.size(),
+                 q.on_device, false);
+}
+
+// Use a prefetched batch if it matches (x, y): switch the staging buffer and
+// order the compute stream after the copy.  Returns true if consumed.
+bool take_prefetch(vnt_engine* e, const double* x, const double* y) {
+  const bool hit = e->pf.valid && e->pf.x == x && e->pf.y == y;
+  e->pf.valid = false;
+  if (!hit) return false;
+  e->cur = e->pf.buf;
+  e->xin = e->xbuf[e->cur];
+  e->yin = e->ybuf[e->cur];
+  VNT_CUDA(cudaStreamWaitEvent(e->stream, e->pf_event, 0));
+  return true;
 }
 
 // Device work of one pass (inputs already staged in xin/yin).
@@ -680,7 +766,14 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
   for (size_t i = 0; i < passes.size(); ++i) {
     const auto& p = passes[i];
     ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
-    stage_inputs(e, p, x, y, on_device);
+    // A prefetched batch is consumed on the first attempt only (on a rescale
+    // retry the prefetch slot already holds the next batch).
+    bool took = false;
+    if (i == 0 && do_stats) {
+      if (passes.size() == 1) took = take_prefetch(e, x, y);
+      else e->pf.valid = false;
+    }
+    if (!took) stage_inputs(e, p, x, y, on_device);
     run_pass(e, p, do_stats ? &stats[i] : nullptr, !e->acc_started);
     e->acc_started = true;
     e->acc_examples += p.rows;
@@ -860,8 +953,8 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
       size_t off = 0;
       const std::vector<StatsLaunch> stats = prep_stats(e, p, off);
-      stage_inputs(e, p, x, y, on_device);
-      std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1};
+      if (!take_prefetch(e, x, y)) stage_inputs(e, p, x, y, on_device);
+      std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur};
       for (const auto& n : local) {
         key.push_back(n.node);
         key.push_back(n.dev);
@@ -902,6 +995,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
         VNT_CUDA(cudaEventRecord(e->ev[4], e->stream));
         graphed = true;
       }
+      start_queued_prefetch(e);   // overlaps the next batch's H2D with this step
       VNT_CUDA(cudaStreamSynchronize(e->stream));
       rb = parse_readback(e);
     } else {
@@ -919,6 +1013,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       VNT_CUDA(cudaEventRecord(e->ev[3], e->stream));
       launch_sgd(e);
       VNT_CUDA(cudaEventRecord(e->ev[4], e->stream));
+      start_queued_prefetch(e);   // overlaps the next batch's H2D with this step
       rb = read_tail(e, true);
     }
     if (rb.nonfinite || !rb.overflow.empty()) {
@@ -1056,6 +1151,8 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     e->P = off;
     bind(e.get());
     VNT_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    VNT_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    VNT_CUDA(cudaEventCreateWithFlags(&e->pf_event, cudaEventDisableTiming));
     for (auto& ev : e->ev) VNT_CUDA(cudaEventCreate(&ev));
     e->w64 = (double*)dalloc(e->P * sizeof(double));
     VNT_CUDA(cudaMemset(e->w64, 0, e->P * sizeof(double)));
@@ -1114,7 +1211,8 @@ void vnt_engine_destroy(vnt_engine* e) {
     for (auto* p : *v)
       if (p) cudaFree(p);
   for (void* p : {(void*)e->w64, (void*)e->v64, (void*)e->w32, (void*)e->wt32, (void*)e->G,
-                  (void*)e->gmax, (void*)e->gout, (void*)e->xin, (void*)e->yin, (void*)e->logits,
+                  (void*)e->gmax, (void*)e->gout, (void*)e->xbuf[0], (void*)e->ybuf[0],
+                  (void*)e->xbuf[1], (void*)e->ybuf[1], (void*)e->logits,
                   (void*)e->vn_mean, (void*)e->vn_m2, (void*)e->d_combine})
     if (p) cudaFree(p);
   for (auto* v : {&e->X, &e->XT, &e->D, &e->DT})
@@ -1135,6 +1233,11 @@ void vnt_engine_destroy(vnt_engine* e) {
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : e->prof_ev) cudaEventDestroy(ev);
+  if (e->copy_stream) {
+    cudaStreamSynchronize(e->copy_stream);
+    cudaStreamDestroy(e->copy_stream);
+  }
+  if (e->pf_event) cudaEventDestroy(e->pf_event);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -1356,6 +1459,28 @@ int vnt_engine_train_step_resident(vnt_engine* e, const double* x, const double*
   return guarded([&] {
     return train_step_impl(e, x, y, batch_rows, node_sizes, node_device, total_nodes, lr, loss,
                            per_device, true);
+  });
+}
+
+int vnt_engine_prefetch(vnt_engine* e, const double* x, const double* y, uint64_t batch_rows,
+                        const uint64_t* node_sizes, const int32_t* node_device,
+                        uint32_t total_nodes, int32_t x_on_device) {
+  return guarded([&] {
+    bind(e);
+    if (e->pf.valid) {   // one batch already in flight: queue this one behind it
+      auto& q = e->pf_next;
+      q.x = x;
+      q.y = y;
+      q.rows = batch_rows;
+      q.sizes.assign(node_sizes, node_sizes + total_nodes);
+      q.devs.assign(node_device, node_device + total_nodes);
+      q.on_device = x_on_device != 0;
+      q.valid = true;
+      return VNT_OK;
+    }
+    start_prefetch(e, x, y, batch_rows, node_sizes, node_device, total_nodes, x_on_device != 0,
+                   true);
+    return VNT_OK;
   });
 }
 

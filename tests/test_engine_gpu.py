@@ -218,3 +218,37 @@ def test_regroup_single_process_keeps_state(port):
         assert la == lb
     assert np.array_equal(a.get_params(), b.get_params())
     assert np.array_equal(a.scales(), b.scales())
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_prefetch_is_bit_identical(port, monkeypatch, graphs):
+    """vnt_engine_prefetch (runner.cpp:64-73 on the device): staging batch i+1 on
+    the copy stream while step i runs — hits, a queued request, a stale
+    prefetch (different pointers) — never changes bits."""
+    import torch
+    if not graphs:
+        monkeypatch.setenv("VNT_GRAPHS", "0")
+    w = [64, 96, 48, 10]
+    steps, B = 7, 96
+    xs, ys = [], []
+    for s in range(steps):
+        x, y = port.synth_batch(8, 96 * 8, 64, 10, (s * B) % (96 * 8), B)
+        xs.append(torch.from_numpy(x).pin_memory())
+        ys.append(torch.from_numpy(y).pin_memory())
+    sizes, dev = vnt().uniform_mapping(B, 24, 1)
+    a = make_engine(w, "relu", "softmax-cross-entropy", 23, port, gemm_mode="auto")
+    b = make_engine(w, "relu", "softmax-cross-entropy", 23, port, gemm_mode="auto")
+    la, lb = [], []
+    for s in range(steps):
+        la.append(a.train_step_ptr(xs[s].data_ptr(), ys[s].data_ptr(), B, sizes, dev, 0.05, False))
+    ptr = lambda i: (xs[i].data_ptr(), ys[i].data_ptr())
+    b.prefetch_ptr(*ptr(0), B, sizes, dev, resident=False)
+    for s in range(steps):
+        if s == 3:
+            # stale: the queued batch is 5, step 4 discards it and stages itself
+            b.prefetch_ptr(*ptr(5), B, sizes, dev, resident=False)
+        elif s + 1 < steps:
+            b.prefetch_ptr(*ptr(s + 1), B, sizes, dev, resident=False)
+        lb.append(b.train_step_ptr(*ptr(s), B, sizes, dev, 0.05, False))
+    assert la == lb
+    assert np.array_equal(a.get_params(), b.get_params())
