@@ -424,10 +424,10 @@ template <int NO>
 struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
                   int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
-                  const float* tscale) {
+                  const float* tscale, float* Dh, float* Dl, float* DTh, float* DTl) {
     dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
     k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
-                                            tscale);
+                                            tscale, Dh, Dl, DTh, DTl);
   }
 };
 template <int NO>
@@ -568,8 +568,11 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
   if (padded) {
     for (int l = 0; l < L; ++l) {
       if (!e->tc_layer[l]) continue;
-      VNT_CUDA(cudaMemsetAsync(e->XT[l], 0, e->widths[l] * p.ldT * sizeof(float), s));
-      VNT_CUDA(cudaMemsetAsync(e->DT[l + 1], 0, e->widths[l + 1] * p.ldT * sizeof(float), s));
+      // the dW reads the 3xTF32 twins when they exist, the plain copies otherwise
+      for (float* t : {e->XT[l], e->XTh[l], e->XTl[l]})
+        if (t) VNT_CUDA(cudaMemsetAsync(t, 0, e->widths[l] * p.ldT * sizeof(float), s));
+      for (float* t : {e->DT[l + 1], e->DTh[l + 1], e->DTl[l + 1]})
+        if (t) VNT_CUDA(cudaMemsetAsync(t, 0, e->widths[l + 1] * p.ldT * sizeof(float), s));
     }
   }
   const int* tcol = p.d_meta;
@@ -579,11 +582,13 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
   const int rows = (int)p.rows, ldT = (int)p.ldT;
   {
     dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(p.rows, 32)), block(32, 8);
-    k_ingest<<<grid, block, 0, s>>>(e->xin, e->X[0], e->XT[0], tcol, rows, (int)in, ldT);
+    // A 3xTF32 first layer reads only the twins (allocated iff it is one).
+    const bool twins = e->Xh[0] != nullptr;
+    k_ingest<<<grid, block, 0, s>>>(e->xin, twins ? nullptr : e->X[0], twins ? nullptr : e->XT[0],
+                                    e->Xh[0], e->Xl[0], e->XTh[0], e->XTl[0], tcol, rows, (int)in,
+                                    ldT);
     VNT_LAUNCH_CHECK();
     e->launches++;
-    split_into(e, e->X[0], e->Xh[0], e->Xl[0], p.rows * in);
-    split_into(e, e->XT[0], e->XTh[0], e->XTl[0], in * p.ldT);
   }
   if (stats) {
     // observe_batch per node then Chan-combine into the node's device lineage
@@ -685,8 +690,10 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       if (e->tc_layer[l]) {
         tc_backward_data(e, l, rows, ldT, tcol, dts(l));
       } else if (out_l <= 32) {
+        // D[l] stays plain for k_db; DT[l] feeds only the (twin-reading) dW of l-1
         dispatch_skinny<BwdSkinny>(out_l, s, e->D[l + 1], e->w32 + e->woff[l], out_l, in_l, rows,
-                                   e->act, e->X[l], e->D[l], e->DT[l], ldT, tcol, dts(l));
+                                   e->act, e->X[l], e->D[l], e->DTh[l] ? nullptr : e->DT[l], ldT,
+                                   tcol, dts(l), e->Dh[l], e->Dl[l], e->DTh[l], e->DTl[l]);
         VNT_LAUNCH_CHECK();
         e->launches++;
       } else {
@@ -699,7 +706,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
         e->launches++;
       }
       prof_end(e, 2.0 * rows * (double)in_l * out_l);
-      if (!e->tc_layer[l]) {
+      if (!e->tc_layer[l] && out_l > 32) {   // tcgen05 and skinny kernels write twins
         split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l);
         split_into(e, e->DT[l], e->DTh[l], e->DTl[l], (uint64_t)in_l * p.ldT);
       }
@@ -802,8 +809,10 @@ void launch_sgd(vnt_engine* e) {
       a.w64 = e->w64 + off;
       a.v64 = e->v64 ? e->v64 + off : nullptr;
       a.G = e->G + off;
-      a.w32 = e->w32 + off;
-      a.wt32 = part ? nullptr : e->wt32 + e->wtoff[l];
+      // a 3xTF32 layer's weight GEMMs read only the twins
+      const bool twins_only = part == 0 && e->split && e->tc_layer[l];
+      a.w32 = twins_only ? nullptr : e->w32 + off;
+      a.wt32 = (part || twins_only) ? nullptr : e->wt32 + e->wtoff[l];
       if (e->split) {
         a.w32h = e->w32h + off;
         a.w32l = e->w32l + off;

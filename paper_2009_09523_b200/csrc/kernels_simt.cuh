@@ -37,9 +37,18 @@ struct StepParams {
 
 // ---------------------------------------------------------------- ingest
 // fp64 rows (reference Batch layout, data.hpp:14-31) -> fp32 X0 and XT0.
+__device__ __forceinline__ void put_twins(float* hi, float* lo, size_t idx, float v) {
+  const float h = tf32_rna(v);   // same split as k_split
+  hi[idx] = h;
+  lo[idx] = v - h;
+}
+
+// fp64 batch rows -> fp32 X0 (row-major) and XT0 (feature-major, padded per
+// node); X0/XT0 may be null when only the 3xTF32 twins are consumed.
 __global__ void k_ingest(const double* __restrict__ x, float* __restrict__ X0,
-                         float* __restrict__ XT0, const int* __restrict__ tcol, int rows,
-                         int in, int ldT) {
+                         float* __restrict__ XT0, float* __restrict__ X0h, float* __restrict__ X0l,
+                         float* __restrict__ XT0h, float* __restrict__ XT0l,
+                         const int* __restrict__ tcol, int rows, int in, int ldT) {
   __shared__ float tile[32][33];
   const int r0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -48,14 +57,21 @@ __global__ void k_ingest(const double* __restrict__ x, float* __restrict__ X0,
     float v = 0.f;
     if (r < rows && j < in) {
       v = __double2float_rn(x[(size_t)r * in + j]);
-      X0[(size_t)r * in + j] = v;
+      const size_t idx = (size_t)r * in + j;
+      if (X0) X0[idx] = v;
+      if (X0h) put_twins(X0h, X0l, idx, v);
     }
     tile[k][tx] = v;
   }
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
     const int j = j0 + k, r = r0 + tx;
-    if (r < rows && j < in) XT0[(size_t)j * ldT + tcol[r]] = tile[tx][k];
+    if (r < rows && j < in) {
+      const size_t o = (size_t)j * ldT + tcol[r];
+      const float v = tile[tx][k];
+      if (XT0) XT0[o] = v;
+      if (XT0h) put_twins(XT0h, XT0l, o, v);
+    }
   }
 }
 
@@ -395,7 +411,10 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
                                                     float* __restrict__ Dout,
                                                     float* __restrict__ DT, int ldT,
                                                     const int* __restrict__ tcol,
-                                                    const float* __restrict__ tscale_p) {
+                                                    const float* __restrict__ tscale_p,
+                                                    float* __restrict__ Dh, float* __restrict__ Dl,
+                                                    float* __restrict__ DTh,
+                                                    float* __restrict__ DTl) {
   const float tscale = tscale_p ? *tscale_p : 1.f;
   // 32 features x 32 rows per block (4 chunks of 32 rows), o ascending per
   // output; transposed copy through smem.
@@ -425,13 +444,19 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
       if (r < rows && i < in) {
         v = acc * act_grad_from_out(act, Xprev[(size_t)r * in + i]);
         Dout[(size_t)r * in + i] = v;
+        if (Dh) put_twins(Dh, Dl, (size_t)r * in + i, v);
       }
       tile[k][tx] = v;
     }
     __syncthreads();
     for (int k = ty; k < 32; k += 8) {
       const int ii = i0 + k, r = r0 + tx;
-      if (r < rows && ii < in) DT[(size_t)ii * ldT + tcol[r]] = tile[tx][k] * tscale;
+      if (r < rows && ii < in) {
+        const size_t o = (size_t)ii * ldT + tcol[r];
+        const float t = tile[tx][k] * tscale;
+        if (DT) DT[o] = t;
+        if (DTh) put_twins(DTh, DTl, o, t);
+      }
     }
   }
 }
@@ -572,7 +597,7 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
       const size_t idx = (size_t)r * a.cols + c;
       a.w64[idx] = wn;
       if (a.v64) a.v64[idx] = u;
-      a.w32[idx] = w32;
+      if (a.w32) a.w32[idx] = w32;
       if (a.w32h) {
         const float h = tf32_rna(w32);
         a.w32h[idx] = h;
@@ -583,7 +608,7 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
     }
   }
   block_max_to(a.gmax, mx);
-  if (!a.wt32) return;
+  if (!a.wt32 && !a.wt32h) return;
   __syncthreads();
   // transposed: WT[c][r], 32 columns x 64 rows -> each warp row writes 64 contiguous rows
 #pragma unroll
@@ -597,7 +622,7 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
       if (r < a.rows) {
         const float v = tile[h * 32 + tx][cc];
         const size_t o = (size_t)col * a.rows + r;
-        a.wt32[o] = v;
+        if (a.wt32) a.wt32[o] = v;
         if (a.wt32h) {
           const float hv = tf32_rna(v);
           a.wt32h[o] = hv;

@@ -129,3 +129,25 @@ def test_3xtf32_trajectory_and_bitwise(port):
     assert dw < 2e-5
     for p, l in finals[1:]:
         assert np.array_equal(p, finals[0][0]) and np.array_equal(l, finals[0][1])
+
+
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+def test_padding_columns_across_uneven_passes(port, mode):
+    """Passes with different node layouts: columns that are one pass's node rows
+    are the next pass's padding.  The per-node dW must not see the stale values
+    (plain or 3xTF32 twin operands), so any grouping is bit-identical."""
+    w = [128, 256, 256, 10]
+    sizes = [40, 24, 64, 7, 57, 64]
+    B = sum(sizes)
+    dev = [0] * len(sizes)
+    outs = []
+    for rr in (0, 64, 100):
+        e = engine(w, "relu", "softmax-cross-entropy", port, gemm_mode=mode, resident_rows=rr)
+        losses = []
+        for s in range(3):
+            x, y = port.synth_batch(9, 4096, w[0], w[-1], s * B, B)
+            losses.append(e.train_step(x, y, sizes, dev, 0.02)[0])
+        outs.append((e.get_params(), losses))
+    for p, l in outs[1:]:
+        assert l == outs[0][1]
+        assert np.array_equal(p, outs[0][0])
