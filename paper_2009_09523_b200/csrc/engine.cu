@@ -416,7 +416,7 @@ template <int NO>
 struct FwdSkinny {
   static void run(cudaStream_t s, const float* X, int K, const float* W, int no, const float* b,
                   int rows, int act, int last, float* out, float* outT, int ldT, const int* tcol) {
-    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
+    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8 * kSkinnyRows), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
                                                                  out, outT, ldT, tcol);
   }
 };

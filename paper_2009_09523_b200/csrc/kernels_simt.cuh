@@ -86,12 +86,32 @@ __global__ void k_vn_stats(const double* __restrict__ x, int in, const int* __re
   const int k = blockIdx.y;
   if (j >= in) return;
   const int r0 = vn_row0[k], n = vn_rows[k];
+  const double* xp = x + (size_t)r0 * in + j;
   double m = 0.0;
-  for (int r = 0; r < n; ++r) m = __dadd_rn(m, x[(size_t)(r0 + r) * in + j]);
+  int r = 0;
+  for (; r + 8 <= n; r += 8) {   // 8 loads in flight, adds in row order
+    double t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = __ldg(xp + (size_t)(r + q) * in);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) m = __dadd_rn(m, t[q]);
+  }
+  for (; r < n; ++r) m = __dadd_rn(m, __ldg(xp + (size_t)r * in));
   m = __ddiv_rn(m, (double)n);
   double s = 0.0;
-  for (int r = 0; r < n; ++r) {
-    const double d = __dsub_rn(x[(size_t)(r0 + r) * in + j], m);
+  r = 0;
+  for (; r + 8 <= n; r += 8) {
+    double t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = __ldg(xp + (size_t)(r + q) * in);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double d = __dsub_rn(t[q], m);
+      s = __dadd_rn(s, __dmul_rn(d, d));
+    }
+  }
+  for (; r < n; ++r) {
+    const double d = __dsub_rn(__ldg(xp + (size_t)r * in), m);
     s = __dadd_rn(s, __dmul_rn(d, d));
   }
   vn_mean[(size_t)k * in + j] = m;
@@ -352,12 +372,22 @@ __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict
   const int r0 = vn_row0[v], n = vn_rows[v];
   const float scale = *scale_p;
   float g = 0.f;
-  for (int r = 0; r < n; ++r) g += D[(size_t)(r0 + r) * out + o];
+  const float* d = D + (size_t)r0 * out + o;
+  int r = 0;
+  for (; r + 8 <= n; r += 8) {   // 8 loads in flight, adds still in row order
+    float t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = __ldg(d + (size_t)(r + j) * out);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g += t[j];
+  }
+  for (; r < n; ++r) g += __ldg(d + (size_t)r * out);
   const long long q = quantise(g, scale, lim, tail, tensor);
   if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&G[o]), (unsigned long long)q);
 }
 
 // ---------------------------------------------- skinny layers (out <= 32)
+constexpr int kSkinnyRows = 4;   // rows per warp in k_fwd_skinny
 // Forward with few outputs (the 4096 -> 10 classifier): one warp per row,
 // lane-strided partial dot products over k then a fixed xor tree, so every
 // output depends only on its row.
@@ -368,36 +398,58 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
                                                     int act, int last, float* __restrict__ out,
                                                     float* __restrict__ outT, int ldT,
                                                     const int* __restrict__ tcol) {
-  // One warp per row, lane-strided k, then a fixed xor tree: each output
-  // depends only on its row.
+  // A warp owns kSkinnyRows rows so each W[k][:] load serves all of them; per
+  // (row, o) the partial sums still run lane-strided over k and meet in a fixed
+  // xor tree, so every output depends only on its row.
+  constexpr int R = kSkinnyRows;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const float* x = X + (size_t)warp * K;
-  float acc[NO];
+  const int row0 = warp * R;
+  if (row0 >= rows) return;
+  const float* x[R];
 #pragma unroll
-  for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+  for (int r = 0; r < R; ++r) x[r] = X + (size_t)min(row0 + r, rows - 1) * K;
+  float acc[R][NO];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int o = 0; o < NO; ++o) acc[r][o] = 0.f;
+#pragma unroll 2
   for (int k = lane; k < K; k += 32) {
-    const float a = x[k];
+    float a[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) a[r] = __ldg(x[r] + k);
     const float* w = W + (size_t)k * no;
 #pragma unroll
-    for (int o = 0; o < NO; ++o)
-      if (o < no) acc[o] = fmaf(a, __ldg(w + o), acc[o]);
+    for (int o = 0; o < NO; ++o) {
+      if (o < no) {
+        const float wo = __ldg(w + o);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r][o] = fmaf(a[r], wo, acc[r][o]);
+      }
+    }
   }
 #pragma unroll
-  for (int o = 0; o < NO; ++o) {
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int s = 16; s; s >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], s);
-  }
+    for (int o = 0; o < NO; ++o) {
+#pragma unroll
+      for (int s = 16; s; s >>= 1) acc[r][o] += __shfl_xor_sync(0xffffffffu, acc[r][o], s);
+    }
   if (lane < no) {
-    float v = 0.f;
 #pragma unroll
-    for (int o = 0; o < NO; ++o)
-      if (o == lane) v = acc[o];
-    v += bias[lane];
-    if (!last) v = act_fwd(act, v);
-    out[(size_t)warp * no + lane] = v;
-    if (!last) outT[(size_t)lane * ldT + tcol[warp]] = v;
+    for (int r = 0; r < R; ++r) {
+      const int row = row0 + r;
+      if (row >= rows) break;
+      float v = 0.f;
+#pragma unroll
+      for (int o = 0; o < NO; ++o)
+        if (o == lane) v = acc[r][o];
+      v += bias[lane];
+      if (!last) v = act_fwd(act, v);
+      out[(size_t)row * no + lane] = v;
+      if (!last) outT[(size_t)lane * ldT + tcol[row]] = v;
+    }
   }
 }
 
@@ -485,8 +537,19 @@ __global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __
       dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
     __syncthreads();
     if (i < in) {
-      for (int rr = 0; rr < cn; ++rr) {
-        const float a = X[(size_t)(r0 + c + rr) * in + i];
+      const float* xp = X + (size_t)(r0 + c) * in + i;
+      int rr = 0;
+      for (; rr + 4 <= cn; rr += 4) {   // loads in flight, FMAs in row order
+        float a[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = __ldg(xp + (size_t)(rr + j) * in);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int o = 0; o < NO; ++o) g[o] = fmaf(a[j], dn[rr + j][o], g[o]);
+      }
+      for (; rr < cn; ++rr) {
+        const float a = __ldg(xp + (size_t)rr * in);
 #pragma unroll
         for (int o = 0; o < NO; ++o) g[o] = fmaf(a, dn[rr][o], g[o]);
       }
@@ -525,11 +588,14 @@ struct SgdArgs {
   int rows, cols;       // tensor shape (bias: rows = 1)
 };
 
-__device__ __forceinline__ bool step_poisoned(const long long* tail, int nflags) {
-  if (tail[kTailNonfinite]) return true;
-  for (int t = 0; t < nflags; ++t)
-    if (tail[kTailOverflow + t]) return true;
-  return false;
+// Block-wide: did the step hit a non-finite value or a fixed-point overflow?
+// One flag per thread (blockDim >= 1 + nflags), no serial chain of loads.
+__device__ __forceinline__ bool block_poisoned(const long long* tail, int nflags) {
+  const int t = threadIdx.x + threadIdx.y * blockDim.x;
+  bool bad = false;
+  if (t == 0) bad = tail[kTailNonfinite] != 0;
+  else if (t <= nflags) bad = tail[kTailOverflow + t - 1] != 0;
+  return __syncthreads_or(bad);
 }
 
 __device__ __forceinline__ double sgd_one(const SgdArgs& a, size_t k, float& w32) {
@@ -562,11 +628,8 @@ __device__ __forceinline__ void block_max_to(unsigned long long* dst, double v) 
 __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
   constexpr int TR = 64, TC = 32, PER = TR / 8;
   __shared__ float tile[TR][TC + 1];
-  __shared__ int poisoned;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  if (tx == 0 && ty == 0) poisoned = step_poisoned(a.tail, a.ntail_flags);
-  __syncthreads();
-  if (poisoned) return;
+  if (block_poisoned(a.tail, a.ntail_flags)) return;
   const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int c = c0 + tx;
   long long S[PER];
@@ -634,10 +697,7 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
 }
 
 __global__ void k_sgd_vec(SgdArgs a) {
-  __shared__ int poisoned;
-  if (threadIdx.x == 0) poisoned = step_poisoned(a.tail, a.ntail_flags);
-  __syncthreads();
-  if (poisoned) return;
+  if (block_poisoned(a.tail, a.ntail_flags)) return;
   const size_t n = (size_t)a.rows * a.cols;
   double mx = 0.0;
   for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
