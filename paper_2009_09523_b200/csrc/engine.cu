@@ -414,10 +414,10 @@ void dispatch_skinny(int no, A&&... a) {
 
 template <int NO>
 struct FwdSkinny {
-  static void run(cudaStream_t s, const float* X, int K, const float* W, int no, const float* b,
+  static void run(cudaStream_t s, const float* X, int K, const float* WT, int no, const float* b,
                   int rows, int act, int last, float* out, float* outT, int ldT, const int* tcol) {
-    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8 * kSkinnyRows), 256, 0, s>>>(X, K, W, no, b, rows, act, last,
-                                                                 out, outT, ldT, tcol);
+    k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8 * skinny_rows<NO>()), 256, 0, s>>>(
+        X, K, WT, no, b, rows, act, last, out, outT, ldT, tcol);
   }
 };
 template <int NO>
@@ -425,7 +425,8 @@ struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
                   int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
                   const float* tscale, float* Dh, float* Dl, float* DTh, float* DTl) {
-    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32 * kBwdSkinnyChunks)),
+        block(32, 8);
     k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
                                             tscale, Dh, Dl, DTh, DTl);
   }
@@ -617,7 +618,8 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     if (e->tc_layer[l]) {
       tc_forward(e, l, rows, ldT, tcol, last);
     } else if (N <= 32) {
-      dispatch_skinny<FwdSkinny>(N, s, e->X[l], K, W, N, b, rows, e->act, last ? 1 : 0,
+      dispatch_skinny<FwdSkinny>(N, s, e->X[l], K, e->wt32 + e->wtoff[l], N, b, rows, e->act,
+                                 last ? 1 : 0,
                                  last ? e->logits : e->X[l + 1], last ? nullptr : e->XT[l + 1],
                                  ldT, tcol);
       VNT_LAUNCH_CHECK();
@@ -829,7 +831,8 @@ void launch_sgd(vnt_engine* e) {
         a.rows = (int)e->widths[l];
         a.cols = (int)e->widths[l + 1];
         dim3 grid((unsigned)ceil_div(a.cols, 32), (unsigned)ceil_div(a.rows, 64)), block(32, 8);
-        k_sgd_weight<<<grid, block, 0, s>>>(a);
+        if (a.v64) k_sgd_weight<true><<<grid, block, 0, s>>>(a);
+        else k_sgd_weight<false><<<grid, block, 0, s>>>(a);
       } else {
         a.rows = 1;
         a.cols = (int)e->widths[l + 1];

@@ -387,21 +387,24 @@ __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict
 }
 
 // ---------------------------------------------- skinny layers (out <= 32)
-constexpr int kSkinnyRows = 4;   // rows per warp in k_fwd_skinny
+template <int NO>   // rows per warp in k_fwd_skinny (R*NO accumulators per lane)
+__host__ __device__ constexpr int skinny_rows() { return NO > 16 ? 2 : 4; }
+constexpr int kBwdSkinnyChunks = 4;   // 32-row chunks per CTA in k_bwd_skinny
 // Forward with few outputs (the 4096 -> 10 classifier): one warp per row,
 // lane-strided partial dot products over k then a fixed xor tree, so every
 // output depends only on its row.
 template <int NO>
 __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X, int K,
-                                                    const float* __restrict__ W, int no,
+                                                    const float* __restrict__ WT, int no,
                                                     const float* __restrict__ bias, int rows,
                                                     int act, int last, float* __restrict__ out,
                                                     float* __restrict__ outT, int ldT,
                                                     const int* __restrict__ tcol) {
-  // A warp owns kSkinnyRows rows so each W[k][:] load serves all of them; per
-  // (row, o) the partial sums still run lane-strided over k and meet in a fixed
-  // xor tree, so every output depends only on its row.
-  constexpr int R = kSkinnyRows;
+  // A warp owns kSkinnyRows rows so each W[k][:] load serves all of them; W is
+  // read through its transposed copy WT[o][k] so a warp's loads are one
+  // coalesced line.  Per (row, o) the partial sums run lane-strided over k and
+  // meet in a fixed xor tree, so every output depends only on its row.
+  constexpr int R = skinny_rows<NO>();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int row0 = warp * R;
@@ -419,11 +422,10 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
     float a[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) a[r] = __ldg(x[r] + k);
-    const float* w = W + (size_t)k * no;
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
       if (o < no) {
-        const float wo = __ldg(w + o);
+        const float wo = __ldg(WT + (size_t)o * K + k);
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r][o] = fmaf(a[r], wo, acc[r][o]);
       }
@@ -468,8 +470,8 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
                                                     float* __restrict__ DTh,
                                                     float* __restrict__ DTl) {
   const float tscale = tscale_p ? *tscale_p : 1.f;
-  // 32 features x 32 rows per block (4 chunks of 32 rows), o ascending per
-  // output; transposed copy through smem.
+  // 32 features x kBwdSkinnyChunks*32 rows per block, o ascending per output;
+  // transposed copy through smem.
   __shared__ float tile[32][33];
   __shared__ float dn[32][NO];
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
@@ -478,8 +480,8 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
   float w[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) w[o] = (i < in && o < no) ? W[(size_t)i * no + o] : 0.f;
-  for (int chunk = 0; chunk < 1; ++chunk) {
-    const int r0 = (blockIdx.y + chunk) * 32;
+  for (int chunk = 0; chunk < kBwdSkinnyChunks; ++chunk) {
+    const int r0 = (blockIdx.y * kBwdSkinnyChunks + chunk) * 32;
     if (r0 >= rows) break;
     __syncthreads();
     for (int k = ty * 32 + tx; k < 32 * NO; k += 256) {
@@ -625,7 +627,8 @@ __device__ __forceinline__ void block_max_to(unsigned long long* dst, double v) 
 // Weight tensor: 64x32 (rows x cols) tiles, 32x8 threads, 8 elements per
 // thread with all loads issued before the dependent math; transposed fp32 copy
 // via smem.
-__global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
+template <bool MOM>   // momentum buffer present (registers for v[] only then)
+__global__ void __launch_bounds__(256, MOM ? 2 : 3) k_sgd_weight(SgdArgs a) {
   constexpr int TR = 64, TC = 32, PER = TR / 8;
   __shared__ float tile[TR][TC + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -633,7 +636,7 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
   const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int c = c0 + tx;
   long long S[PER];
-  double w[PER], v[PER];
+  double w[PER], v[MOM ? PER : 1];
   const double inv_scale = a.sp->inv_scale[a.tensor], inv_b = a.sp->inv_b;
   const double lr = a.sp->lr, mu = a.sp->mu;
 #pragma unroll
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
     const size_t idx = (size_t)r * a.cols + c;
     S[k] = ok ? __ldg(a.G + idx) : 0;
     w[k] = ok ? a.w64[idx] : 0.0;
-    v[k] = (ok && a.v64) ? a.v64[idx] : 0.0;
+    if constexpr (MOM) v[k] = ok ? a.v64[idx] : 0.0;
   }
   double mx = 0.0;
 #pragma unroll
@@ -652,14 +655,14 @@ __global__ void __launch_bounds__(256) k_sgd_weight(SgdArgs a) {
     const bool ok = r < a.rows && c < a.cols;
     const double g = __dmul_rn(__ll2double_rn(S[k]) * inv_scale, inv_b);
     double u = g;
-    if (a.v64) u = __dadd_rn(__dmul_rn(mu, v[k]), g);
+    if constexpr (MOM) u = __dadd_rn(__dmul_rn(mu, v[k]), g);
     const double wn = __dsub_rn(w[k], __dmul_rn(lr, u));
     const float w32 = __double2float_rn(wn);
     tile[ty + 8 * k][tx] = ok ? w32 : 0.f;
     if (ok) {
       const size_t idx = (size_t)r * a.cols + c;
       a.w64[idx] = wn;
-      if (a.v64) a.v64[idx] = u;
+      if constexpr (MOM) a.v64[idx] = u;
       if (a.w32) a.w32[idx] = w32;
       if (a.w32h) {
         const float h = tf32_rna(w32);
