@@ -389,7 +389,7 @@ __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict
 // ---------------------------------------------- skinny layers (out <= 32)
 template <int NO>   // rows per warp in k_fwd_skinny (R*NO accumulators per lane)
 __host__ __device__ constexpr int skinny_rows() { return NO > 16 ? 2 : 4; }
-constexpr int kBwdSkinnyChunks = 4;   // 32-row chunks per CTA in k_bwd_skinny
+constexpr int kBwdSkinnyChunks = 1;   // 32-row chunks per CTA in k_bwd_skinny
 // Forward with few outputs (the 4096 -> 10 classifier): one warp per row,
 // lane-strided partial dot products over k then a fixed xor tree, so every
 // output depends only on its row.
@@ -400,15 +400,16 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
                                                     int act, int last, float* __restrict__ out,
                                                     float* __restrict__ outT, int ldT,
                                                     const int* __restrict__ tcol) {
-  // A warp owns kSkinnyRows rows so each W[k][:] load serves all of them; W is
-  // read through its transposed copy WT[o][k] so a warp's loads are one
-  // coalesced line.  Per (row, o) the partial sums run lane-strided over k and
-  // meet in a fixed xor tree, so every output depends only on its row.
+  // A warp owns R rows so each W value read serves all of them; W^T is staged
+  // through shared memory in k-chunks ([o][k], conflict-free).  Per (row, o)
+  // the partial sums run lane-strided over k in ascending order and meet in a
+  // fixed xor tree, so every output depends only on its row.
   constexpr int R = skinny_rows<NO>();
+  constexpr int KC = 8192 / NO;   // 32 KB of W^T per chunk
+  __shared__ float ws[NO][KC];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int row0 = warp * R;
-  if (row0 >= rows) return;
   const float* x[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) x[r] = X + (size_t)min(row0 + r, rows - 1) * K;
@@ -417,20 +418,32 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int o = 0; o < NO; ++o) acc[r][o] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    const int kn = min(KC, K - k0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < NO * KC; t += blockDim.x) {
+      const int o = t / KC, kk = t % KC;
+      ws[o][kk] = (o < no && kk < kn) ? __ldg(WT + (size_t)o * K + k0 + kk) : 0.f;
+    }
+    __syncthreads();
+    if (row0 < rows) {
 #pragma unroll 2
-  for (int k = lane; k < K; k += 32) {
-    float a[R];
+      for (int kk = lane; kk < kn; kk += 32) {
+        float a[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) a[r] = __ldg(x[r] + k);
+        for (int r = 0; r < R; ++r) a[r] = __ldg(x[r] + k0 + kk);
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      if (o < no) {
-        const float wo = __ldg(WT + (size_t)o * K + k);
+        for (int o = 0; o < NO; ++o) {
+          if (o < no) {
+            const float wo = ws[o][kk];
 #pragma unroll
-        for (int r = 0; r < R; ++r) acc[r][o] = fmaf(a[r], wo, acc[r][o]);
+            for (int r = 0; r < R; ++r) acc[r][o] = fmaf(a[r], wo, acc[r][o]);
+          }
+        }
       }
     }
   }
+  if (row0 >= rows) return;
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -632,15 +645,12 @@ __global__ void __launch_bounds__(256, MOM ? 2 : 3) k_sgd_weight(SgdArgs a) {
   constexpr int TR = 64, TC = 32, PER = TR / 8;
   __shared__ float tile[TR][TC + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
-  if (block_poisoned(a.tail, a.ntail_flags)) return;
   const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int c = c0 + tx;
   long long S[PER];
   double w[PER], v[MOM ? PER : 1];
-  const double inv_scale = a.sp->inv_scale[a.tensor], inv_b = a.sp->inv_b;
-  const double lr = a.sp->lr, mu = a.sp->mu;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
+  for (int k = 0; k < PER; ++k) {   // loads first: the poison check overlaps them
     const int r = r0 + ty + 8 * k;
     const bool ok = r < a.rows && c < a.cols;
     const size_t idx = (size_t)r * a.cols + c;
@@ -648,6 +658,9 @@ __global__ void __launch_bounds__(256, MOM ? 2 : 3) k_sgd_weight(SgdArgs a) {
     w[k] = ok ? a.w64[idx] : 0.0;
     if constexpr (MOM) v[k] = ok ? a.v64[idx] : 0.0;
   }
+  if (block_poisoned(a.tail, a.ntail_flags)) return;
+  const double inv_scale = a.sp->inv_scale[a.tensor], inv_b = a.sp->inv_b;
+  const double lr = a.sp->lr, mu = a.sp->mu;
   double mx = 0.0;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
