@@ -22,6 +22,7 @@
 #include "../../include/vnt_engine.h"
 #include "common.cuh"
 #include "kernels_simt.cuh"
+#include "kernels_node.cuh"
 
 using namespace vntb;
 
@@ -111,6 +112,9 @@ struct vnt_engine {
   std::vector<float*> X, XT, D, DT;
   // 3xTF32 operand twins (hi = rna_tf32(x), lo = x - hi), only when split.
   bool split = false;
+  // whole-node kernel for small all-FFMA models (kernels_node.cuh)
+  bool node_path = false;
+  int node_rc_max = 0;
   std::vector<float*> Xh, Xl, XTh, XTl, Dh, Dl, DTh, DTl;
   float *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
   float* logits = nullptr;
@@ -555,9 +559,93 @@ bool take_prefetch(vnt_engine* e, const double* x, const double* y) {
   return true;
 }
 
+// Shared-memory floats per row of the whole-node kernel: activations of every
+// layer plus deltas padded to kNodeOC (+3 for the float4 alignment of the deltas).
+uint64_t node_row_floats(const vnt_engine* e) {
+  uint64_t f = 4;
+  for (int l = 0; l <= e->L; ++l) {
+    f += e->widths[l];
+    if (l > 0) f += (uint64_t)node_ld((int)e->widths[l]);
+  }
+  return f;
+}
+
+uint64_t node_wt_floats(const vnt_engine* e) {
+  uint64_t f = 0;
+  for (int l = 0; l < e->L; ++l) f += e->widths[l] * e->widths[l + 1];
+  return f;
+}
+
+// LayerStats::combine of each device's nodes into its lineage (ascending node id).
+void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats) {
+  const uint64_t in = e->widths[0];
+  cudaStream_t s = e->stream;
+  for (const auto& sl : stats) {
+    VNT_CUDA(cudaMemcpyAsync(e->d_combine + sl.off, e->h_combine + sl.off,
+                             sl.n * sizeof(CombineStep), cudaMemcpyHostToDevice, s));
+    k_stats_combine<<<(unsigned)ceil_div(in, 128), 128, 0, s>>>(
+        e->devs[sl.dev].mean, e->devs[sl.dev].m2, (int)in, e->vn_mean, e->vn_m2,
+        e->d_combine + sl.off, sl.n);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+  }
+}
+
+// Small models: one k_node_step CTA per node does the whole pass.
+void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats) {
+  const size_t nn = p.nodes.size();
+  const int* row0 = p.d_meta + p.rows;
+  const int* nrows = row0 + nn;
+  NodeArgs a{};
+  a.x = e->xin;
+  a.y = e->yin;
+  a.row0 = row0;
+  a.nrows = nrows;
+  a.w32 = e->w32;
+  a.wt32 = e->wt32;
+  a.L = e->L;
+  for (int l = 0; l <= e->L; ++l) a.w[l] = (int)e->widths[l];
+  a.nstrips = 0;
+  for (int l = 0; l < e->L; ++l) {
+    a.woff[l] = (int)e->woff[l];
+    a.boff[l] = (int)e->boff[l];
+    a.wtoff[l] = (int)e->wtoff[l];
+    a.nstrips += (int)((e->widths[l] + 1) * ceil_div(e->widths[l + 1], (uint64_t)kNodeOC));
+  }
+  a.wt_total = (int)node_wt_floats(e);
+  a.act = e->act;
+  a.loss = e->loss;
+  uint64_t maxrows = 1;
+  for (const auto& pn : p.nodes) maxrows = std::max<uint64_t>(maxrows, pn.rows);
+  a.rc = (int)std::min<uint64_t>(maxrows, (uint64_t)e->node_rc_max);
+  a.sp = e->d_sp;
+  a.lim = pow2f(kLimBits);
+  a.G = e->G;
+  a.tail = e->G + e->P;
+  a.vn_mean = stats ? e->vn_mean : nullptr;
+  a.vn_m2 = stats ? e->vn_m2 : nullptr;
+  const size_t smem = ((size_t)a.rc * node_row_floats(e) + node_wt_floats(e) + 8) * sizeof(float);
+  static size_t smem_attr = 0;
+  if (smem > smem_attr) {
+    VNT_CUDA(cudaFuncSetAttribute(k_node_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(smem, 48 * 1024)));
+    smem_attr = std::max<size_t>(smem, 48 * 1024);
+  }
+  k_node_step<<<(unsigned)nn, kNodeThreads, smem, e->stream>>>(a);
+  VNT_LAUNCH_CHECK();
+  e->launches++;
+  if (stats) combine_stats(e, *stats);
+}
+
 // Device work of one pass (inputs already staged in xin/yin).
+void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats);
+
 void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats,
               bool first_write) {
+  if (e->node_path) {
+    run_node_pass(e, p, stats);
+    return;
+  }
   const int L = e->L;
   const uint64_t in = e->widths[0], out = e->widths[L];
   const size_t nn = p.nodes.size();
@@ -598,15 +686,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     k_vn_stats<<<grid, 128, 0, s>>>(e->xin, (int)in, row0, nrows, e->vn_mean, e->vn_m2);
     VNT_LAUNCH_CHECK();
     e->launches++;
-    for (const auto& sl : *stats) {
-      VNT_CUDA(cudaMemcpyAsync(e->d_combine + sl.off, e->h_combine + sl.off,
-                               sl.n * sizeof(CombineStep), cudaMemcpyHostToDevice, s));
-      k_stats_combine<<<(unsigned)ceil_div(in, 128), 128, 0, s>>>(
-          e->devs[sl.dev].mean, e->devs[sl.dev].m2, (int)in, e->vn_mean, e->vn_m2,
-          e->d_combine + sl.off, sl.n);
-      VNT_LAUNCH_CHECK();
-      e->launches++;
-    }
+    combine_stats(e, *stats);
   }
   // Forward (model.cpp:275-287).
   for (int l = 0; l < L; ++l) {
@@ -731,11 +811,15 @@ void begin_round_device(vnt_engine* e) {
   tail_reset(e);
   // Slices filled by exact int64 atomics start from zero (bias always, weights
   // of non-tcgen05 layers); tcgen05 dW tiles store on the first pass.
+  if (e->node_path) {
+    VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
+  } else {
   for (int l = 0; l < e->L; ++l) {
     VNT_CUDA(cudaMemsetAsync(e->G + e->boff[l], 0, e->widths[l + 1] * sizeof(long long), e->stream));
     if (!e->tc_layer[l])
       VNT_CUDA(cudaMemsetAsync(e->G + e->woff[l], 0, e->widths[l] * e->widths[l + 1] * sizeof(long long),
                                e->stream));
+  }
   }
   const uint64_t in = e->widths[0];
   for (auto& d : e->devs) {
@@ -803,6 +887,34 @@ void collective(vnt_engine* e) {
 void launch_sgd(vnt_engine* e) {
   cudaStream_t s = e->stream;
   VNT_CUDA(cudaMemsetAsync(e->gmax, 0, ntensors(e) * sizeof(unsigned long long), s));
+  if (e->node_path) {   // all tensors in one launch, row-major fp32 copies only
+    SgdMulti m{};
+    uint64_t maxn = 1;
+    for (int t = 0; t < (int)ntensors(e); ++t) {
+      const int l = t / 2;
+      SgdArgs& a = m.t[t];
+      const uint64_t off = (t & 1) ? e->boff[l] : e->woff[l];
+      a.w64 = e->w64 + off;
+      a.v64 = e->v64 ? e->v64 + off : nullptr;
+      a.G = e->G + off;
+      a.w32 = e->w32 + off;
+      a.wt32 = (t & 1) ? nullptr : e->wt32 + e->wtoff[l];
+      a.gout = e->gout ? e->gout + off : nullptr;
+      a.gmax = e->gmax + t;
+      a.tail = e->G + e->P;
+      a.ntail_flags = (int)ntensors(e);
+      a.sp = e->d_sp;
+      a.tensor = t;
+      a.rows = (t & 1) ? 1 : (int)e->widths[l];
+      a.cols = (int)e->widths[l + 1];
+      maxn = std::max<uint64_t>(maxn, (uint64_t)a.rows * a.cols);
+    }
+    dim3 grid((unsigned)std::min<uint64_t>(ceil_div(maxn, 256), 64), (unsigned)ntensors(e));
+    k_sgd_multi<<<grid, 256, 0, s>>>(m);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+    return;
+  }
   for (int l = 0; l < e->L; ++l) {
     for (int part = 0; part < 2; ++part) {
       const int t = 2 * l + part;
@@ -1161,6 +1273,22 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
       e->tc_layer.push_back(tc_layer_eligible(e->opt.gemm_mode, e->widths[l], e->widths[l + 1]));
     }
     e->P = off;
+    {
+      // Chosen from the widths alone, so every run of a model takes the same path.
+      bool any_tc = false;
+      uint64_t strips = 0;
+      for (int l = 0; l < e->L; ++l) {
+        any_tc |= e->tc_layer[l] != 0;
+        strips += (e->widths[l] + 1) * ceil_div(e->widths[l + 1], (uint64_t)vntb::kNodeOC);
+      }
+      const uint64_t budget = 200 * 1024 / sizeof(float);
+      const uint64_t per_row = node_row_floats(e.get()), wt = node_wt_floats(e.get()) + 8;
+      e->node_rc_max = wt >= budget ? 0
+                                    : (int)std::min<uint64_t>(256, (budget - wt) / std::max<uint64_t>(per_row, 1));
+      const bool off_env = getenv("VNT_NODE_KERNEL") && getenv("VNT_NODE_KERNEL")[0] == '0';
+      e->node_path = !off_env && !any_tc && e->L <= vntb::kNodeMaxLayers &&
+                     strips <= (uint64_t)vntb::kNodeMaxStrips && e->node_rc_max >= 1;
+    }
     bind(e.get());
     VNT_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     VNT_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));

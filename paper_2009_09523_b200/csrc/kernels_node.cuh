@@ -1,0 +1,302 @@
+// Whole-node kernel for small all-FFMA models (the reference's smallest MLP,
+// BASELINE configs 1/2: [784, 16, 10], micro-batch 16).
+//
+// At that size the layered kernels are launch-latency bound (~25 dependent
+// launches per step for a few MFLOP).  Here one CTA runs one virtual node
+// end to end out of shared memory — fp64 rows in, input statistics
+// (model.cpp:101-121), forward (model.cpp:270-287), loss and output delta
+// (model.cpp:289-315), backward (model.cpp:317-338), and the node's dW/db sums
+// — then quantises the per-node partials and adds them into the exact int64
+// gradient sum G, exactly like the layered path does.
+//
+// Determinism: every value is a fixed-order fp32 chain over one row (forward,
+// backward) or over the node's rows in ascending order (dW, db), so the
+// result is a function of the node's rows only — independent of which device
+// or pass runs the node.  The engine picks this path from the layer widths
+// alone (never from rows or mapping), so every run of a model uses it.
+#pragma once
+
+namespace vntb {
+
+constexpr int kNodeMaxLayers = 8;
+constexpr int kNodeThreads = 512;
+constexpr int kNodeOC = 16;       // outputs per strip / per forward task
+constexpr int kNodeStrips = 2;    // dW strips per thread
+constexpr int kNodeMaxStrips = kNodeThreads * kNodeStrips;
+
+struct NodeArgs {
+  const double* x;       // staged pass rows (row-major, fp64)
+  const double* y;
+  const int* row0;       // per node of the pass: first row, row count
+  const int* nrows;
+  const float* w32;      // fp32 parameters, reference layout (model.cpp:62-77)
+  const float* wt32;     // transposed weights WT[l][o][i]
+  int L;
+  int w[kNodeMaxLayers + 1];
+  int woff[kNodeMaxLayers], boff[kNodeMaxLayers], wtoff[kNodeMaxLayers];
+  int nstrips;           // sum_l (w[l] + 1) * ceil(w[l+1] / kNodeOC)
+  int wt_total;          // sum_l w[l] * w[l+1]: W^T staged in shared memory
+  int act, loss;
+  int rc;                // rows per shared-memory chunk
+  const StepParams* sp;  // per-tensor 2^s
+  float lim;
+  long long* G;          // exact gradient sum (zeroed) + tail
+  long long* tail;
+  double* vn_mean;       // per-node input stats, or null
+  double* vn_m2;
+};
+
+__host__ __device__ constexpr int node_ld(int w) { return (w + kNodeOC - 1) / kNodeOC * kNodeOC; }
+
+// Row loss + output delta of one row (k_loss's arithmetic), one warp.
+__device__ __forceinline__ void node_row_loss(const float* z, const double* yr, int outw,
+                                              int loss_kind, float* d, long long* tail) {
+  const int lane = threadIdx.x & 31;
+  double loss = 0.0;
+  if (loss_kind == 0) {
+    for (int o = lane; o < outw; o += 32) {
+      const double df = (double)z[o] - yr[o];
+      loss += df * df;
+      d[o] = (float)(2.0 * df / (double)outw);
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
+    loss /= (double)outw;
+  } else {
+    double mx = -1e300;
+    for (int o = lane; o < outw; o += 32) mx = fmax(mx, (double)z[o]);
+#pragma unroll
+    for (int s = 16; s; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    double norm = 0.0;
+    for (int o = lane; o < outw; o += 32) norm += exp((double)z[o] - mx);
+#pragma unroll
+    for (int s = 16; s; s >>= 1) norm += __shfl_xor_sync(0xffffffffu, norm, s);
+    const double lognorm = log(norm);
+    for (int o = lane; o < outw; o += 32) {
+      const double zm = (double)z[o] - mx;
+      loss -= yr[o] * (zm - lognorm);
+      d[o] = (float)(exp(zm) / norm - yr[o]);
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
+  }
+  if (lane == 0) {
+    if (!isfinite(loss)) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
+    } else {
+      const long long q = __double2ll_rn(ldexp(loss, kLossScaleBits));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailLoss]), (unsigned long long)q);
+    }
+  }
+}
+
+// dW/db strip s -> (layer l, input row i (== w[l]: the bias), first output o0).
+// Strips run i fastest so a warp shares one D row segment (smem broadcast).
+__device__ __forceinline__ void node_strip(const NodeArgs& a, int s, int& l, int& i, int& o0) {
+  l = 0;
+  for (;;) {
+    const int nch = (a.w[l + 1] + kNodeOC - 1) / kNodeOC;
+    const int cnt = (a.w[l] + 1) * nch;
+    if (s < cnt || l + 1 == a.L) break;
+    s -= cnt;
+    ++l;
+  }
+  const int rowsl = a.w[l] + 1;
+  o0 = (s / rowsl) * kNodeOC;
+  i = s - (s / rowsl) * rowsl;
+}
+
+__global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
+  extern __shared__ float sm[];
+  __shared__ int aoff[kNodeMaxLayers + 1], doff[kNodeMaxLayers + 1];
+  __shared__ int wts_off;
+  const int node = blockIdx.x;
+  const int r0 = a.row0[node], n = a.nrows[node];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  const int L = a.L, in = a.w[0], outw = a.w[L];
+  if (tid == 0) {
+    int off = 0;
+    for (int l = 0; l <= L; ++l) {
+      aoff[l] = off;
+      off += a.rc * a.w[l];
+    }
+    off = (off + 3) & ~3;
+    doff[0] = 0;
+    for (int l = 1; l <= L; ++l) {
+      doff[l] = off;
+      off += a.rc * node_ld(a.w[l]);
+    }
+    wts_off = (off + 3) & ~3;
+  }
+  __syncthreads();
+  // every layer's W^T into shared memory once (coalesced, all threads)
+  {
+    const float4* src = reinterpret_cast<const float4*>(a.wt32);
+    float4* dst = reinterpret_cast<float4*>(sm + wts_off);
+    const int n4 = a.wt_total / 4;
+    for (int t = tid; t < n4; t += nt) dst[t] = __ldg(src + t);
+    for (int t = 4 * n4 + tid; t < a.wt_total; t += nt) sm[wts_off + t] = __ldg(a.wt32 + t);
+  }
+  // LayerStats::observe of this node (same arithmetic as k_vn_stats)
+  if (a.vn_mean) {
+    for (int j = tid; j < in; j += nt)
+      node_feature_stats(a.x, in, r0, n, j, &a.vn_mean[(size_t)node * in + j],
+                         &a.vn_m2[(size_t)node * in + j]);
+  }
+  float g[kNodeStrips][kNodeOC];
+#pragma unroll
+  for (int q = 0; q < kNodeStrips; ++q)
+#pragma unroll
+    for (int j = 0; j < kNodeOC; ++j) g[q][j] = 0.f;
+
+  for (int c0 = 0; c0 < n; c0 += a.rc) {
+    const int rn = min(a.rc, n - c0);
+    __syncthreads();
+    {   // fp64 rows -> fp32 activations of layer 0
+      float* A0 = sm + aoff[0];
+      const double* xs = a.x + (size_t)(r0 + c0) * in;
+      for (int t = tid; t < rn * in; t += nt) A0[t] = __double2float_rn(xs[t]);
+    }
+    __syncthreads();
+    // forward (model.cpp:280-286): one warp per (row, 16 outputs); lanes take
+    // k = lane, lane+32, ... in ascending order, then a fixed xor tree, + bias.
+    for (int l = 0; l < L; ++l) {
+      const int K = a.w[l], N = a.w[l + 1];
+      const int nch = (N + kNodeOC - 1) / kNodeOC;
+      const float* WT = sm + wts_off + a.wtoff[l];
+      const float* b = a.w32 + a.boff[l];
+      const float* Ain = sm + aoff[l];
+      float* Aout = sm + aoff[l + 1];
+      const bool hidden = l < L - 1;
+      for (int task = warp; task < rn * nch; task += nwarps) {
+        const int r = task / nch, o0 = (task - (task / nch) * nch) * kNodeOC;
+        const int on = min(kNodeOC, N - o0);
+        const float* ar = Ain + r * K;
+        float acc[kNodeOC];
+#pragma unroll
+        for (int j = 0; j < kNodeOC; ++j) acc[j] = 0.f;
+#pragma unroll 2
+        for (int k = lane; k < K; k += 32) {
+          const float av = ar[k];
+#pragma unroll
+          for (int j = 0; j < kNodeOC; ++j)
+            if (j < on) acc[j] = fmaf(av, WT[(o0 + j) * K + k], acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kNodeOC; ++j) {
+#pragma unroll
+          for (int sft = 16; sft; sft >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], sft);
+        }
+        float v = 0.f;
+#pragma unroll
+        for (int j = 0; j < kNodeOC; ++j)
+          if (j == lane) v = acc[j];
+        if (lane < on) {
+          const float z = v + __ldg(b + o0 + lane);
+          Aout[r * N + o0 + lane] = hidden ? act_fwd(a.act, z) : z;
+        }
+      }
+      __syncthreads();
+    }
+    // loss + output delta, one warp per row
+    for (int r = warp; r < rn; r += nwarps)
+      node_row_loss(sm + aoff[L] + r * outw, a.y + (size_t)(r0 + c0 + r) * outw, outw, a.loss,
+                    sm + doff[L] + r * node_ld(outw), a.tail);
+    __syncthreads();
+    // backward (model.cpp:328-337): d[l][r][i] = (sum_o d[l+1][r][o] W[i][o]) f'(a[l][r][i]),
+    // o ascending; lanes over i read W^T rows (coalesced).
+    for (int l = L - 1; l >= 1; --l) {
+      const int K = a.w[l], N = a.w[l + 1];
+      const int ldn = node_ld(N), ldl = node_ld(K);
+      const float* WT = sm + wts_off + a.wtoff[l];
+      const float* Dn = sm + doff[l + 1];
+      const float* Al = sm + aoff[l];
+      float* Dl = sm + doff[l];
+      const int nic = (K + 31) / 32;
+      for (int task = warp; task < rn * nic; task += nwarps) {
+        const int r = task / nic, i = (task - (task / nic) * nic) * 32 + lane;
+        if (i < K) {
+          const float* dr = Dn + r * ldn;
+          float acc = 0.f;
+          for (int o = 0; o < N; ++o) acc = fmaf(dr[o], WT[o * K + i], acc);
+          Dl[r * ldl + i] = acc * act_grad_from_out(a.act, Al[r * K + i]);
+        }
+      }
+      __syncthreads();
+    }
+    // this chunk's rows into the node's dW / db strips, rows ascending
+#pragma unroll
+    for (int q = 0; q < kNodeStrips; ++q) {
+      const int st = tid + q * nt;
+      if (st < a.nstrips) {
+        int l, i, o0;
+        node_strip(a, st, l, i, o0);
+        const int K = a.w[l];
+        const bool bias = i == K;
+        const float* dc = sm + doff[l + 1] + o0;
+        const int ldn = node_ld(a.w[l + 1]);
+        const float* ac = sm + aoff[l] + (bias ? 0 : i);
+        for (int r = 0; r < rn; ++r) {
+          const float av = bias ? 1.f : ac[r * K];   // 1 * d is exact: db = sum_r d
+          const float4* d4 = reinterpret_cast<const float4*>(dc + r * ldn);
+#pragma unroll
+          for (int j4 = 0; j4 < kNodeOC / 4; ++j4) {
+            const float4 dv = d4[j4];
+            g[q][4 * j4 + 0] = fmaf(av, dv.x, g[q][4 * j4 + 0]);
+            g[q][4 * j4 + 1] = fmaf(av, dv.y, g[q][4 * j4 + 1]);
+            g[q][4 * j4 + 2] = fmaf(av, dv.z, g[q][4 * j4 + 2]);
+            g[q][4 * j4 + 3] = fmaf(av, dv.w, g[q][4 * j4 + 3]);
+          }
+        }
+      }
+    }
+  }
+  // per-node quantisation into the exact sum (order-free int64 atomics)
+#pragma unroll
+  for (int q = 0; q < kNodeStrips; ++q) {
+    const int st = tid + q * nt;
+    if (st < a.nstrips) {
+      int l, i, o0;
+      node_strip(a, st, l, i, o0);
+      const int K = a.w[l], N = a.w[l + 1];
+      const bool bias = i == K;
+      const int t = 2 * l + (bias ? 1 : 0);
+      const float scale = a.sp->scale[t];
+      long long* gp = a.G + (bias ? a.boff[l] : a.woff[l] + i * N) + o0;
+#pragma unroll
+      for (int j = 0; j < kNodeOC; ++j) {
+        if (o0 + j < N) {
+          const long long qv = quantise(g[q][j], scale, a.lim, a.tail, t);
+          if (qv) atomicAdd(reinterpret_cast<unsigned long long*>(gp + j), (unsigned long long)qv);
+        }
+      }
+    }
+  }
+}
+
+// SGD of every tensor of a small model in one launch (blockIdx.y = tensor):
+// k_sgd_vec's arithmetic on each flat tensor, plus the transposed fp32 copy.
+struct SgdMulti {
+  SgdArgs t[2 * kNodeMaxLayers];
+};
+
+__global__ void __launch_bounds__(256) k_sgd_multi(const __grid_constant__ SgdMulti m) {
+  const SgdArgs& a = m.t[blockIdx.y];
+  if (block_poisoned(a.tail, a.ntail_flags)) return;
+  const size_t n = (size_t)a.rows * a.cols;
+  double mx = 0.0;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+       k += (size_t)gridDim.x * blockDim.x) {
+    float w32;
+    mx = fmax(mx, sgd_one(a, k, w32));
+    a.w32[k] = w32;
+    if (a.wt32) {   // W^T[o][i] for the whole-node forward / backward
+      const size_t i = k / a.cols, o = k - (k / a.cols) * a.cols;
+      a.wt32[o * a.rows + i] = w32;
+    }
+  }
+  block_max_to(a.gmax, mx);
+}
+
+}  // namespace vntb

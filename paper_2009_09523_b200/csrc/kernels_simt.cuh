@@ -79,13 +79,9 @@ __global__ void k_ingest(const double* __restrict__ x, float* __restrict__ X0,
 // LayerStats::observe batch part (model.cpp:101-121): per node, per feature,
 // sequential fp64 sums in row order; __d*_rn forbid FMA contraction so the
 // result is bit-identical to the reference's x86-64 build.
-__global__ void k_vn_stats(const double* __restrict__ x, int in, const int* __restrict__ vn_row0,
-                           const int* __restrict__ vn_rows, double* __restrict__ vn_mean,
-                           double* __restrict__ vn_m2) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k = blockIdx.y;
-  if (j >= in) return;
-  const int r0 = vn_row0[k], n = vn_rows[k];
+// One feature j of one node (rows r0..r0+n-1 of x): fp64 mean and M2 in row order.
+__device__ __forceinline__ void node_feature_stats(const double* __restrict__ x, int in, int r0,
+                                                   int n, int j, double* mean, double* m2) {
   const double* xp = x + (size_t)r0 * in + j;
   double m = 0.0;
   int r = 0;
@@ -114,8 +110,18 @@ __global__ void k_vn_stats(const double* __restrict__ x, int in, const int* __re
     const double d = __dsub_rn(__ldg(xp + (size_t)r * in), m);
     s = __dadd_rn(s, __dmul_rn(d, d));
   }
-  vn_mean[(size_t)k * in + j] = m;
-  vn_m2[(size_t)k * in + j] = s;
+  *mean = m;
+  *m2 = s;
+}
+
+__global__ void k_vn_stats(const double* __restrict__ x, int in, const int* __restrict__ vn_row0,
+                           const int* __restrict__ vn_rows, double* __restrict__ vn_mean,
+                           double* __restrict__ vn_m2) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (j >= in) return;
+  node_feature_stats(x, in, vn_row0[k], vn_rows[k], j, &vn_mean[(size_t)k * in + j],
+                     &vn_m2[(size_t)k * in + j]);
 }
 
 // LayerStats::combine (model.cpp:123-139) of a device's nodes, ascending id.
@@ -134,16 +140,30 @@ __global__ void k_stats_combine(double* __restrict__ mean, double* __restrict__ 
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= in) return;
   double mu = mean[j], s = m2[j];
-  for (int t = 0; t < nsteps; ++t) {
-    const CombineStep st = steps[t];
-    const double om = vn_mean[(size_t)st.vn * in + j], os = vn_m2[(size_t)st.vn * in + j];
-    if (st.copy) {
-      mu = om;
-      s = os;
-    } else {
-      const double delta = __dsub_rn(om, mu);
-      s = __dadd_rn(s, __dadd_rn(os, __dmul_rn(__dmul_rn(delta, delta), st.f1)));
-      mu = __dadd_rn(mu, __dmul_rn(delta, st.f2));
+  for (int t0 = 0; t0 < nsteps; t0 += 8) {   // 8 nodes' stats in flight, applied in order
+    const int tn = min(8, nsteps - t0);
+    CombineStep st[8];
+    double om[8], os[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < tn) st[q] = steps[t0 + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < tn) {
+        om[q] = vn_mean[(size_t)st[q].vn * in + j];
+        os[q] = vn_m2[(size_t)st[q].vn * in + j];
+      }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q >= tn) break;
+      if (st[q].copy) {
+        mu = om[q];
+        s = os[q];
+      } else {
+        const double delta = __dsub_rn(om[q], mu);
+        s = __dadd_rn(s, __dadd_rn(os[q], __dmul_rn(__dmul_rn(delta, delta), st[q].f1)));
+        mu = __dadd_rn(mu, __dmul_rn(delta, st[q].f2));
+      }
     }
   }
   mean[j] = mu;
