@@ -115,6 +115,10 @@ struct vnt_engine {
   // whole-node kernel for small all-FFMA models (kernels_node.cuh)
   bool node_path = false;
   int node_rc_max = 0;
+  float* wpad = nullptr;               // padded weight image of k_node_step
+  cudaStream_t aux_stream = nullptr;   // input-statistics branch beside k_node_step
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  uint64_t tail_examples = 0;          // examples node kernels already added to the tail
   std::vector<float*> Xh, Xl, XTh, XTl, Dh, Dl, DTh, DTl;
   float *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
   float* logits = nullptr;
@@ -399,7 +403,10 @@ void split_into(vnt_engine* e, const float* x, float* hi, float* lo, size_t n) {
   e->launches++;
 }
 
+void node_pad(vnt_engine* e);
+
 void split_weights(vnt_engine* e) {
+  if (e->node_path) node_pad(e);
   if (!e->split) return;
   split_into(e, e->w32, e->w32h, e->w32l, e->P);
   uint64_t tot = 0;
@@ -570,16 +577,28 @@ uint64_t node_row_floats(const vnt_engine* e) {
   return f;
 }
 
-uint64_t node_wt_floats(const vnt_engine* e) {
-  uint64_t f = 0;
-  for (int l = 0; l < e->L; ++l) f += e->widths[l] * e->widths[l + 1];
-  return f;
+// Padded weight image (float4 multiple) + float4 over-read slack + alignment.
+uint64_t node_wpad_floats(const vnt_engine* e) {
+  int w[kNodeMaxLayers + 1] = {};
+  for (int l = 0; l <= e->L && l <= kNodeMaxLayers; ++l) w[l] = (int)e->widths[l];
+  return (uint64_t)node_wpad_offset(w, std::min(e->L, kNodeMaxLayers));
+}
+uint64_t node_wt_floats(const vnt_engine* e) { return node_wpad_floats(e) + 20; }
+
+void node_pad(vnt_engine* e) {
+  int w[kNodeMaxLayers + 1] = {};
+  for (int l = 0; l <= e->L; ++l) w[l] = (int)e->widths[l];
+  for (int l = 0; l < e->L; ++l) {
+    const int K = w[l], N = w[l + 1];
+    k_node_pad<<<(unsigned)std::min<uint64_t>(ceil_div((uint64_t)K * N, 256), 256), 256, 0,
+                 e->stream>>>(e->w32 + e->woff[l], e->wpad + node_wpad_offset(w, l), K, N);
+    VNT_LAUNCH_CHECK();
+  }
 }
 
 // LayerStats::combine of each device's nodes into its lineage (ascending node id).
-void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats) {
+void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStream_t s) {
   const uint64_t in = e->widths[0];
-  cudaStream_t s = e->stream;
   for (const auto& sl : stats) {
     VNT_CUDA(cudaMemcpyAsync(e->d_combine + sl.off, e->h_combine + sl.off,
                              sl.n * sizeof(CombineStep), cudaMemcpyHostToDevice, s));
@@ -602,17 +621,16 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   a.row0 = row0;
   a.nrows = nrows;
   a.w32 = e->w32;
-  a.wt32 = e->wt32;
+  a.wpad = e->wpad;
+  a.wpad_floats = (int)node_wpad_floats(e);
   a.L = e->L;
   for (int l = 0; l <= e->L; ++l) a.w[l] = (int)e->widths[l];
   a.nstrips = 0;
   for (int l = 0; l < e->L; ++l) {
     a.woff[l] = (int)e->woff[l];
     a.boff[l] = (int)e->boff[l];
-    a.wtoff[l] = (int)e->wtoff[l];
     a.nstrips += (int)((e->widths[l] + 1) * ceil_div(e->widths[l + 1], (uint64_t)kNodeOC));
   }
-  a.wt_total = (int)node_wt_floats(e);
   a.act = e->act;
   a.loss = e->loss;
   uint64_t maxrows = 1;
@@ -622,8 +640,7 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   a.lim = pow2f(kLimBits);
   a.G = e->G;
   a.tail = e->G + e->P;
-  a.vn_mean = stats ? e->vn_mean : nullptr;
-  a.vn_m2 = stats ? e->vn_m2 : nullptr;
+  a.examples = (long long)p.rows;
   const size_t smem = ((size_t)a.rc * node_row_floats(e) + node_wt_floats(e) + 8) * sizeof(float);
   static size_t smem_attr = 0;
   if (smem > smem_attr) {
@@ -631,10 +648,23 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
                                   (int)std::max<size_t>(smem, 48 * 1024)));
     smem_attr = std::max<size_t>(smem, 48 * 1024);
   }
+  // Input statistics depend on x only: a side-stream branch beside the node kernel.
+  if (stats) {
+    VNT_CUDA(cudaEventRecord(e->fork_ev, e->stream));
+    VNT_CUDA(cudaStreamWaitEvent(e->aux_stream, e->fork_ev, 0));
+    dim3 grid((unsigned)ceil_div(e->widths[0], 128), (unsigned)nn);
+    k_vn_stats<<<grid, 128, 0, e->aux_stream>>>(e->xin, (int)e->widths[0], row0, nrows, e->vn_mean,
+                                                e->vn_m2);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+    combine_stats(e, *stats, e->aux_stream);
+    VNT_CUDA(cudaEventRecord(e->join_ev, e->aux_stream));
+  }
   k_node_step<<<(unsigned)nn, kNodeThreads, smem, e->stream>>>(a);
   VNT_LAUNCH_CHECK();
   e->launches++;
-  if (stats) combine_stats(e, *stats);
+  e->tail_examples += p.rows;
+  if (stats) VNT_CUDA(cudaStreamWaitEvent(e->stream, e->join_ev, 0));
 }
 
 // Device work of one pass (inputs already staged in xin/yin).
@@ -686,7 +716,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     k_vn_stats<<<grid, 128, 0, s>>>(e->xin, (int)in, row0, nrows, e->vn_mean, e->vn_m2);
     VNT_LAUNCH_CHECK();
     e->launches++;
-    combine_stats(e, *stats);
+    combine_stats(e, *stats, e->stream);
   }
   // Forward (model.cpp:275-287).
   for (int l = 0; l < L; ++l) {
@@ -798,6 +828,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
 
 void begin_round_host(vnt_engine* e, uint64_t batch_hint) {
   e->acc_examples = 0;
+  e->tail_examples = 0;
   e->acc_started = false;
   e->round_open = true;
   if (!e->scales_init) {
@@ -898,7 +929,6 @@ void launch_sgd(vnt_engine* e) {
       a.v64 = e->v64 ? e->v64 + off : nullptr;
       a.G = e->G + off;
       a.w32 = e->w32 + off;
-      a.wt32 = (t & 1) ? nullptr : e->wt32 + e->wtoff[l];
       a.gout = e->gout ? e->gout + off : nullptr;
       a.gmax = e->gmax + t;
       a.tail = e->G + e->P;
@@ -907,6 +937,12 @@ void launch_sgd(vnt_engine* e) {
       a.tensor = t;
       a.rows = (t & 1) ? 1 : (int)e->widths[l];
       a.cols = (int)e->widths[l + 1];
+      if (!(t & 1)) {
+        int w[kNodeMaxLayers + 1] = {};
+        for (int k = 0; k <= e->L; ++k) w[k] = (int)e->widths[k];
+        a.wpad = e->wpad + node_wpad_offset(w, l);
+        a.ldw = node_ldw(a.cols);
+      }
       maxn = std::max<uint64_t>(maxn, (uint64_t)a.rows * a.cols);
     }
     dim3 grid((unsigned)std::min<uint64_t>(ceil_div(maxn, 256), 64), (unsigned)ntensors(e));
@@ -1001,10 +1037,21 @@ void update_scales(vnt_engine* e, uint64_t batch) {
 // Adds the examples count into the exact tail (so it is summed by the collective).
 __global__ void k_tail_add(long long* tail, int slot, long long v) { tail[slot] += v; }
 
+// Examples of this round not yet in the tail (whole-node kernels add their own).
+void add_examples_tail(vnt_engine* e) {
+  const long long rest = (long long)e->acc_examples - (long long)e->tail_examples;
+  if (rest == 0) return;
+  k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, rest);
+  VNT_LAUNCH_CHECK();
+  e->launches++;
+  e->tail_examples = e->acc_examples;
+}
+
 void reset_acc(vnt_engine* e) {
   e->round_open = false;
   e->acc_started = false;
   e->acc_examples = 0;
+  e->tail_examples = 0;
   e->synced = false;
 }
 
@@ -1055,8 +1102,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
         e->acc_started = true;
         e->acc_examples += passes[0].rows;
       }
-      k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
-      e->launches++;
+      add_examples_tail(e);
       if (events) VNT_CUDA(cudaEventRecord(e->ev[2], e->stream));
       collective(e);
       if (events) VNT_CUDA(cudaEventRecord(e->ev[3], e->stream));
@@ -1126,8 +1172,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
       begin_round_device(e);
       if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0);
-      k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
-      e->launches++;
+      add_examples_tail(e);
       if (local.empty()) {
         // This process hosts no node this step: contribute zeros.
         VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
@@ -1293,6 +1338,9 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     VNT_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     VNT_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     VNT_CUDA(cudaEventCreateWithFlags(&e->pf_event, cudaEventDisableTiming));
+    VNT_CUDA(cudaStreamCreateWithFlags(&e->aux_stream, cudaStreamNonBlocking));
+    VNT_CUDA(cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
+    VNT_CUDA(cudaEventCreateWithFlags(&e->join_ev, cudaEventDisableTiming));
     for (auto& ev : e->ev) VNT_CUDA(cudaEventCreate(&ev));
     e->w64 = (double*)dalloc(e->P * sizeof(double));
     VNT_CUDA(cudaMemset(e->w64, 0, e->P * sizeof(double)));
@@ -1314,6 +1362,10 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     e->ntail = kTailOverflow + ntensors(e.get());
     e->G = (long long*)dalloc((e->P + e->ntail) * sizeof(long long));
     e->gmax = (unsigned long long*)dalloc(ntensors(e.get()) * sizeof(unsigned long long));
+    if (e->node_path) {
+      e->wpad = (float*)dalloc(node_wt_floats(e.get()) * sizeof(float));
+      VNT_CUDA(cudaMemset(e->wpad, 0, node_wt_floats(e.get()) * sizeof(float)));
+    }
     VNT_CUDA(cudaMallocHost(&e->h_tail, e->ntail * sizeof(long long)));
     VNT_CUDA(cudaMallocHost(&e->h_gmax, ntensors(e.get()) * sizeof(unsigned long long)));
     e->scales.assign(ntensors(e.get()), 0);
@@ -1351,7 +1403,7 @@ void vnt_engine_destroy(vnt_engine* e) {
     for (auto* p : *v)
       if (p) cudaFree(p);
   for (void* p : {(void*)e->w64, (void*)e->v64, (void*)e->w32, (void*)e->wt32, (void*)e->G,
-                  (void*)e->gmax, (void*)e->gout, (void*)e->xbuf[0], (void*)e->ybuf[0],
+                  (void*)e->gmax, (void*)e->gout, (void*)e->xbuf[0], (void*)e->ybuf[0], (void*)e->wpad,
                   (void*)e->xbuf[1], (void*)e->ybuf[1], (void*)e->logits,
                   (void*)e->vn_mean, (void*)e->vn_m2, (void*)e->d_combine})
     if (p) cudaFree(p);
@@ -1378,6 +1430,12 @@ void vnt_engine_destroy(vnt_engine* e) {
     cudaStreamDestroy(e->copy_stream);
   }
   if (e->pf_event) cudaEventDestroy(e->pf_event);
+  if (e->aux_stream) {
+    cudaStreamSynchronize(e->aux_stream);
+    cudaStreamDestroy(e->aux_stream);
+  }
+  if (e->fork_ev) cudaEventDestroy(e->fork_ev);
+  if (e->join_ev) cudaEventDestroy(e->join_ev);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -1480,8 +1538,9 @@ int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum, uint64_t
       VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
       e->acc_started = true;
     }
-    k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
+    add_examples_tail(e);
     e->acc_examples = 0;
+    e->tail_examples = 0;
     collective(e);
     Readback rb = read_tail(e, false);
     if (rb.nonfinite) {
@@ -1525,7 +1584,7 @@ int vnt_engine_take_gradient_sum(vnt_engine* e, double* sum, double* loss_sum,
   return guarded([&] {
     bind(e);
     if (!e->acc_started) throw EngineError(VNT_ERR_CONFIG, "no gradients accumulated");
-    k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, (long long)e->acc_examples);
+    add_examples_tail(e);
     Readback rb = read_tail(e, false);
     if (rb.nonfinite) {
       restore_stats(e);

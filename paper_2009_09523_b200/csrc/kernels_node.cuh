@@ -3,11 +3,12 @@
 //
 // At that size the layered kernels are launch-latency bound (~25 dependent
 // launches per step for a few MFLOP).  Here one CTA runs one virtual node
-// end to end out of shared memory — fp64 rows in, input statistics
-// (model.cpp:101-121), forward (model.cpp:270-287), loss and output delta
-// (model.cpp:289-315), backward (model.cpp:317-338), and the node's dW/db sums
-// — then quantises the per-node partials and adds them into the exact int64
-// gradient sum G, exactly like the layered path does.
+// end to end out of shared memory — fp64 rows in, forward (model.cpp:270-287),
+// loss and output delta (model.cpp:289-315), backward (model.cpp:317-338), and
+// the node's dW/db sums — then quantises the per-node partials and adds them
+// into the exact int64 gradient sum G, exactly like the layered
+// path does.  The input statistics (model.cpp:101-121) depend on x only and
+// run concurrently on the engine's side stream (k_vn_stats, k_stats_combine).
 //
 // Determinism: every value is a fixed-order fp32 chain over one row (forward,
 // backward) or over the node's rows in ascending order (dW, db), so the
@@ -30,23 +31,41 @@ struct NodeArgs {
   const int* row0;       // per node of the pass: first row, row count
   const int* nrows;
   const float* w32;      // fp32 parameters, reference layout (model.cpp:62-77)
-  const float* wt32;     // transposed weights WT[l][o][i]
+  const float* wpad;     // weights as staged in shared memory: [K][node_ldw(N)] per layer
+  int wpad_floats;       // multiple of 4
   int L;
   int w[kNodeMaxLayers + 1];
-  int woff[kNodeMaxLayers], boff[kNodeMaxLayers], wtoff[kNodeMaxLayers];
+  int woff[kNodeMaxLayers], boff[kNodeMaxLayers];
   int nstrips;           // sum_l (w[l] + 1) * ceil(w[l+1] / kNodeOC)
-  int wt_total;          // sum_l w[l] * w[l+1]: W^T staged in shared memory
   int act, loss;
   int rc;                // rows per shared-memory chunk
   const StepParams* sp;  // per-tensor 2^s
   float lim;
   long long* G;          // exact gradient sum (zeroed) + tail
   long long* tail;
-  double* vn_mean;       // per-node input stats, or null
-  double* vn_m2;
+  long long examples;    // the pass's rows, added to the tail by CTA 0
 };
 
+// Shared-memory row strides: deltas padded to kNodeOC (aligned float4 strips),
+// staged weights W[i][:] padded so ld/4 is odd (conflict-free float4 rows).
 __host__ __device__ constexpr int node_ld(int w) { return (w + kNodeOC - 1) / kNodeOC * kNodeOC; }
+__host__ __device__ constexpr int node_ldw(int n) { return (((n + 3) / 4) | 1) * 4; }
+
+// Offset of layer l in the padded weight image (float4-aligned layers).
+__host__ __device__ inline int node_wpad_offset(const int* w, int l) {
+  int off = 0;
+  for (int k = 0; k < l; ++k) off += (w[k] * node_ldw(w[k + 1]) + 3) & ~3;
+  return off;
+}
+
+// w32 -> padded image of one layer (set_params / resize; the SGD keeps it current).
+__global__ void k_node_pad(const float* __restrict__ W, float* __restrict__ wpad, int K, int N) {
+  const int ldw = node_ldw(N);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < K * N; t += gridDim.x * blockDim.x) {
+    const int i = t / N;
+    wpad[i * ldw + (t - i * N)] = W[t];
+  }
+}
 
 // Row loss + output delta of one row (k_loss's arithmetic), one warp.
 __device__ __forceinline__ void node_row_loss(const float* z, const double* yr, int outw,
@@ -108,8 +127,7 @@ __device__ __forceinline__ void node_strip(const NodeArgs& a, int s, int& l, int
 
 __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
   extern __shared__ float sm[];
-  __shared__ int aoff[kNodeMaxLayers + 1], doff[kNodeMaxLayers + 1];
-  __shared__ int wts_off;
+  __shared__ int aoff[kNodeMaxLayers + 1], doff[kNodeMaxLayers + 1], wso[kNodeMaxLayers];
   const int node = blockIdx.x;
   const int r0 = a.row0[node], n = a.nrows[node];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -127,22 +145,30 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
       doff[l] = off;
       off += a.rc * node_ld(a.w[l]);
     }
-    wts_off = (off + 3) & ~3;
+    off = (off + 3) & ~3;
+    for (int l = 0; l < L; ++l) wso[l] = off + node_wpad_offset(a.w, l);
   }
   __syncthreads();
-  // every layer's W^T into shared memory once (coalesced, all threads)
+  // the padded weight image (written by the SGD) into shared memory, flat float4
   {
-    const float4* src = reinterpret_cast<const float4*>(a.wt32);
-    float4* dst = reinterpret_cast<float4*>(sm + wts_off);
-    const int n4 = a.wt_total / 4;
-    for (int t = tid; t < n4; t += nt) dst[t] = __ldg(src + t);
-    for (int t = 4 * n4 + tid; t < a.wt_total; t += nt) sm[wts_off + t] = __ldg(a.wt32 + t);
+    const float4* src = reinterpret_cast<const float4*>(a.wpad);
+    float4* dst = reinterpret_cast<float4*>(sm + wso[0]);
+    for (int t = tid; t < a.wpad_floats / 4; t += nt) dst[t] = __ldg(src + t);
   }
-  // LayerStats::observe of this node (same arithmetic as k_vn_stats)
-  if (a.vn_mean) {
-    for (int j = tid; j < in; j += nt)
-      node_feature_stats(a.x, in, r0, n, j, &a.vn_mean[(size_t)node * in + j],
-                         &a.vn_m2[(size_t)node * in + j]);
+  if (node == 0 && tid == 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.tail[kTailExamples]),
+              (unsigned long long)a.examples);
+  // per-strip quantisation scales, loaded before they are needed
+  float qscale[kNodeStrips];
+#pragma unroll
+  for (int q = 0; q < kNodeStrips; ++q) {
+    const int st = tid + q * nt;
+    qscale[q] = 0.f;
+    if (st < a.nstrips) {
+      int l, i, o0;
+      node_strip(a, st, l, i, o0);
+      qscale[q] = a.sp->scale[2 * l + (i == a.w[l] ? 1 : 0)];
+    }
   }
   float g[kNodeStrips][kNodeOC];
 #pragma unroll
@@ -162,9 +188,9 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
     // forward (model.cpp:280-286): one warp per (row, 16 outputs); lanes take
     // k = lane, lane+32, ... in ascending order, then a fixed xor tree, + bias.
     for (int l = 0; l < L; ++l) {
-      const int K = a.w[l], N = a.w[l + 1];
+      const int K = a.w[l], N = a.w[l + 1], ldw = node_ldw(N);
       const int nch = (N + kNodeOC - 1) / kNodeOC;
-      const float* WT = sm + wts_off + a.wtoff[l];
+      const float* Wl = sm + wso[l];
       const float* b = a.w32 + a.boff[l];
       const float* Ain = sm + aoff[l];
       float* Aout = sm + aoff[l + 1];
@@ -179,9 +205,17 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
 #pragma unroll 2
         for (int k = lane; k < K; k += 32) {
           const float av = ar[k];
+          const float4* wr = reinterpret_cast<const float4*>(Wl + k * ldw + o0);
 #pragma unroll
-          for (int j = 0; j < kNodeOC; ++j)
-            if (j < on) acc[j] = fmaf(av, WT[(o0 + j) * K + k], acc[j]);
+          for (int j4 = 0; j4 < kNodeOC / 4; ++j4) {
+            if (4 * j4 < on) {   // lanes beyond `on` accumulate padding, never stored
+              const float4 wv = wr[j4];
+              acc[4 * j4 + 0] = fmaf(av, wv.x, acc[4 * j4 + 0]);
+              acc[4 * j4 + 1] = fmaf(av, wv.y, acc[4 * j4 + 1]);
+              acc[4 * j4 + 2] = fmaf(av, wv.z, acc[4 * j4 + 2]);
+              acc[4 * j4 + 3] = fmaf(av, wv.w, acc[4 * j4 + 3]);
+            }
+          }
         }
 #pragma unroll
         for (int j = 0; j < kNodeOC; ++j) {
@@ -208,8 +242,8 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
     // o ascending; lanes over i read W^T rows (coalesced).
     for (int l = L - 1; l >= 1; --l) {
       const int K = a.w[l], N = a.w[l + 1];
-      const int ldn = node_ld(N), ldl = node_ld(K);
-      const float* WT = sm + wts_off + a.wtoff[l];
+      const int ldn = node_ld(N), ldl = node_ld(K), ldw = node_ldw(N);
+      const float* Wl = sm + wso[l];
       const float* Dn = sm + doff[l + 1];
       const float* Al = sm + aoff[l];
       float* Dl = sm + doff[l];
@@ -218,8 +252,16 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
         const int r = task / nic, i = (task - (task / nic) * nic) * 32 + lane;
         if (i < K) {
           const float* dr = Dn + r * ldn;
+          const float* wr = Wl + i * ldw;
           float acc = 0.f;
-          for (int o = 0; o < N; ++o) acc = fmaf(dr[o], WT[o * K + i], acc);
+          for (int o = 0; o < N; o += 4) {   // o ascending
+            const float4 wv = *reinterpret_cast<const float4*>(wr + o);
+            const float4 dv = *reinterpret_cast<const float4*>(dr + o);
+            acc = fmaf(dv.x, wv.x, acc);
+            if (o + 1 < N) acc = fmaf(dv.y, wv.y, acc);
+            if (o + 2 < N) acc = fmaf(dv.z, wv.z, acc);
+            if (o + 3 < N) acc = fmaf(dv.w, wv.w, acc);
+          }
           Dl[r * ldl + i] = acc * act_grad_from_out(a.act, Al[r * K + i]);
         }
       }
@@ -262,7 +304,7 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
       const int K = a.w[l], N = a.w[l + 1];
       const bool bias = i == K;
       const int t = 2 * l + (bias ? 1 : 0);
-      const float scale = a.sp->scale[t];
+      const float scale = qscale[q];
       long long* gp = a.G + (bias ? a.boff[l] : a.woff[l] + i * N) + o0;
 #pragma unroll
       for (int j = 0; j < kNodeOC; ++j) {
@@ -276,7 +318,8 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
 }
 
 // SGD of every tensor of a small model in one launch (blockIdx.y = tensor):
-// k_sgd_vec's arithmetic on each flat tensor, plus the transposed fp32 copy.
+// k_sgd_vec's arithmetic on each flat tensor, plus the padded weight image the
+// whole-node kernel stages (no transposed copy is kept).
 struct SgdMulti {
   SgdArgs t[2 * kNodeMaxLayers];
 };
@@ -291,9 +334,9 @@ __global__ void __launch_bounds__(256) k_sgd_multi(const __grid_constant__ SgdMu
     float w32;
     mx = fmax(mx, sgd_one(a, k, w32));
     a.w32[k] = w32;
-    if (a.wt32) {   // W^T[o][i] for the whole-node forward / backward
-      const size_t i = k / a.cols, o = k - (k / a.cols) * a.cols;
-      a.wt32[o * a.rows + i] = w32;
+    if (a.wpad) {
+      const size_t i = k / a.cols;
+      a.wpad[i * a.ldw + (k - i * a.cols)] = w32;
     }
   }
   block_max_to(a.gmax, mx);

@@ -133,14 +133,15 @@ struct CombineStep {
   double f1, f2;
 };
 
-__global__ void k_stats_combine(double* __restrict__ mean, double* __restrict__ m2, int in,
-                                const double* __restrict__ vn_mean,
-                                const double* __restrict__ vn_m2,
-                                const CombineStep* __restrict__ steps, int nsteps) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= in) return;
+// One feature j: fold nsteps node stats into (mean, m2) in step order; 8 steps'
+// loads in flight.  __ldcg: the node stats may come from other CTAs of the
+// same launch (k_node_step's last CTA).
+__device__ __forceinline__ void combine_feature(double* __restrict__ mean, double* __restrict__ m2,
+                                                int in, int j, const double* vn_mean,
+                                                const double* vn_m2, const CombineStep* steps,
+                                                int nsteps) {
   double mu = mean[j], s = m2[j];
-  for (int t0 = 0; t0 < nsteps; t0 += 8) {   // 8 nodes' stats in flight, applied in order
+  for (int t0 = 0; t0 < nsteps; t0 += 8) {
     const int tn = min(8, nsteps - t0);
     CombineStep st[8];
     double om[8], os[8];
@@ -150,8 +151,8 @@ __global__ void k_stats_combine(double* __restrict__ mean, double* __restrict__ 
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       if (q < tn) {
-        om[q] = vn_mean[(size_t)st[q].vn * in + j];
-        os[q] = vn_m2[(size_t)st[q].vn * in + j];
+        om[q] = __ldcg(vn_mean + (size_t)st[q].vn * in + j);
+        os[q] = __ldcg(vn_m2 + (size_t)st[q].vn * in + j);
       }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -168,6 +169,15 @@ __global__ void k_stats_combine(double* __restrict__ mean, double* __restrict__ 
   }
   mean[j] = mu;
   m2[j] = s;
+}
+
+__global__ void k_stats_combine(double* __restrict__ mean, double* __restrict__ m2, int in,
+                                const double* __restrict__ vn_mean,
+                                const double* __restrict__ vn_m2,
+                                const CombineStep* __restrict__ steps, int nsteps) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= in) return;
+  combine_feature(mean, m2, in, j, vn_mean, vn_m2, steps, nsteps);
 }
 
 // ------------------------------------------------------ FFMA dense layer
@@ -619,6 +629,8 @@ struct SgdArgs {
   const long long* tail;
   int ntail_flags;
   const StepParams* sp; // 2^-s per tensor, 1/B (virtual_exec.cpp:165), lr, mu
+  float* wpad;          // whole-node kernel's padded weight image (or nullptr)
+  int ldw;
   int tensor;
   int rows, cols;       // tensor shape (bias: rows = 1)
 };
