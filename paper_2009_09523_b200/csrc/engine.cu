@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -116,7 +117,12 @@ struct vnt_engine {
   bool node_path = false;
   int node_rc_max = 0;
   float* wpad = nullptr;               // padded weight image of k_node_step
+  bool stats_backed = false;           // lineage stats backed up this round
   cudaStream_t aux_stream = nullptr;   // input-statistics branch beside k_node_step
+  // VNT_HOST_PROFILE=1: host-side time per train_step phase (printed at destroy)
+  bool host_prof = false;
+  double host_t[8] = {};
+  uint64_t host_n = 0;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   uint64_t tail_examples = 0;          // examples node kernels already added to the tail
   std::vector<float*> Xh, Xl, XTh, XTl, Dh, Dl, DTh, DTl;
@@ -246,7 +252,7 @@ void drop_graphs(vnt_engine* e) {
 }
 
 // Stage this step's kernel parameters (scales, 1/B, lr, momentum) for the device.
-void upload_step_params(vnt_engine* e, double lr, double inv_b) {
+void fill_step_params(vnt_engine* e, double lr, double inv_b) {
   StepParams& h = *e->h_sp;
   for (uint32_t t = 0; t < ntensors(e); ++t) {
     h.scale[t] = pow2f(e->scales[t]);
@@ -256,7 +262,17 @@ void upload_step_params(vnt_engine* e, double lr, double inv_b) {
   h.lr = lr;
   h.mu = e->opt.momentum;
   h.inv_b = inv_b;
+}
+
+// Pinned h_sp -> d_sp on the stream; inside a captured step this is a graph
+// memcpy node that re-reads h_sp at every replay.
+void copy_step_params(vnt_engine* e) {
   VNT_CUDA(cudaMemcpyAsync(e->d_sp, e->h_sp, sizeof(StepParams), cudaMemcpyHostToDevice, e->stream));
+}
+
+void upload_step_params(vnt_engine* e, double lr, double inv_b) {
+  fill_step_params(e, lr, inv_b);
+  copy_step_params(e);
 }
 
 int initial_scale(uint64_t batch) {
@@ -391,8 +407,9 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
   return e->plans.emplace(key, std::move(passes)).first->second;
 }
 
+// Tail and the per-tensor max|g| words sit back to back after G: one memset, one readback.
 void tail_reset(vnt_engine* e) {
-  VNT_CUDA(cudaMemsetAsync(e->G + e->P, 0, e->ntail * sizeof(long long), e->stream));
+  VNT_CUDA(cudaMemsetAsync(e->G + e->P, 0, (e->ntail + ntensors(e)) * sizeof(long long), e->stream));
 }
 
 void split_into(vnt_engine* e, const float* x, float* hi, float* lo, size_t n) {
@@ -610,6 +627,8 @@ void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStr
   }
 }
 
+void backup_stats(vnt_engine* e, cudaStream_t s);
+
 // Small models: one k_node_step CTA per node does the whole pass.
 void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats) {
   const size_t nn = p.nodes.size();
@@ -652,6 +671,7 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   if (stats) {
     VNT_CUDA(cudaEventRecord(e->fork_ev, e->stream));
     VNT_CUDA(cudaStreamWaitEvent(e->aux_stream, e->fork_ev, 0));
+    if (!e->stats_backed) backup_stats(e, e->aux_stream);
     dim3 grid((unsigned)ceil_div(e->widths[0], 128), (unsigned)nn);
     k_vn_stats<<<grid, 128, 0, e->aux_stream>>>(e->xin, (int)e->widths[0], row0, nrows, e->vn_mean,
                                                 e->vn_m2);
@@ -827,6 +847,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
 }
 
 void begin_round_host(vnt_engine* e, uint64_t batch_hint) {
+  e->stats_backed = false;
   e->acc_examples = 0;
   e->tail_examples = 0;
   e->acc_started = false;
@@ -852,11 +873,17 @@ void begin_round_device(vnt_engine* e) {
                                e->stream));
   }
   }
+  if (!e->node_path) backup_stats(e, e->stream);   // node path: on the stats branch
+}
+
+// Lineage statistics as of the round start (restored if the step is redone).
+void backup_stats(vnt_engine* e, cudaStream_t s) {
   const uint64_t in = e->widths[0];
   for (auto& d : e->devs) {
-    VNT_CUDA(cudaMemcpyAsync(d.mean_bak, d.mean, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
-    VNT_CUDA(cudaMemcpyAsync(d.m2_bak, d.m2, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    VNT_CUDA(cudaMemcpyAsync(d.mean_bak, d.mean, in * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    VNT_CUDA(cudaMemcpyAsync(d.m2_bak, d.m2, in * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
+  e->stats_backed = true;
 }
 
 void begin_round(vnt_engine* e, uint64_t batch_hint) {
@@ -917,7 +944,6 @@ void collective(vnt_engine* e) {
 // lr, 1/B (virtual_exec.cpp:165), momentum and 2^-s come from the step params.
 void launch_sgd(vnt_engine* e) {
   cudaStream_t s = e->stream;
-  VNT_CUDA(cudaMemsetAsync(e->gmax, 0, ntensors(e) * sizeof(unsigned long long), s));
   if (e->node_path) {   // all tensors in one launch, row-major fp32 copies only
     SgdMulti m{};
     uint64_t maxn = 1;
@@ -1001,11 +1027,9 @@ struct Readback {
 
 void enqueue_readback(vnt_engine* e, bool with_gmax) {
   cudaStream_t s = e->stream;
-  VNT_CUDA(cudaMemcpyAsync(e->h_tail, e->G + e->P, e->ntail * sizeof(long long),
+  VNT_CUDA(cudaMemcpyAsync(e->h_tail, e->G + e->P,
+                           (e->ntail + (with_gmax ? ntensors(e) : 0)) * sizeof(long long),
                            cudaMemcpyDeviceToHost, s));
-  if (with_gmax)
-    VNT_CUDA(cudaMemcpyAsync(e->h_gmax, e->gmax, ntensors(e) * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s));
 }
 
 Readback parse_readback(vnt_engine* e) {
@@ -1080,10 +1104,25 @@ std::vector<PassNode> local_nodes(vnt_engine* e, const uint64_t* node_sizes,
   return local;
 }
 
+struct HostClock {
+  vnt_engine* e;
+  std::chrono::steady_clock::time_point t;
+  int i = 0;
+  explicit HostClock(vnt_engine* en) : e(en), t(std::chrono::steady_clock::now()) {}
+  void mark() {
+    if (!e->host_prof) return;
+    const auto n = std::chrono::steady_clock::now();
+    e->host_t[i++ & 7] += std::chrono::duration<double, std::micro>(n - t).count();
+    t = n;
+  }
+};
+
 int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t batch_rows,
                     const uint64_t* node_sizes, const int32_t* node_device,
                     uint32_t total_nodes, double lr, double* loss, vnt_device_metrics* per_dev,
                     bool on_device) {
+  HostClock hc(e);
+  if (e->host_prof) e->host_n++;
   bind(e);
   if (!(lr > 0.0)) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: learning rate must be positive");
   auto local = local_nodes(e, node_sizes, node_device, total_nodes, batch_rows);
@@ -1095,6 +1134,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
     // Device work of the step, in order; recorded once per plan as a CUDA graph.
     auto enqueue_step = [&](const std::vector<StatsLaunch>* stats, bool events) {
       if (events) VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
+      copy_step_params(e);
       begin_round_device(e);
       auto& passes = plan_for(e, local);
       if (passes.size() == 1) {
@@ -1111,8 +1151,10 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       enqueue_readback(e, true);
     };
     bool graphed = false;
+    hc.mark();   // 0: entry, local_nodes
     begin_round_host(e, batch_rows);
-    upload_step_params(e, lr, inv_b);
+    fill_step_params(e, lr, inv_b);
+    hc.mark();   // 1: step params
     Readback rb;
     const std::vector<Pass>* passes = local.empty() ? nullptr : &plan_for(e, local);
     const bool single = passes && passes->size() == 1;
@@ -1123,7 +1165,9 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
       size_t off = 0;
       const std::vector<StatsLaunch> stats = prep_stats(e, p, off);
+      hc.mark();   // 2: plan, capacity, stats prep
       if (!take_prefetch(e, x, y)) stage_inputs(e, p, x, y, on_device);
+      hc.mark();   // 3: input staging
       std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur};
       for (const auto& n : local) {
         key.push_back(n.node);
@@ -1166,10 +1210,13 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
         graphed = true;
       }
       start_queued_prefetch(e);   // overlaps the next batch's H2D with this step
+      hc.mark();   // 4: graph key, launch
       VNT_CUDA(cudaStreamSynchronize(e->stream));
+      hc.mark();   // 5: synchronize
       rb = parse_readback(e);
     } else {
       VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
+      copy_step_params(e);
       begin_round_device(e);
       if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0);
       add_examples_tail(e);
@@ -1237,6 +1284,8 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
     }
   }
   reset_acc(e);
+  hc.i = 6;
+  hc.mark();   // 6: readback, scales, timings, metrics
   return VNT_OK;
 }
 
@@ -1360,14 +1409,15 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
       e->wt32l = (float*)dalloc(toff * sizeof(float));
     }
     e->ntail = kTailOverflow + ntensors(e.get());
-    e->G = (long long*)dalloc((e->P + e->ntail) * sizeof(long long));
-    e->gmax = (unsigned long long*)dalloc(ntensors(e.get()) * sizeof(unsigned long long));
+    e->G = (long long*)dalloc((e->P + e->ntail + ntensors(e.get())) * sizeof(long long));
+    VNT_CUDA(cudaMemset(e->G, 0, (e->P + e->ntail + ntensors(e.get())) * sizeof(long long)));
+    e->gmax = reinterpret_cast<unsigned long long*>(e->G + e->P + e->ntail);
     if (e->node_path) {
       e->wpad = (float*)dalloc(node_wt_floats(e.get()) * sizeof(float));
       VNT_CUDA(cudaMemset(e->wpad, 0, node_wt_floats(e.get()) * sizeof(float)));
     }
-    VNT_CUDA(cudaMallocHost(&e->h_tail, e->ntail * sizeof(long long)));
-    VNT_CUDA(cudaMallocHost(&e->h_gmax, ntensors(e.get()) * sizeof(unsigned long long)));
+    VNT_CUDA(cudaMallocHost(&e->h_tail, (e->ntail + ntensors(e.get())) * sizeof(long long)));
+    e->h_gmax = reinterpret_cast<unsigned long long*>(e->h_tail + e->ntail);
     e->scales.assign(ntensors(e.get()), 0);
     if (e->L > vntb::kMaxLayers) throw EngineError(VNT_ERR_CONFIG, "too many layers (max 64)");
     e->d_sp = (StepParams*)dalloc(sizeof(StepParams));
@@ -1375,6 +1425,7 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     std::memset(e->h_sp, 0, sizeof(StepParams));
     // Events recorded inside a graph cannot be timed: profiling runs eagerly.
     e->graphs = !(getenv("VNT_GRAPHS") && getenv("VNT_GRAPHS")[0] == '0') && !e->profile;
+    e->host_prof = getenv("VNT_HOST_PROFILE") && getenv("VNT_HOST_PROFILE")[0] == '1';
     tc_init(e.get());
     if (e->opt.world_size > 1) {
       if (!options->nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
@@ -1403,7 +1454,7 @@ void vnt_engine_destroy(vnt_engine* e) {
     for (auto* p : *v)
       if (p) cudaFree(p);
   for (void* p : {(void*)e->w64, (void*)e->v64, (void*)e->w32, (void*)e->wt32, (void*)e->G,
-                  (void*)e->gmax, (void*)e->gout, (void*)e->xbuf[0], (void*)e->ybuf[0], (void*)e->wpad,
+                  (void*)e->gout, (void*)e->xbuf[0], (void*)e->ybuf[0], (void*)e->wpad,
                   (void*)e->xbuf[1], (void*)e->ybuf[1], (void*)e->logits,
                   (void*)e->vn_mean, (void*)e->vn_m2, (void*)e->d_combine})
     if (p) cudaFree(p);
@@ -1421,7 +1472,6 @@ void vnt_engine_destroy(vnt_engine* e) {
   if (e->h_sp) cudaFreeHost(e->h_sp);
   if (e->d_sp) cudaFree(e->d_sp);
   drop_graphs(e);
-  if (e->h_gmax) cudaFreeHost(e->h_gmax);
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : e->prof_ev) cudaEventDestroy(ev);
@@ -1430,6 +1480,11 @@ void vnt_engine_destroy(vnt_engine* e) {
     cudaStreamDestroy(e->copy_stream);
   }
   if (e->pf_event) cudaEventDestroy(e->pf_event);
+  if (e->host_prof && e->host_n) {
+    std::fprintf(stderr, "vnt host profile (us/step over %llu steps):", (unsigned long long)e->host_n);
+    for (int i = 0; i < 7; ++i) std::fprintf(stderr, " %d:%.2f", i, e->host_t[i] / (double)e->host_n);
+    std::fprintf(stderr, "\n");
+  }
   if (e->aux_stream) {
     cudaStreamSynchronize(e->aux_stream);
     cudaStreamDestroy(e->aux_stream);

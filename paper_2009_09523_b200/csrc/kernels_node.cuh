@@ -153,7 +153,16 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
   {
     const float4* src = reinterpret_cast<const float4*>(a.wpad);
     float4* dst = reinterpret_cast<float4*>(sm + wso[0]);
-    for (int t = tid; t < a.wpad_floats / 4; t += nt) dst[t] = __ldg(src + t);
+    const int n4 = a.wpad_floats / 4;
+    for (int t0 = tid; t0 < n4; t0 += 4 * nt) {
+      float4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (t0 + q * nt < n4) v[q] = __ldg(src + t0 + q * nt);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (t0 + q * nt < n4) dst[t0 + q * nt] = v[q];
+    }
   }
   if (node == 0 && tid == 0)
     atomicAdd(reinterpret_cast<unsigned long long*>(&a.tail[kTailExamples]),
@@ -182,7 +191,20 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
     {   // fp64 rows -> fp32 activations of layer 0
       float* A0 = sm + aoff[0];
       const double* xs = a.x + (size_t)(r0 + c0) * in;
-      for (int t = tid; t < rn * in; t += nt) A0[t] = __double2float_rn(xs[t]);
+      const int total = rn * in;
+      for (int t0 = tid; t0 < total; t0 += 8 * nt) {   // 8 loads in flight per thread
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int t = t0 + q * nt;
+          v[q] = t < total ? __ldg(xs + t) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int t = t0 + q * nt;
+          if (t < total) A0[t] = __double2float_rn(v[q]);
+        }
+      }
     }
     __syncthreads();
     // forward (model.cpp:280-286): one warp per (row, 16 outputs); lanes take

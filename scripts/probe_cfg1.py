@@ -40,3 +40,4 @@ t0 = time.perf_counter()
 for _ in range(n):
     e._mapping_args(sizes, dev)
 print(f"_mapping_args {1e6 * (time.perf_counter() - t0) / n:.1f} us")
+e.close()
