@@ -132,8 +132,11 @@ struct vnt_engine {
   double* vn_m2 = nullptr;
   CombineStep* d_combine = nullptr;
   CombineStep* h_combine = nullptr;
+  CombineStep* m_combine = nullptr;    // device view of the pinned h_combine
   size_t combine_cap = 0;
   long long* h_tail = nullptr;
+  long long* m_tail = nullptr;         // device view of the pinned h_tail
+  StepParams* m_sp = nullptr;          // device view of the pinned h_sp
   unsigned long long* h_gmax = nullptr;
 
   struct LDev {
@@ -264,10 +267,15 @@ void fill_step_params(vnt_engine* e, double lr, double inv_b) {
   h.inv_b = inv_b;
 }
 
-// Pinned h_sp -> d_sp on the stream; inside a captured step this is a graph
-// memcpy node that re-reads h_sp at every replay.
+// Pinned h_sp -> d_sp on the stream (a kernel reading mapped host memory, so it
+// never waits behind an input prefetch on the copy engine); inside a captured
+// step it re-reads h_sp at every replay.
 void copy_step_params(vnt_engine* e) {
-  VNT_CUDA(cudaMemcpyAsync(e->d_sp, e->h_sp, sizeof(StepParams), cudaMemcpyHostToDevice, e->stream));
+  static_assert(sizeof(StepParams) % 8 == 0, "StepParams words");
+  k_copy_words<<<1, 256, 0, e->stream>>>(reinterpret_cast<const unsigned long long*>(e->m_sp),
+                                         reinterpret_cast<unsigned long long*>(e->d_sp),
+                                         (int)(sizeof(StepParams) / 8));
+  VNT_LAUNCH_CHECK();
 }
 
 void upload_step_params(vnt_engine* e, double lr, double inv_b) {
@@ -359,6 +367,7 @@ void ensure_combine(vnt_engine* e, size_t n) {
   n = std::max<size_t>(n, 64);
   e->d_combine = (CombineStep*)dalloc(n * sizeof(CombineStep));
   VNT_CUDA(cudaMallocHost(&e->h_combine, n * sizeof(CombineStep)));
+  VNT_CUDA(cudaHostGetDevicePointer((void**)&e->m_combine, e->h_combine, 0));
   e->combine_cap = n;
 }
 
@@ -617,11 +626,10 @@ void node_pad(vnt_engine* e) {
 void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStream_t s) {
   const uint64_t in = e->widths[0];
   for (const auto& sl : stats) {
-    VNT_CUDA(cudaMemcpyAsync(e->d_combine + sl.off, e->h_combine + sl.off,
-                             sl.n * sizeof(CombineStep), cudaMemcpyHostToDevice, s));
+    // the host-computed factors are read in place from pinned, mapped memory
     k_stats_combine<<<(unsigned)ceil_div(in, 128), 128, 0, s>>>(
         e->devs[sl.dev].mean, e->devs[sl.dev].m2, (int)in, e->vn_mean, e->vn_m2,
-        e->d_combine + sl.off, sl.n);
+        e->m_combine + sl.off, sl.n);
     VNT_LAUNCH_CHECK();
     e->launches++;
   }
@@ -880,8 +888,9 @@ void begin_round_device(vnt_engine* e) {
 void backup_stats(vnt_engine* e, cudaStream_t s) {
   const uint64_t in = e->widths[0];
   for (auto& d : e->devs) {
-    VNT_CUDA(cudaMemcpyAsync(d.mean_bak, d.mean, in * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    VNT_CUDA(cudaMemcpyAsync(d.m2_bak, d.m2, in * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    k_copy_f64x2<<<(unsigned)std::min<uint64_t>(ceil_div(in, 256), 64), 256, 0, s>>>(
+        d.mean, d.mean_bak, d.m2, d.m2_bak, (int)in);
+    VNT_LAUNCH_CHECK();
   }
   e->stats_backed = true;
 }
@@ -1027,9 +1036,10 @@ struct Readback {
 
 void enqueue_readback(vnt_engine* e, bool with_gmax) {
   cudaStream_t s = e->stream;
-  VNT_CUDA(cudaMemcpyAsync(e->h_tail, e->G + e->P,
-                           (e->ntail + (with_gmax ? ntensors(e) : 0)) * sizeof(long long),
-                           cudaMemcpyDeviceToHost, s));
+  k_copy_words<<<1, 64, 0, s>>>(reinterpret_cast<const unsigned long long*>(e->G + e->P),
+                                reinterpret_cast<unsigned long long*>(e->m_tail),
+                                (int)(e->ntail + (with_gmax ? ntensors(e) : 0)));
+  VNT_LAUNCH_CHECK();
 }
 
 Readback parse_readback(vnt_engine* e) {
@@ -1418,10 +1428,12 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     }
     VNT_CUDA(cudaMallocHost(&e->h_tail, (e->ntail + ntensors(e.get())) * sizeof(long long)));
     e->h_gmax = reinterpret_cast<unsigned long long*>(e->h_tail + e->ntail);
+    VNT_CUDA(cudaHostGetDevicePointer((void**)&e->m_tail, e->h_tail, 0));
     e->scales.assign(ntensors(e.get()), 0);
     if (e->L > vntb::kMaxLayers) throw EngineError(VNT_ERR_CONFIG, "too many layers (max 64)");
     e->d_sp = (StepParams*)dalloc(sizeof(StepParams));
     VNT_CUDA(cudaMallocHost(&e->h_sp, sizeof(StepParams)));
+    VNT_CUDA(cudaHostGetDevicePointer((void**)&e->m_sp, e->h_sp, 0));
     std::memset(e->h_sp, 0, sizeof(StepParams));
     // Events recorded inside a graph cannot be timed: profiling runs eagerly.
     e->graphs = !(getenv("VNT_GRAPHS") && getenv("VNT_GRAPHS")[0] == '0') && !e->profile;

@@ -75,6 +75,23 @@ __global__ void k_ingest(const double* __restrict__ x, float* __restrict__ X0,
   }
 }
 
+// ------------------------------------------------------- small copies
+// Kernel copies for the per-step control words (step parameters in, tail and
+// max|g| out, lineage-stat backups): the host side is pinned, mapped memory,
+// so none of them queues on a copy engine behind a large input prefetch.
+__global__ void k_copy_words(const unsigned long long* __restrict__ src,
+                             unsigned long long* __restrict__ dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void k_copy_f64x2(const double* __restrict__ a, double* __restrict__ a_out,
+                             const double* __restrict__ b, double* __restrict__ b_out, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    a_out[i] = a[i];
+    b_out[i] = b[i];
+  }
+}
+
 // ------------------------------------------------------------ input stats
 // LayerStats::observe batch part (model.cpp:101-121): per node, per feature,
 // sequential fp64 sums in row order; __d*_rn forbid FMA contraction so the

@@ -41,3 +41,25 @@ for _ in range(n):
     e._mapping_args(sizes, dev)
 print(f"_mapping_args {1e6 * (time.perf_counter() - t0) / n:.1f} us")
 e.close()
+
+# e2e-style: pinned host batches, with and without prefetch
+e = vnt.Engine(w, "tanh", "softmax-cross-entropy")
+e.add_device(1 << 20)
+e.set_params(np.concatenate([g.standard_normal(784 * 16) / 28, np.zeros(16),
+                             g.standard_normal(160) / 4, np.zeros(10)]))
+hx = [torch.randn(B, 784, dtype=torch.float64).pin_memory() for _ in range(4)]
+hy = [torch.softmax(torch.randn(B, 10, dtype=torch.float64), 1).pin_memory() for _ in range(4)]
+for pf in (False, True):
+    for it in range(2):
+        t0 = time.perf_counter()
+        if pf:
+            e.prefetch_ptr(hx[0].data_ptr(), hy[0].data_ptr(), B, sizes, dev, resident=False)
+        for i in range(n):
+            if pf and i + 1 < n:
+                e.prefetch_ptr(hx[(i + 1) % 4].data_ptr(), hy[(i + 1) % 4].data_ptr(), B, sizes, dev,
+                               resident=False)
+            e.train_step_ptr(hx[i % 4].data_ptr(), hy[i % 4].data_ptr(), B, sizes, dev, 0.05,
+                             resident=False)
+        t1 = time.perf_counter()
+    print(f"host inputs, prefetch={pf}: wall/step {1e6 * (t1 - t0) / n:.1f} us")
+e.close()
