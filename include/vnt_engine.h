@@ -38,6 +38,8 @@ extern "C" {
 #define VNT_ERR_INTERNAL 1        /* vnt::Error (generic)                */
 #define VNT_ERR_CONFIG 2          /* vnt::ConfigError                    */
 #define VNT_ERR_CAPACITY 3        /* vnt::CapacityError                  */
+#define VNT_ERR_PROFILE 4         /* vnt::ProfileError (hetero)          */
+#define VNT_ERR_INFEASIBLE 5      /* vnt::InfeasibleError (hetero solve) */
 #define VNT_ERR_SHAPE 6           /* vnt::ShapeError                     */
 #define VNT_ERR_CONSISTENCY 7     /* vnt::ConsistencyError               */
 #define VNT_ERR_MIGRATION 8       /* vnt::MigrationError                 */

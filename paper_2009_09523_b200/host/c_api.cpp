@@ -4,6 +4,7 @@
 #include <string>
 
 #include "vnt/errors.hpp"
+#include "vnt/hetero.hpp"
 #include "vnt/runner.hpp"
 #include "vnt_trainer.h"
 
@@ -33,6 +34,12 @@ int guard(F&& f) {
   } catch (const vnt::MigrationError& e) {
     g_err = e.what();
     return VNT_ERR_MIGRATION;
+  } catch (const vnt::InfeasibleError& e) {
+    g_err = e.what();
+    return VNT_ERR_INFEASIBLE;
+  } catch (const vnt::ProfileError& e) {
+    g_err = e.what();
+    return VNT_ERR_PROFILE;
   } catch (const std::exception& e) {
     g_err = e.what();
     return VNT_ERR_INTERNAL;
@@ -148,6 +155,70 @@ int vnt_init_params(const uint64_t* widths, uint32_t nw, uint64_t seed, double* 
     s.seed = seed;
     const auto p = vnt::Model(s).init_params();
     std::memcpy(out, p.values.data(), p.values.size() * sizeof(double));
+    return VNT_OK;
+  });
+}
+
+
+int vnt_hetero_solve(uint32_t ntypes, const char* const* names, const uint64_t* counts,
+                     const uint64_t* caps, const double* comm, const uint32_t* npts,
+                     const uint64_t* pt_batch, const double* pt_time, uint64_t global_batch,
+                     uint64_t max_virtual_nodes, int32_t collect, uint32_t* out_ntypes,
+                     uint32_t* out_type, uint64_t* out_n, uint64_t* out_b, uint64_t* out_v,
+                     double* out_time, uint64_t* out_candidates) {
+  return guard([&] {
+    std::vector<vnt::hetero::ProfileCurve> curves(ntypes);
+    vnt::hetero::DevicePool pool;
+    std::size_t at = 0;
+    for (uint32_t i = 0; i < ntypes; ++i) {
+      curves[i].device_type = names[i];
+      curves[i].comm_overhead_s = comm[i];
+      for (uint32_t k = 0; k < npts[i]; ++k, ++at) curves[i].points.push_back({pt_batch[at], pt_time[at]});
+      pool.entries[names[i]] = {counts[i], caps[i]};
+    }
+    vnt::hetero::SolveOptions o;
+    o.max_virtual_nodes = max_virtual_nodes;
+    o.collect_candidates = collect != 0;
+    const auto r = vnt::hetero::solve(curves, pool, global_batch, o);
+    *out_ntypes = (uint32_t)r.best.types.size();
+    for (std::size_t j = 0; j < r.best.types.size(); ++j) {
+      const auto& t = r.best.types[j];
+      for (uint32_t i = 0; i < ntypes; ++i)
+        if (t.device_type == names[i]) out_type[j] = i;
+      out_n[j] = t.devices_used;
+      out_b[j] = t.per_device_batch;
+      out_v[j] = t.virtual_nodes;
+    }
+    *out_time = r.best.predicted_step_time_s;
+    *out_candidates = r.candidates.size();
+    return VNT_OK;
+  });
+}
+
+int vnt_hetero_profile_device(const uint64_t* widths, uint32_t nw, int32_t activation,
+                              int32_t loss, uint64_t seed, const char* device_type,
+                              uint64_t memory_capacity, const uint64_t* batch_sizes, uint32_t nb,
+                              uint64_t steps, uint64_t warmup_cutoff, int32_t cuda_device,
+                              int32_t gemm_mode, uint64_t* out_batch, double* out_time,
+                              uint32_t* out_npts, double* out_comm) {
+  return guard([&] {
+    vnt::ModelSpec spec;
+    spec.layer_widths.assign(widths, widths + nw);
+    spec.activation = static_cast<vnt::Activation>(activation);
+    spec.loss = static_cast<vnt::Loss>(loss);
+    spec.seed = seed;
+    vnt::hetero::ProfileOptions o;
+    o.steps = steps;
+    o.warmup_cutoff = warmup_cutoff;
+    const auto r = vnt::hetero::profile_device(
+        spec, device_type, memory_capacity, std::vector<std::size_t>(batch_sizes, batch_sizes + nb), o,
+        cuda_device, gemm_mode);
+    *out_npts = (uint32_t)r.curve.points.size();
+    for (std::size_t k = 0; k < r.curve.points.size(); ++k) {
+      out_batch[k] = r.curve.points[k].batch_size;
+      out_time[k] = r.curve.points[k].step_time_s;
+    }
+    *out_comm = r.curve.comm_overhead_s;
     return VNT_OK;
   });
 }
