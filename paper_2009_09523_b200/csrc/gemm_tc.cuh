@@ -490,6 +490,14 @@ bool tc_use_pair() {
   return on;
 }
 
+// dW on 256x128 CTA pairs (3xTF32 only) is opt-in: VNT_TC_DW_PAIR=1.  Measured
+// on cfg3 it runs the 4096x4096 dW at 60 % tensor-pipe activity against 74 %
+// for the single-CTA kernel (profiles/r01_summary.md), so the default stays single.
+bool tc_dw_pair() {
+  static const bool on = getenv("VNT_TC_DW_PAIR") && getenv("VNT_TC_DW_PAIR")[0] == '1';
+  return on;
+}
+
 bool tc_layer_eligible(int mode, uint64_t in, uint64_t out) {
   if (mode == VNT_GEMM_FFMA) return false;
   return in >= 64 && out >= 64 && in % 4 == 0 && out % 4 == 0;
@@ -521,15 +529,15 @@ template <int EPI>
 void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M, int N, int K,
                int nseg, const int* seg_k0, const int* seg_rows, const vntb::tc::EpiArgs& ep) {
   using namespace vntb::tc;
-  if constexpr (EPI != kTcDw) {
-    if (pair) {
-      if (e->split)
-        launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, ep, e->sm_count, e->stream);
-      else
-        launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, ep, e->sm_count, e->stream);
-      e->launches++;
-      return;
-    }
+  if (pair) {
+    if (e->split)
+      launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
+                               e->sm_count, e->stream);
+    else if constexpr (EPI != kTcDw)
+      launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
+                               e->sm_count, e->stream);
+    e->launches++;
+    return;
   }
   if (e->split)
     launch_gemm<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->sm_count,
@@ -601,11 +609,12 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   using namespace vntb::tc;
   const int M = (int)e->widths[l], N = (int)e->widths[l + 1];
   const uint64_t ldT = p.ldT;
-  // dW stays on the single-CTA kernel: its per-node epilogue, not operand
-  // traffic, bounds it once tiles are paired (measured).
+  // Single-CTA 128x128 by default; the 3xTF32 CTA-pair variant (256x128, B's
+  // smem traffic halved) is opt-in, see tc_dw_pair().
+  const bool pair = e->split && tc_use_pair() && tc_dw_pair();
+  const uint32_t bn = pair ? PairCfg<kTcDw, 3>::BNH : TileCfg<kTcDw>::BN;
   const OpMaps a = op_maps(e, e->XT[l], e->XTh[l], e->XTl[l], M, ldT, ldT, BM);
-  const OpMaps b = op_maps(e, e->DT[l + 1], e->DTh[l + 1], e->DTl[l + 1], N, ldT, ldT,
-                           TileCfg<kTcDw>::BN);
+  const OpMaps b = op_maps(e, e->DT[l + 1], e->DTh[l + 1], e->DTl[l + 1], N, ldT, ldT, bn);
   EpiArgs ep{};
   ep.M = M;
   ep.N = N;
@@ -616,7 +625,7 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   ep.lim = lim;
   ep.tail = e->G + e->P;
   ep.tensor = tensor;
-  tc_launch<kTcDw>(e, false, a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep);
+  tc_launch<kTcDw>(e, pair, a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep);
 }
 
 }  // namespace

@@ -11,14 +11,16 @@
 namespace vntb {
 namespace tc {
 
+// fwd / bwd-data: 256x256 pair tiles; dW: 256x128 (each CTA keeps the int64
+// per-node accumulators of its 128x128 half in registers, as the single-CTA dW).
 template <int EPI, int SPLIT = 1>
 struct PairCfg {
-  static constexpr int BN = 256;
+  static constexpr int BN = EPI == kTcDw ? 128 : 256;
   static constexpr int BNH = BN / 2;
   static constexpr int kBytesA = BM * BK * 4;
   static constexpr int kBytesB = BNH * BK * 4;
   static constexpr int kStageBytes = (SPLIT == 3 ? 2 : 1) * (kBytesA + kBytesB);
-  static constexpr int STAGES = 192 * 1024 / kStageBytes;
+  static constexpr int STAGES = (192 * 1024 / kStageBytes) < 6 ? (192 * 1024 / kStageBytes) : 6;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256;
 };
@@ -44,12 +46,16 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-// Arrive on the leader CTA's copy of `bar` (same smem offset).
+// Arrive on the leader CTA's copy of `bar` (same smem offset).  Used for the
+// TMEM-empty handshake only: the TMEM reads are ordered by the caller's
+// tcgen05.fence::before_thread_sync, so no cluster-scope release of generic
+// memory is needed (a .release.cluster fence per virtual node stalls the dW
+// epilogue on its own spill stores).
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(su32(bar))
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n}" ::"r"(su32(bar))
       : "memory");
 }
 
@@ -86,8 +92,8 @@ template <int EPI, int SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmAl,
-                   const __grid_constant__ CUtensorMap tmBl, int K, EpiArgs ep) {
-  static_assert(EPI != kTcDw, "pair kernel: forward / bwd-data epilogues only");
+                   const __grid_constant__ CUtensorMap tmBl, int K, int nseg,
+                   const int* __restrict__ seg_k0, const int* __restrict__ seg_rows, EpiArgs ep) {
   using C = PairCfg<EPI, SPLIT>;
   constexpr int BN = C::BN, BNH = C::BNH, STAGES = C::STAGES, PM = 2 * BM;
   extern __shared__ uint8_t smem_raw[];
@@ -105,6 +111,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int segs = nseg > 0 ? nseg : 1;   // dW: one K-chain per virtual node
   const int tiles_n = (int)ceil_div(ep.N, BN);
   const int tiles = (int)ceil_div(ep.M, PM) * tiles_n;
 
@@ -140,18 +147,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int tile = pair; tile < tiles; tile += npairs) {
         const int m0 = (tile / tiles_n) * PM + (int)rank * BM;
         const int n0 = (tile % tiles_n) * BN + (int)rank * BNH;
-        for (int k = 0; k < K; k += BK) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
-          tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], k, m0);
-          tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], k, n0);
-          if (SPLIT == 3) {
-            tma_load_2d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], k, m0);
-            tma_load_2d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], k, n0);
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+        for (int sg = 0; sg < segs; ++sg) {
+          const int kb = nseg > 0 ? seg_k0[sg] : 0;
+          const int kl = nseg > 0 ? (int)round_up(seg_rows[sg], 32) : K;
+          for (int k = 0; k < kl; k += BK) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+            tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
+            tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
+            if (SPLIT == 3) {
+              tma_load_2d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
+              tma_load_2d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -162,12 +173,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;
-      for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+      for (int tile = pair; tile < tiles; tile += npairs)
+      for (int sg = 0; sg < segs; ++sg, ++it) {
         const int b = it & 1;
         mbar_wait_cluster(&tempty[b], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * BN);
-        for (int k = 0; k < K; k += BK) {
+        const int kl = nseg > 0 ? (int)round_up(seg_rows[sg], 32) : K;
+        for (int k = 0; k < kl; k += BK) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
@@ -197,11 +210,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int h = (warp - 4) >> 2;
     const int row = q * 32 + lane;
-    const float tscale = ep.tscale_p ? *ep.tscale_p : 1.f;
+    const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
-    for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+    float amax = 0.f, canary = 0.f;
+    for (int tile = pair; tile < tiles; tile += npairs) {
       const int m0 = (tile / tiles_n) * PM + (int)rank * BM, n0 = (tile % tiles_n) * BN;
       const int r = m0 + row;
+      long long acc[EPI == kTcDw ? COLS : 1];
+      if (EPI == kTcDw) {
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) acc[j] = 0;
+      }
+      for (int sg = 0; sg < segs; ++sg, ++it) {
       const int b = it & 1;
       mbar_wait(&tfull[b], (it >> 1) & 1);
       tc_fence_after();
@@ -211,7 +231,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int col = h * COLS + c * 32;
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
         const int nb = n0 + col;
-        if (r < ep.M) {
+        if (EPI == kTcDw) {
+          // per-node quantisation, as k_gemm_tc's dW epilogue
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = v[j];
+            amax = fmaxf(amax, fabsf(x));
+            canary = fmaf(x, 0.f, canary);
+            acc[c * 32 + j] += __float2ll_rn(x);
+          }
+        } else if (r < ep.M) {
           const int tc = ep.tcol[r];
           if (EPI == kTcBwd && nb + 32 <= ep.N) {
             const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
@@ -272,6 +301,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty[b]);
+      }
+      if (EPI == kTcDw && r < ep.M) {
+        long long* g = ep.G + (size_t)r * ep.ldg + n0 + h * COLS;
+        const int nvalid = ep.N - (n0 + h * COLS);
+        if (nvalid >= COLS) {
+#pragma unroll
+          for (int j = 0; j < COLS; j += 2) {
+            longlong2* gp = reinterpret_cast<longlong2*>(g + j);
+            longlong2 o = ep.first ? make_longlong2(0, 0) : *gp;
+            o.x += acc[j];
+            o.y += acc[j + 1];
+            *gp = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < COLS; ++j)
+            if (j < nvalid) g[j] = ep.first ? acc[j] : g[j] + acc[j];
+        }
+      }
+    }
+    if (EPI == kTcDw) {
+      if (canary != 0.f)   // NaN: some partial was NaN or inf
+        atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
+      else if (!(amax < ep.lim))
+        atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);
     }
   }
   tc_fence_before();
@@ -286,8 +340,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 template <int EPI, int SPLIT>
 inline void launch_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& al,
-                             const CUtensorMap& bl, int M, int N, int K, const EpiArgs& ep,
-                             int sms, cudaStream_t s) {
+                             const CUtensorMap& bl, int M, int N, int K, int nseg,
+                             const int* seg_k0, const int* seg_rows, const EpiArgs& ep, int sms,
+                             cudaStream_t s) {
   using C = PairCfg<EPI, SPLIT>;
   static bool attr = false;
   if (!attr) {
@@ -297,7 +352,8 @@ inline void launch_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const C
   }
   const int tiles = (int)(ceil_div(M, 2 * BM) * ceil_div(N, C::BN));
   const int pairs = std::max(1, std::min(tiles, sms / 2));
-  k_gemm_tc_pair<EPI, SPLIT><<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a, b, al, bl, K, ep);
+  k_gemm_tc_pair<EPI, SPLIT><<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a, b, al, bl, K, nseg,
+                                                                        seg_k0, seg_rows, ep);
   VNT_LAUNCH_CHECK();
 }
 
