@@ -151,3 +151,40 @@ def test_padding_columns_across_uneven_passes(port, mode):
     for p, l in outs[1:]:
         assert l == outs[0][1]
         assert np.array_equal(p, outs[0][0])
+
+
+def test_pair_dw_opt_in_matches_reference(port):
+    """VNT_TC_DW_PAIR=1 (256x128 CTA-pair dW, opt-in): fp32-grade gradients and
+    bit-identical across pass groupings, like the default single-CTA dW."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle_lib, paper_2009_09523_b200 as vnt
+port = oracle_lib.port()
+w = [256, 512, 384, 10]
+sizes = [24, 40, 7, 57, 128]
+B = sum(sizes)
+x, y = port.synth_batch(3, 4096, w[0], w[-1], 0, B)
+p0 = port.init_params(w, 1)
+want, _ = port.forward_backward(w, "relu", "softmax-cross-entropy", p0, x, y)
+out = []
+for rr in (0, 64):
+    e = vnt.Engine(w, "relu", "softmax-cross-entropy", gemm_mode="3xtf32", resident_rows=rr)
+    e.add_device(1 << 20)
+    e.set_params(p0)
+    e.device_step(0, x, y, sizes)
+    g, _, _ = e.sync()
+    out.append(g)
+err = float(np.abs(out[0] - want).max() / np.abs(want).max())
+print(json.dumps({"err": err, "bitwise": bool(np.array_equal(out[0], out[1]))}))
+'''
+    env = dict(os.environ, VNT_TC_DW_PAIR="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=str(GOLDEN.parents[1]), timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    print(res)
+    assert res["err"] < 2e-5 and res["bitwise"]
