@@ -676,22 +676,35 @@ __device__ __forceinline__ double sgd_one(const SgdArgs& a, size_t k, float& w32
   return fabs(g);
 }
 
+// max |g| of the block into *dst: warp xor-max, then one atomic per block
+// (per-warp atomics on one address serialise in L2 across thousands of blocks).
+// Every thread of the block must call it.
 __device__ __forceinline__ void block_max_to(unsigned long long* dst, double v) {
+  __shared__ unsigned long long wmax[32];
   unsigned long long b = (unsigned long long)__double_as_longlong(v);
 #pragma unroll
   for (int s = 16; s; s >>= 1) {
     const unsigned long long o = __shfl_xor_sync(0xffffffffu, b, s);
     b = o > b ? o : b;
   }
-  if ((threadIdx.x & 31) == 0 && b) atomicMax(dst, b);
+  const int t = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+  if ((t & 31) == 0) wmax[t >> 5] = b;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long m = 0;
+    for (int i = 0; i < nw; ++i) m = wmax[i] > m ? wmax[i] : m;
+    if (m) atomicMax(dst, m);
+  }
 }
 
 // Weight tensor: 64x32 (rows x cols) tiles, 32x8 threads, 8 elements per
 // thread with all loads issued before the dependent math; transposed fp32 copy
 // via smem.
-template <bool MOM>   // momentum buffer present (registers for v[] only then)
-__global__ void __launch_bounds__(256, MOM ? 2 : 3) k_sgd_weight(SgdArgs a) {
-  constexpr int TR = 64, TC = 32, PER = TR / 8;
+// MOM: momentum buffer present (registers for v[] only then); TR: rows per tile.
+template <bool MOM, int TR = 64>
+__global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weight(SgdArgs a) {
+  constexpr int TC = 32, PER = TR / 8;
   __shared__ float tile[TR][TC + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
@@ -738,14 +751,14 @@ __global__ void __launch_bounds__(256, MOM ? 2 : 3) k_sgd_weight(SgdArgs a) {
   block_max_to(a.gmax, mx);
   if (!a.wt32 && !a.wt32h) return;
   __syncthreads();
-  // transposed: WT[c][r], 32 columns x 64 rows -> each warp row writes 64 contiguous rows
+  // transposed: WT[c][r], 32 columns x TR rows -> each warp row writes TR contiguous rows
 #pragma unroll
   for (int k = 0; k < TC / 8; ++k) {
     const int cc = ty + 8 * k;
     const int col = c0 + cc;
     if (col >= a.cols) continue;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < TR / 32; ++h) {
       const int r = r0 + h * 32 + tx;
       if (r < a.rows) {
         const float v = tile[h * 32 + tx][cc];
