@@ -281,53 +281,60 @@ __global__ void k_loss(const float* __restrict__ logits, const double* __restric
                        int ldT, const int* __restrict__ tcol, long long* __restrict__ tail,
                        const float* __restrict__ tscale_p) {
   const float tscale = tscale_p ? *tscale_p : 1.f;
+  __shared__ unsigned long long block_loss;   // exact int64 sum of this block's rows
+  if (threadIdx.x == 0) block_loss = 0;
+  __syncthreads();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
   const int r = warp;
-  const float* z = logits + (size_t)r * outw;
-  const double* yr = y + (size_t)r * outw;
-  const int tc = tcol[r];
-  double loss = 0.0;
-  if (loss_kind == 0) {
-    for (int o = lane; o < outw; o += 32) {
-      const double d = (double)z[o] - yr[o];
-      loss += d * d;
-      const float dl = (float)(2.0 * d / (double)outw);
-      D[(size_t)r * outw + o] = dl;
-      DT[(size_t)o * ldT + tc] = dl * tscale;
-    }
+  if (warp < rows) {
+    const float* z = logits + (size_t)r * outw;
+    const double* yr = y + (size_t)r * outw;
+    const int tc = tcol[r];
+    double loss = 0.0;
+    if (loss_kind == 0) {
+      for (int o = lane; o < outw; o += 32) {
+        const double d = (double)z[o] - yr[o];
+        loss += d * d;
+        const float dl = (float)(2.0 * d / (double)outw);
+        D[(size_t)r * outw + o] = dl;
+        DT[(size_t)o * ldT + tc] = dl * tscale;
+      }
 #pragma unroll
-    for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
-    loss /= (double)outw;
-  } else {
-    double mx = -1e300;
-    for (int o = lane; o < outw; o += 32) mx = fmax(mx, (double)z[o]);
-#pragma unroll
-    for (int s = 16; s; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
-    double norm = 0.0;
-    for (int o = lane; o < outw; o += 32) norm += exp((double)z[o] - mx);
-#pragma unroll
-    for (int s = 16; s; s >>= 1) norm += __shfl_xor_sync(0xffffffffu, norm, s);
-    const double lognorm = log(norm);
-    for (int o = lane; o < outw; o += 32) {
-      const double zm = (double)z[o] - mx;
-      loss -= yr[o] * (zm - lognorm);
-      const float dl = (float)(exp(zm) / norm - yr[o]);
-      D[(size_t)r * outw + o] = dl;
-      DT[(size_t)o * ldT + tc] = dl * tscale;
-    }
-#pragma unroll
-    for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
-  }
-  if (lane == 0) {
-    if (!isfinite(loss)) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
+      for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
+      loss /= (double)outw;
     } else {
-      const long long q = __double2ll_rn(ldexp(loss, kLossScaleBits));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailLoss]), (unsigned long long)q);
+      double mx = -1e300;
+      for (int o = lane; o < outw; o += 32) mx = fmax(mx, (double)z[o]);
+#pragma unroll
+      for (int s = 16; s; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+      double norm = 0.0;
+      for (int o = lane; o < outw; o += 32) norm += exp((double)z[o] - mx);
+#pragma unroll
+      for (int s = 16; s; s >>= 1) norm += __shfl_xor_sync(0xffffffffu, norm, s);
+      const double lognorm = log(norm);
+      for (int o = lane; o < outw; o += 32) {
+        const double zm = (double)z[o] - mx;
+        loss -= yr[o] * (zm - lognorm);
+        const float dl = (float)(exp(zm) / norm - yr[o]);
+        D[(size_t)r * outw + o] = dl;
+        DT[(size_t)o * ldT + tc] = dl * tscale;
+      }
+#pragma unroll
+      for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
+    }
+    if (lane == 0) {
+      if (!isfinite(loss)) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
+      } else {
+        const long long q = __double2ll_rn(ldexp(loss, kLossScaleBits));
+        atomicAdd(&block_loss, (unsigned long long)q);   // shared memory, order-free
+      }
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && block_loss)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailLoss]), block_loss);
 }
 
 // Fixed-point quantisation of one per-node partial:
