@@ -188,13 +188,22 @@ __device__ __forceinline__ void combine_feature(double* __restrict__ mean, doubl
   m2[j] = s;
 }
 
+// `steps` may live in pinned host memory (read over the bus): each block first
+// copies a chunk of them into shared memory with all threads at once.
 __global__ void k_stats_combine(double* __restrict__ mean, double* __restrict__ m2, int in,
                                 const double* __restrict__ vn_mean,
                                 const double* __restrict__ vn_m2,
                                 const CombineStep* __restrict__ steps, int nsteps) {
+  constexpr int kChunk = 256;
+  __shared__ CombineStep st[kChunk];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= in) return;
-  combine_feature(mean, m2, in, j, vn_mean, vn_m2, steps, nsteps);
+  for (int t0 = 0; t0 < nsteps; t0 += kChunk) {
+    const int tn = min(kChunk, nsteps - t0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < tn; t += blockDim.x) st[t] = steps[t0 + t];
+    __syncthreads();
+    if (j < in) combine_feature(mean, m2, in, j, vn_mean, vn_m2, st, tn);
+  }
 }
 
 // ------------------------------------------------------ FFMA dense layer
