@@ -130,7 +130,6 @@ struct vnt_engine {
   float* logits = nullptr;
   double* vn_mean = nullptr;
   double* vn_m2 = nullptr;
-  CombineStep* d_combine = nullptr;
   CombineStep* h_combine = nullptr;
   CombineStep* m_combine = nullptr;    // device view of the pinned h_combine
   size_t combine_cap = 0;
@@ -362,10 +361,8 @@ void ensure_combine(vnt_engine* e, size_t n) {
   if (n <= e->combine_cap) return;
   VNT_CUDA(cudaStreamSynchronize(e->stream));
   drop_graphs(e);
-  if (e->d_combine) cudaFree(e->d_combine);
   if (e->h_combine) cudaFreeHost(e->h_combine);
   n = std::max<size_t>(n, 64);
-  e->d_combine = (CombineStep*)dalloc(n * sizeof(CombineStep));
   VNT_CUDA(cudaMallocHost(&e->h_combine, n * sizeof(CombineStep)));
   VNT_CUDA(cudaHostGetDevicePointer((void**)&e->m_combine, e->h_combine, 0));
   e->combine_cap = n;
@@ -1473,7 +1470,7 @@ void vnt_engine_destroy(vnt_engine* e) {
   for (void* p : {(void*)e->w64, (void*)e->v64, (void*)e->w32, (void*)e->wt32, (void*)e->G,
                   (void*)e->gout, (void*)e->xbuf[0], (void*)e->ybuf[0], (void*)e->wpad,
                   (void*)e->xbuf[1], (void*)e->ybuf[1], (void*)e->logits,
-                  (void*)e->vn_mean, (void*)e->vn_m2, (void*)e->d_combine})
+                  (void*)e->vn_mean, (void*)e->vn_m2})
     if (p) cudaFree(p);
   for (auto* v : {&e->X, &e->XT, &e->D, &e->DT})
     for (auto* p : *v)
