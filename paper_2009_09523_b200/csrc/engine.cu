@@ -68,6 +68,14 @@ struct vnt_engine {
   std::vector<int> tc_layer;   // 1: layer runs on tcgen05 tiles
   vnt_engine_options opt{};
   ncclComm_t comm = nullptr;
+  // Per-layer gradient all-reduce overlapped with the rest of the backward:
+  // layer l's slice of G is reduced on comm_stream as soon as its dW/db are
+  // final, while the compute stream continues (VNT_COMM_OVERLAP=0 disables).
+  bool comm_overlap = false;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> layer_ev;   // per layer: its dW/db done (compute stream)
+  cudaEvent_t comm_ev = nullptr;       // comm_stream caught up
+  int gemm_sms = 0;                    // CTAs the persistent GEMMs may occupy
   cudaStream_t stream = nullptr;
   int sm_count = 0;
 
@@ -633,6 +641,7 @@ void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStr
 }
 
 void backup_stats(vnt_engine* e, cudaStream_t s);
+void layer_collective(vnt_engine* e, int l);
 
 // Small models: one k_node_step CTA per node does the whole pass.
 void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats) {
@@ -696,7 +705,7 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
 void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats);
 
 void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats,
-              bool first_write) {
+              bool first_write, bool layer_comm = false) {
   if (e->node_path) {
     run_node_pass(e, p, stats);
     return;
@@ -822,6 +831,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
+    if (layer_comm) layer_collective(e, l);   // layer l's gradient is final in this process
     if (l > 0) {
       prof_begin(e);
       if (e->tc_layer[l]) {
@@ -910,7 +920,7 @@ void restore_stats(vnt_engine* e) {
 }
 
 void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, const double* y,
-                bool on_device, bool do_stats) {
+                bool on_device, bool do_stats, bool layer_comm = false) {
   auto& passes = plan_for(e, local);
   std::vector<std::vector<StatsLaunch>> stats(passes.size());
   if (do_stats) {
@@ -931,20 +941,56 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
       else e->pf.valid = false;
     }
     if (!took) stage_inputs(e, p, x, y, on_device);
-    run_pass(e, p, do_stats ? &stats[i] : nullptr, !e->acc_started);
+    run_pass(e, p, do_stats ? &stats[i] : nullptr, !e->acc_started,
+             layer_comm && i + 1 == passes.size());
     e->acc_started = true;
     e->acc_examples += p.rows;
   }
 }
 
+// With an NCCL group, overlap the per-layer reductions with the backward; the
+// persistent GEMMs then leave a few SMs to the NCCL kernels running beside them.
+void setup_comm_overlap(vnt_engine* e) {
+  e->gemm_sms = e->sm_count;
+  e->comm_overlap = e->comm && !(getenv("VNT_COMM_OVERLAP") && getenv("VNT_COMM_OVERLAP")[0] == '0');
+  if (!e->comm_overlap) return;
+  if (!e->comm_stream) {   // idempotent (regroup calls it again)
+    VNT_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
+    e->layer_ev.assign(e->L, nullptr);
+    for (auto& ev : e->layer_ev) VNT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    VNT_CUDA(cudaEventCreateWithFlags(&e->comm_ev, cudaEventDisableTiming));
+  }
+  e->gemm_sms = std::max(2, (e->sm_count - 16) & ~1);   // even: CTA pairs
+}
+
+void allreduce(vnt_engine* e, long long* p, size_t n, cudaStream_t s) {
+  const ncclResult_t r = ncclAllReduce(p, p, n, ncclInt64, ncclSum, e->comm, s);
+  if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+}
+
 void collective(vnt_engine* e) {
   // Exact int64 sum over processes; associative, so any NCCL algorithm or
   // topology gives the same bits.
-  if (e->opt.world_size > 1) {
-    const ncclResult_t r = ncclAllReduce(e->G, e->G, e->P + e->ntail, ncclInt64, ncclSum,
-                                         e->comm, e->stream);
-    if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
-  }
+  if (e->comm) allreduce(e, e->G, e->P + e->ntail, e->stream);
+}
+
+// Overlapped variant, issued identically (same calls, same order) on every
+// rank: layer l's G slice once its dW/db are final, from the compute stream's
+// point of view (run_pass records layer_ev[l] after them).
+void layer_collective(vnt_engine* e, int l) {
+  VNT_CUDA(cudaEventRecord(e->layer_ev[l], e->stream));
+  VNT_CUDA(cudaStreamWaitEvent(e->comm_stream, e->layer_ev[l], 0));
+  const uint64_t n = e->widths[l] * e->widths[l + 1] + e->widths[l + 1];   // W then b, contiguous
+  allreduce(e, e->G + e->woff[l], n, e->comm_stream);
+}
+
+// The tail (loss, examples, flags) last, then the compute stream waits for all.
+void finish_layer_collectives(vnt_engine* e) {
+  VNT_CUDA(cudaEventRecord(e->layer_ev[0], e->stream));
+  VNT_CUDA(cudaStreamWaitEvent(e->comm_stream, e->layer_ev[0], 0));
+  allreduce(e, e->G + e->P, e->ntail, e->comm_stream);
+  VNT_CUDA(cudaEventRecord(e->comm_ev, e->comm_stream));
+  VNT_CUDA(cudaStreamWaitEvent(e->stream, e->comm_ev, 0));
 }
 
 // lr, 1/B (virtual_exec.cpp:165), momentum and 2^-s come from the step params.
@@ -1170,7 +1216,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
     Readback rb;
     const std::vector<Pass>* passes = local.empty() ? nullptr : &plan_for(e, local);
     const bool single = passes && passes->size() == 1;
-    if (single && attempt == 0 && e->graphs && e->opt.world_size == 1) {
+    if (single && attempt == 0 && e->graphs && !e->comm) {
       // Graph path: host prep outside, the whole device step as one graph launch.
       const Pass& p = (*passes)[0];
       ensure_combine(e, p.nodes.size());
@@ -1230,14 +1276,20 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
       copy_step_params(e);
       begin_round_device(e);
-      if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0);
+      // every rank issues the same collective sequence: per layer (overlapped)
+      // on the layered path, one reduction otherwise
+      const bool overlap = e->comm && e->comm_overlap && !e->node_path;
+      if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0, overlap);
       add_examples_tail(e);
       if (local.empty()) {
         // This process hosts no node this step: contribute zeros.
         VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
+        if (overlap)
+          for (int l = e->L - 1; l >= 0; --l) layer_collective(e, l);
       }
       VNT_CUDA(cudaEventRecord(e->ev[2], e->stream));
-      collective(e);
+      if (overlap) finish_layer_collectives(e);
+      else collective(e);
       VNT_CUDA(cudaEventRecord(e->ev[3], e->stream));
       launch_sgd(e);
       VNT_CUDA(cudaEventRecord(e->ev[4], e->stream));
@@ -1441,13 +1493,23 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     e->graphs = !(getenv("VNT_GRAPHS") && getenv("VNT_GRAPHS")[0] == '0') && !e->profile;
     e->host_prof = getenv("VNT_HOST_PROFILE") && getenv("VNT_HOST_PROFILE")[0] == '1';
     tc_init(e.get());
-    if (e->opt.world_size > 1) {
-      if (!options->nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
+    // VNT_FORCE_COMM=1: a one-rank NCCL group on a single process, so the
+    // collective code paths (including the overlapped per-layer reduction) run
+    // and can be tested on one GPU.
+    const bool force = getenv("VNT_FORCE_COMM") && getenv("VNT_FORCE_COMM")[0] == '1';
+    if (e->opt.world_size > 1 || force) {
       ncclUniqueId id;
-      std::memcpy(&id, options->nccl_id, sizeof id);
+      if (e->opt.world_size > 1) {
+        if (!options->nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
+        std::memcpy(&id, options->nccl_id, sizeof id);
+      } else {
+        const ncclResult_t g = ncclGetUniqueId(&id);
+        if (g != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(g));
+      }
       const ncclResult_t r = ncclCommInitRank(&e->comm, e->opt.world_size, id, e->opt.rank);
       if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
     }
+    setup_comm_overlap(e.get());
     *out = e.release();
     return VNT_OK;
   });
@@ -1504,6 +1566,13 @@ void vnt_engine_destroy(vnt_engine* e) {
     cudaStreamDestroy(e->aux_stream);
   }
   if (e->fork_ev) cudaEventDestroy(e->fork_ev);
+  if (e->comm_stream) {
+    cudaStreamSynchronize(e->comm_stream);
+    cudaStreamDestroy(e->comm_stream);
+  }
+  for (auto& ev : e->layer_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (e->comm_ev) cudaEventDestroy(e->comm_ev);
   if (e->join_ev) cudaEventDestroy(e->join_ev);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
@@ -1808,6 +1877,7 @@ int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const ui
         source_rank >= world_size)
       throw EngineError(VNT_ERR_CONFIG, "bad rank/world_size/source_rank");
     VNT_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->comm_stream) VNT_CUDA(cudaStreamSynchronize(e->comm_stream));
     if (e->comm) {
       ncclCommDestroy(e->comm);
       e->comm = nullptr;
@@ -1816,12 +1886,16 @@ int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const ui
     reset_acc(e);
     e->opt.rank = rank;
     e->opt.world_size = world_size;
-    if (world_size == 1) return VNT_OK;
+    if (world_size == 1) {
+      setup_comm_overlap(e);
+      return VNT_OK;
+    }
     if (!nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&e->comm, world_size, id, rank);
     if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+    setup_comm_overlap(e);
     // Replica state from the source rank: fp64 master, momentum, fixed-point
     // scale history (part of the numerical state).
     auto bcast = [&](void* p, size_t n, ncclDataType_t t) {

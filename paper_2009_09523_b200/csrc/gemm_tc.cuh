@@ -532,18 +532,18 @@ void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M
   if (pair) {
     if (e->split)
       launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
-                               e->sm_count, e->stream);
+                               e->gemm_sms, e->stream);
     else if constexpr (EPI != kTcDw)
       launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
-                               e->sm_count, e->stream);
+                               e->gemm_sms, e->stream);
     e->launches++;
     return;
   }
   if (e->split)
-    launch_gemm<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->sm_count,
+    launch_gemm<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->gemm_sms,
                         e->stream);
   else
-    launch_gemm<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->sm_count,
+    launch_gemm<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->gemm_sms,
                         e->stream);
   e->launches++;
 }

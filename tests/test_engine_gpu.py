@@ -252,3 +252,30 @@ def test_prefetch_is_bit_identical(port, monkeypatch, graphs):
         lb.append(b.train_step_ptr(*ptr(s), B, sizes, dev, 0.05, False))
     assert la == lb
     assert np.array_equal(a.get_params(), b.get_params())
+
+
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_collective_paths_bit_identical(port, monkeypatch, overlap):
+    """VNT_FORCE_COMM=1 gives the engine a one-rank NCCL group, so the collective
+    code runs on one GPU: the single reduction (VNT_COMM_OVERLAP=0) and the
+    per-layer reductions overlapped with the backward on a comm stream (default)
+    must leave every bit of the trajectory unchanged, for any pass grouping."""
+    w = [128, 256, 256, 10]
+    sizes, dev = vnt().uniform_mapping(256, 8, 1)
+
+    def trajectory(rr):
+        e = make_engine(w, "relu", "softmax-cross-entropy", 4, port, gemm_mode="auto",
+                        resident_rows=rr)
+        losses = []
+        for s in range(3):
+            x, y = port.synth_batch(4, 2048, w[0], w[-1], s * 256, 256)
+            losses.append(e.train_step(x, y, sizes, dev, 0.02)[0])
+        return e.get_params(), losses
+
+    want = trajectory(0)
+    monkeypatch.setenv("VNT_FORCE_COMM", "1")
+    monkeypatch.setenv("VNT_COMM_OVERLAP", overlap)
+    for rr in (0, 96):
+        got = trajectory(rr)
+        assert got[1] == want[1]
+        assert np.array_equal(got[0], want[0])
