@@ -75,7 +75,7 @@ struct vnt_engine {
   cudaStream_t comm_stream = nullptr;
   std::vector<cudaEvent_t> layer_ev;   // per layer: its dW/db done (compute stream)
   cudaEvent_t comm_ev = nullptr;       // comm_stream caught up
-  int gemm_sms = 0;                    // CTAs the persistent GEMMs may occupy
+  int gemm_sms = 0;                    // CTAs the backward GEMMs may occupy
   cudaStream_t stream = nullptr;
   int sm_count = 0;
 
@@ -948,11 +948,26 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
   }
 }
 
+constexpr int kCommSms = 16;   // SMs left to NCCL while the backward GEMMs run
+
+bool overlap_wanted() {
+  return !(getenv("VNT_COMM_OVERLAP") && getenv("VNT_COMM_OVERLAP")[0] == '0');
+}
+
+// NCCL group of (opt.rank, opt.world_size); with overlap its kernels are capped
+// at kCommSms CTAs so they fit beside the backward GEMMs.
+void comm_init(vnt_engine* e, const ncclUniqueId& id) {
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  if (overlap_wanted()) cfg.maxCTAs = kCommSms;
+  const ncclResult_t r = ncclCommInitRankConfig(&e->comm, e->opt.world_size, id, e->opt.rank, &cfg);
+  if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+}
+
 // With an NCCL group, overlap the per-layer reductions with the backward; the
-// persistent GEMMs then leave a few SMs to the NCCL kernels running beside them.
+// backward GEMMs then leave kCommSms SMs to the NCCL kernels beside them.
 void setup_comm_overlap(vnt_engine* e) {
   e->gemm_sms = e->sm_count;
-  e->comm_overlap = e->comm && !(getenv("VNT_COMM_OVERLAP") && getenv("VNT_COMM_OVERLAP")[0] == '0');
+  e->comm_overlap = e->comm && overlap_wanted();
   if (!e->comm_overlap) return;
   if (!e->comm_stream) {   // idempotent (regroup calls it again)
     VNT_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
@@ -960,7 +975,7 @@ void setup_comm_overlap(vnt_engine* e) {
     for (auto& ev : e->layer_ev) VNT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     VNT_CUDA(cudaEventCreateWithFlags(&e->comm_ev, cudaEventDisableTiming));
   }
-  e->gemm_sms = std::max(2, (e->sm_count - 16) & ~1);   // even: CTA pairs
+  e->gemm_sms = std::max(2, (e->sm_count - kCommSms) & ~1);   // even: CTA pairs
 }
 
 void allreduce(vnt_engine* e, long long* p, size_t n, cudaStream_t s) {
@@ -1506,8 +1521,7 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
         const ncclResult_t g = ncclGetUniqueId(&id);
         if (g != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(g));
       }
-      const ncclResult_t r = ncclCommInitRank(&e->comm, e->opt.world_size, id, e->opt.rank);
-      if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+      comm_init(e.get(), id);
     }
     setup_comm_overlap(e.get());
     *out = e.release();
@@ -1893,8 +1907,7 @@ int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const ui
     if (!nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof id);
-    ncclResult_t r = ncclCommInitRank(&e->comm, world_size, id, rank);
-    if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+    comm_init(e, id);
     setup_comm_overlap(e);
     // Replica state from the source rank: fp64 master, momentum, fixed-point
     // scale history (part of the numerical state).

@@ -529,21 +529,23 @@ template <int EPI>
 void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M, int N, int K,
                int nseg, const int* seg_k0, const int* seg_rows, const vntb::tc::EpiArgs& ep) {
   using namespace vntb::tc;
+  // forward GEMMs never share the GPU with the gradient reductions
+  const int sms = EPI == kTcFwd ? e->sm_count : e->gemm_sms;
   if (pair) {
     if (e->split)
       launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
-                               e->gemm_sms, e->stream);
+                               sms, e->stream);
     else if constexpr (EPI != kTcDw)
       launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
-                               e->gemm_sms, e->stream);
+                               sms, e->stream);
     e->launches++;
     return;
   }
   if (e->split)
-    launch_gemm<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->gemm_sms,
+    launch_gemm<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, sms,
                         e->stream);
   else
-    launch_gemm<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, e->gemm_sms,
+    launch_gemm<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep, sms,
                         e->stream);
   e->launches++;
 }
