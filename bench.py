@@ -209,6 +209,16 @@ def cpu_reference(work, steps, warmup):
             "sample": sample}, step_s
 
 
+def run_config(args, work, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    return {"workload": args.workload, "baseline_config_index": work["config_index"],
+            "layer_widths": work["widths"], "activation": work["act"], "loss": work["loss"],
+            "global_batch": work["B"], "virtual_nodes": work["V"], "lr": work["lr"],
+            "parallelism": f"vn-dp{world}", "gemm_mode": args.gemm_mode,
+            "l2": "per-step working set (fp64+fp32 params, activations) >> 126 MB L2; "
+                  "4 resident batches rotate"}
+
+
 def run_reference(args, work):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -219,8 +229,7 @@ def run_reference(args, work):
         "value": base["value"], "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "layer_widths": work["widths"],
-                   "global_batch": work["B"], "virtual_nodes": work["V"]},
+        "config": run_config(args, work, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -361,12 +370,7 @@ def run_ours(args, work):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.workload, "baseline_config_index": work["config_index"],
-                   "layer_widths": w, "activation": work["act"], "loss": work["loss"],
-                   "global_batch": B, "virtual_nodes": V, "lr": lr,
-                   "parallelism": f"vn-dp{world}", "gemm_mode": args.gemm_mode,
-                   "l2": "per-step working set (fp64+fp32 params, activations) >> 126 MB L2; "
-                         "4 resident batches rotate"},
+        "config": run_config(args, work, world),
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "prefetch": not args.no_prefetch,
                 "wall_ms_per_step": e2e_wall_ms / args.steps},
