@@ -53,7 +53,7 @@ struct Pass {
   std::vector<PassNode> nodes;
   uint64_t rows = 0;
   uint64_t ldT = 0;
-  int* d_meta = nullptr;   // [tcol(rows) | row0(n) | rows(n) | col0(n)]
+  int* d_meta = nullptr;   // [tcol(rows) | row0(n) | rows(n) | col0(n) | src_row(n)]
 };
 
 }  // namespace
@@ -407,13 +407,14 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
   if (!cur.nodes.empty()) passes.push_back(cur);
   for (auto& p : passes) {
     const size_t nn = p.nodes.size();
-    std::vector<int> meta(p.rows + 3 * nn);
+    std::vector<int> meta(p.rows + 4 * nn);
     for (size_t k = 0; k < nn; ++k) {
       const auto& pn = p.nodes[k];
       for (uint64_t r = 0; r < pn.rows; ++r) meta[pn.prow + r] = (int)(pn.pcol + r);
       meta[p.rows + k] = (int)pn.prow;
       meta[p.rows + nn + k] = (int)pn.rows;
       meta[p.rows + 2 * nn + k] = (int)pn.pcol;
+      meta[p.rows + 3 * nn + k] = (int)pn.src_row;
     }
     p.d_meta = (int*)dalloc(meta.size() * sizeof(int));
     VNT_CUDA(cudaMemcpy(p.d_meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -642,6 +643,21 @@ void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStr
 
 void backup_stats(vnt_engine* e, cudaStream_t s);
 void layer_collective(vnt_engine* e, int l);
+
+void launch_stage_rows(vnt_engine* e, const Pass& p) {
+  const size_t nn = p.nodes.size();
+  const int* row0 = p.d_meta + p.rows;
+  // ~16 KB per CTA: enough CTAs in flight for the copy to run at bandwidth
+  uint64_t maxrows = 1;
+  for (const auto& pn : p.nodes) maxrows = std::max<uint64_t>(maxrows, pn.rows);
+  const unsigned slices = (unsigned)std::min<uint64_t>(
+      64, ceil_div(maxrows * (e->widths[0] + e->widths[e->L]) * sizeof(double), 16384));
+  k_stage_rows<<<dim3((unsigned)nn, slices), 256, 0, e->stream>>>(e->d_sp, e->xin, e->yin, row0, row0 + nn,
+                                                    row0 + 3 * nn, (int)e->widths[0],
+                                                    (int)e->widths[e->L]);
+  VNT_LAUNCH_CHECK();
+  e->launches++;
+}
 
 // Small models: one k_node_step CTA per node does the whole pass.
 void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stats) {
@@ -1205,9 +1221,11 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
   const double inv_b = 1.0 / (double)batch_rows;   // virtual_exec.cpp:165
   for (int attempt = 0;; ++attempt) {
     // Device work of the step, in order; recorded once per plan as a CUDA graph.
+    const Pass* graph_stage = nullptr;   // resident batch staged inside the graph
     auto enqueue_step = [&](const std::vector<StatsLaunch>* stats, bool events) {
       if (events) VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
       copy_step_params(e);
+      if (graph_stage) launch_stage_rows(e, *graph_stage);
       begin_round_device(e);
       auto& passes = plan_for(e, local);
       if (passes.size() == 1) {
@@ -1239,9 +1257,17 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       size_t off = 0;
       const std::vector<StatsLaunch> stats = prep_stats(e, p, off);
       hc.mark();   // 2: plan, capacity, stats prep
-      if (!take_prefetch(e, x, y)) stage_inputs(e, p, x, y, on_device);
+      // A device-resident batch is copied by k_stage_rows inside the graph (its
+      // pointers travel in the step parameters); host batches are staged here
+      // or arrive through the prefetch.
+      const bool took = take_prefetch(e, x, y);
+      const bool stage_in_graph = !took && on_device;
+      if (!took && !on_device) stage_inputs(e, p, x, y, false);
+      e->h_sp->x = stage_in_graph ? x : nullptr;
+      e->h_sp->y = stage_in_graph ? y : nullptr;
+      graph_stage = stage_in_graph ? &p : nullptr;
       hc.mark();   // 3: input staging
-      std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur};
+      std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur, stage_in_graph ? 1 : 0};
       for (const auto& n : local) {
         key.push_back(n.node);
         key.push_back(n.dev);

@@ -33,6 +33,8 @@ struct StepParams {
   float dts[kMaxLayers + 1];         // DT[l] copy scale (2^s of the dW consuming it, or 1)
   double inv_scale[2 * kMaxLayers];  // 2^-s_t
   double lr, mu, inv_b;
+  const double* x;                   // this step's device-resident batch (k_stage_rows)
+  const double* y;
 };
 
 // ---------------------------------------------------------------- ingest
@@ -90,6 +92,34 @@ __global__ void k_copy_f64x2(const double* __restrict__ a, double* __restrict__ 
     a_out[i] = a[i];
     b_out[i] = b[i];
   }
+}
+
+// Device-resident batch -> the pass's input buffers, one CTA per node; the
+// source pointers come from the step parameters, so a captured step graph
+// stages whatever batch the step is given.
+__global__ void k_stage_rows(const StepParams* __restrict__ sp, double* __restrict__ xin,
+                             double* __restrict__ yin, const int* __restrict__ row0,
+                             const int* __restrict__ nrows, const int* __restrict__ src_row, int in,
+                             int out) {
+  // blockIdx.x = node, blockIdx.y = slice of its (contiguous) rows
+  const int k = blockIdx.x;
+  const size_t nx = (size_t)nrows[k] * in, ny = (size_t)nrows[k] * out;
+  const double* xs = sp->x + (size_t)src_row[k] * in;
+  const double* ys = sp->y + (size_t)src_row[k] * out;
+  double* xd = xin + (size_t)row0[k] * in;
+  double* yd = yin + (size_t)row0[k] * out;
+  const size_t stride = (size_t)gridDim.y * blockDim.x;
+  const size_t t0 = (size_t)blockIdx.y * blockDim.x + threadIdx.x;
+  // 16-byte moves when both ends are 16-byte aligned (even row offsets)
+  if ((((uintptr_t)xs | (uintptr_t)xd) & 15) == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(xs);
+    double2* d2 = reinterpret_cast<double2*>(xd);
+    for (size_t t = t0; t < nx / 2; t += stride) d2[t] = __ldg(s2 + t);
+    if ((nx & 1) && t0 == 0) xd[nx - 1] = xs[nx - 1];
+  } else {
+    for (size_t t = t0; t < nx; t += stride) xd[t] = __ldg(xs + t);
+  }
+  for (size_t t = t0; t < ny; t += stride) yd[t] = __ldg(ys + t);
 }
 
 // ------------------------------------------------------------ input stats

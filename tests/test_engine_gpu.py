@@ -279,3 +279,30 @@ def test_collective_paths_bit_identical(port, monkeypatch, overlap):
         got = trajectory(rr)
         assert got[1] == want[1]
         assert np.array_equal(got[0], want[0])
+
+
+@pytest.mark.parametrize("widths", [[784, 16, 10], [128, 256, 256, 10]])
+def test_resident_batches_match_host_batches(port, widths):
+    """Device-resident batches are staged inside the captured step graph
+    (k_stage_rows, pointers via the step parameters), host batches by copies:
+    rotating resident batches through one graph give the host-path bits."""
+    import torch
+    B = 128
+    sizes, dev = vnt().uniform_mapping(B, 8, 1)
+    batches = [port.synth_batch(6, 4096, widths[0], widths[-1], s * B, B) for s in range(3)]
+    res = []
+    for resident in (False, True):
+        e = make_engine(widths, "relu", "softmax-cross-entropy", 9, port, gemm_mode="auto")
+        dx = [torch.from_numpy(x).cuda() for x, _ in batches]
+        dy = [torch.from_numpy(y).cuda() for _, y in batches]
+        losses = []
+        for s in range(7):   # graph captured on the 2nd step, replayed with new pointers
+            x, y = batches[s % 3]
+            if resident:
+                losses.append(e.train_step_ptr(dx[s % 3].data_ptr(), dy[s % 3].data_ptr(), B,
+                                               sizes, dev, 0.02, resident=True))
+            else:
+                losses.append(e.train_step(x, y, sizes, dev, 0.02)[0])
+        res.append((e.get_params(), losses))
+    assert res[0][1] == res[1][1]
+    assert np.array_equal(res[0][0], res[1][0])
