@@ -244,17 +244,19 @@ class Engine:
 
     def train_step_ptr(self, x_ptr: int, y_ptr: int, rows: int, node_sizes, node_device, lr,
                        resident: bool):
-        """x_ptr / y_ptr: fp64 host (pinned) or device pointers."""
-        ns, nd, pm = self._mapping_args(node_sizes, node_device)
+        """x_ptr / y_ptr: fp64 host (pinned) or device pointers.  Returns the loss only
+        (no per-device metrics are gathered on this hot path)."""
+        ns = np.ascontiguousarray(node_sizes, np.uint64)
+        nd = np.ascontiguousarray(node_device, np.int32)
         loss = C.c_double()
         fn = self.lib.vnt_engine_train_step_resident if resident else self.lib.vnt_engine_train_step
         if resident:
             rc = fn(self.h, _vp(x_ptr), _vp(y_ptr), rows, ns.ctypes.data_as(_u64p),
-                    nd.ctypes.data_as(_i32p), ns.size, lr, C.byref(loss), pm)
+                    nd.ctypes.data_as(_i32p), ns.size, lr, C.byref(loss), None)
         else:
             rc = fn(self.h, C.cast(_vp(x_ptr), _f64p), C.cast(_vp(y_ptr), _f64p), rows,
                     ns.ctypes.data_as(_u64p), nd.ctypes.data_as(_i32p), ns.size, lr,
-                    C.byref(loss), pm)
+                    C.byref(loss), None)
         _check(rc)
         return loss.value
 
