@@ -644,6 +644,23 @@ void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStr
 void backup_stats(vnt_engine* e, cudaStream_t s);
 void layer_collective(vnt_engine* e, int l);
 
+// Whole-node path, single pass: step parameters, zeroed G/tail/max|g| and the
+// resident batch in one launch (what copy_step_params + begin_round_device +
+// launch_stage_rows do in three or more).
+void step_prologue(vnt_engine* e, const Pass& p, bool stage) {
+  const size_t nn = p.nodes.size();
+  const int* row0 = p.d_meta + p.rows;
+  uint64_t maxrows = 1;
+  for (const auto& pn : p.nodes) maxrows = std::max<uint64_t>(maxrows, pn.rows);
+  const unsigned slices = stage ? (unsigned)std::min<uint64_t>(
+      64, ceil_div(maxrows * (e->widths[0] + e->widths[e->L]) * sizeof(double), 16384)) : 4;
+  k_step_prologue<<<dim3(stage ? (unsigned)nn : 16u, slices), 256, 0, e->stream>>>(
+      e->m_sp, e->d_sp, e->G, e->P + e->ntail + ntensors(e), stage ? 1 : 0, e->xin, e->yin, row0,
+      row0 + nn, row0 + 3 * nn, (int)e->widths[0], (int)e->widths[e->L]);
+  VNT_LAUNCH_CHECK();
+  e->launches++;
+}
+
 void launch_stage_rows(vnt_engine* e, const Pass& p) {
   const size_t nn = p.nodes.size();
   const int* row0 = p.d_meta + p.rows;
@@ -1224,10 +1241,14 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
     const Pass* graph_stage = nullptr;   // resident batch staged inside the graph
     auto enqueue_step = [&](const std::vector<StatsLaunch>* stats, bool events) {
       if (events) VNT_CUDA(cudaEventRecord(e->ev[0], e->stream));
-      copy_step_params(e);
-      if (graph_stage) launch_stage_rows(e, *graph_stage);
-      begin_round_device(e);
       auto& passes = plan_for(e, local);
+      if (e->node_path && passes.size() == 1) {
+        step_prologue(e, passes[0], graph_stage != nullptr);   // params + zeroing + staging
+      } else {
+        copy_step_params(e);
+        if (graph_stage) launch_stage_rows(e, *graph_stage);
+        begin_round_device(e);
+      }
       if (passes.size() == 1) {
         run_pass(e, passes[0], stats, true);
         e->acc_started = true;

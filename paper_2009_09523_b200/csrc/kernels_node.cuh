@@ -149,21 +149,6 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
     for (int l = 0; l < L; ++l) wso[l] = off + node_wpad_offset(a.w, l);
   }
   __syncthreads();
-  // the padded weight image (written by the SGD) into shared memory, flat float4
-  {
-    const float4* src = reinterpret_cast<const float4*>(a.wpad);
-    float4* dst = reinterpret_cast<float4*>(sm + wso[0]);
-    const int n4 = a.wpad_floats / 4;
-    for (int t0 = tid; t0 < n4; t0 += 4 * nt) {
-      float4 v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (t0 + q * nt < n4) v[q] = __ldg(src + t0 + q * nt);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (t0 + q * nt < n4) dst[t0 + q * nt] = v[q];
-    }
-  }
   if (node == 0 && tid == 0)
     atomicAdd(reinterpret_cast<unsigned long long*>(&a.tail[kTailExamples]),
               (unsigned long long)a.examples);
@@ -188,22 +173,34 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
   for (int c0 = 0; c0 < n; c0 += a.rc) {
     const int rn = min(a.rc, n - c0);
     __syncthreads();
-    {   // fp64 rows -> fp32 activations of layer 0
+    {   // fp64 rows -> fp32 activations of layer 0; on the first chunk also the
+        // padded weight image (written by the SGD).  Loads of both are issued
+        // together, 8 x values and 4 weight float4s per thread in flight.
       float* A0 = sm + aoff[0];
       const double* xs = a.x + (size_t)(r0 + c0) * in;
       const int total = rn * in;
-      for (int t0 = tid; t0 < total; t0 += 8 * nt) {   // 8 loads in flight per thread
+      const float4* wsrc = reinterpret_cast<const float4*>(a.wpad);
+      float4* wdst = reinterpret_cast<float4*>(sm + wso[0]);
+      const int n4 = c0 == 0 ? a.wpad_floats / 4 : 0;
+      for (int t0 = tid, u0 = tid; t0 < total || u0 < n4; t0 += 8 * nt, u0 += 4 * nt) {
         double v[8];
+        float4 wv[4];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int t = t0 + q * nt;
           v[q] = t < total ? __ldg(xs + t) : 0.0;
         }
 #pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (u0 + q * nt < n4) wv[q] = __ldg(wsrc + u0 + q * nt);
+#pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int t = t0 + q * nt;
           if (t < total) A0[t] = __double2float_rn(v[q]);
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (u0 + q * nt < n4) wdst[u0 + q * nt] = wv[q];
       }
     }
     __syncthreads();

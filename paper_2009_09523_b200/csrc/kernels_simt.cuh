@@ -122,6 +122,39 @@ __global__ void k_stage_rows(const StepParams* __restrict__ sp, double* __restri
   for (size_t t = t0; t < ny; t += stride) yd[t] = __ldg(ys + t);
 }
 
+// One launch for the head of a small-model step (whole-node path): block
+// (0,0) copies the step parameters from mapped pinned memory, every block
+// zeroes a share of G + tail + max|g| words, and (stage != 0) the device-
+// resident batch is staged as in k_stage_rows, with its pointers read straight
+// from the mapped parameters.
+__global__ void k_step_prologue(const StepParams* __restrict__ host_sp, StepParams* __restrict__ sp,
+                                long long* __restrict__ G, size_t nzero, int stage,
+                                double* __restrict__ xin, double* __restrict__ yin,
+                                const int* __restrict__ row0, const int* __restrict__ nrows,
+                                const int* __restrict__ src_row, int in, int out) {
+  const int bid = blockIdx.x + blockIdx.y * gridDim.x, nb = gridDim.x * gridDim.y;
+  if (bid == 0) {
+    const unsigned long long* s = reinterpret_cast<const unsigned long long*>(host_sp);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(sp);
+    for (int i = threadIdx.x; i < (int)(sizeof(StepParams) / 8); i += blockDim.x) d[i] = s[i];
+  }
+  for (size_t i = (size_t)bid * blockDim.x + threadIdx.x; i < nzero; i += (size_t)nb * blockDim.x)
+    G[i] = 0;
+  if (!stage) return;
+  const int k = blockIdx.x;
+  const double* xsrc = host_sp->x;
+  const double* ysrc = host_sp->y;
+  const size_t nx = (size_t)nrows[k] * in, ny = (size_t)nrows[k] * out;
+  const double* xs = xsrc + (size_t)src_row[k] * in;
+  const double* ys = ysrc + (size_t)src_row[k] * out;
+  double* xd = xin + (size_t)row0[k] * in;
+  double* yd = yin + (size_t)row0[k] * out;
+  const size_t stride = (size_t)gridDim.y * blockDim.x;
+  const size_t t0 = (size_t)blockIdx.y * blockDim.x + threadIdx.x;
+  for (size_t t = t0; t < nx; t += stride) xd[t] = __ldg(xs + t);
+  for (size_t t = t0; t < ny; t += stride) yd[t] = __ldg(ys + t);
+}
+
 // ------------------------------------------------------------ input stats
 // LayerStats::observe batch part (model.cpp:101-121): per node, per feature,
 // sequential fp64 sums in row order; __d*_rn forbid FMA contraction so the
