@@ -122,7 +122,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 16);   // 8 epilogue warps x 2 CTAs (leader copy used)
+      // dW: one arrival per CTA after its 8 epilogue warps meet on a named
+      // barrier (per virtual node); fwd/bwd: every epilogue warp of both CTAs
+      mbar_init(&tempty[b], EPI == kTcDw ? 2 : 16);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -299,8 +301,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(&tempty[b]);
+      if (EPI == kTcDw) {
+        asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 epilogue warps of this CTA
+        if (warp == 4 && lane == 0) mbar_arrive_leader(&tempty[b]);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty[b]);
+      }
       }
       if (EPI == kTcDw && r < ep.M) {
         long long* g = ep.G + (size_t)r * ep.ldg + n0 + h * COLS;
