@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
     }
     __syncthreads();
     if (row0 < rows) {
-#pragma unroll 2
+#pragma unroll 4
       for (int kk = lane; kk < kn; kk += 32) {
         float a[R];
 #pragma unroll
@@ -680,12 +680,12 @@ __global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __
     if (i < in) {
       const float* xp = X + (size_t)(r0 + c) * in + i;
       int rr = 0;
-      for (; rr + 4 <= cn; rr += 4) {   // loads in flight, FMAs in row order
-        float a[4];
+      for (; rr + 8 <= cn; rr += 8) {   // 8 loads in flight, FMAs in row order
+        float a[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) a[j] = __ldg(xp + (size_t)(rr + j) * in);
+        for (int j = 0; j < 8; ++j) a[j] = __ldg(xp + (size_t)(rr + j) * in);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 8; ++j)
 #pragma unroll
           for (int o = 0; o < NO; ++o) g[o] = fmaf(a[j], dn[rr + j][o], g[o]);
       }
