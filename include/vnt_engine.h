@@ -1,5 +1,5 @@
 /* vnt_engine.h — the thin C-ABI between the reference-compatible C++ host
- * layer (include/vnt/*.hpp, the `vnt::` drop-in) and the B200 CUDA engine
+ * layer (include/vnt/ headers, the `vnt::` drop-in) and the B200 CUDA engine
  * (paper_2009_09523_b200/csrc/).  Plain pointers and sizes only; all CUDA /
  * NCCL state lives behind the opaque `vnt_engine`.  There is no CPU fallback:
  * every compute entry point fails with VNT_ERR_CUDA when no sm_100 device is
