@@ -222,6 +222,15 @@ class Engine:
                                         C.byref(ex)))
         return g, ls.value, ex.value
 
+    def take_gradient_sum(self):
+        """Process-local exact gradient sum (no collective), closes the round:
+        (sum[P] = double(S) * 2^-s per tensor, loss_sum, examples)."""
+        g = np.empty(self.P, np.float64)
+        ls = C.c_double()
+        ex = C.c_uint64()
+        _check(self.lib.vnt_engine_take_gradient_sum(self.h, _fp(g), C.byref(ls), C.byref(ex)))
+        return g, ls.value, ex.value
+
     def sgd_apply(self, lr):
         _check(self.lib.vnt_engine_sgd_apply(self.h, lr))
 

@@ -935,6 +935,19 @@ void backup_stats(vnt_engine* e, cudaStream_t s) {
   e->stats_backed = true;
 }
 
+// Sum of a host count over the process group (blocking; first round only).
+uint64_t global_count(vnt_engine* e, uint64_t local) {
+  long long* d = (long long*)dalloc(sizeof(long long));
+  long long v = (long long)local;
+  VNT_CUDA(cudaMemcpyAsync(d, &v, sizeof v, cudaMemcpyHostToDevice, e->stream));
+  const ncclResult_t r = ncclAllReduce(d, d, 1, ncclInt64, ncclSum, e->comm, e->stream);
+  if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+  VNT_CUDA(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, e->stream));
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  cudaFree(d);
+  return (uint64_t)v;
+}
+
 void begin_round(vnt_engine* e, uint64_t batch_hint) {
   if (e->round_open) return;
   begin_round_host(e, batch_hint);
@@ -1721,7 +1734,12 @@ int vnt_engine_device_step(vnt_engine* e, int32_t device, const double* x, const
     m.buffer_bytes = e->P * sizeof(double);
     if (e->synced) reset_acc(e);
     if (!e->round_open) e->launches = 0;
-    begin_round(e, off * std::max<uint64_t>(1, e->devs.size()) * (uint64_t)e->opt.world_size);
+    // The first fixed-point scale comes from a batch estimate that every rank
+    // must share (partials in different units cannot be summed): across
+    // processes it is the sum of the local estimates.
+    uint64_t hint = off * std::max<uint64_t>(1, e->devs.size());
+    if (!e->round_open && !e->scales_init && e->comm) hint = global_count(e, hint);
+    begin_round(e, hint);
     accumulate(e, local, x, y, false, true);
     if (metrics) *metrics = m;
     return VNT_OK;
@@ -1926,6 +1944,7 @@ int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n) {
   return guarded([&] {
     if (n != ntensors(e)) throw EngineError(VNT_ERR_SHAPE, "scale count mismatch");
     e->scales.assign(scales, scales + n);
+    e->scales_init = true;   // explicit scales are not replaced by the first-round estimate
     return VNT_OK;
   });
 }

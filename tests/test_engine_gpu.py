@@ -306,3 +306,35 @@ def test_resident_batches_match_host_batches(port, widths):
         res.append((e.get_params(), losses))
     assert res[0][1] == res[1][1]
     assert np.array_equal(res[0][0], res[1][0])
+
+
+@pytest.mark.parametrize("widths", [[64, 96, 48, 10], [128, 256, 256, 10]])
+def test_rank_partition_sums_add_up_exactly(port, widths):
+    """The N > 1 contract on one GPU: processes holding disjoint node sets
+    (round-robin, as make_uniform_mapping deals them to ranks) produce exact
+    local sums that add up to the single-process sum bit for bit — what the
+    int64 NCCL all-reduce then does across GPUs (both model paths)."""
+    V, m = 8, 16
+    B = V * m
+    x, y = port.synth_batch(8, 4096, widths[0], widths[-1], 0, B)
+    p0 = port.init_params(widths, 3)
+    nt = 2 * (len(widths) - 1)
+
+    def local_sum(nodes):
+        e = vnt().Engine(widths, "relu", "softmax-cross-entropy", gemm_mode="auto")
+        e.add_device(1 << 20)
+        e.set_params(p0)
+        e.set_scales(np.full(nt, 30, np.int32))   # every process quantises at the same scale
+        rows = np.concatenate([np.arange(n * m, (n + 1) * m) for n in nodes])
+        e.device_step(0, x[rows], y[rows], [m] * len(nodes))
+        g, loss, ex = e.take_gradient_sum()
+        e.close()
+        return g, loss, ex
+
+    g_all, l_all, ex_all = local_sum(list(range(V)))
+    for world in (2, 4):
+        parts = [local_sum([n for n in range(V) if n % world == r]) for r in range(world)]
+        g = np.sum([p[0] for p in parts], axis=0)
+        assert np.array_equal(g, g_all)
+        assert sum(p[2] for p in parts) == ex_all == B
+        assert abs(sum(p[1] for p in parts) - l_all) <= 1e-9 * abs(l_all)
