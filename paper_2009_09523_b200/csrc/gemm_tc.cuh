@@ -353,20 +353,22 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + j < ep.N) {
                 const size_t o = (size_t)(nb + j) * ep.ldT + tc;
                 const float t = v[j] * tscale;
-                ep.outT[o] = t;
+                if (ep.outT) ep.outT[o] = t;
                 if (ep.outTh) {
                   const float th = tf32_rna(t);
                   ep.outTh[o] = th;
                   ep.outTl[o] = t - th;
                 }
               }
-            float* orow = ep.out + (size_t)r * ep.ldo + nb;
-            if (nb + 32 <= ep.N) {
+            if (ep.out) {   // null: only the 3xTF32 twins are consumed
+              float* orow = ep.out + (size_t)r * ep.ldo + nb;
+              if (nb + 32 <= ep.N) {
 #pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
-              for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+                for (int j = 0; j < 32; j += 4)
+                  *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              } else {
+                for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+              }
             }
             if (ep.outh) {
               const size_t o = (size_t)r * ep.ldo + nb;
@@ -564,9 +566,13 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   ep.N = N;
   ep.bias = e->w32 + e->boff[l];
   ep.act = e->act;
-  ep.out = e->X[l + 1];
+  // Plain X / Xᵀ only when a consumer reads them: a 3xTF32 layer l+1 reads the
+  // twins, and its bwd-data takes relu' from the hi twin (sign of hi == sign of
+  // x); tanh' needs the full value, so tanh keeps the plain X.
+  const bool twins = e->Xh[l + 1] != nullptr;
+  ep.out = twins && e->act != VNT_ACT_TANH ? nullptr : e->X[l + 1];
   ep.ldo = N;
-  ep.outT = e->XT[l + 1];
+  ep.outT = twins ? nullptr : e->XT[l + 1];
   ep.ldT = ldT;
   ep.tcol = tcol;
   ep.tscale_p = nullptr;
@@ -591,12 +597,13 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol,
   ep.M = rows;
   ep.N = N;
   ep.act = e->act;
-  ep.out = e->D[l];
+  ep.out = e->D[l];          // k_db reads the plain delta
   ep.ldo = N;
-  ep.outT = e->DT[l];
+  ep.outT = e->DTh[l] ? nullptr : e->DT[l];   // a 3xTF32 dW reads only the twins
   ep.ldT = ldT;
   ep.tcol = tcol;
-  ep.Xprev = e->X[l];
+  // relu' / identity' from the hi twin when the plain X was not written (above)
+  ep.Xprev = (e->Xh[l] && e->act != VNT_ACT_TANH) ? e->Xh[l] : e->X[l];
   ep.ldx = N;
   ep.tscale_p = tscale;
   ep.outh = e->Dh[l];

@@ -271,20 +271,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (nb + j < ep.N) {
               const size_t o = (size_t)(nb + j) * ep.ldT + tc;
               const float t = v[j] * tscale;
-              ep.outT[o] = t;
+              if (ep.outT) ep.outT[o] = t;
               if (ep.outTh) {
                 const float th = tf32_rna(t);
                 ep.outTh[o] = th;
                 ep.outTl[o] = t - th;
               }
             }
-          float* orow = ep.out + (size_t)r * ep.ldo + nb;
-          if (nb + 32 <= ep.N) {
+          if (ep.out) {   // null: only the 3xTF32 twins are consumed
+            float* orow = ep.out + (size_t)r * ep.ldo + nb;
+            if (nb + 32 <= ep.N) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
-            for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+              for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+            }
           }
           if (ep.outh) {
             const size_t o = (size_t)r * ep.ldo + nb;
