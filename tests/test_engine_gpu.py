@@ -338,3 +338,19 @@ def test_rank_partition_sums_add_up_exactly(port, widths):
         assert np.array_equal(g, g_all)
         assert sum(p[2] for p in parts) == ex_all == B
         assert abs(sum(p[1] for p in parts) - l_all) <= 1e-9 * abs(l_all)
+
+
+@pytest.mark.parametrize("widths,mode", [([4, 16, 4], "auto"), ([64, 96, 48, 10], "ffma"),
+                                         ([128, 256, 256, 10], "auto")])
+def test_zero_params_loss_is_mean_square_label(port, widths, mode):
+    """test_model.cpp:76-91 on the engine: with all parameters zero the network
+    outputs zero, so the MSE loss is mean(y^2) over the output width (every path:
+    whole-node kernel, layered FFMA, tcgen05)."""
+    e = vnt().Engine(widths, "tanh", "mse", gemm_mode=mode)
+    e.add_device(1 << 20)
+    e.set_params(np.zeros(vnt().param_count(widths)))
+    x, y = port.synth_batch(2, 512, widths[0], widths[-1], 0, 64)
+    sizes, dev = vnt().uniform_mapping(64, 8, 1)
+    loss, _ = e.train_step(x, y, sizes, dev, 0.01)
+    want = float(np.mean(np.sum(y * y, axis=1) / widths[-1]))
+    assert abs(loss - want) <= 1e-9 * want
