@@ -701,18 +701,31 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   a.loss = e->loss;
   uint64_t maxrows = 1;
   for (const auto& pn : p.nodes) maxrows = std::max<uint64_t>(maxrows, pn.rows);
-  a.rc = (int)std::min<uint64_t>(maxrows, (uint64_t)e->node_rc_max);
+  // VNT_NODE_CLUSTER (default 4): CTAs per node (rows split, strips summed over DSMEM)
+  static const int cl_env = getenv("VNT_NODE_CLUSTER") ? atoi(getenv("VNT_NODE_CLUSTER")) : 4;
+  int CL = (cl_env == 2 || cl_env == 4 || cl_env == 8) ? cl_env : 1;
+  a.rc = (int)std::min<uint64_t>(ceil_div(maxrows, (uint64_t)CL), (uint64_t)e->node_rc_max);
   a.sp = e->d_sp;
   a.lim = pow2f(kLimBits);
   a.G = e->G;
   a.tail = e->G + e->P;
   a.examples = (long long)p.rows;
-  const size_t smem = ((size_t)a.rc * node_row_floats(e) + node_wt_floats(e) + 8) * sizeof(float);
-  static size_t smem_attr = 0;
-  if (smem > smem_attr) {
-    VNT_CUDA(cudaFuncSetAttribute(k_node_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t base = ((size_t)a.rc * node_row_floats(e) + node_wt_floats(e) + 8 + 3) & ~(size_t)3;
+  a.part_off = (int)base;
+  size_t smem = (base + (CL > 1 ? (size_t)a.nstrips * kNodeOC : 0)) * sizeof(float);
+  if (smem > 227 * 1024) {   // no room for the exchange area: one CTA per node
+    CL = 1;
+    smem = base * sizeof(float);
+  }
+  static size_t smem_attr[9] = {};
+  if (smem > smem_attr[CL]) {
+    const void* fn = CL == 8   ? (const void*)k_node_step<8>
+                     : CL == 4 ? (const void*)k_node_step<4>
+                     : CL == 2 ? (const void*)k_node_step<2>
+                               : (const void*)k_node_step<1>;
+    VNT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)std::max<size_t>(smem, 48 * 1024)));
-    smem_attr = std::max<size_t>(smem, 48 * 1024);
+    smem_attr[CL] = std::max<size_t>(smem, 48 * 1024);
   }
   // Input statistics depend on x only: a side-stream branch beside the node kernel.
   if (stats) {
@@ -727,7 +740,25 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
     combine_stats(e, *stats, e->aux_stream);
     VNT_CUDA(cudaEventRecord(e->join_ev, e->aux_stream));
   }
-  k_node_step<<<(unsigned)nn, kNodeThreads, smem, e->stream>>>(a);
+  if (CL == 1) {
+    k_node_step<1><<<(unsigned)nn, kNodeThreads, smem, e->stream>>>(a);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nn * CL));
+    cfg.blockDim = dim3(kNodeThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = e->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (CL == 8) VNT_CUDA(cudaLaunchKernelEx(&cfg, k_node_step<8>, a));
+    else if (CL == 4) VNT_CUDA(cudaLaunchKernelEx(&cfg, k_node_step<4>, a));
+    else VNT_CUDA(cudaLaunchKernelEx(&cfg, k_node_step<2>, a));
+  }
   VNT_LAUNCH_CHECK();
   e->launches++;
   e->tail_examples += p.rows;

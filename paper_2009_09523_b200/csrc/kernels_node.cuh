@@ -17,6 +17,8 @@
 // alone (never from rows or mapping), so every run of a model uses it.
 #pragma once
 
+#include <cooperative_groups.h>
+
 namespace vntb {
 
 constexpr int kNodeMaxLayers = 8;
@@ -44,6 +46,7 @@ struct NodeArgs {
   long long* G;          // exact gradient sum (zeroed) + tail
   long long* tail;
   long long examples;    // the pass's rows, added to the tail by CTA 0
+  int part_off;          // CL > 1: smem float offset of the partial-strip exchange area
 };
 
 // Shared-memory row strides: deltas padded to kNodeOC (aligned float4 strips),
@@ -125,11 +128,20 @@ __device__ __forceinline__ void node_strip(const NodeArgs& a, int s, int& l, int
   i = s - (s / rowsl) * rowsl;
 }
 
+// CL > 1: a cluster of CL CTAs per node; CTA k runs rows [k n / CL, (k+1) n / CL)
+// of the node (a split fixed by the node's row count), and the CTAs' dW/db
+// strips are added in rank order over distributed shared memory before the
+// quantisation — a fixed summation tree per node, so still a function of the
+// node's rows only.
+template <int CL>
 __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
   extern __shared__ float sm[];
   __shared__ int aoff[kNodeMaxLayers + 1], doff[kNodeMaxLayers + 1], wso[kNodeMaxLayers];
-  const int node = blockIdx.x;
-  const int r0 = a.row0[node], n = a.nrows[node];
+  const int node = blockIdx.x / CL;
+  const int crank = (int)(blockIdx.x % CL);   // == %cluster_ctarank for 1-D clusters of CL
+  const int node_rows = a.nrows[node];
+  const int lo = crank * node_rows / CL, hi = (crank + 1) * node_rows / CL;
+  const int r0 = a.row0[node] + lo, n = hi - lo;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int L = a.L, in = a.w[0], outw = a.w[L];
@@ -149,7 +161,7 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
     for (int l = 0; l < L; ++l) wso[l] = off + node_wpad_offset(a.w, l);
   }
   __syncthreads();
-  if (node == 0 && tid == 0)
+  if (blockIdx.x == 0 && tid == 0)
     atomicAdd(reinterpret_cast<unsigned long long*>(&a.tail[kTailExamples]),
               (unsigned long long)a.examples);
   // per-strip quantisation scales, loaded before they are needed
@@ -158,7 +170,7 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
   for (int q = 0; q < kNodeStrips; ++q) {
     const int st = tid + q * nt;
     qscale[q] = 0.f;
-    if (st < a.nstrips) {
+    if (CL == 1 && st < a.nstrips) {
       int l, i, o0;
       node_strip(a, st, l, i, o0);
       qscale[q] = a.sp->scale[2 * l + (i == a.w[l] ? 1 : 0)];
@@ -313,26 +325,62 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
       }
     }
   }
-  // per-node quantisation into the exact sum (order-free int64 atomics)
+  if constexpr (CL == 1) {
+    // per-node quantisation into the exact sum (order-free int64 atomics)
 #pragma unroll
-  for (int q = 0; q < kNodeStrips; ++q) {
-    const int st = tid + q * nt;
-    if (st < a.nstrips) {
-      int l, i, o0;
-      node_strip(a, st, l, i, o0);
-      const int K = a.w[l], N = a.w[l + 1];
-      const bool bias = i == K;
-      const int t = 2 * l + (bias ? 1 : 0);
-      const float scale = qscale[q];
-      long long* gp = a.G + (bias ? a.boff[l] : a.woff[l] + i * N) + o0;
+    for (int q = 0; q < kNodeStrips; ++q) {
+      const int st = tid + q * nt;
+      if (st < a.nstrips) {
+        int l, i, o0;
+        node_strip(a, st, l, i, o0);
+        const int K = a.w[l], N = a.w[l + 1];
+        const bool bias = i == K;
+        const int t = 2 * l + (bias ? 1 : 0);
+        const float scale = qscale[q];
+        long long* gp = a.G + (bias ? a.boff[l] : a.woff[l] + i * N) + o0;
 #pragma unroll
-      for (int j = 0; j < kNodeOC; ++j) {
-        if (o0 + j < N) {
-          const long long qv = quantise(g[q][j], scale, a.lim, a.tail, t);
-          if (qv) atomicAdd(reinterpret_cast<unsigned long long*>(gp + j), (unsigned long long)qv);
+        for (int j = 0; j < kNodeOC; ++j) {
+          if (o0 + j < N) {
+            const long long qv = quantise(g[q][j], scale, a.lim, a.tail, t);
+            if (qv) atomicAdd(reinterpret_cast<unsigned long long*>(gp + j), (unsigned long long)qv);
+          }
         }
       }
     }
+  } else {
+    // rank-order sum of the CTAs' partial strips over DSMEM, then quantise;
+    // each CTA finishes a contiguous 1/CL of the strips
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    float* part = sm + a.part_off;
+#pragma unroll
+    for (int q = 0; q < kNodeStrips; ++q) {
+      const int st = tid + q * nt;
+      if (st < a.nstrips)
+#pragma unroll
+        for (int j = 0; j < kNodeOC; ++j) part[st * kNodeOC + j] = g[q][j];
+    }
+    cluster.sync();
+    const float* parts[CL];
+#pragma unroll
+    for (int k = 0; k < CL; ++k) parts[k] = cluster.map_shared_rank(part, k);
+    const int s0 = crank * a.nstrips / CL, s1 = (crank + 1) * a.nstrips / CL;
+    for (int e = tid; e < (s1 - s0) * kNodeOC; e += nt) {
+      const int st = s0 + e / kNodeOC, j = e % kNodeOC;
+      int l, i, o0;
+      node_strip(a, st, l, i, o0);
+      const int K = a.w[l], N = a.w[l + 1];
+      if (o0 + j >= N) continue;
+      float v = parts[0][st * kNodeOC + j];
+#pragma unroll
+      for (int k = 1; k < CL; ++k) v += parts[k][st * kNodeOC + j];
+      const bool bias = i == K;
+      const int t = 2 * l + (bias ? 1 : 0);
+      const long long qv = quantise(v, a.sp->scale[t], a.lim, a.tail, t);
+      long long* gp = a.G + (bias ? a.boff[l] : a.woff[l] + i * N) + o0 + j;
+      if (qv) atomicAdd(reinterpret_cast<unsigned long long*>(gp), (unsigned long long)qv);
+    }
+    cluster.sync();   // no CTA leaves while its partials may still be read
   }
 }
 
