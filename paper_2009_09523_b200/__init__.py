@@ -273,7 +273,8 @@ class Engine:
                      resident: bool):
         """Stage a future step's rows on the copy stream (vnt_engine_prefetch):
         call prefetch(i) once, then before each step(i) queue prefetch(i+1)."""
-        ns, nd, _ = self._mapping_args(node_sizes, node_device)
+        ns = np.ascontiguousarray(node_sizes, np.uint64)
+        nd = np.ascontiguousarray(node_device, np.int32)
         _check(self.lib.vnt_engine_prefetch(self.h, _vp(x_ptr), _vp(y_ptr), rows,
                                             ns.ctypes.data_as(_u64p), nd.ctypes.data_as(_i32p),
                                             ns.size, 1 if resident else 0))
