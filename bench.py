@@ -255,11 +255,12 @@ def run_ours(args, work):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
 
-    # GEMM-bound workloads time every GEMM launch with CUDA events inside the
-    # timed region (eager launches).  The latency-bound cfg1 runs the timed
-    # region as CUDA-graph replays (events inside graphs cannot be timed) and
-    # takes its GEMM timings from a short eager profiled run afterwards.
-    graph_mode = work["widths"][1] <= 256
+    # The timed region runs every step as one CUDA-graph replay (host prep, one
+    # graph launch, one synchronize); the GEMM roofline numbers come from a short
+    # eager run afterwards with CUDA events around each GEMM launch (events inside
+    # graphs cannot be timed).  --eager times the eager, profiled launches instead.
+    # (with an NCCL group the engine launches eagerly anyway: profile in place)
+    graph_mode = not args.eager and world == 1
     os.environ["VNT_PROFILE_KERNELS"] = "0" if graph_mode else "1"
     w, B, V, lr = work["widths"], work["B"], work["V"], work["lr"]
     eng = vnt.Engine(w, work["act"], work["loss"], cuda_device=local, rank=rank,
@@ -515,6 +516,8 @@ def main():
     ap.add_argument("--gemm-mode", default="auto", choices=["auto", "ffma", "tf32", "3xtf32"])
     ap.add_argument("--resident-rows", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="time eager launches with CUDA events around every GEMM (no graphs)")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="e2e: stage each batch inside its own step instead of prefetching")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary 1-pass TF32 timing")
