@@ -188,3 +188,29 @@ print(json.dumps({"err": err, "bitwise": bool(np.array_equal(out[0], out[1]))}))
     res = json.loads(r.stdout.strip().splitlines()[-1])
     print(res)
     assert res["err"] < 2e-5 and res["bitwise"]
+
+
+def test_rescale_retry_on_tcgen05_graph_path(port):
+    """A fixed-point overflow inside a graph-replayed tcgen05 step: the engine
+    lowers the scale, redoes the step eagerly (input statistics observed once,
+    SGD skipped on the device for the flagged attempt) and lands within fp32
+    grade of the undisturbed run."""
+    w = [128, 256, 256, 10]
+    sizes, dev = vnt().uniform_mapping(256, 8, 1)
+    batches = [port.synth_batch(4, 2048, w[0], w[-1], s * 256, 256) for s in range(4)]
+    runs = []
+    for force in (False, True):
+        e = engine(w, "relu", "softmax-cross-entropy", port, seed=4, gemm_mode="auto")
+        losses = []
+        for s, (x, y) in enumerate(batches):
+            if force and s == 2:               # graphs are live by now (steps 0, 1)
+                e.set_scales(np.full(e.ntensors, 90, np.int32))
+            losses.append(e.train_step(x, y, sizes, dev, 0.02)[0])
+            if force and s == 2:
+                assert e.timings()["rescale_retries"] >= 1
+        cnt, _, _ = e.input_stats(0)
+        assert cnt == 4 * 256
+        runs.append((e.get_params(), np.array(losses)))
+    assert np.array_equal(runs[0][1][:2], runs[1][1][:2])
+    assert np.abs(runs[0][1] - runs[1][1]).max() <= 2e-5 * np.abs(runs[0][1]).max()
+    assert np.abs(runs[0][0] - runs[1][0]).max() <= 2e-5
