@@ -644,6 +644,35 @@ void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStr
 void backup_stats(vnt_engine* e, cudaStream_t s);
 void layer_collective(vnt_engine* e, int l);
 
+// Input statistics of a pass depend on x only: observe_batch per node then the
+// Chan combine into each device lineage in ascending node id
+// (virtual_exec.cpp:137-138, model.cpp:152-154) run on the side stream, forked
+// here; the caller joins (cudaStreamWaitEvent on join_ev) before xin changes or
+// the step ends.
+void fork_stats(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>& stats,
+                bool side = true) {
+  const size_t nn = p.nodes.size();
+  const int* row0 = p.d_meta + p.rows;
+  cudaStream_t st = side ? e->aux_stream : e->stream;
+  if (side) {
+    VNT_CUDA(cudaEventRecord(e->fork_ev, e->stream));
+    VNT_CUDA(cudaStreamWaitEvent(e->aux_stream, e->fork_ev, 0));
+  }
+  if (!e->stats_backed) backup_stats(e, st);
+  dim3 grid((unsigned)ceil_div(e->widths[0], 128), (unsigned)nn);
+  k_vn_stats<<<grid, 128, 0, st>>>(e->xin, (int)e->widths[0], row0, row0 + nn, e->vn_mean,
+                                   e->vn_m2);
+  VNT_LAUNCH_CHECK();
+  e->launches++;
+  combine_stats(e, stats, st);
+  VNT_CUDA(cudaEventRecord(e->join_ev, st));
+}
+
+bool stats_side_branch_layered() {
+  static const bool on = getenv("VNT_STATS_BRANCH") && getenv("VNT_STATS_BRANCH")[0] == '1';
+  return on;
+}
+
 // Whole-node path, single pass: step parameters, zeroed G/tail/max|g| and the
 // resident batch in one launch (what copy_step_params + begin_round_device +
 // launch_stage_rows do in three or more).
@@ -728,18 +757,7 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
     smem_attr[CL] = std::max<size_t>(smem, 48 * 1024);
   }
   // Input statistics depend on x only: a side-stream branch beside the node kernel.
-  if (stats) {
-    VNT_CUDA(cudaEventRecord(e->fork_ev, e->stream));
-    VNT_CUDA(cudaStreamWaitEvent(e->aux_stream, e->fork_ev, 0));
-    if (!e->stats_backed) backup_stats(e, e->aux_stream);
-    dim3 grid((unsigned)ceil_div(e->widths[0], 128), (unsigned)nn);
-    k_vn_stats<<<grid, 128, 0, e->aux_stream>>>(e->xin, (int)e->widths[0], row0, nrows, e->vn_mean,
-                                                e->vn_m2);
-    VNT_LAUNCH_CHECK();
-    e->launches++;
-    combine_stats(e, *stats, e->aux_stream);
-    VNT_CUDA(cudaEventRecord(e->join_ev, e->aux_stream));
-  }
+  if (stats) fork_stats(e, p, *stats);
   if (CL == 1) {
     k_node_step<1><<<(unsigned)nn, kNodeThreads, smem, e->stream>>>(a);
   } else {
@@ -807,15 +825,11 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     VNT_LAUNCH_CHECK();
     e->launches++;
   }
-  if (stats) {
-    // observe_batch per node then Chan-combine into the node's device lineage
-    // in ascending node id (virtual_exec.cpp:137-138, model.cpp:152-154).
-    dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
-    k_vn_stats<<<grid, 128, 0, s>>>(e->xin, (int)in, row0, nrows, e->vn_mean, e->vn_m2);
-    VNT_LAUNCH_CHECK();
-    e->launches++;
-    combine_stats(e, *stats, e->stream);
-  }
+  // observe_batch + combine: beside the persistent GEMMs they would hold SMs the
+  // GEMM's CTAs wait for, so on the layered path they run in line by default
+  // (VNT_STATS_BRANCH=1: side stream, joined at the end of the pass)
+  const bool side = stats_side_branch_layered();
+  if (stats) fork_stats(e, p, *stats, side);
   // Forward (model.cpp:275-287).
   for (int l = 0; l < L; ++l) {
     const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
@@ -923,6 +937,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       }
     }
   }
+  if (stats) VNT_CUDA(cudaStreamWaitEvent(e->stream, e->join_ev, 0));
 }
 
 void begin_round_host(vnt_engine* e, uint64_t batch_hint) {
@@ -952,7 +967,7 @@ void begin_round_device(vnt_engine* e) {
                                e->stream));
   }
   }
-  if (!e->node_path) backup_stats(e, e->stream);   // node path: on the stats branch
+  // lineage backups run on the statistics branch (fork_stats), before the combine
 }
 
 // Lineage statistics as of the round start (restored if the step is redone).
@@ -991,6 +1006,7 @@ void restore_stats(vnt_engine* e) {
   const uint64_t in = e->widths[0];
   for (auto& d : e->devs) {
     d.count = d.count_bak;
+    if (!e->stats_backed) continue;   // nothing observed this round: the lineage is untouched
     VNT_CUDA(cudaMemcpyAsync(d.mean, d.mean_bak, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
     VNT_CUDA(cudaMemcpyAsync(d.m2, d.m2_bak, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
   }
