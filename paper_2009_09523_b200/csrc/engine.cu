@@ -6,7 +6,14 @@
 // Step structure (train_step, virtual_exec.cpp:207-282):
 //   passes of resident virtual nodes -> ingest + input stats -> forward layers
 //   -> loss/delta -> backward (per-node dW/db quantised into the exact int64
-//   sum, bwd-data) -> [ncclAllReduce int64] -> fused rescale + SGD.
+//   sum, bwd-data; with an NCCL group each layer's slice is all-reduced as soon
+//   as it is final, overlapped with the rest of the backward) -> fused rescale
+//   + SGD -> control words (loss, examples, flags, max|g|) to mapped host memory.
+// Small all-FFMA models replace the layered kernels of a pass with one
+// whole-node kernel (kernels_node.cuh).  A single-pass step without an NCCL
+// group is recorded once as a CUDA graph and replayed: every per-step value
+// (scales, lr, batch pointers) reaches the kernels through the device
+// StepParams block, so the launch sequence is static.
 #include <nccl.h>
 
 #include <algorithm>
