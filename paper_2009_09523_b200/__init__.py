@@ -97,6 +97,7 @@ def load_engine() -> C.CDLL:
                                              C.POINTER(DeviceMetrics)]),
         "vnt_engine_sync": (C.c_int, [_vp, _f64p, _f64p, _u64p]),
         "vnt_engine_sgd_apply": (C.c_int, [_vp, C.c_double]),
+        "vnt_engine_take_gradient_sum": (C.c_int, [_vp, _f64p, _f64p, _u64p]),
         "vnt_engine_train_step": (C.c_int, [_vp, _f64p, _f64p, C.c_uint64, _u64p, _i32p,
                                             C.c_uint32, C.c_double, _f64p,
                                             C.POINTER(DeviceMetrics)]),
@@ -251,21 +252,31 @@ class Engine:
                                               ns.size, lr, C.byref(loss), pm))
         return loss.value, [m.as_dict() for m in pm]
 
+    def _mapping_ptrs(self, node_sizes, node_device):
+        """ctypes views of a mapping, cached for the last (node_sizes, node_device)
+        objects seen (the arrays are kept alive and re-read by C every call)."""
+        c = getattr(self, "_map_cache", None)
+        if c is not None and c[0] is node_sizes and c[1] is node_device:
+            return c[2]
+        ns = np.ascontiguousarray(node_sizes, np.uint64)
+        nd = np.ascontiguousarray(node_device, np.int32)
+        ptrs = (ns.ctypes.data_as(_u64p), nd.ctypes.data_as(_i32p), ns.size, ns, nd)
+        self._map_cache = (node_sizes, node_device, ptrs)
+        return ptrs
+
     def train_step_ptr(self, x_ptr: int, y_ptr: int, rows: int, node_sizes, node_device, lr,
                        resident: bool):
         """x_ptr / y_ptr: fp64 host (pinned) or device pointers.  Returns the loss only
         (no per-device metrics are gathered on this hot path)."""
-        ns = np.ascontiguousarray(node_sizes, np.uint64)
-        nd = np.ascontiguousarray(node_device, np.int32)
+        nsp, ndp, n = self._mapping_ptrs(node_sizes, node_device)[:3]
         loss = C.c_double()
-        fn = self.lib.vnt_engine_train_step_resident if resident else self.lib.vnt_engine_train_step
         if resident:
-            rc = fn(self.h, _vp(x_ptr), _vp(y_ptr), rows, ns.ctypes.data_as(_u64p),
-                    nd.ctypes.data_as(_i32p), ns.size, lr, C.byref(loss), None)
+            rc = self.lib.vnt_engine_train_step_resident(self.h, _vp(x_ptr), _vp(y_ptr), rows, nsp,
+                                                         ndp, n, lr, C.byref(loss), None)
         else:
-            rc = fn(self.h, C.cast(_vp(x_ptr), _f64p), C.cast(_vp(y_ptr), _f64p), rows,
-                    ns.ctypes.data_as(_u64p), nd.ctypes.data_as(_i32p), ns.size, lr,
-                    C.byref(loss), None)
+            rc = self.lib.vnt_engine_train_step(self.h, C.cast(_vp(x_ptr), _f64p),
+                                                C.cast(_vp(y_ptr), _f64p), rows, nsp, ndp, n, lr,
+                                                C.byref(loss), None)
         _check(rc)
         return loss.value
 
@@ -273,11 +284,9 @@ class Engine:
                      resident: bool):
         """Stage a future step's rows on the copy stream (vnt_engine_prefetch):
         call prefetch(i) once, then before each step(i) queue prefetch(i+1)."""
-        ns = np.ascontiguousarray(node_sizes, np.uint64)
-        nd = np.ascontiguousarray(node_device, np.int32)
-        _check(self.lib.vnt_engine_prefetch(self.h, _vp(x_ptr), _vp(y_ptr), rows,
-                                            ns.ctypes.data_as(_u64p), nd.ctypes.data_as(_i32p),
-                                            ns.size, 1 if resident else 0))
+        nsp, ndp, n = self._mapping_ptrs(node_sizes, node_device)[:3]
+        _check(self.lib.vnt_engine_prefetch(self.h, _vp(x_ptr), _vp(y_ptr), rows, nsp, ndp, n,
+                                            1 if resident else 0))
 
     # ---- kernel state / scales / timings
     def input_stats(self, device):
