@@ -188,6 +188,16 @@ struct vnt_engine {
   bool graphs = true;
   bool timings_graphed = false;   // last step replayed a graph: only total_ms is timed
   std::map<std::vector<int64_t>, GraphEntry> graph_cache;
+  // The mapping of the previous train_step and its graph entries by (cur,
+  // stage-in-graph): a step with the same mapping skips rebuilding the node
+  // list and the graph key (host time per step).  Cleared with the graphs.
+  struct {
+    std::vector<uint64_t> sizes;
+    std::vector<int32_t> devs;
+    uint64_t rows = 0;
+    bool valid = false;
+    GraphEntry* ge[2][2] = {};
+  } memo;
 
   vnt_step_timings timings{};
   cudaEvent_t ev[6] = {};
@@ -266,6 +276,9 @@ void drop_graphs(vnt_engine* e) {
   for (auto& kv : e->graph_cache)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   e->graph_cache.clear();
+  e->memo.valid = false;
+  for (auto& row : e->memo.ge)
+    for (auto& g : row) g = nullptr;
 }
 
 // Stage this step's kernel parameters (scales, 1/B, lr, momentum) for the device.
@@ -1355,14 +1368,32 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       e->h_sp->y = stage_in_graph ? y : nullptr;
       graph_stage = stage_in_graph ? &p : nullptr;
       hc.mark();   // 3: input staging
-      std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur, stage_in_graph ? 1 : 0};
-      for (const auto& n : local) {
-        key.push_back(n.node);
-        key.push_back(n.dev);
-        key.push_back((int64_t)n.rows);
-        key.push_back((int64_t)n.src_row);
+      // graph entry: from the memo when the mapping is the previous step's
+      const bool same = e->memo.valid && e->memo.rows == batch_rows &&
+                        e->memo.sizes.size() == total_nodes &&
+                        std::equal(e->memo.sizes.begin(), e->memo.sizes.end(), node_sizes) &&
+                        std::equal(e->memo.devs.begin(), e->memo.devs.end(), node_device);
+      if (!same) {
+        e->memo.sizes.assign(node_sizes, node_sizes + total_nodes);
+        e->memo.devs.assign(node_device, node_device + total_nodes);
+        e->memo.rows = batch_rows;
+        e->memo.valid = true;
+        for (auto& row : e->memo.ge)
+          for (auto& g : row) g = nullptr;
       }
-      auto& ge = e->graph_cache[key];
+      vnt_engine::GraphEntry*& slot = e->memo.ge[e->cur & 1][stage_in_graph ? 1 : 0];
+      if (!slot) {
+        std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur,
+                                    stage_in_graph ? 1 : 0};
+        for (const auto& n : local) {
+          key.push_back(n.node);
+          key.push_back(n.dev);
+          key.push_back((int64_t)n.rows);
+          key.push_back((int64_t)n.src_row);
+        }
+        slot = &e->graph_cache[key];
+      }
+      auto& ge = *slot;
       if (ge.exec == nullptr && ge.seen == 0) {
         ge.seen = 1;   // first encounter runs eagerly (allocations, attributes)
         enqueue_step(&stats, true);
