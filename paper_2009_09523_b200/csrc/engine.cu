@@ -133,6 +133,7 @@ struct vnt_engine {
   int node_rc_max = 0;
   float* wpad = nullptr;               // padded weight image of k_node_step
   bool stats_backed = false;           // lineage stats backed up this round
+  bool stats_join_pending = false;     // statistics branch not yet joined into the stream
   cudaStream_t aux_stream = nullptr;   // input-statistics branch beside k_node_step
   // VNT_HOST_PROFILE=1: host-side time per train_step phase (printed at destroy)
   bool host_prof = false;
@@ -323,6 +324,8 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
   vns = std::max(vns, e->cap_vns);
   VNT_CUDA(cudaStreamSynchronize(e->stream));
   if (e->copy_stream) VNT_CUDA(cudaStreamSynchronize(e->copy_stream));
+  if (e->aux_stream) VNT_CUDA(cudaStreamSynchronize(e->aux_stream));
+  e->stats_join_pending = false;
   e->pf.valid = false;
   drop_graphs(e);
   auto fre = [](auto*& p) {
@@ -663,6 +666,7 @@ void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStr
 
 void backup_stats(vnt_engine* e, cudaStream_t s);
 void layer_collective(vnt_engine* e, int l);
+void join_stats(vnt_engine* e);
 
 // Input statistics of a pass depend on x only: observe_batch per node then the
 // Chan combine into each device lineage in ascending node id
@@ -800,7 +804,9 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   VNT_LAUNCH_CHECK();
   e->launches++;
   e->tail_examples += p.rows;
-  if (stats) VNT_CUDA(cudaStreamWaitEvent(e->stream, e->join_ev, 0));
+  // Nothing in the step reads the lineage statistics: join the branch only
+  // before xin is restaged or the step's control words are read (join_stats).
+  if (stats) e->stats_join_pending = true;
 }
 
 // Device work of one pass (inputs already staged in xin/yin).
@@ -1046,6 +1052,7 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
   for (size_t i = 0; i < passes.size(); ++i) {
     const auto& p = passes[i];
     ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
+    join_stats(e);   // the previous pass's statistics still read xin
     // A prefetched batch is consumed on the first attempt only (on a rescale
     // retry the prefetch slot already holds the next batch).
     bool took = false;
@@ -1210,7 +1217,15 @@ struct Readback {
   std::vector<int> overflow;   // tensor ids
 };
 
+// The statistics side branch of a whole-node pass, joined lazily.
+void join_stats(vnt_engine* e) {
+  if (!e->stats_join_pending) return;
+  VNT_CUDA(cudaStreamWaitEvent(e->stream, e->join_ev, 0));
+  e->stats_join_pending = false;
+}
+
 void enqueue_readback(vnt_engine* e, bool with_gmax) {
+  join_stats(e);   // the step ends here: its statistics branch must have finished
   cudaStream_t s = e->stream;
   k_copy_words<<<1, 64, 0, s>>>(reinterpret_cast<const unsigned long long*>(e->G + e->P),
                                 reinterpret_cast<unsigned long long*>(e->m_tail),
@@ -1994,6 +2009,7 @@ int vnt_engine_get_input_stats(vnt_engine* e, int32_t device, double* count, dou
     const auto& d = e->devs[device];
     const uint64_t in = e->widths[0];
     VNT_CUDA(cudaStreamSynchronize(e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->aux_stream));   // a statistics branch may be in flight
     if (count) *count = d.count;
     if (mean) VNT_CUDA(cudaMemcpy(mean, d.mean, in * sizeof(double), cudaMemcpyDeviceToHost));
     if (m2) VNT_CUDA(cudaMemcpy(m2, d.m2, in * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2010,6 +2026,7 @@ int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count, cons
     auto& d = e->devs[device];
     const uint64_t in = e->widths[0];
     VNT_CUDA(cudaStreamSynchronize(e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->aux_stream));
     d.count = count;
     VNT_CUDA(cudaMemcpy(d.mean, mean, in * sizeof(double), cudaMemcpyHostToDevice));
     VNT_CUDA(cudaMemcpy(d.m2, m2, in * sizeof(double), cudaMemcpyHostToDevice));
