@@ -182,7 +182,9 @@ int vnt_engine_get_input_stats(vnt_engine* e, int32_t device, double* count, dou
 int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count,
                                const double* mean, const double* m2);
 
-/* Fixed-point scale state (part of the numerical state: migrated on resize). */
+/* Fixed-point scale state (part of the numerical state: migrated on resize).
+ * Scales set here are authoritative: the first round does not replace them
+ * with its batch-size estimate. */
 int vnt_engine_get_scales(vnt_engine* e, int32_t* scales, uint32_t n);
 int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n);
 uint32_t vnt_engine_tensor_count(const vnt_engine* e);

@@ -533,7 +533,9 @@ void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M
   using namespace vntb::tc;
   // forward GEMMs never share the GPU with the gradient reductions
   const int sms = EPI == kTcFwd ? e->sm_count : e->gemm_sms;
-  if (pair) {
+  // CTA-pair kernels: fwd / bwd-data in both modes, dW in 3xTF32 only (a 1-pass
+  // pair dW is not instantiated; such a request runs the single-CTA kernel)
+  if (pair && (e->split || EPI != kTcDw)) {
     if (e->split)
       launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
                                sms, e->stream);
