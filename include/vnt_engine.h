@@ -203,6 +203,11 @@ int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const ui
 int vnt_engine_reset_scales(vnt_engine* e);
 
 int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out);
+/* Diagnostics: the gradient all-reduces issued since the last call, as
+ * (offset into the gradient buffer, element count) pairs in issue order (up to
+ * cap pairs copied, *count = pairs logged).  Every rank of a group must issue
+ * the identical sequence; clears the log. */
+int vnt_engine_comm_log(vnt_engine* e, uint64_t* out, uint32_t cap, uint32_t* count);
 /* The CUDA stream the engine launches on (cudaStream_t as void*). */
 void* vnt_engine_stream(vnt_engine* e);
 /* Scratch device allocation owned by the engine (bench/test staging). */

@@ -110,6 +110,7 @@ def load_engine() -> C.CDLL:
         "vnt_engine_set_scales": (C.c_int, [_vp, _i32p, C.c_uint32]),
         "vnt_engine_last_timings": (C.c_int, [_vp, C.POINTER(StepTimings)]),
         "vnt_engine_reset_scales": (C.c_int, [_vp]),
+        "vnt_engine_comm_log": (C.c_int, [_vp, _u64p, C.c_uint32, C.POINTER(C.c_uint32)]),
         "vnt_engine_prefetch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _u64p, _i32p, C.c_uint32,
                                           C.c_int32]),
         "vnt_engine_regroup": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32]),
@@ -222,6 +223,14 @@ class Engine:
         _check(self.lib.vnt_engine_sync(self.h, _fp(g) if want_grad else None, C.byref(ls),
                                         C.byref(ex)))
         return g, ls.value, ex.value
+
+    def comm_log(self, cap=2048):
+        """(offset, count) of each gradient all-reduce issued since the last call
+        (vnt_engine_comm_log; clears the log)."""
+        out = np.zeros(2 * cap, np.uint64)
+        n = C.c_uint32()
+        _check(self.lib.vnt_engine_comm_log(self.h, out.ctypes.data_as(_u64p), cap, C.byref(n)))
+        return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(min(n.value, cap))]
 
     def take_gradient_sum(self):
         """Process-local exact gradient sum (no collective), closes the round:

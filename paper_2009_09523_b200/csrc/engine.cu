@@ -83,6 +83,7 @@ struct vnt_engine {
   std::vector<cudaEvent_t> layer_ev;   // per layer: its dW/db done (compute stream)
   cudaEvent_t comm_ev = nullptr;       // comm_stream caught up
   int gemm_sms = 0;                    // CTAs the backward GEMMs may occupy
+  std::vector<uint64_t> comm_log;      // (G offset, count) of every gradient all-reduce
   cudaStream_t stream = nullptr;
   int sm_count = 0;
 
@@ -1099,6 +1100,9 @@ void setup_comm_overlap(vnt_engine* e) {
 }
 
 void allreduce(vnt_engine* e, long long* p, size_t n, cudaStream_t s) {
+  e->comm_log.push_back((uint64_t)(p - e->G));   // every rank must log the same sequence
+  e->comm_log.push_back((uint64_t)n);
+  if (e->comm_log.size() > 4096) e->comm_log.erase(e->comm_log.begin(), e->comm_log.begin() + 2048);
   const ncclResult_t r = ncclAllReduce(p, p, n, ncclInt64, ncclSum, e->comm, s);
   if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
 }
@@ -2109,6 +2113,19 @@ int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const ui
     }
     split_weights(e);
     VNT_CUDA(cudaStreamSynchronize(e->stream));
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_comm_log(vnt_engine* e, uint64_t* out, uint32_t cap, uint32_t* count) {
+  return guarded([&] {
+    const uint32_t n = (uint32_t)(e->comm_log.size() / 2);
+    if (count) *count = n;
+    for (uint32_t i = 0; out && i < std::min(n, cap); ++i) {
+      out[2 * i] = e->comm_log[2 * i];
+      out[2 * i + 1] = e->comm_log[2 * i + 1];
+    }
+    e->comm_log.clear();
     return VNT_OK;
   });
 }

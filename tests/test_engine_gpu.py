@@ -354,3 +354,30 @@ def test_zero_params_loss_is_mean_square_label(port, widths, mode):
     loss, _ = e.train_step(x, y, sizes, dev, 0.01)
     want = float(np.mean(np.sum(y * y, axis=1) / widths[-1]))
     assert abs(loss - want) <= 1e-9 * want
+
+
+def test_collective_sequence_is_rank_independent(port, monkeypatch):
+    """Every rank must issue the same all-reduces in the same order (NCCL
+    matches collectives by order): a process with all nodes, one with none
+    (it reduces zeros), and one whose nodes need three passes all log the same
+    (offset, count) sequence — per layer L-1..0 overlapped, then the tail."""
+    monkeypatch.setenv("VNT_FORCE_COMM", "1")
+    w = [128, 256, 256, 10]
+    sizes, _ = vnt().uniform_mapping(256, 8, 1)
+    x, y = port.synth_batch(4, 2048, w[0], w[-1], 0, 256)
+    logs = []
+    for node_device, rr in (([0] * 8, 0), ([-1] * 8, 0), ([0] * 8, 96)):
+        e = make_engine(w, "relu", "softmax-cross-entropy", 4, port, gemm_mode="auto",
+                        resident_rows=rr)
+        e.comm_log()   # creation-time traffic, if any
+        e.train_step(x, y, sizes, np.array(node_device, np.int32), 0.02)
+        logs.append(e.comm_log())
+    P = vnt().param_count(w)
+    L = len(w) - 1
+    offs, p = [], 0
+    for l in range(L):
+        offs.append((p, w[l] * w[l + 1] + w[l + 1]))
+        p += w[l] * w[l + 1] + w[l + 1]
+    want = list(reversed(offs)) + [(P, logs[0][-1][1])]
+    assert logs[0] == want
+    assert logs[1] == logs[0] and logs[2] == logs[0]
