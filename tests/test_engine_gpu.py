@@ -356,6 +356,25 @@ def test_zero_params_loss_is_mean_square_label(port, widths, mode):
     assert abs(loss - want) <= 1e-9 * want
 
 
+def test_collective_sequence_node_path(port, monkeypatch):
+    """Small models (whole-node kernel) reduce G and its tail in one call on
+    every rank layout."""
+    monkeypatch.setenv("VNT_FORCE_COMM", "1")
+    w = [64, 96, 48, 10]
+    sizes, _ = vnt().uniform_mapping(128, 8, 1)
+    x, y = port.synth_batch(4, 2048, w[0], w[-1], 0, 128)
+    logs = []
+    for node_device in ([0] * 8, [-1] * 8, [0, -1] * 4):
+        # ffma: every layer on FFMA kernels, so the whole-node path (auto would put
+        # the 64->96 layer on tcgen05 and take the layered path)
+        e = make_engine(w, "relu", "softmax-cross-entropy", 4, port, gemm_mode="ffma")
+        e.comm_log()
+        e.train_step(x, y, sizes, np.array(node_device, np.int32), 0.02)
+        logs.append(e.comm_log())
+    assert len(logs[0]) == 1 and logs[0][0][0] == 0
+    assert logs[1] == logs[0] and logs[2] == logs[0]
+
+
 def test_collective_sequence_is_rank_independent(port, monkeypatch):
     """Every rank must issue the same all-reduces in the same order (NCCL
     matches collectives by order): a process with all nodes, one with none
