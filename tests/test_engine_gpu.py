@@ -308,12 +308,14 @@ def test_resident_batches_match_host_batches(port, widths):
     assert np.array_equal(res[0][0], res[1][0])
 
 
-@pytest.mark.parametrize("widths", [[64, 96, 48, 10], [128, 256, 256, 10]])
-def test_rank_partition_sums_add_up_exactly(port, widths):
+@pytest.mark.parametrize("widths,mode", [([64, 96, 48, 10], "ffma"), ([64, 96, 48, 10], "auto"),
+                                         ([128, 256, 256, 10], "auto")])
+def test_rank_partition_sums_add_up_exactly(port, widths, mode):
     """The N > 1 contract on one GPU: processes holding disjoint node sets
     (round-robin, as make_uniform_mapping deals them to ranks) produce exact
     local sums that add up to the single-process sum bit for bit — what the
-    int64 NCCL all-reduce then does across GPUs (both model paths)."""
+    int64 NCCL all-reduce then does across GPUs (whole-node kernel, layered
+    FFMA + tcgen05, all-tcgen05)."""
     V, m = 8, 16
     B = V * m
     x, y = port.synth_batch(8, 4096, widths[0], widths[-1], 0, B)
@@ -321,7 +323,7 @@ def test_rank_partition_sums_add_up_exactly(port, widths):
     nt = 2 * (len(widths) - 1)
 
     def local_sum(nodes):
-        e = vnt().Engine(widths, "relu", "softmax-cross-entropy", gemm_mode="auto")
+        e = vnt().Engine(widths, "relu", "softmax-cross-entropy", gemm_mode=mode)
         e.add_device(1 << 20)
         e.set_params(p0)
         e.set_scales(np.full(nt, 30, np.int32))   # every process quantises at the same scale
