@@ -214,3 +214,24 @@ def test_rescale_retry_on_tcgen05_graph_path(port):
     assert np.array_equal(runs[0][1][:2], runs[1][1][:2])
     assert np.abs(runs[0][1] - runs[1][1]).max() <= 2e-5 * np.abs(runs[0][1]).max()
     assert np.abs(runs[0][0] - runs[1][0]).max() <= 2e-5
+
+
+def test_momentum_on_tcgen05_layers(port):
+    """Momentum (no reference oracle: model.cpp:364-374 is plain SGD) on the
+    tcgen05 path and its fused SGD tiles: v <- mu v + g; w <- w - lr v against
+    the CPU restatement on oracle gradients, within the 3xTF32 tolerance."""
+    w = [128, 256, 192, 10]
+    mu, lr = 0.9, 0.05
+    e = engine(w, "relu", "softmax-cross-entropy", port, seed=2, gemm_mode="auto", momentum=mu)
+    p = port.init_params(w, 2)
+    v = np.zeros_like(p)
+    sizes, dev = vnt().uniform_mapping(128, 4, 1)
+    for s in range(4):
+        x, y = port.synth_batch(3, 4096, w[0], w[-1], s * 128, 128)
+        e.train_step(x, y, sizes, dev, lr)
+        g, _ = port.forward_backward(w, "relu", "softmax-cross-entropy", p, x, y)
+        v = mu * v + g
+        p = p - lr * v
+    dev_ = np.abs(e.get_params() - p).max()
+    print(f"tcgen05 momentum: max |w - w_ref| {dev_:.2e}")
+    assert dev_ <= 2e-5
