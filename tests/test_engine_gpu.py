@@ -220,8 +220,8 @@ def test_regroup_single_process_keeps_state(port):
     assert np.array_equal(a.scales(), b.scales())
 
 
-@pytest.mark.parametrize("graphs", [True, False])
-def test_prefetch_is_bit_identical(port, monkeypatch, graphs):
+@pytest.mark.parametrize("graphs,mode", [(True, "auto"), (False, "auto"), (True, "ffma")])
+def test_prefetch_is_bit_identical(port, monkeypatch, graphs, mode):
     """vnt_engine_prefetch (runner.cpp:64-73 on the device): staging batch i+1 on
     the copy stream while step i runs — hits, a queued request, a stale
     prefetch (different pointers) — never changes bits."""
@@ -236,8 +236,8 @@ def test_prefetch_is_bit_identical(port, monkeypatch, graphs):
         xs.append(torch.from_numpy(x).pin_memory())
         ys.append(torch.from_numpy(y).pin_memory())
     sizes, dev = vnt().uniform_mapping(B, 24, 1)
-    a = make_engine(w, "relu", "softmax-cross-entropy", 23, port, gemm_mode="auto")
-    b = make_engine(w, "relu", "softmax-cross-entropy", 23, port, gemm_mode="auto")
+    a = make_engine(w, "relu", "softmax-cross-entropy", 23, port, gemm_mode=mode)
+    b = make_engine(w, "relu", "softmax-cross-entropy", 23, port, gemm_mode=mode)
     la, lb = [], []
     for s in range(steps):
         la.append(a.train_step_ptr(xs[s].data_ptr(), ys[s].data_ptr(), B, sizes, dev, 0.05, False))
