@@ -254,17 +254,18 @@ def test_prefetch_is_bit_identical(port, monkeypatch, graphs, mode):
     assert np.array_equal(a.get_params(), b.get_params())
 
 
-@pytest.mark.parametrize("overlap", ["1", "0"])
-def test_collective_paths_bit_identical(port, monkeypatch, overlap):
+@pytest.mark.parametrize("overlap,w,mode", [("1", [128, 256, 256, 10], "auto"),
+                                            ("0", [128, 256, 256, 10], "auto"),
+                                            ("1", [64, 96, 48, 10], "ffma")])
+def test_collective_paths_bit_identical(port, monkeypatch, overlap, w, mode):
     """VNT_FORCE_COMM=1 gives the engine a one-rank NCCL group, so the collective
     code runs on one GPU: the single reduction (VNT_COMM_OVERLAP=0) and the
     per-layer reductions overlapped with the backward on a comm stream (default)
     must leave every bit of the trajectory unchanged, for any pass grouping."""
-    w = [128, 256, 256, 10]
     sizes, dev = vnt().uniform_mapping(256, 8, 1)
 
     def trajectory(rr):
-        e = make_engine(w, "relu", "softmax-cross-entropy", 4, port, gemm_mode="auto",
+        e = make_engine(w, "relu", "softmax-cross-entropy", 4, port, gemm_mode=mode,
                         resident_rows=rr)
         losses = []
         for s in range(3):
