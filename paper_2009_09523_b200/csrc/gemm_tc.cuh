@@ -73,6 +73,14 @@ struct EpiArgs {
   int tensor;
 };
 
+// max with NaN propagation (max.NaN.f32): one instruction tracks both the
+// range check and the non-finite check of the per-node partials.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -294,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;        // tile row == TMEM lane
     const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
-    float amax = 0.f, canary = 0.f;
+    float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
       const int r = m0 + row;
@@ -316,12 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (EPI == kTcDw) {
             // Per-node quantisation.  The 2^s scale is already in
             // the DT operand (exact power-of-two scaling), so TMEM holds g*2^s:
-            // track max|x| and a NaN/inf canary, convert, accumulate.
+            // track max|x| (NaN-propagating), convert, accumulate.
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const float x = v[j];
-              amax = fmaxf(amax, fabsf(x));
-              canary = fmaf(x, 0.f, canary);
+              amax = fmax_nan(amax, fabsf(x));
               acc[c * 32 + j] += __float2ll_rn(x);
             }
           } else if (r < ep.M) {
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (EPI == kTcDw) {
-      if (canary != 0.f)   // NaN: some partial was NaN or inf
+      if (!(amax <= 3.402823466e38f))   // NaN or inf: some partial was non-finite
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
       else if (!(amax < ep.lim))
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);

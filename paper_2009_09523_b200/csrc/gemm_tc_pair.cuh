@@ -214,7 +214,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
-    float amax = 0.f, canary = 0.f;
+    float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     for (int tile = pair; tile < tiles; tile += npairs) {
       const int m0 = (tile / tiles_n) * PM + (int)rank * BM, n0 = (tile % tiles_n) * BN;
       const int r = m0 + row;
@@ -238,8 +238,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float x = v[j];
-            amax = fmaxf(amax, fabsf(x));
-            canary = fmaf(x, 0.f, canary);
+            amax = fmax_nan(amax, fabsf(x));
             acc[c * 32 + j] += __float2ll_rn(x);
           }
         } else if (r < ep.M) {
@@ -331,7 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
     if (EPI == kTcDw) {
-      if (canary != 0.f)   // NaN: some partial was NaN or inf
+      if (!(amax <= 3.402823466e38f))   // NaN or inf: some partial was non-finite
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
       else if (!(amax < ep.lim))
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);

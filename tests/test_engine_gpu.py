@@ -403,3 +403,27 @@ def test_collective_sequence_is_rank_independent(port, monkeypatch):
     want = list(reversed(offs)) + [(P, logs[0][-1][1])]
     assert logs[0] == want
     assert logs[1] == logs[0] and logs[2] == logs[0]
+
+
+@pytest.mark.parametrize("w,mode", [([64, 96, 48, 10], "ffma"), ([128, 256, 256, 10], "auto")])
+def test_nonfinite_step_raises_and_leaves_state(port, w, mode):
+    """ExactAccumulator rejects non-finite values (exact_sum.cpp:17-19): a NaN in
+    the batch fails the step with VNT_ERR_NONFINITE, skips the SGD on the
+    device and restores the input statistics; the next finite step proceeds."""
+    V = vnt()
+    e = make_engine(w, "relu", "softmax-cross-entropy", 6, port, gemm_mode=mode)
+    sizes, dev = V.uniform_mapping(64, 4, 1)
+    x, y = port.synth_batch(5, 1024, w[0], w[-1], 0, 64)
+    e.train_step(x, y, sizes, dev, 0.02)
+    p1 = e.get_params()
+    cnt1, mean1, m21 = e.input_stats(0)
+    bad = x.copy()
+    bad[3, 5] = np.nan
+    with pytest.raises(V.VntError) as ei:
+        e.train_step(bad, y, sizes, dev, 0.02)
+    assert ei.value.code == 11
+    assert np.array_equal(e.get_params(), p1)
+    cnt2, mean2, m22 = e.input_stats(0)
+    assert cnt2 == cnt1 and np.array_equal(mean2, mean1) and np.array_equal(m22, m21)
+    loss, _ = e.train_step(x, y, sizes, dev, 0.02)
+    assert np.isfinite(loss)
