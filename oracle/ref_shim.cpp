@@ -91,6 +91,33 @@ void* vntref_trainer_create(const uint64_t* widths, uint32_t nw, int act, int lo
   }
 }
 
+// Same, with the data-order options (runner.hpp:28-30): shuffled epochs and
+// the background prefetch future.
+void* vntref_trainer_create_ex(const uint64_t* widths, uint32_t nw, int act, int loss,
+                               uint64_t seed, uint64_t global_batch, uint64_t virtual_nodes,
+                               double lr, uint64_t data_seed, uint64_t dataset_size,
+                               uint32_t n_devices, uint64_t capacity, int parallel,
+                               int shuffle_epochs, uint64_t shuffle_seed, int prefetch) {
+  try {
+    RunnerConfig c;
+    c.model = spec_of(widths, nw, act, loss, seed);
+    c.global_batch = global_batch;
+    c.virtual_nodes = virtual_nodes;
+    c.lr = lr;
+    c.data_seed = data_seed;
+    c.dataset_size = dataset_size;
+    c.devices = devices(n_devices, capacity);
+    c.parallel_devices = parallel != 0;
+    c.shuffle_epochs = shuffle_epochs != 0;
+    c.shuffle_seed = shuffle_seed;
+    c.prefetch = prefetch != 0;
+    return new Trainer(c);
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
 void vntref_trainer_destroy(void* h) { delete static_cast<Trainer*>(h); }
 
 int vntref_trainer_step(void* h, double* loss) {

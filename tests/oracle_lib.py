@@ -116,8 +116,21 @@ class Oracle:
         return g, lo.value
 
     def trainer(self, widths, act, loss, seed, global_batch, virtual_nodes, lr,
-                data_seed, dataset_size, n_devices, capacity=1 << 20, parallel=False):
+                data_seed, dataset_size, n_devices, capacity=1 << 20, parallel=False,
+                shuffle_seed=None, prefetch=False):
         w, n = _widths(widths)
+        if shuffle_seed is not None or prefetch:
+            assert self.kind == "ref", "shuffled epochs / prefetch: reference trainer only"
+            f = self.lib.vntref_trainer_create_ex
+            f.restype = C.c_void_p
+            h = f(w, C.c_uint32(n), C.c_int(ACT[act]), C.c_int(LOSS[loss]),
+                  C.c_uint64(seed), C.c_uint64(global_batch), C.c_uint64(virtual_nodes),
+                  C.c_double(lr), C.c_uint64(data_seed), C.c_uint64(dataset_size),
+                  C.c_uint32(n_devices), C.c_uint64(capacity), C.c_int(1 if parallel else 0),
+                  C.c_int(0 if shuffle_seed is None else 1), C.c_uint64(shuffle_seed or 0),
+                  C.c_int(1 if prefetch else 0))
+            assert h, "trainer_create_ex failed"
+            return _Trainer(self, h, self.param_count(widths), widths[0])
         if self.kind == "port":
             h = self._tc(w, C.c_uint32(n), C.c_int(ACT[act]), C.c_int(LOSS[loss]),
                          C.c_uint64(seed), C.c_uint64(global_batch), C.c_uint64(virtual_nodes),

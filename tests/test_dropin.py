@@ -90,26 +90,33 @@ def _devs(n):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["headline", "cfg1"])
+@pytest.mark.parametrize("case", ["headline", "cfg1", "shuffled"])
 def test_dropin_trainer_matches_reference_trainer(port, ref, case):
     """Trainer::step through the drop-in vs the reference's Trainer, same config,
-    including a resize 8 -> 4 -> 8 (cfg5 shape) for the headline case."""
+    including a resize 8 -> 4 -> 8 (cfg5 shape) for the headline case; the
+    shuffled case runs shuffled epochs (runner.cpp:47-62, rng.cpp:65-73) with
+    prefetch on both sides across 7 epochs and the same resizes."""
     lib = _host()
     o = ref if ref is not None else port
-    if case == "headline":
+    shuffle = case == "shuffled"
+    if shuffle and ref is None:
+        pytest.skip("shuffled epochs: the reference trainer (oracle/_ref) is the checker")
+    if case in ("headline", "shuffled"):
         w, act, loss, seed, B, V, lr, ds, n, G, steps = [4, 16, 4], 1, 0, 11, 64, 8, 0.05, 11, 256, 8, 30
     else:
         w, act, loss, seed, B, V, lr, ds, n, G, steps = [784, 16, 10], 1, 1, 11, 256, 16, 0.05, 11, 60000, 1, 10
     wa = (C.c_uint64 * len(w))(*w)
     devs = _devs(G)
-    cfg = _Cfg(wa, len(w), act, loss, seed, B, V, lr, ds, n, 0, 0, devs, G, 0, 0, 1, 0.0)
+    cfg = _Cfg(wa, len(w), act, loss, seed, B, V, lr, ds, n, int(shuffle), 7 if shuffle else 0,
+               devs, G, 0, int(shuffle), 1, 0.0)
     h = C.c_void_p()
     assert lib.vnt_trainer_create(C.byref(cfg), C.byref(h)) == 0, lib.vnt_host_last_error()
+    extra = dict(shuffle_seed=7, prefetch=True) if shuffle else {}
     t = o.trainer(w, ["relu", "tanh", "identity"][act], ["mse", "softmax-cross-entropy"][loss], seed,
-                  B, V, lr, ds, n, G)
+                  B, V, lr, ds, n, G, **extra)
     lo = C.c_double()
     for s in range(steps):
-        if case == "headline" and s in (10, 20):
+        if case != "cfg1" and s in (10, 20):
             k = 4 if s == 10 else 8
             assert lib.vnt_trainer_resize(h, _devs(k), k) == 0, lib.vnt_host_last_error()
             t.resize(k)
