@@ -9,7 +9,7 @@
 //                 accumulation fused into the GEMM epilogue).
 // CTA = 128x128 output tile.  Warp roles: w0 TMA producer (one elected lane),
 // w1 MMA issuer (one lane, tcgen05.mma.cta_group::1.kind::tf32, accumulators
-// in TMEM), w2 TMEM allocator, w4..w11 epilogue (tcgen05.ld, 32x32b).  Smem
+// in TMEM), w2 TMEM allocator, w2..w9 epilogue (tcgen05.ld, 32x32b).  Smem
 // operand tiles are 128B-swizzled K-major (TMA SWIZZLE_128B <-> UMMA
 // SWIZZLE_128B descriptors); a 4-stage mbarrier ring feeds the MMA warp; two
 // TMEM accumulators let the epilogue of segment s overlap the MMAs of s+1.
@@ -27,7 +27,10 @@ namespace vntb {
 namespace tc {
 
 constexpr int BM = 128, BK = 32;
-constexpr int kThreads = 384;
+// w0 TMA, w1 MMA, w2..w9 epilogue (w2 also allocates TMEM): 320 threads leave
+// the dW epilogue 204 registers for its 64 int64 accumulators (no spills).
+constexpr int kEpiWarp0 = 2;
+constexpr int kThreads = (kEpiWarp0 + 8) * 32;
 
 enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
 
@@ -175,6 +178,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16-column variant for the dW epilogue: its 64 int64 accumulators per thread
+// leave no room for a 32-register staging array under the 168-register cap
+// (3 warps per SM sub-partition).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // Persistent: CTA b processes tiles b, b + gridDim.x, ... (n fastest).  Per
 // tile, nseg == 0 means one segment covering K; otherwise segment s covers K
 // columns [seg_k0[s], seg_k0[s] + round_up(seg_rows[s], 32)) — one virtual node.
@@ -295,10 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= kEpiWarp0) {
     constexpr int COLS = BN / 2;          // columns per epilogue thread
     const int q = warp & 3;               // TMEM lane quarter this warp may access
-    const int h = (warp - 4) >> 2;        // column half
+    const int h = (warp - kEpiWarp0) >> 2;        // column half
     const int row = q * 32 + lane;        // tile row == TMEM lane
     const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
@@ -315,23 +335,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = it & 1;
         mbar_wait(&tfull[b], (it >> 1) & 1);
         tc_fence_after();
+        if constexpr (EPI == kTcDw) {
+          // Per-node quantisation.  The 2^s scale is already in
+          // the DT operand (exact power-of-two scaling), so TMEM holds g*2^s:
+          // track max|x| (NaN-propagating), convert, accumulate.
+#pragma unroll
+          for (int c = 0; c < COLS / 16; ++c) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float x = v[j];
+              amax = fmax_nan(amax, fabsf(x));
+              acc[c * 16 + j] += __float2ll_rn(x);
+            }
+          }
+        } else {
 #pragma unroll
         for (int c = 0; c < COLS / 32; ++c) {
           float v[32];
           const int col = h * COLS + c * 32;
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
           const int nb = n0 + col;
-          if (EPI == kTcDw) {
-            // Per-node quantisation.  The 2^s scale is already in
-            // the DT operand (exact power-of-two scaling), so TMEM holds g*2^s:
-            // track max|x| (NaN-propagating), convert, accumulate.
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float x = v[j];
-              amax = fmax_nan(amax, fabsf(x));
-              acc[c * 32 + j] += __float2ll_rn(x);
-            }
-          } else if (r < ep.M) {
+          if (r < ep.M) {
             const int tc = ep.tcol[r];
             if (EPI == kTcBwd && nb + 32 <= ep.N) {
               const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
@@ -374,12 +400,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = 0; j < 32; j += 4)
                   *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
               } else {
-                for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (nb + j < ep.N) orow[j] = v[j];
               }
             }
             if (ep.outh) {
               const size_t o = (size_t)r * ep.ldo + nb;
-              for (int j = 0; j < 32 && nb + j < ep.N; j += 4) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                if (nb + j >= ep.N) break;
                 float4 hv, lv;
                 hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
                 hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
@@ -390,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+        }
         }
         tc_fence_before();
         __syncwarp();

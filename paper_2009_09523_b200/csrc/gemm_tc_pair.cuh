@@ -207,10 +207,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mma_commit_pair(&tfull[b]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= kEpiWarp0) {
     constexpr int COLS = BN / 2;
     const int q = warp & 3;
-    const int h = (warp - 4) >> 2;
+    const int h = (warp - kEpiWarp0) >> 2;
     const int row = q * 32 + lane;
     const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
@@ -227,21 +227,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int b = it & 1;
       mbar_wait(&tfull[b], (it >> 1) & 1);
       tc_fence_after();
+      if constexpr (EPI == kTcDw) {
+        // per-node quantisation, as k_gemm_tc's dW epilogue
+#pragma unroll
+        for (int c = 0; c < COLS / 16; ++c) {
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float x = v[j];
+            amax = fmax_nan(amax, fabsf(x));
+            acc[c * 16 + j] += __float2ll_rn(x);
+          }
+        }
+      } else {
 #pragma unroll
       for (int c = 0; c < COLS / 32; ++c) {
         float v[32];
         const int col = h * COLS + c * 32;
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
         const int nb = n0 + col;
-        if (EPI == kTcDw) {
-          // per-node quantisation, as k_gemm_tc's dW epilogue
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = v[j];
-            amax = fmax_nan(amax, fabsf(x));
-            acc[c * 32 + j] += __float2ll_rn(x);
-          }
-        } else if (r < ep.M) {
+        if (r < ep.M) {
           const int tc = ep.tcol[r];
           if (EPI == kTcBwd && nb + 32 <= ep.N) {
             const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
@@ -284,12 +290,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 32; j += 4)
                 *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             } else {
-              for (int j = 0; j < 32 && nb + j < ep.N; ++j) orow[j] = v[j];
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < ep.N) orow[j] = v[j];
             }
           }
           if (ep.outh) {
             const size_t o = (size_t)r * ep.ldo + nb;
-            for (int j = 0; j < 32 && nb + j < ep.N; j += 4) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              if (nb + j >= ep.N) break;
               float4 hv, lv;
               hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
               hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
@@ -300,6 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
+      }
       }
       tc_fence_before();
       if (EPI == kTcDw) {
