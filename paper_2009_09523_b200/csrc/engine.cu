@@ -2173,4 +2173,16 @@ int vnt_engine_memcpy_h2d(vnt_engine* e, void* dst, const void* src, uint64_t by
   });
 }
 
+#ifdef VNT_TC_PROBE
+// Diagnostics build only: read and clear the tcgen05 GEMM barrier-wait probe
+// (6 kernel kinds x {producer wait, total, MMA tempty wait, total, epilogue
+// wait, total, MMA full wait, -}, summed cycles over CTAs).
+int vnt_debug_tc_probe(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, vntb::tc::g_tc_probe, sizeof(vntb::tc::g_tc_probe)) != cudaSuccess)
+    return 1;
+  static const unsigned long long zero[6 * 8] = {};
+  return cudaMemcpyToSymbol(vntb::tc::g_tc_probe, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 }  // extern "C"

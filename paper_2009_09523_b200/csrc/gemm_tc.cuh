@@ -34,6 +34,28 @@ constexpr int kThreads = (kEpiWarp0 + 8) * 32;
 
 enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
 
+// Diagnostics build only (-DVNT_TC_PROBE, scripts/tc_probe.py): cycles each
+// role spends waiting on its barriers, per kernel kind (EPI + 3 * pair).
+#ifdef VNT_TC_PROBE
+__device__ unsigned long long g_tc_probe[6][8];
+#define TC_PROBE_DECL long long _pw = 0, _pt = clock64()
+#define TC_PROBE_WAIT(stmt)          \
+  do {                               \
+    const long long _t = clock64();  \
+    stmt;                            \
+    _pw += clock64() - _t;           \
+  } while (0)
+#define TC_PROBE_DONE(kind, slot)                                               \
+  do {                                                                          \
+    atomicAdd(&g_tc_probe[kind][slot], (unsigned long long)_pw);                \
+    atomicAdd(&g_tc_probe[kind][slot + 1], (unsigned long long)(clock64() - _pt)); \
+  } while (0)
+#else
+#define TC_PROBE_DECL
+#define TC_PROBE_WAIT(stmt) stmt
+#define TC_PROBE_DONE(kind, slot)
+#endif
+
 // fwd / bwd-data: 128x256 tiles (A 4 KB + B 8 KB of smem per 128-cycle MMA);
 // dW: 128x128 (the int64 per-node accumulators live in registers).
 template <int EPI, int SPLIT = 1>
@@ -254,13 +276,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
+      TC_PROBE_DECL;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
         for (int s = 0; s < segs; ++s) {
           const int kb = nseg > 0 ? seg_k0[s] : 0;
           const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
           for (int k = 0; k < kl; k += BK) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             mbar_expect_tx(&full[stage], C::kStageBytes);
             tma_load_2d(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
             tma_load_2d(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
@@ -275,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      TC_PROBE_DONE(EPI, 0);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -282,15 +306,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;  // global (tile, segment) counter
+      TC_PROBE_DECL;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         for (int s = 0; s < segs; ++s, ++it) {
           const int b = it & 1;
-          mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+          TC_PROBE_WAIT(mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(b * BN);
           const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
           for (int k = 0; k < kl; k += BK) {
+#ifdef VNT_TC_PROBE
+            { const long long _t = clock64(); mbar_wait(&full[stage], phase);
+              atomicAdd(&g_tc_probe[EPI][6], (unsigned long long)(clock64() - _t)); }
+#else
             mbar_wait(&full[stage], phase);
+#endif
             tc_fence_after();
             const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
             const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
@@ -314,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&tfull[b]);
         }
       }
+      TC_PROBE_DONE(EPI, 2);
     }
   } else if (warp >= kEpiWarp0) {
     constexpr int COLS = BN / 2;          // columns per epilogue thread
@@ -323,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
+    TC_PROBE_DECL;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
       const int r = m0 + row;
@@ -333,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int s = 0; s < segs; ++s, ++it) {
         const int b = it & 1;
-        mbar_wait(&tfull[b], (it >> 1) & 1);
+        TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
         tc_fence_after();
         if constexpr (EPI == kTcDw) {
           // Per-node quantisation.  The 2^s scale is already in
@@ -351,7 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else {
-#pragma unroll
+        // one 32-column chunk per iteration, not unrolled: the unrolled
+        // epilogue overflowed the instruction cache (stall_no_inst at K = 784)
+#pragma unroll 1
         for (int c = 0; c < COLS / 32; ++c) {
           float v[32];
           const int col = h * COLS + c * 32;
@@ -445,6 +479,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+#ifdef VNT_TC_PROBE
+    if (warp == kEpiWarp0 && lane == 0) TC_PROBE_DONE(EPI, 4);
+#endif
     if (EPI == kTcDw) {
       if (!(amax <= 3.402823466e38f))   // NaN or inf: some partial was non-finite
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);

@@ -146,6 +146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
+      TC_PROBE_DECL;
       for (int tile = pair; tile < tiles; tile += npairs) {
         const int m0 = (tile / tiles_n) * PM + (int)rank * BM;
         const int n0 = (tile % tiles_n) * BN + (int)rank * BNH;
@@ -153,7 +154,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int kb = nseg > 0 ? seg_k0[sg] : 0;
           const int kl = nseg > 0 ? (int)round_up(seg_rows[sg], 32) : K;
           for (int k = 0; k < kl; k += BK) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
             tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
             tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
@@ -168,6 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (rank == 0) TC_PROBE_DONE(EPI + 3, 0);
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
@@ -175,15 +177,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;
+      TC_PROBE_DECL;
       for (int tile = pair; tile < tiles; tile += npairs)
       for (int sg = 0; sg < segs; ++sg, ++it) {
         const int b = it & 1;
-        mbar_wait_cluster(&tempty[b], ((it >> 1) & 1) ^ 1);
+        TC_PROBE_WAIT(mbar_wait_cluster(&tempty[b], ((it >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * BN);
         const int kl = nseg > 0 ? (int)round_up(seg_rows[sg], 32) : K;
         for (int k = 0; k < kl; k += BK) {
+#ifdef VNT_TC_PROBE
+          { const long long _t = clock64(); mbar_wait(&full[stage], phase);
+            atomicAdd(&g_tc_probe[EPI + 3][6], (unsigned long long)(clock64() - _t)); }
+#else
           mbar_wait(&full[stage], phase);
+#endif
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
           const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
@@ -206,6 +214,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         mma_commit_pair(&tfull[b]);
       }
+      TC_PROBE_DONE(EPI + 3, 2);
     }
   } else if (warp >= kEpiWarp0) {
     constexpr int COLS = BN / 2;
@@ -215,6 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
     uint32_t it = 0;
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
+    TC_PROBE_DECL;
     for (int tile = pair; tile < tiles; tile += npairs) {
       const int m0 = (tile / tiles_n) * PM + (int)rank * BM, n0 = (tile % tiles_n) * BN;
       const int r = m0 + row;
@@ -225,7 +235,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       for (int sg = 0; sg < segs; ++sg, ++it) {
       const int b = it & 1;
-      mbar_wait(&tfull[b], (it >> 1) & 1);
+      TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
       tc_fence_after();
       if constexpr (EPI == kTcDw) {
         // per-node quantisation, as k_gemm_tc's dW epilogue
@@ -241,7 +251,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-#pragma unroll
+        // one 32-column chunk per iteration, not unrolled: the unrolled
+        // epilogue overflowed the instruction cache (stall_no_inst at K = 784)
+#pragma unroll 1
       for (int c = 0; c < COLS / 32; ++c) {
         float v[32];
         const int col = h * COLS + c * 32;
@@ -340,6 +352,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
+#ifdef VNT_TC_PROBE
+    if (warp == kEpiWarp0 && lane == 0 && rank == 0) TC_PROBE_DONE(EPI + 3, 4);
+#endif
     if (EPI == kTcDw) {
       if (!(amax <= 3.402823466e38f))   // NaN or inf: some partial was non-finite
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
