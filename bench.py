@@ -409,15 +409,17 @@ def run_ours(args, work):
             peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
             peak_note = "fp32 FFMA peak 148 SM x 128 FMA/clk x 2 x sm_max_mhz"
         else:
-            # The GEMMs run inside a long step: the sustained bf16 figure applies
-            # (B200_PROFILING: burst for a kernel timed alone, sustained inside a long step).
-            bf16 = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-            peak = bf16 / 2
+            # The burst bf16 figure: the sustained one (cuBLAS bf16 held for 4 s at
+            # its power cap) is not binding for these TF32 GEMMs, which run at
+            # higher clocks inside the step and exceed bf16_sustained/2/3; the
+            # sustained fraction is reported beside it.
+            peak = peaks["bf16_tflops"] / 2
             if mode == "3xtf32":
                 peak /= 3
-                peak_note = f"TF32 = sustained bf16/2 ({peak_src}), /3 for 3xTF32 passes"
+                peak_note = (f"TF32 = burst bf16/2 ({peak_src}), /3 for 3xTF32 passes; "
+                             "the sustained bf16 figure is below what these GEMMs reach")
             else:
-                peak_note = f"TF32 = sustained bf16/2 ({peak_src})"
+                peak_note = f"TF32 = burst bf16/2 ({peak_src})"
         line["roofline"] = {
             "bound": "tensor", "kernel": "dense-layer GEMMs (fwd, bwd-data, per-node dW)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -425,7 +427,8 @@ def run_ours(args, work):
             "gemm_share_of_step": (gemm_ms / args.steps) / ms_per_step,
             "algorithmic_flops_per_step": flops_step,
             "gemm_launches_per_step": gemm_n / args.steps,
-            "frac_vs_burst_peak": achieved / (peaks["bf16_tflops"] / 2 / (3 if mode == "3xtf32" else 1))
+            "frac_vs_sustained_peak": achieved / (peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+                                                  / 2 / (3 if mode == "3xtf32" else 1))
             if mode != "ffma" else None,
         }
         # DRAM bytes per GEMM launch from the committed `ncu --set full` capture of
@@ -463,7 +466,7 @@ def run_ours(args, work):
             f1.record(fstream)
             torch.cuda.synchronize()
             fstep = f0.elapsed_time(f1) / args.steps
-            tf32_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 2
+            tf32_peak = peaks["bf16_tflops"] / 2
             line["also_tf32_1pass"] = {
                 "value": B / (fstep / 1e3), "unit": "samples/s", "ms_per_step": fstep,
                 "gemm_tflops": ffl / (fms / 1e3) / 1e12 if fms else None,

@@ -167,20 +167,27 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          ((uint32_t)(M >> 4) << 24);
 }
 
+// The MMA role runs on a whole warp with warp-uniform operands; one elected
+// lane issues (elect.sync inside the asm), so the compiler keeps descriptors in
+// uniform registers instead of wrapping every tcgen05.mma in a per-lane loop.
 __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   su32(bar))
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+          su32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -301,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       TC_PROBE_DONE(EPI, 0);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc = idesc_tf32(BM, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -567,11 +574,12 @@ bool tc_use_pair() {
   return on;
 }
 
-// dW on 256x128 CTA pairs (3xTF32 only) is opt-in: VNT_TC_DW_PAIR=1.  Measured
-// on cfg3 it runs the 4096x4096 dW at 60 % tensor-pipe activity against 74 %
-// for the single-CTA kernel (profiles/r01_summary.md), so the default stays single.
+// dW on 256x128 CTA pairs (VNT_TC_DW_PAIR=0 selects the single-CTA 128x128
+// kernel).  Per SM the pair reads half of B and writes half of B's
+// stages into smem; with the whole-warp MMA issue it beats the single-CTA dW
+// on cfg3 (profiles/r01_summary.md).
 bool tc_dw_pair() {
-  static const bool on = getenv("VNT_TC_DW_PAIR") && getenv("VNT_TC_DW_PAIR")[0] == '1';
+  static const bool on = !(getenv("VNT_TC_DW_PAIR") && getenv("VNT_TC_DW_PAIR")[0] == '0');
   return on;
 }
 
@@ -608,13 +616,12 @@ void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M
   using namespace vntb::tc;
   // forward GEMMs never share the GPU with the gradient reductions
   const int sms = EPI == kTcFwd ? e->sm_count : e->gemm_sms;
-  // CTA-pair kernels: fwd / bwd-data in both modes, dW in 3xTF32 only (a 1-pass
-  // pair dW is not instantiated; such a request runs the single-CTA kernel)
-  if (pair && (e->split || EPI != kTcDw)) {
+  // CTA-pair kernels for all three GEMMs in both modes
+  if (pair) {
     if (e->split)
       launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
                                sms, e->stream);
-    else if constexpr (EPI != kTcDw)
+    else
       launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
                                sms, e->stream);
     e->launches++;
@@ -695,9 +702,8 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   using namespace vntb::tc;
   const int M = (int)e->widths[l], N = (int)e->widths[l + 1];
   const uint64_t ldT = p.ldT;
-  // Single-CTA 128x128 by default; the 3xTF32 CTA-pair variant (256x128, B's
-  // smem traffic halved) is opt-in, see tc_dw_pair().
-  const bool pair = e->split && tc_use_pair() && tc_dw_pair();
+  // CTA pairs (256x128, B's smem traffic per SM halved), see tc_dw_pair().
+  const bool pair = tc_use_pair() && tc_dw_pair();
   const uint32_t bn = pair ? PairCfg<kTcDw, 3>::BNH : TileCfg<kTcDw>::BN;
   const OpMaps a = op_maps(e, e->XT[l], e->XTh[l], e->XTl[l], M, ldT, ldT, BM);
   const OpMaps b = op_maps(e, e->DT[l + 1], e->DTh[l + 1], e->DTl[l + 1], N, ldT, ldT, bn);
