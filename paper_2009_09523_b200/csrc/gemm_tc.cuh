@@ -96,7 +96,26 @@ struct EpiArgs {
   float scale, lim;
   long long* tail;
   int tensor;
+  // tile raster: groups of group_m tile rows, column-major inside a group, so
+  // the tiles resident at once share A and B panels in L2 (0/1: row-major)
+  int group_m;
 };
+
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int gm, int& tm,
+                                            int& tn) {
+  if (gm <= 1) {
+    tm = tile / tiles_n;
+    tn = tile % tiles_n;
+    return;
+  }
+  const int per_group = gm * tiles_n;
+  const int g = tile / per_group;
+  const int first = g * gm;
+  const int rows = min(gm, tiles_m - first);
+  const int t = tile - g * per_group;
+  tm = first + t % rows;
+  tn = t / rows;
+}
 
 // max with NaN propagation (max.NaN.f32): one instruction tracks both the
 // range check and the non-finite check of the per-node partials.
@@ -252,7 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int segs = nseg > 0 ? nseg : 1;
   const int tiles_n = (int)ceil_div(ep.N, BN);
-  const int tiles = (int)ceil_div(ep.M, BM) * tiles_n;
+  const int tiles_m = (int)ceil_div(ep.M, BM);
+  const int tiles = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -285,7 +305,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       TC_PROBE_DECL;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+        int tm, tn;
+        tile_coords(tile, tiles_m, tiles_n, ep.group_m, tm, tn);
+        const int m0 = tm * BM, n0 = tn * BN;
         for (int s = 0; s < segs; ++s) {
           const int kb = nseg > 0 ? seg_k0[s] : 0;
           const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
@@ -363,7 +385,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     TC_PROBE_DECL;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, ep.group_m, tm, tn);
+      const int m0 = tm * BM, n0 = tn * BN;
       const int r = m0 + row;
       long long acc[EPI == kTcDw ? COLS : 1];
       if (EPI == kTcDw) {
@@ -583,6 +607,15 @@ bool tc_dw_pair() {
   return on;
 }
 
+// Tile-raster group height (VNT_TC_GROUP_M, default 8; 1 = row-major order).
+int tc_group_m() {
+  static const int g = [] {
+    const char* v = getenv("VNT_TC_GROUP_M");
+    return v ? std::max(1, atoi(v)) : 8;
+  }();
+  return g;
+}
+
 bool tc_layer_eligible(int mode, uint64_t in, uint64_t out) {
   if (mode == VNT_GEMM_FFMA) return false;
   return in >= 64 && out >= 64 && in % 4 == 0 && out % 4 == 0;
@@ -612,10 +645,11 @@ OpMaps op_maps(const vnt_engine* e, const float* full, const float* hi, const fl
 
 template <int EPI>
 void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M, int N, int K,
-               int nseg, const int* seg_k0, const int* seg_rows, const vntb::tc::EpiArgs& ep) {
+               int nseg, const int* seg_k0, const int* seg_rows, vntb::tc::EpiArgs ep) {
   using namespace vntb::tc;
   // forward GEMMs never share the GPU with the gradient reductions
   const int sms = EPI == kTcFwd ? e->sm_count : e->gemm_sms;
+  ep.group_m = tc_group_m();
   // CTA-pair kernels for all three GEMMs in both modes
   if (pair) {
     if (e->split)

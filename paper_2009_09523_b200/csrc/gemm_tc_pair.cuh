@@ -117,7 +117,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int segs = nseg > 0 ? nseg : 1;   // dW: one K-chain per virtual node
   const int tiles_n = (int)ceil_div(ep.N, BN);
-  const int tiles = (int)ceil_div(ep.M, PM) * tiles_n;
+  const int tiles_m = (int)ceil_div(ep.M, PM);
+  const int tiles = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -152,8 +153,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       TC_PROBE_DECL;
       for (int tile = pair; tile < tiles; tile += npairs) {
-        const int m0 = (tile / tiles_n) * PM + (int)rank * BM;
-        const int n0 = (tile % tiles_n) * BN + (int)rank * BNH;
+        int tm, tn;
+        tile_coords(tile, tiles_m, tiles_n, ep.group_m, tm, tn);
+        const int m0 = tm * PM + (int)rank * BM;
+        const int n0 = tn * BN + (int)rank * BNH;
         for (int sg = 0; sg < segs; ++sg) {
           const int kb = nseg > 0 ? seg_k0[sg] : 0;
           const int kl = nseg > 0 ? (int)round_up(seg_rows[sg], 32) : K;
@@ -230,7 +233,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     TC_PROBE_DECL;
     for (int tile = pair; tile < tiles; tile += npairs) {
-      const int m0 = (tile / tiles_n) * PM + (int)rank * BM, n0 = (tile % tiles_n) * BN;
+      int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, ep.group_m, tm, tn);
+      const int m0 = tm * PM + (int)rank * BM, n0 = tn * BN;
       const int r = m0 + row;
       long long acc[EPI == kTcDw ? COLS : 1];
       if (EPI == kTcDw) {
