@@ -192,6 +192,43 @@ print(json.dumps({"err": err, "bitwise": bool(np.array_equal(out[0], out[1]))}))
     assert res["err"] < 2e-5 and res["bitwise"]
 
 
+def test_tile_raster_does_not_change_bits(port, tmp_path):
+    """VNT_TC_GROUP_M only reorders which CTA computes which tile: losses and
+    parameters after a few steps are bit-identical for row-major (1) and
+    grouped rasters."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle_lib, paper_2009_09523_b200 as vnt
+port = oracle_lib.port()
+w = [512, 768, 640, 10]
+sizes = [128] * 8
+B = sum(sizes)
+p0 = port.init_params(w, 1)
+e = vnt.Engine(w, "relu", "softmax-cross-entropy", gemm_mode="3xtf32")
+e.add_device(1 << 20)
+e.set_params(p0)
+node_dev = np.zeros(len(sizes), dtype=np.int32)
+losses = []
+for s in range(3):
+    x, y = port.synth_batch(3, 4096, w[0], w[-1], s * B, B)
+    losses.append(e.train_step(x, y, sizes, node_dev, 0.01)[0])
+np.save(sys.argv[1], np.concatenate([np.array(losses), e.get_params()]))
+'''
+    outs = []
+    for gm in ("1", "8", "3"):
+        path = str(tmp_path / f"raster_{gm}.npy")
+        env = dict(os.environ, VNT_TC_GROUP_M=gm)
+        r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True,
+                           env=env, cwd=str(GOLDEN.parents[1]), timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
 def test_rescale_retry_on_tcgen05_graph_path(port):
     """A fixed-point overflow inside a graph-replayed tcgen05 step: the engine
     lowers the scale, redoes the step eagerly (input statistics observed once,
