@@ -663,7 +663,8 @@ __global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __
                             const int* __restrict__ vn_row0, const int* __restrict__ vn_rows,
                             const float* __restrict__ scale_p, float lim,
                             long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
-  __shared__ float dn[64][NO];
+  static_assert(NO % 4 == 0, "dn rows are read as float4");
+  __shared__ __align__(16) float dn[64][NO];
   const float scale = *scale_p;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
@@ -685,9 +686,17 @@ __global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __
 #pragma unroll
         for (int j = 0; j < 8; ++j) a[j] = __ldg(xp + (size_t)(rr + j) * in);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 8; ++j) {
+          const float4* d4 = reinterpret_cast<const float4*>(&dn[rr + j][0]);
 #pragma unroll
-          for (int o = 0; o < NO; ++o) g[o] = fmaf(a[j], dn[rr + j][o], g[o]);
+          for (int o = 0; o < NO; o += 4) {   // broadcast float4 reads: 4x fewer LDS
+            const float4 d = d4[o / 4];
+            g[o] = fmaf(a[j], d.x, g[o]);
+            g[o + 1] = fmaf(a[j], d.y, g[o + 1]);
+            g[o + 2] = fmaf(a[j], d.z, g[o + 2]);
+            g[o + 3] = fmaf(a[j], d.w, g[o + 3]);
+          }
+        }
       }
       for (; rr < cn; ++rr) {
         const float a = __ldg(xp + (size_t)rr * in);
