@@ -22,7 +22,10 @@ struct PairCfg {
   static constexpr int kStageBytes = (SPLIT == 3 ? 2 : 1) * (kBytesA + kBytesB);
   static constexpr int STAGES = (192 * 1024 / kStageBytes) < 6 ? (192 * 1024 / kStageBytes) : 6;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256;
+  // fwd / bwd epilogue: a 32x33 fp32 transpose tile per epilogue warp
+  static constexpr int kEpiStageBytes = EPI == kTcDw ? 0 : 8 * 32 * 33 * 4;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256 + kEpiStageBytes;
+  static_assert(kSmemBytes <= 232448, "exceeds the opt-in shared memory per block");
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -111,6 +114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  float* stile = (float*)(smem + STAGES * C::kStageBytes + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -292,6 +296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
           }
+          // feature-major copies: lanes are consecutive rows -> 128 B per store
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (nb + j < ep.N) {
@@ -304,32 +309,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ep.outTl[o] = t - th;
               }
             }
-          if (ep.out) {   // null: only the 3xTF32 twins are consumed
-            float* orow = ep.out + (size_t)r * ep.ldo + nb;
-            if (nb + 32 <= ep.N) {
+        }
+        // row-major copies: transpose the warp's 32x32 block through smem so
+        // every store writes 128 contiguous bytes of one row (a per-thread
+        // float4 row store touches 32 lines per instruction)
+        if (ep.out || ep.outh) {
+          float* st = stile + (warp - kEpiWarp0) * (32 * 33);
 #pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (nb + j < ep.N) orow[j] = v[j];
+          for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
+          __syncwarp();
+          const int n = nb + lane;
+          const int rb = m0 + q * 32;
+#pragma unroll 4
+          for (int k = 0; k < 32; ++k) {
+            const float x = st[k * 33 + lane];
+            if (rb + k < ep.M && n < ep.N) {
+              const size_t o = (size_t)(rb + k) * ep.ldo + n;
+              if (ep.out) ep.out[o] = x;
+              if (ep.outh) {
+                const float hx = tf32_rna(x);
+                ep.outh[o] = hx;
+                ep.outl[o] = x - hx;
+              }
             }
           }
-          if (ep.outh) {
-            const size_t o = (size_t)r * ep.ldo + nb;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              if (nb + j >= ep.N) break;
-              float4 hv, lv;
-              hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
-              hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
-              hv.z = tf32_rna(v[j + 2]); lv.z = v[j + 2] - hv.z;
-              hv.w = tf32_rna(v[j + 3]); lv.w = v[j + 3] - hv.w;
-              *reinterpret_cast<float4*>(ep.outh + o + j) = hv;
-              *reinterpret_cast<float4*>(ep.outl + o + j) = lv;
-            }
-          }
+          __syncwarp();
         }
       }
       }
