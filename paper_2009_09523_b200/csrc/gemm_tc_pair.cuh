@@ -241,6 +241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile, tiles_m, tiles_n, ep.group_m, tm, tn);
       const int m0 = tm * PM + (int)rank * BM, n0 = tn * BN;
       const int r = m0 + row;
+      const int tc = (EPI != kTcDw && r < ep.M) ? ep.tcol[r] : 0;
       long long acc[EPI == kTcDw ? COLS : 1];
       if (EPI == kTcDw) {
 #pragma unroll
@@ -272,8 +273,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int col = h * COLS + c * 32;
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
         const int nb = n0 + col;
+        if constexpr (EPI == kTcFwd) {
+          // bias: one coalesced load per warp, broadcast by shuffles
+          const float bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float bj = __shfl_sync(0xffffffffu, bl, j);
+            if (nb + j < ep.N) v[j] = act_fwd(ep.act, v[j] + bj);
+          }
+        }
         if (r < ep.M) {
-          const int tc = ep.tcol[r];
           if (EPI == kTcBwd && nb + 32 <= ep.N) {
             const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
 #pragma unroll
@@ -284,16 +293,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               v[j + 2] *= act_grad_from_out(ep.act, xv.z);
               v[j + 3] *= act_grad_from_out(ep.act, xv.w);
             }
-          } else {
+          } else if (EPI == kTcBwd) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int n = nb + j;
-              if (n < ep.N) {
-                if (EPI == kTcFwd)
-                  v[j] = act_fwd(ep.act, v[j] + __ldg(ep.bias + n));
-                else
-                  v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
-              }
+              if (n < ep.N) v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
             }
           }
           // feature-major copies: lanes are consecutive rows -> 128 B per store
