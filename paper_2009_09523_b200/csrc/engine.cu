@@ -492,10 +492,13 @@ struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
                   int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
                   const float* tscale, float* Dh, float* Dl, float* DTh, float* DTl) {
-    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32 * kBwdSkinnyChunks)),
-        block(32, 8);
+    static const int chunks = [] {   // 32-row chunks per CTA (VNT_BWD_SKINNY_CHUNKS)
+      const char* v = getenv("VNT_BWD_SKINNY_CHUNKS");
+      return v ? std::max(1, atoi(v)) : 4;
+    }();
+    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32 * chunks)), block(32, 8);
     k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
-                                            tscale, Dh, Dl, DTh, DTl);
+                                            tscale, Dh, Dl, DTh, DTl, chunks);
   }
 };
 template <int NO>

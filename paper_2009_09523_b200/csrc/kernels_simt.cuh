@@ -515,7 +515,6 @@ __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict
 // ---------------------------------------------- skinny layers (out <= 32)
 template <int NO>   // rows per warp in k_fwd_skinny (R*NO accumulators per lane)
 __host__ __device__ constexpr int skinny_rows() { return NO > 16 ? 2 : 4; }
-constexpr int kBwdSkinnyChunks = 1;   // 32-row chunks per CTA in k_bwd_skinny
 // Forward with few outputs (the 4096 -> 10 classifier): one warp per row,
 // lane-strided partial dot products over k then a fixed xor tree, so every
 // output depends only on its row.
@@ -607,9 +606,9 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
                                                     const float* __restrict__ tscale_p,
                                                     float* __restrict__ Dh, float* __restrict__ Dl,
                                                     float* __restrict__ DTh,
-                                                    float* __restrict__ DTl) {
+                                                    float* __restrict__ DTl, int chunks) {
   const float tscale = tscale_p ? *tscale_p : 1.f;
-  // 32 features x kBwdSkinnyChunks*32 rows per block, o ascending per output;
+  // 32 features x chunks*32 rows per block, o ascending per output;
   // transposed copy through smem.
   __shared__ float tile[32][33];
   __shared__ float dn[32][NO];
@@ -619,8 +618,8 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
   float w[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) w[o] = (i < in && o < no) ? W[(size_t)i * no + o] : 0.f;
-  for (int chunk = 0; chunk < kBwdSkinnyChunks; ++chunk) {
-    const int r0 = (blockIdx.y * kBwdSkinnyChunks + chunk) * 32;
+  for (int chunk = 0; chunk < chunks; ++chunk) {
+    const int r0 = (blockIdx.y * chunks + chunk) * 32;
     if (r0 >= rows) break;
     __syncthreads();
     for (int k = ty * 32 + tx; k < 32 * NO; k += 256) {
