@@ -427,3 +427,45 @@ def test_nonfinite_step_raises_and_leaves_state(port, w, mode):
     assert cnt2 == cnt1 and np.array_equal(mean2, mean1) and np.array_equal(m22, m21)
     loss, _ = e.train_step(x, y, sizes, dev, 0.02)
     assert np.isfinite(loss)
+
+
+def test_single_layer_identity_least_squares_known_answer():
+    """test_model.cpp:93-111 on the engine: [2,1] identity/MSE, params
+    (0.5, -0.25, 0.1), x = (2, 3), y = 1.5 -> residual r = -1.15, loss r^2,
+    gradient (2r*2, 2r*3, 2r); fp32 compute, tolerance 1e-6 relative."""
+    e = vnt().Engine([2, 1], "identity", "mse", gemm_mode="ffma")
+    e.add_device(1 << 20)
+    e.set_params(np.array([0.5, -0.25, 0.1]))
+    e.device_step(0, np.array([[2.0, 3.0]]), np.array([[1.5]]), [1])
+    g, loss_sum, ex = e.sync()
+    r = 2.0 * 0.5 + 3.0 * -0.25 + 0.1 - 1.5
+    assert ex == 1
+    assert abs(loss_sum - r * r) <= 1e-6 * r * r
+    want = np.array([2 * r * 2.0, 2 * r * 3.0, 2 * r])
+    assert np.abs(g - want).max() <= 1e-6 * np.abs(want).max()
+    e.close()
+
+
+@pytest.mark.parametrize("mode", ["ffma", "3xtf32"])
+def test_union_gradient_is_size_weighted_mean_of_parts(port, mode):
+    """test_model.cpp:148-163: the gradient of a union is the size-weighted mean
+    of the parts' gradients.  On the engine the 5:3 split as two virtual nodes
+    is compared with the two parts run alone (1e-12, the reference's bound: the
+    int64 node sums add exactly; only the fp64 divisions by 8, 5, 3 round)."""
+    w = [64, 96, 80, 3] if mode == "3xtf32" else [4, 6, 3]
+    p0 = port.init_params(w, 33)
+    x, y = port.synth_batch(99, 64, w[0], w[-1], 0, 8)
+
+    def grad(xs, ys, sizes):
+        e = vnt().Engine(w, "tanh", "softmax-cross-entropy", gemm_mode=mode)
+        e.add_device(1 << 20)
+        e.set_params(p0)
+        e.device_step(0, xs, ys, sizes)
+        g, _, _ = e.sync()
+        e.close()
+        return g
+
+    g = grad(x, y, [5, 3])
+    ga, gb = grad(x[:5], y[:5], [5]), grad(x[5:], y[5:], [3])
+    expect = (5.0 * ga + 3.0 * gb) / 8.0
+    assert np.all(np.abs(g - expect) <= 1e-12 * np.maximum(1.0, np.abs(expect)))
