@@ -7,12 +7,16 @@
 //              -> quantised to int64 and summed over the pass's nodes in
 //                 registers, one store per tile (the virtual-node gradient
 //                 accumulation fused into the GEMM epilogue).
-// CTA = 128x128 output tile.  Warp roles: w0 TMA producer (one elected lane),
-// w1 MMA issuer (one lane, tcgen05.mma.cta_group::1.kind::tf32, accumulators
-// in TMEM), w2 TMEM allocator, w2..w9 epilogue (tcgen05.ld, 32x32b).  Smem
-// operand tiles are 128B-swizzled K-major (TMA SWIZZLE_128B <-> UMMA
-// SWIZZLE_128B descriptors); a 4-stage mbarrier ring feeds the MMA warp; two
-// TMEM accumulators let the epilogue of segment s overlap the MMAs of s+1.
+// This file: the single-CTA kernel (128x128 dW tiles with VNT_TC_DW_PAIR=0,
+// 128x256 fwd/bwd with VNT_TC_PAIR=0) and the shared pieces; the default
+// CTA-pair kernels are in gemm_tc_pair.cuh.  Warp roles: w0 TMA producer (one
+// lane), w1 MMA issuer (the whole warp runs the loop, one elected lane issues
+// tcgen05.mma.kind::tf32; accumulators in TMEM), w2 TMEM allocator, w2..w9
+// epilogue (tcgen05.ld, 32x32b).  Smem operand tiles are 128B-swizzled
+// K-major (TMA SWIZZLE_128B <-> UMMA SWIZZLE_128B descriptors); an mbarrier
+// ring feeds the MMA warp; two TMEM accumulators let the epilogue of segment s
+// overlap the MMAs of s+1.  Tiles are visited in groups of tile rows
+// (tile_coords) so the resident tiles share operand panels in L2.
 //
 // Every output element is one K-chain over the same k-blocks in the same
 // order whatever the row count or tile position, so results are independent

@@ -1,11 +1,11 @@
-// CTA-pair (cta_group::2) variant of the tcgen05 GEMM, used for the forward
-// and bwd-data layers.  A cluster of two CTAs (the two SMs of a TPC) computes
-// a 256 x BN tile: CTA r owns A rows [m0 + 128 r, +128) and B rows
+// CTA-pair (cta_group::2) variant of the tcgen05 GEMM, the default for all
+// three GEMMs.  A cluster of two CTAs (the two SMs of a TPC) computes a
+// 256 x BN tile: CTA r owns A rows [m0 + 128 r, +128) and B rows
 // [n0 + r BN/2, +BN/2) in its own smem; the leader (r = 0) issues
 // tcgen05.mma.cta_group::2 on the pair's operands and each CTA receives its
-// 128 accumulator rows in its own TMEM.  Per SM this cuts the TMA bytes
-// written into smem per MAC by a third (B loaded once per pair), which is the
-// shared-memory bound of the single-CTA kernel.
+// 128 accumulator rows in its own TMEM.  Per SM each CTA stages only half of
+// B.  The fwd/bwd epilogue writes the row-major outputs through
+// a per-warp smem transpose tile (kEpiStageBytes) so stores are 128 B rows.
 #pragma once
 
 namespace vntb {
