@@ -228,7 +228,7 @@ def run_reference(args, work):
         "metric": "samples/sec at fixed global batch & V", "impl": "reference",
         "value": base["value"], "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": run_config(args, work, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -369,7 +369,7 @@ def run_ours(args, work):
     line = {
         "metric": "samples/sec at fixed global batch & V", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": run_config(args, work, world),
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
