@@ -41,7 +41,7 @@ params = np.concatenate([np.concatenate([r.standard_normal(WIDE[i] * WIDE[i + 1]
                                          np.zeros(WIDE[i + 1])]) for i in range(len(WIDE) - 1)])
 x = torch.randn(B, 784, device="cuda", dtype=torch.float64)
 y = torch.softmax(torch.randn(B, 10, device="cuda", dtype=torch.float64), dim=1)
-e = vnt.Engine(WIDE, "relu", "softmax-cross-entropy", gemm_mode="auto")
+e = vnt.Engine(WIDE, "relu", "softmax-cross-entropy", gemm_mode=sys.argv[2] if len(sys.argv) > 2 else "auto")
 e.add_device(1 << 20)
 e.set_params(params)
 sizes, dev = vnt.uniform_mapping(B, V, 1, 1 << 20)
