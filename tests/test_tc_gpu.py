@@ -153,11 +153,12 @@ def test_padding_columns_across_uneven_passes(port, mode):
         assert np.array_equal(p, outs[0][0])
 
 
-@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("pair", ["0", "1", "single"])
 def test_dw_kernels_match_reference(port, pair):
-    """Both 3xTF32 dW kernels — VNT_TC_DW_PAIR=1 (256x128 CTA pairs, default)
-    and VNT_TC_DW_PAIR=0 (single-CTA 128x128) — give fp32-grade gradients,
-    bit-identical across pass groupings."""
+    """Every tcgen05 kernel variant gives fp32-grade gradients, bit-identical
+    across pass groupings: VNT_TC_DW_PAIR=1 (256x128 CTA-pair dW, default),
+    VNT_TC_DW_PAIR=0 (single-CTA 128x128 dW) and VNT_TC_PAIR=0 (single-CTA
+    kernels for all three GEMMs)."""
     import os
     import subprocess
     import sys
@@ -183,7 +184,8 @@ for rr in (0, 64):
 err = float(np.abs(out[0] - want).max() / np.abs(want).max())
 print(json.dumps({"err": err, "bitwise": bool(np.array_equal(out[0], out[1]))}))
 '''
-    env = dict(os.environ, VNT_TC_DW_PAIR=pair)
+    env = dict(os.environ, VNT_TC_PAIR="0") if pair == "single" else \
+        dict(os.environ, VNT_TC_DW_PAIR=pair)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=str(GOLDEN.parents[1]), timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
