@@ -194,6 +194,44 @@ print(json.dumps({"err": err, "bitwise": bool(np.array_equal(out[0], out[1]))}))
     assert res["err"] < 2e-5 and res["bitwise"]
 
 
+def test_kernel_variants_are_bit_identical(port, tmp_path):
+    """CTA-pair and single-CTA tcgen05 kernels run the same per-element K-chains
+    (same k order, same three MMAs per k-step): a few training steps give
+    bit-identical losses and parameters with VNT_TC_PAIR=0, VNT_TC_DW_PAIR=0
+    and the defaults."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle_lib, paper_2009_09523_b200 as vnt
+port = oracle_lib.port()
+w = [256, 512, 384, 10]
+sizes = [24, 40, 7, 57, 128, 64]
+B = sum(sizes)
+e = vnt.Engine(w, "relu", "softmax-cross-entropy", gemm_mode=sys.argv[2])
+e.add_device(1 << 20)
+e.set_params(port.init_params(w, 1))
+node_dev = np.zeros(len(sizes), dtype=np.int32)
+losses = []
+for s in range(3):
+    x, y = port.synth_batch(3, 4096, w[0], w[-1], s * B, B)
+    losses.append(e.train_step(x, y, sizes, node_dev, 0.01)[0])
+np.save(sys.argv[1], np.concatenate([np.array(losses), e.get_params()]))
+'''
+    for mode in ("3xtf32", "tf32"):
+        outs = []
+        for k, env_kv in enumerate(({}, {"VNT_TC_DW_PAIR": "0"}, {"VNT_TC_PAIR": "0"})):
+            path = str(tmp_path / f"v{mode}{k}.npy")
+            r = subprocess.run([sys.executable, "-c", code, path, mode], capture_output=True,
+                               text=True, env=dict(os.environ, **env_kv),
+                               cwd=str(GOLDEN.parents[1]), timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), mode
+
+
 def test_tile_raster_does_not_change_bits(port, tmp_path):
     """VNT_TC_GROUP_M only reorders which CTA computes which tile: losses and
     parameters after a few steps are bit-identical for row-major (1) and
