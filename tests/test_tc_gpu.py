@@ -29,9 +29,6 @@ def engine(widths, act, loss, port, seed=1, n_devices=1, **kw):
 
 
 def synced_grad(e, x, y, sizes):
-    off = 0
-    for k, s in enumerate(sizes):
-        pass
     e.device_step(0, x, y, sizes)
     g, loss_sum, ex = e.sync()
     return g, loss_sum / ex
@@ -106,6 +103,29 @@ def test_3xtf32_gradient_is_fp32_grade(port, sizes):
     print(f"3xtf32 sizes {sizes}: rel grad err {err:.2e}, loss {loss:.9f} vs {want_loss:.9f}")
     assert err < 2e-5
     assert abs(loss - want_loss) < 2e-6 * abs(want_loss)
+
+
+@pytest.mark.parametrize("act,loss", [("tanh", "mse"), ("identity", "softmax-cross-entropy"),
+                                      ("tanh", "softmax-cross-entropy"), ("relu", "mse")])
+def test_3xtf32_activations_and_losses(port, act, loss):
+    """Every activation/loss pair of the reference (model.cpp:289-338) through the
+    tcgen05 epilogues (tanh keeps the fp32 activation for its derivative, relu and
+    identity read the hi twin): fp32-grade gradients and loss against the fp64
+    oracle."""
+    w = [128, 192, 160, 8]
+    sizes = [32, 17, 47, 32]
+    B = sum(sizes)
+    x, y = port.synth_batch(5, 4096, w[0], w[-1], 0, B)
+    p0 = port.init_params(w, 3)
+    want, want_loss = port.forward_backward(w, act, loss, p0, x, y)
+    e = engine(w, act, loss, port, seed=3, gemm_mode="3xtf32")
+    g, lo = synced_grad(e, x, y, sizes)
+    err = np.abs(g - want).max() / np.abs(want).max()
+    print(f"3xtf32 {act}/{loss}: rel grad err {err:.2e}, loss {lo:.9f} vs {want_loss:.9f}")
+    assert err < 2e-5
+    # the loss is formed from fp32 logits; an MSE of small residuals magnifies
+    # their ~1e-7 relative error, hence 1e-5 here (2e-6 for the CE cases above)
+    assert abs(lo - want_loss) < 1e-5 * abs(want_loss)
 
 
 def test_3xtf32_trajectory_and_bitwise(port):
