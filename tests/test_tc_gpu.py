@@ -89,7 +89,7 @@ def test_tc_trajectory_vs_reference(port):
     assert dw < 1e-4
 
 
-@pytest.mark.parametrize("sizes", [[64, 64, 64, 64], [24, 40, 7, 57, 128]])
+@pytest.mark.parametrize("sizes", [[64, 64, 64, 64], [24, 40, 7, 57, 128], [700, 3, 301]])
 def test_3xtf32_gradient_is_fp32_grade(port, sizes):
     """3xTF32 (hi*hi + hi*lo + lo*hi): the tensor-core path meets the fp32 tier."""
     w = [256, 512, 384, 10]
