@@ -25,6 +25,8 @@
 
 #include <cuda.h>
 
+#include "raster.cuh"
+
 #include <algorithm>
 
 namespace vntb {
@@ -105,21 +107,7 @@ struct EpiArgs {
   int group_m;
 };
 
-__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int gm, int& tm,
-                                            int& tn) {
-  if (gm <= 1) {
-    tm = tile / tiles_n;
-    tn = tile % tiles_n;
-    return;
-  }
-  const int per_group = gm * tiles_n;
-  const int g = tile / per_group;
-  const int first = g * gm;
-  const int rows = min(gm, tiles_m - first);
-  const int t = tile - g * per_group;
-  tm = first + t % rows;
-  tn = t / rows;
-}
+
 
 // max with NaN propagation (max.NaN.f32): one instruction tracks both the
 // range check and the non-finite check of the per-node partials.
