@@ -60,20 +60,6 @@ int vnt_synth_batch(uint64_t data_seed, uint64_t dataset_size, uint64_t in_w, ui
                     uint64_t start, uint64_t count, double* x, double* y);
 int vnt_init_params(const uint64_t* widths, uint32_t nw, uint64_t seed, double* out);
 
-/* hetero::solve (reference hetero.hpp:112-118) on flat arrays.  Type i has
- * name names[i], pool entry (counts[i], caps[i]) and a profile curve of
- * npts[i] points (the next npts[i] entries of pt_batch / pt_time) with
- * comm[i].  Out: the best assignment as out_ntypes entries (index into the
- * input types, n, b, v), its predicted time, and the number of feasible
- * assignments (when collect != 0).  VNT_ERR_INFEASIBLE / VNT_ERR_CONFIG as the
- * reference throws InfeasibleError / ConfigError. */
-int vnt_hetero_solve(uint32_t ntypes, const char* const* names, const uint64_t* counts,
-                     const uint64_t* caps, const double* comm, const uint32_t* npts,
-                     const uint64_t* pt_batch, const double* pt_time, uint64_t global_batch,
-                     uint64_t max_virtual_nodes, int32_t collect, uint32_t* out_ntypes,
-                     uint32_t* out_type, uint64_t* out_n, uint64_t* out_b, uint64_t* out_v,
-                     double* out_time, uint64_t* out_candidates);
-
 /* hetero::profile_device: measured B200 step times of the workload, one
  * virtual node of b rows per point (CUDA events), on cuda_device.  out_* hold
  * up to nb points (out_npts set); warnings (skipped sizes) are not returned. */

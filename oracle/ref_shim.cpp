@@ -15,8 +15,6 @@
 //   vntref_accumulate_sample -> Model::accumulate_example_grads (model.cpp:238-343)
 //   vntref_sync_sgd_sample   -> sync_gradients + sgd_apply (virtual_exec.cpp:146-168,
 //                               model.cpp:364-374)
-//   vntref_hetero_solve      -> hetero::solve (hetero.cpp:233-339), same flat
-//                               signature as vnt_hetero_solve (include/vnt_trainer.h)
 
 #include <chrono>
 #include <thread>
@@ -28,7 +26,6 @@
 #include <vector>
 
 #include "vnt/errors.hpp"
-#include "vnt/hetero.hpp"
 #include "vnt/runner.hpp"
 
 using namespace vntref;
@@ -286,41 +283,5 @@ int vntref_accumulate_sample_mt(const uint64_t* widths, uint32_t nw, int act, in
   }
 }
 
-int vntref_hetero_solve(uint32_t ntypes, const char* const* names, const uint64_t* counts,
-                        const uint64_t* caps, const double* comm, const uint32_t* npts,
-                        const uint64_t* pt_batch, const double* pt_time, uint64_t global_batch,
-                        uint64_t max_virtual_nodes, int32_t collect, uint32_t* out_ntypes,
-                        uint32_t* out_type, uint64_t* out_n, uint64_t* out_b, uint64_t* out_v,
-                        double* out_time, uint64_t* out_candidates) {
-  try {
-    std::vector<hetero::ProfileCurve> curves(ntypes);
-    hetero::DevicePool pool;
-    std::size_t at = 0;
-    for (uint32_t i = 0; i < ntypes; ++i) {
-      curves[i].device_type = names[i];
-      curves[i].comm_overhead_s = comm[i];
-      for (uint32_t k = 0; k < npts[i]; ++k, ++at) curves[i].points.push_back({pt_batch[at], pt_time[at]});
-      pool.entries[names[i]] = {counts[i], caps[i]};
-    }
-    hetero::SolveOptions o;
-    o.max_virtual_nodes = max_virtual_nodes;
-    o.collect_candidates = collect != 0;
-    const auto r = hetero::solve(curves, pool, global_batch, o);
-    *out_ntypes = (uint32_t)r.best.types.size();
-    for (std::size_t j = 0; j < r.best.types.size(); ++j) {
-      const auto& t = r.best.types[j];
-      for (uint32_t i = 0; i < ntypes; ++i)
-        if (t.device_type == names[i]) out_type[j] = i;
-      out_n[j] = t.devices_used;
-      out_b[j] = t.per_device_batch;
-      out_v[j] = t.virtual_nodes;
-    }
-    *out_time = r.best.predicted_step_time_s;
-    *out_candidates = r.candidates.size();
-    return 0;
-  } catch (const std::exception& e) {
-    return fail(e);
-  }
-}
 
 }  // extern "C"

@@ -160,41 +160,6 @@ int vnt_init_params(const uint64_t* widths, uint32_t nw, uint64_t seed, double* 
 }
 
 
-int vnt_hetero_solve(uint32_t ntypes, const char* const* names, const uint64_t* counts,
-                     const uint64_t* caps, const double* comm, const uint32_t* npts,
-                     const uint64_t* pt_batch, const double* pt_time, uint64_t global_batch,
-                     uint64_t max_virtual_nodes, int32_t collect, uint32_t* out_ntypes,
-                     uint32_t* out_type, uint64_t* out_n, uint64_t* out_b, uint64_t* out_v,
-                     double* out_time, uint64_t* out_candidates) {
-  return guard([&] {
-    std::vector<vnt::hetero::ProfileCurve> curves(ntypes);
-    vnt::hetero::DevicePool pool;
-    std::size_t at = 0;
-    for (uint32_t i = 0; i < ntypes; ++i) {
-      curves[i].device_type = names[i];
-      curves[i].comm_overhead_s = comm[i];
-      for (uint32_t k = 0; k < npts[i]; ++k, ++at) curves[i].points.push_back({pt_batch[at], pt_time[at]});
-      pool.entries[names[i]] = {counts[i], caps[i]};
-    }
-    vnt::hetero::SolveOptions o;
-    o.max_virtual_nodes = max_virtual_nodes;
-    o.collect_candidates = collect != 0;
-    const auto r = vnt::hetero::solve(curves, pool, global_batch, o);
-    *out_ntypes = (uint32_t)r.best.types.size();
-    for (std::size_t j = 0; j < r.best.types.size(); ++j) {
-      const auto& t = r.best.types[j];
-      for (uint32_t i = 0; i < ntypes; ++i)
-        if (t.device_type == names[i]) out_type[j] = i;
-      out_n[j] = t.devices_used;
-      out_b[j] = t.per_device_batch;
-      out_v[j] = t.virtual_nodes;
-    }
-    *out_time = r.best.predicted_step_time_s;
-    *out_candidates = r.candidates.size();
-    return VNT_OK;
-  });
-}
-
 int vnt_hetero_profile_device(const uint64_t* widths, uint32_t nw, int32_t activation,
                               int32_t loss, uint64_t seed, const char* device_type,
                               uint64_t memory_capacity, const uint64_t* batch_sizes, uint32_t nb,

@@ -107,80 +107,3 @@ def test_rerun_bytes_and_mapping_invariance(tmp_path):
     assert r.returncode == 0, r.stderr
     s = json.loads(r.stdout)
     assert s["max_divergence"] == 0.0 and s["bitwise_identical"] is True
-
-
-def test_profile_and_solve_commands(tmp_path, ref):
-    """`vnt profile` / `vnt solve` (tools/vnt.cpp:154-263): curves from the cost
-    model over the candidate grid, then the heterogeneous assignment — the same
-    assignment the reference's own solver (oracle/_ref) finds on those curves."""
-    wl = {"layer_widths": [4, 8, 2], "activation": "tanh", "loss": "mse", "seed": 1}
-    models = [{"device_type": "V100", "fixed_overhead_s": 0.002, "per_example_cost_s": 0.00025,
-               "comm_s": 0.01, "memory_capacity": 3072},
-              {"device_type": "P100", "fixed_overhead_s": 0.002, "per_example_cost_s": 0.001,
-               "comm_s": 0.01, "memory_capacity": 3072}]
-    pcfg = tmp_path / "profile.json"
-    pcfg.write_text(json.dumps({"workload": wl, "max_batch": 4096, "device_models": models,
-                                "out_dir": str(tmp_path / "curves")}))
-    r = run("profile", "--config", pcfg, "--json")
-    assert r.returncode == 0, r.stderr
-    paths = json.loads(r.stdout)["profiles"]
-    curves = [json.loads(Path(p).read_text()) for p in paths]
-    for m, c in zip(models, curves):
-        # 2-device minus 1-device mean (reference semantics), so only up to rounding
-        assert c["device_type"] == m["device_type"] and abs(c["comm_overhead_s"] - m["comm_s"]) < 1e-15
-        for pt in c["points"]:   # mean of identical simulated times is that time, exactly
-            assert pt["step_time_s"] == m["fixed_overhead_s"] + m["per_example_cost_s"] * pt["batch_size"]
-        assert max(pt["batch_size"] for pt in c["points"]) <= m["memory_capacity"]
-    scfg = tmp_path / "solve.json"
-    scfg.write_text(json.dumps({"profiles": paths, "global_batch": 8192,
-                                "pool": {"V100": {"count": 2, "memory_capacity": 3072},
-                                         "P100": {"count": 2, "memory_capacity": 3072}},
-                                "out": str(tmp_path / "plan" / "assignment.json")}))
-    r = run("solve", "--config", scfg, "--json", "--explain")
-    assert r.returncode == 0, r.stderr
-    out = json.loads(r.stdout)
-    a = out["assignment"]
-    assert a == json.loads((tmp_path / "plan" / "assignment.json").read_text())
-    got = {t["device_type"]: (t["count"], t["per_device_batch"], t["virtual_nodes"]) for t in a["types"]}
-    assert got["V100"][1] == 3072 and got["P100"][1] == 1024          # test_hetero.cpp:107-134
-    if ref is not None:
-        import ctypes as C
-        from test_hetero import _solve
-        types = [dict(name=c["device_type"], count=2, cap=3072, comm=c["comm_overhead_s"],
-                      points=[(p["batch_size"], p["step_time_s"]) for p in c["points"]])
-                 for c in sorted(curves, key=lambda c: c["device_type"])]
-        rc, res = _solve(ref.lib.vntref_hetero_solve, types, 8192)
-        assert rc == 0
-        best, t, cand = res
-        assert t == a["predicted_step_time_s"] and cand == len(out["candidates"])
-        assert {n: (k, b, v) for n, k, b, v in best} == got
-    # infeasible -> exit 5 (vnt.cpp:395-413)
-    scfg.write_text(json.dumps({"profiles": paths, "global_batch": 100000,
-                                "pool": {"V100": {"count": 1, "memory_capacity": 64}}}))
-    r = run("solve", "--config", scfg)
-    assert r.returncode == 5 and "capacity" in r.stderr
-
-
-@pytest.mark.gpu
-def test_profile_measured_on_b200(tmp_path):
-    """Extension key "measure": true — the curve is timed on this B200
-    (hetero::profile_device) and feeds `vnt solve` like a synthetic one."""
-    wl = {"layer_widths": [784, 16, 10], "activation": "tanh", "loss": "softmax-cross-entropy",
-          "seed": 11}
-    pcfg = tmp_path / "profile.json"
-    pcfg.write_text(json.dumps({"workload": wl, "max_batch": 64, "steps": 20, "out_dir": str(tmp_path),
-                                "device_models": [{"device_type": "B200", "fixed_overhead_s": 0.0,
-                                                   "per_example_cost_s": 1e-6, "comm_s": 0.0,
-                                                   "memory_capacity": 64, "measure": True}]}))
-    r = run("profile", "--config", pcfg, "--json")
-    assert r.returncode == 0, r.stderr
-    c = json.loads((tmp_path / "B200.json").read_text())
-    assert [p["batch_size"] for p in c["points"]] == [1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64]
-    assert all(0 < p["step_time_s"] < 0.05 for p in c["points"])
-    scfg = tmp_path / "solve.json"
-    scfg.write_text(json.dumps({"profiles": [str(tmp_path / "B200.json")], "global_batch": 256,
-                                "pool": {"B200": {"count": 8, "memory_capacity": 64}}}))
-    r = run("solve", "--config", scfg, "--json")
-    assert r.returncode == 0, r.stderr
-    (t,) = json.loads(r.stdout)["assignment"]["types"]
-    assert t["count"] * t["per_device_batch"] == 256
