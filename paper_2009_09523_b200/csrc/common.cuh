@@ -26,10 +26,16 @@ struct EngineError : std::runtime_error {
 
 #define VNT_LAUNCH_CHECK() VNT_CUDA(cudaGetLastError())
 
-constexpr int kLossScaleBits = 32;   // per-row loss quantisation 2^32 (exact int64 sum)
+constexpr int kLossScaleBits = 32;   // default per-row loss quantisation 2^32 (exact int64 sum)
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
+// smallest k with 2^k >= n (0 for n <= 1)
+inline int ceil_log2(uint64_t n) {
+  int k = 0;
+  while (k < 63 && (1ull << k) < n) ++k;
+  return k;
+}
 
 // Activation codes follow model.hpp:20 (relu, tanh, identity).
 __device__ __forceinline__ float act_fwd(int act, float z) {

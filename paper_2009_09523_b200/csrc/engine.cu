@@ -44,7 +44,9 @@ int set_error(int code, const std::string& msg) {
 }
 
 constexpr int kScaleTargetBits = 40;   // |sum| of the largest element ~ 2^40 after scaling
-constexpr int kLimBits = 50;           // per-node partial bound (2^12 nodes x 2^50 < 2^62)
+constexpr int kLimBits = 50;           // per-node partial bound for up to 2^12 partials
+constexpr int kMaxPartialsLog2 = 21;   // beyond 2^21 partials the bound drops under the scale target
+constexpr int kLossRescale = 16;       // loss quantum step on a loss-range redo
 constexpr int kRescaleStep = 12;
 
 struct PassNode {
@@ -98,6 +100,10 @@ struct vnt_engine {
   double* gout = nullptr;
   std::vector<int> scales;
   bool scales_init = false;
+  int lim_bits = kLimBits;             // |per-node partial| < 2^lim_bits (62 - log2 of the partial count)
+  int loss_bits = kLossScaleBits;      // per-row loss quantum 2^-loss_bits (adapts on range flags)
+  double loss_rows = 1;                // rows bound of the loss sum (power of two)
+  uint64_t acc_partials = 0;           // per-node partials this process added in the round
 
   // pass buffers
   uint64_t cap_rows = 0, cap_ldT = 0, cap_vns = 0;
@@ -114,6 +120,7 @@ struct vnt_engine {
     const double* y = nullptr;
     int buf = -1;
     bool valid = false;
+    std::vector<int64_t> layout;   // (node, dev, rows, src_row) of the staged rows
   } pf;
   // a second request waits until the in-flight one is consumed, then starts
   // right after the consuming step has launched its own work
@@ -132,6 +139,7 @@ struct vnt_engine {
   // whole-node kernel for small all-FFMA models (kernels_node.cuh)
   bool node_path = false;
   int node_rc_max = 0;
+  int node_cl = 1;                     // CTAs per node (cluster size), fixed per model
   float* wpad = nullptr;               // padded weight image of k_node_step
   bool stats_backed = false;           // lineage stats backed up this round
   bool stats_join_pending = false;     // statistics branch not yet joined into the stream
@@ -294,6 +302,8 @@ void fill_step_params(vnt_engine* e, double lr, double inv_b) {
   h.lr = lr;
   h.mu = e->opt.momentum;
   h.inv_b = inv_b;
+  h.loss_scale = std::ldexp(1.0, e->loss_bits);
+  h.loss_lim = std::ldexp(1.0, 62) / e->loss_rows;
 }
 
 // Pinned h_sp -> d_sp on the stream (a kernel reading mapped host memory, so it
@@ -582,6 +592,18 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local);
 
 // Copy the rows this process needs from (x, y) into the spare input buffer on
 // the copy stream (single-pass plans only: multi-pass steps stage per pass).
+std::vector<int64_t> staging_layout(const std::vector<PassNode>& local) {
+  std::vector<int64_t> k;
+  k.reserve(local.size() * 4);
+  for (const auto& n : local) {
+    k.push_back(n.node);
+    k.push_back(n.dev);
+    k.push_back((int64_t)n.rows);
+    k.push_back((int64_t)n.src_row);
+  }
+  return k;
+}
+
 void start_prefetch(vnt_engine* e, const double* x, const double* y, uint64_t batch_rows,
                     const uint64_t* node_sizes, const int32_t* node_device, uint32_t total_nodes,
                     bool on_device, bool may_grow) {
@@ -600,6 +622,7 @@ void start_prefetch(vnt_engine* e, const double* x, const double* y, uint64_t ba
   e->pf.x = x;
   e->pf.y = y;
   e->pf.buf = b;
+  e->pf.layout = staging_layout(local);
   e->pf.valid = true;
 }
 
@@ -612,10 +635,13 @@ void start_queued_prefetch(vnt_engine* e) {
                  q.on_device, false);
 }
 
-// Use a prefetched batch if it matches (x, y): switch the staging buffer and
-// order the compute stream after the copy.  Returns true if consumed.
-bool take_prefetch(vnt_engine* e, const double* x, const double* y) {
-  const bool hit = e->pf.valid && e->pf.x == x && e->pf.y == y;
+// Use a prefetched batch if it matches (x, y) and was staged for the same
+// rows (mapping, node sizes, devices): switch the staging buffer and order the
+// compute stream after the copy.  Returns true if consumed.
+bool take_prefetch(vnt_engine* e, const double* x, const double* y,
+                   const std::vector<PassNode>& local) {
+  const bool hit = e->pf.valid && e->pf.x == x && e->pf.y == y &&
+                   e->pf.layout == staging_layout(local);
   e->pf.valid = false;
   if (!hit) return false;
   e->cur = e->pf.buf;
@@ -758,22 +784,18 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   a.loss = e->loss;
   uint64_t maxrows = 1;
   for (const auto& pn : p.nodes) maxrows = std::max<uint64_t>(maxrows, pn.rows);
-  // VNT_NODE_CLUSTER (default 4): CTAs per node (rows split, strips summed over DSMEM)
-  static const int cl_env = getenv("VNT_NODE_CLUSTER") ? atoi(getenv("VNT_NODE_CLUSTER")) : 4;
-  int CL = (cl_env == 2 || cl_env == 4 || cl_env == 8) ? cl_env : 1;
+  // CTAs per node (rows split, strips summed over DSMEM): fixed per model at creation
+  const int CL = e->node_cl;
   a.rc = (int)std::min<uint64_t>(ceil_div(maxrows, (uint64_t)CL), (uint64_t)e->node_rc_max);
   a.sp = e->d_sp;
-  a.lim = pow2f(kLimBits);
+  a.lim = pow2f(e->lim_bits);
   a.G = e->G;
   a.tail = e->G + e->P;
   a.examples = (long long)p.rows;
   const size_t base = ((size_t)a.rc * node_row_floats(e) + node_wt_floats(e) + 8 + 3) & ~(size_t)3;
   a.part_off = (int)base;
-  size_t smem = (base + (CL > 1 ? (size_t)a.nstrips * kNodeOC : 0)) * sizeof(float);
-  if (smem > 227 * 1024) {   // no room for the exchange area: one CTA per node
-    CL = 1;
-    smem = base * sizeof(float);
-  }
+  const size_t smem = (base + (CL > 1 ? (size_t)a.nstrips * kNodeOC : 0)) * sizeof(float);
+  if (smem > 227 * 1024) throw EngineError(VNT_ERR_INTERNAL, "whole-node kernel: shared memory plan exceeded");
   static size_t smem_attr[9] = {};
   if (smem > smem_attr[CL]) {
     const void* fn = CL == 8   ? (const void*)k_node_step<8>
@@ -905,14 +927,14 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     const unsigned warps_per_block = 8;
     k_loss<<<(unsigned)ceil_div(p.rows, warps_per_block), warps_per_block * 32, 0, s>>>(
         e->logits, e->yin, rows, (int)out, e->loss, e->D[L], e->DT[L], ldT, tcol, e->G + e->P,
-        dts(L));
+        dts(L), e->d_sp);
     VNT_LAUNCH_CHECK();
     e->launches++;
     split_into(e, e->D[L], e->Dh[L], e->Dl[L], p.rows * out);
     split_into(e, e->DT[L], e->DTh[L], e->DTl[L], out * p.ldT);
   }
   // Backward (model.cpp:317-338): dW/db per node into the exact sum, then delta.
-  const float lim = pow2f(kLimBits);
+  const float lim = pow2f(e->lim_bits);
   for (int l = L - 1; l >= 0; --l) {
     const int in_l = (int)e->widths[l], out_l = (int)e->widths[l + 1];
     const int tw = 2 * l, tb = 2 * l + 1;
@@ -973,6 +995,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
 void begin_round_host(vnt_engine* e, uint64_t batch_hint) {
   e->stats_backed = false;
   e->acc_examples = 0;
+  e->acc_partials = 0;
   e->tail_examples = 0;
   e->acc_started = false;
   e->round_open = true;
@@ -1061,7 +1084,7 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
     // retry the prefetch slot already holds the next batch).
     bool took = false;
     if (i == 0 && do_stats) {
-      if (passes.size() == 1) took = take_prefetch(e, x, y);
+      if (passes.size() == 1) took = take_prefetch(e, x, y, local);
       else e->pf.valid = false;
     }
     if (!took) stage_inputs(e, p, x, y, on_device);
@@ -1069,6 +1092,7 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
              layer_comm && i + 1 == passes.size());
     e->acc_started = true;
     e->acc_examples += p.rows;
+    e->acc_partials += p.nodes.size();
   }
 }
 
@@ -1220,7 +1244,9 @@ void launch_sgd(vnt_engine* e) {
 struct Readback {
   double loss_sum;
   uint64_t examples;
+  uint64_t partials;
   bool nonfinite;
+  bool loss_range;             // a row loss outside the int64 range at this quantum
   std::vector<int> overflow;   // tensor ids
 };
 
@@ -1242,9 +1268,11 @@ void enqueue_readback(vnt_engine* e, bool with_gmax) {
 
 Readback parse_readback(vnt_engine* e) {
   Readback r;
-  r.loss_sum = std::ldexp((double)e->h_tail[kTailLoss], -kLossScaleBits);
+  r.loss_sum = std::ldexp((double)e->h_tail[kTailLoss], -e->loss_bits);
   r.examples = (uint64_t)e->h_tail[kTailExamples];
+  r.partials = (uint64_t)e->h_tail[kTailPartials];
   r.nonfinite = e->h_tail[kTailNonfinite] != 0;
+  r.loss_range = e->h_tail[kTailLossRange] != 0;
   for (uint32_t t = 0; t < ntensors(e); ++t)
     if (e->h_tail[kTailOverflow + t]) r.overflow.push_back((int)t);
   return r;
@@ -1254,6 +1282,14 @@ Readback read_tail(vnt_engine* e, bool with_gmax) {
   enqueue_readback(e, with_gmax);
   VNT_CUDA(cudaStreamSynchronize(e->stream));
   return parse_readback(e);
+}
+
+// Back to the default loss quantum once the mean row loss is 2^8 below the
+// range of the default (a function of global values: identical on every rank).
+void relax_loss_bits(vnt_engine* e, double mean_loss) {
+  if (e->loss_bits >= kLossScaleBits) return;
+  if (std::fabs(mean_loss) * std::ldexp(1.0, kLossScaleBits + 8) < std::ldexp(1.0, 62) / e->loss_rows)
+    e->loss_bits = kLossScaleBits;
 }
 
 void update_scales(vnt_engine* e, uint64_t batch) {
@@ -1283,6 +1319,7 @@ void reset_acc(vnt_engine* e) {
   e->round_open = false;
   e->acc_started = false;
   e->acc_examples = 0;
+  e->acc_partials = 0;
   e->tail_examples = 0;
   e->synced = false;
 }
@@ -1334,6 +1371,11 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
   bind(e);
   if (!(lr > 0.0)) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: learning rate must be positive");
   auto local = local_nodes(e, node_sizes, node_device, total_nodes, batch_rows);
+  if (total_nodes > (1u << kMaxPartialsLog2))
+    throw EngineError(VNT_ERR_CONFIG, "more than 2^21 virtual nodes: the exact int64 sum has no headroom");
+  // any sum of total_nodes partials below 2^lim_bits fits int64
+  e->lim_bits = std::min(kLimBits, 62 - ceil_log2(total_nodes));
+  e->loss_rows = std::ldexp(1.0, ceil_log2(batch_rows));
   reset_acc(e);
   e->launches = 0;
   uint32_t retries = 0;
@@ -1383,7 +1425,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       // A device-resident batch is copied by k_stage_rows inside the graph (its
       // pointers travel in the step parameters); host batches are staged here
       // or arrive through the prefetch.
-      const bool took = take_prefetch(e, x, y);
+      const bool took = take_prefetch(e, x, y, local);
       const bool stage_in_graph = !took && on_device;
       if (!took && !on_device) stage_inputs(e, p, x, y, false);
       e->h_sp->x = stage_in_graph ? x : nullptr;
@@ -1406,7 +1448,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       vnt_engine::GraphEntry*& slot = e->memo.ge[e->cur & 1][stage_in_graph ? 1 : 0];
       if (!slot) {
         std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur,
-                                    stage_in_graph ? 1 : 0};
+                                    stage_in_graph ? 1 : 0, (int64_t)total_nodes};
         for (const auto& n : local) {
           key.push_back(n.node);
           key.push_back(n.dev);
@@ -1487,15 +1529,18 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       reset_acc(e);
       throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
     }
-    if (!rb.overflow.empty()) {
+    if (!rb.overflow.empty() || rb.loss_range) {
       for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
+      if (rb.loss_range) e->loss_bits -= kLossRescale;
       ++retries;
       reset_acc(e);
       if (retries > 8) throw EngineError(VNT_ERR_RESCALE, "fixed-point range could not be found");
       continue;
     }
     update_scales(e, batch_rows);
-    if (loss) *loss = rb.loss_sum / (double)batch_rows;   // virtual_exec.cpp:275
+    const double mean_loss = rb.loss_sum / (double)batch_rows;   // virtual_exec.cpp:275
+    relax_loss_bits(e, mean_loss);
+    if (loss) *loss = mean_loss;
     e->timings_graphed = graphed;
     break;
   }
@@ -1621,10 +1666,27 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
         any_tc |= e->tc_layer[l] != 0;
         strips += (e->widths[l] + 1) * ceil_div(e->widths[l + 1], (uint64_t)vntb::kNodeOC);
       }
-      const uint64_t budget = 200 * 1024 / sizeof(float);
-      const uint64_t per_row = node_row_floats(e.get()), wt = node_wt_floats(e.get()) + 8;
-      e->node_rc_max = wt >= budget ? 0
-                                    : (int)std::min<uint64_t>(256, (budget - wt) / std::max<uint64_t>(per_row, 1));
+      // CTAs per node (VNT_NODE_CLUSTER, default 4) and the rows per smem chunk
+      // are fixed here, from the widths alone: the cluster size decides how a
+      // node's dW rows are split and summed, so it must never depend on which
+      // nodes share a pass.  The chunk bound leaves room for the
+      // DSMEM exchange area at the largest chunk.
+      const char* cl_env = getenv("VNT_NODE_CLUSTER");
+      const int cl_req = cl_env ? atoi(cl_env) : 4;
+      e->node_cl = (cl_req == 2 || cl_req == 4 || cl_req == 8) ? cl_req : 1;
+      const uint64_t smem_floats = 227 * 1024 / sizeof(float) - 64;
+      const uint64_t per_row = node_row_floats(e.get()), wt = node_wt_floats(e.get()) + 16;
+      auto rows_fit = [&](uint64_t exchange) -> int {
+        const uint64_t fixed = wt + exchange;
+        return fixed >= smem_floats
+                   ? 0
+                   : (int)std::min<uint64_t>(256, (smem_floats - fixed) / std::max<uint64_t>(per_row, 1));
+      };
+      e->node_rc_max = rows_fit(e->node_cl > 1 ? strips * vntb::kNodeOC : 0);
+      if (e->node_rc_max < 1 && e->node_cl > 1) {   // no room to exchange strips: one CTA per node
+        e->node_cl = 1;
+        e->node_rc_max = rows_fit(0);
+      }
       const bool off_env = getenv("VNT_NODE_KERNEL") && getenv("VNT_NODE_KERNEL")[0] == '0';
       e->node_path = !off_env && !any_tc && e->L <= vntb::kNodeMaxLayers &&
                      strips <= (uint64_t)vntb::kNodeMaxStrips && e->node_rc_max >= 1;
@@ -1845,7 +1907,13 @@ int vnt_engine_device_step(vnt_engine* e, int32_t device, const double* x, const
     // must share (partials in different units cannot be summed): across
     // processes it is the sum of the local estimates.
     uint64_t hint = off * std::max<uint64_t>(1, e->devs.size());
-    if (!e->round_open && !e->scales_init && e->comm) hint = global_count(e, hint);
+    if (!e->round_open) {
+      // Partials per round are counted and checked at sync (kTailPartials);
+      // the loss rows bound is 2^24 examples per round.
+      e->lim_bits = kLimBits;
+      e->loss_rows = std::ldexp(1.0, 24);
+      if (!e->scales_init && e->comm) hint = global_count(e, hint);
+    }
     begin_round(e, hint);
     accumulate(e, local, x, y, false, true);
     if (metrics) *metrics = m;
@@ -1858,11 +1926,24 @@ int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum, uint64_t
     bind(e);
     if (!e->acc_started) {
       // This process accumulated nothing: contribute zeros to the collective.
-      begin_round(e, 1);
+      // On the first round the ranks that ran device_step agreed on the
+      // initial scale with a count all-reduce; this rank takes part in it
+      // with a zero count, so every rank issues the same collectives.
+      uint64_t hint = 1;
+      if (!e->round_open) {
+        e->lim_bits = kLimBits;
+        e->loss_rows = std::ldexp(1.0, 24);
+        if (!e->scales_init && e->comm) hint = std::max<uint64_t>(1, global_count(e, 0));
+      }
+      begin_round(e, hint);
       VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
       e->acc_started = true;
     }
     add_examples_tail(e);
+    if (e->acc_partials) {
+      k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailPartials, (long long)e->acc_partials);
+      VNT_LAUNCH_CHECK();
+    }
     e->acc_examples = 0;
     e->tail_examples = 0;
     collective(e);
@@ -1871,8 +1952,14 @@ int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum, uint64_t
       reset_acc(e);
       throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
     }
-    if (!rb.overflow.empty()) {
+    if (rb.partials > (1ull << (62 - e->lim_bits))) {
+      reset_acc(e);
+      throw EngineError(VNT_ERR_CONFIG, "sync_gradients: " + std::to_string(rb.partials) +
+                                            " virtual-node partials exceed the exact int64 headroom");
+    }
+    if (!rb.overflow.empty() || rb.loss_range) {
       for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
+      if (rb.loss_range) e->loss_bits -= kLossRescale;
       restore_stats(e);
       reset_acc(e);
       throw EngineError(VNT_ERR_RESCALE, "fixed-point range exceeded; scale lowered, redo the step");
@@ -1915,8 +2002,9 @@ int vnt_engine_take_gradient_sum(vnt_engine* e, double* sum, double* loss_sum,
       reset_acc(e);
       throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
     }
-    if (!rb.overflow.empty()) {
+    if (!rb.overflow.empty() || rb.loss_range) {
       for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
+      if (rb.loss_range) e->loss_bits -= kLossRescale;
       restore_stats(e);
       reset_acc(e);
       throw EngineError(VNT_ERR_RESCALE, "fixed-point range exceeded; scale lowered, redo the step");

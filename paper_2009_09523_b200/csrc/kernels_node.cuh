@@ -72,7 +72,8 @@ __global__ void k_node_pad(const float* __restrict__ W, float* __restrict__ wpad
 
 // Row loss + output delta of one row (k_loss's arithmetic), one warp.
 __device__ __forceinline__ void node_row_loss(const float* z, const double* yr, int outw,
-                                              int loss_kind, float* d, long long* tail) {
+                                              int loss_kind, float* d, long long* tail,
+                                              const StepParams* sp) {
   const int lane = threadIdx.x & 31;
   double loss = 0.0;
   if (loss_kind == 0) {
@@ -102,14 +103,9 @@ __device__ __forceinline__ void node_row_loss(const float* z, const double* yr, 
 #pragma unroll
     for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
   }
-  if (lane == 0) {
-    if (!isfinite(loss)) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
-    } else {
-      const long long q = __double2ll_rn(ldexp(loss, kLossScaleBits));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailLoss]), (unsigned long long)q);
-    }
-  }
+  long long q;
+  if (lane == 0 && row_loss_q(loss, sp, tail, q))
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailLoss]), (unsigned long long)q);
 }
 
 // dW/db strip s -> (layer l, input row i (== w[l]: the bias), first output o0).
@@ -267,7 +263,7 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
     // loss + output delta, one warp per row
     for (int r = warp; r < rn; r += nwarps)
       node_row_loss(sm + aoff[L] + r * outw, a.y + (size_t)(r0 + c0 + r) * outw, outw, a.loss,
-                    sm + doff[L] + r * node_ld(outw), a.tail);
+                    sm + doff[L] + r * node_ld(outw), a.tail, a.sp);
     __syncthreads();
     // backward (model.cpp:328-337): d[l][r][i] = (sum_o d[l+1][r][o] W[i][o]) f'(a[l][r][i]),
     // o ascending; lanes over i read W^T rows (coalesced).

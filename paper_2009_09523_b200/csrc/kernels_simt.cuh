@@ -22,7 +22,13 @@ __device__ __forceinline__ float tf32_rna(float x) {
 }
 
 // Tail slots of the int64 accumulator (all summed exactly by the collective).
-enum : int { kTailLoss = 0, kTailExamples = 1, kTailNonfinite = 2, kTailOverflow = 3 };
+// kTailLossRange counts rows whose quantised loss could overflow the int64 sum
+// (the step is redone at a coarser loss quantum); kTailPartials counts the
+// per-node partials of a device_step round (int64 headroom check at sync).
+enum : int {
+  kTailLoss = 0, kTailExamples = 1, kTailNonfinite = 2, kTailLossRange = 3, kTailPartials = 4,
+  kTailOverflow = 5
+};
 
 // Per-step values the kernels read from device memory (one small H2D copy per
 // step), so the launch sequence of a step is static and can be replayed as a
@@ -33,6 +39,8 @@ struct StepParams {
   float dts[kMaxLayers + 1];         // DT[l] copy scale (2^s of the dW consuming it, or 1)
   double inv_scale[2 * kMaxLayers];  // 2^-s_t
   double lr, mu, inv_b;
+  double loss_scale;                 // 2^b: per-row loss quantum 2^-b
+  double loss_lim;                   // |row loss| * 2^b must stay below this (2^62 / rows bound)
   const double* x;                   // this step's device-resident batch (k_stage_rows)
   const double* y;
 };
@@ -345,13 +353,32 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
   }
 }
 
+// One row's loss into the exact int64 loss sum: q = rint(loss * 2^b).  Rows
+// outside the range that keeps any sum of the step's rows in int64 are
+// counted (kTailLossRange) instead, and the host redoes the step with a
+// coarser quantum; non-finite rows are counted as such.
+__device__ __forceinline__ bool row_loss_q(double loss, const StepParams* sp, long long* tail,
+                                           long long& q) {
+  if (!isfinite(loss)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
+    return false;
+  }
+  const double v = loss * sp->loss_scale;
+  if (!(fabs(v) < sp->loss_lim)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailLossRange]), 1ull);
+    return false;
+  }
+  q = __double2ll_rn(v);
+  return true;
+}
+
 // ------------------------------------------------------------- loss/delta
 // model.cpp:289-315, one warp per row, fp64 from fp32 logits.  Row loss is
 // quantised at 2^-32 and summed exactly (int64 atomics: order-free).
 __global__ void k_loss(const float* __restrict__ logits, const double* __restrict__ y, int rows,
                        int outw, int loss_kind, float* __restrict__ D, float* __restrict__ DT,
                        int ldT, const int* __restrict__ tcol, long long* __restrict__ tail,
-                       const float* __restrict__ tscale_p) {
+                       const float* __restrict__ tscale_p, const StepParams* __restrict__ sp) {
   const float tscale = tscale_p ? *tscale_p : 1.f;
   __shared__ unsigned long long block_loss;   // exact int64 sum of this block's rows
   if (threadIdx.x == 0) block_loss = 0;
@@ -395,14 +422,9 @@ __global__ void k_loss(const float* __restrict__ logits, const double* __restric
 #pragma unroll
       for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
     }
-    if (lane == 0) {
-      if (!isfinite(loss)) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&tail[kTailNonfinite]), 1ull);
-      } else {
-        const long long q = __double2ll_rn(ldexp(loss, kLossScaleBits));
-        atomicAdd(&block_loss, (unsigned long long)q);   // shared memory, order-free
-      }
-    }
+    long long q;
+    if (lane == 0 && row_loss_q(loss, sp, tail, q))
+      atomicAdd(&block_loss, (unsigned long long)q);   // shared memory, order-free
   }
   __syncthreads();
   if (threadIdx.x == 0 && block_loss)
@@ -744,7 +766,7 @@ struct SgdArgs {
 __device__ __forceinline__ bool block_poisoned(const long long* tail, int nflags) {
   const int t = threadIdx.x + threadIdx.y * blockDim.x;
   bool bad = false;
-  if (t == 0) bad = tail[kTailNonfinite] != 0;
+  if (t == 0) bad = tail[kTailNonfinite] != 0 || tail[kTailLossRange] != 0;
   else if (t <= nflags) bad = tail[kTailOverflow + t - 1] != 0;
   return __syncthreads_or(bad);
 }
