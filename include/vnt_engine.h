@@ -64,6 +64,33 @@ extern "C" {
 
 typedef struct vnt_engine vnt_engine;
 
+/* Host-callback process group (emulation / testing backend).  The product
+ * path is NCCL (vnt_engine_options::nccl_id); with comm_ops set instead, every
+ * collective of the engine is carried out by these callbacks on pinned HOST
+ * buffers after the engine synchronised its stream — e.g. several processes or
+ * threads sharing one GPU, exchanging through gloo or shared memory.  Every
+ * callback returns 0 on success; all members call collectives in the same
+ * order (as NCCL requires). */
+#define VNT_COMM_SUM_I64 0   /* allreduce op: int64 sum                    */
+#define VNT_COMM_MAX_U64 1   /* allreduce op: uint64 max                   */
+typedef struct vnt_comm_ops {
+  void* ctx;
+  int32_t rank;
+  int32_t size;
+  int (*allreduce)(void* ctx, void* buf, uint64_t count, int32_t op);
+  /* recv[recv_count] = this rank's block of the int64 sum of send[size * recv_count] */
+  int (*reduce_scatter)(void* ctx, const void* send, void* recv, uint64_t recv_count);
+  /* recv[size * bytes] = concatenation over ranks of send[bytes] */
+  int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes);
+  int (*broadcast)(void* ctx, void* buf, uint64_t bytes, int32_t root);
+  int (*send)(void* ctx, const void* buf, uint64_t bytes, int32_t peer);
+  int (*recv)(void* ctx, void* buf, uint64_t bytes, int32_t peer);
+  /* Collective: members with color >= 0 form a sub-group ranked by key; fills
+   * *out (out->ctx = NULL for non-members). */
+  int (*split)(void* ctx, int32_t color, int32_t key, struct vnt_comm_ops* out);
+  void (*release)(void* ctx);  /* nullable: called when the engine drops the group */
+} vnt_comm_ops;
+
 typedef struct vnt_model_desc {
   const uint64_t* layer_widths; /* ModelSpec::layer_widths (model.hpp:27-37) */
   uint32_t num_widths;
@@ -79,6 +106,7 @@ typedef struct vnt_engine_options {
   int32_t gemm_mode;       /* VNT_GEMM_*                                           */
   double momentum;         /* 0: plain SGD exactly as the reference                */
   uint64_t resident_rows;  /* rows kept resident per pass on the GPU (0: all)      */
+  const vnt_comm_ops* comm_ops; /* host-callback group instead of NCCL (NULL: NCCL) */
 } vnt_engine_options;
 
 typedef struct vnt_device_metrics { /* DeviceStepMetrics, virtual_exec.hpp:72-78 */
@@ -198,15 +226,27 @@ uint32_t vnt_engine_tensor_count(const vnt_engine* e);
 int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const uint8_t* nccl_id,
                        int32_t source_rank);
 
+/* Same with a host-callback group (vnt_comm_ops) as the new process group. */
+int vnt_engine_regroup_ops(vnt_engine* e, const vnt_comm_ops* ops, int32_t source_rank);
+/* Elastic resize within the job's process pool (the group the engine was
+ * created with): collective over the pool.  Processes passing member != 0
+ * form the group that trains from now on (ranked by pool rank); the others
+ * stay idle until a later call makes them members again.  Every process
+ * receives the replica state — fp64 parameters, momentum, scale history —
+ * from pool rank source_pool_rank (a member of the previous training group). */
+int vnt_engine_set_membership(vnt_engine* e, int32_t member, int32_t source_pool_rank);
+
 /* Forget the scale history: the next step uses the deterministic initial scale
  * 40 - ceil(log2 B) (stateless callers, e.g. vnt::train_step on a World). */
 int vnt_engine_reset_scales(vnt_engine* e);
 
 int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out);
-/* Diagnostics: the gradient all-reduces issued since the last call, as
- * (offset into the gradient buffer, element count) pairs in issue order (up to
- * cap pairs copied, *count = pairs logged).  Every rank of a group must issue
- * the identical sequence; clears the log. */
+/* Diagnostics: the collectives issued since the last call, as (op, offset,
+ * count) triples in issue order (up to cap triples copied, *count = triples
+ * logged).  op: 1 all-reduce (int64 sum), 2 reduce-scatter, 3 all-gather,
+ * 4 max all-reduce, 5 count agreement, 6 replica broadcast, 7 send, 8 recv;
+ * offset = position in the parameter layout (gradient buffer words).  Every
+ * rank of a group must issue the identical sequence; clears the log. */
 int vnt_engine_comm_log(vnt_engine* e, uint64_t* out, uint32_t cap, uint32_t* count);
 /* The CUDA stream the engine launches on (cudaStream_t as void*). */
 void* vnt_engine_stream(vnt_engine* e);

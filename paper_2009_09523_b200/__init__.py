@@ -43,7 +43,8 @@ class _ModelDesc(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("cuda_device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("nccl_id", C.POINTER(C.c_uint8)), ("gemm_mode", C.c_int32),
-                ("momentum", C.c_double), ("resident_rows", C.c_uint64)]
+                ("momentum", C.c_double), ("resident_rows", C.c_uint64),
+                ("comm_ops", C.c_void_p)]
 
 
 class DeviceMetrics(C.Structure):
@@ -111,6 +112,8 @@ def load_engine() -> C.CDLL:
         "vnt_engine_last_timings": (C.c_int, [_vp, C.POINTER(StepTimings)]),
         "vnt_engine_reset_scales": (C.c_int, [_vp]),
         "vnt_engine_comm_log": (C.c_int, [_vp, _u64p, C.c_uint32, C.POINTER(C.c_uint32)]),
+        "vnt_engine_regroup_ops": (C.c_int, [_vp, _vp, C.c_int32]),
+        "vnt_engine_set_membership": (C.c_int, [_vp, C.c_int32, C.c_int32]),
         "vnt_engine_prefetch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _u64p, _i32p, C.c_uint32,
                                           C.c_int32]),
         "vnt_engine_regroup": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32]),
@@ -161,7 +164,9 @@ class Engine:
 
     def __init__(self, widths, activation="tanh", loss="mse", cuda_device=0, rank=0,
                  world_size=1, nccl_id: bytes | None = None, gemm_mode="auto",
-                 momentum=0.0, resident_rows=0):
+                 momentum=0.0, resident_rows=0, comm=None):
+        """comm: a hostcomm.GlooGroup (host-callback process group, several
+        processes on one GPU) instead of NCCL (rank / world_size / nccl_id)."""
         lib = load_engine()
         self.lib = lib
         self.widths = [int(w) for w in widths]
@@ -170,9 +175,11 @@ class Engine:
         self._nid = None
         if nccl_id is not None:
             self._nid = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self._comm = comm   # keeps the callbacks alive
         opt = _Options(cuda_device, rank, world_size,
                        C.cast(self._nid, C.POINTER(C.c_uint8)) if self._nid else None,
-                       GEMM_MODES[gemm_mode], momentum, resident_rows)
+                       GEMM_MODES[gemm_mode], momentum, resident_rows,
+                       C.cast(C.pointer(comm.ops), C.c_void_p) if comm is not None else None)
         h = _vp()
         _check(lib.vnt_engine_create(C.byref(desc), C.byref(opt), C.byref(h)))
         self.h = h
@@ -224,13 +231,17 @@ class Engine:
                                         C.byref(ex)))
         return g, ls.value, ex.value
 
-    def comm_log(self, cap=2048):
-        """(offset, count) of each gradient all-reduce issued since the last call
-        (vnt_engine_comm_log; clears the log)."""
-        out = np.zeros(2 * cap, np.uint64)
+    COMM_OPS = {1: "allreduce", 2: "reduce_scatter", 3: "allgather", 4: "max", 5: "count",
+                6: "broadcast", 7: "send", 8: "recv"}
+
+    def comm_log(self, cap=4096):
+        """(op, offset, count) of each collective issued since the last call
+        (vnt_engine_comm_log; clears the log); op named as in COMM_OPS."""
+        out = np.zeros(3 * cap, np.uint64)
         n = C.c_uint32()
         _check(self.lib.vnt_engine_comm_log(self.h, out.ctypes.data_as(_u64p), cap, C.byref(n)))
-        return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(min(n.value, cap))]
+        return [(self.COMM_OPS.get(int(out[3 * i]), "?"), int(out[3 * i + 1]), int(out[3 * i + 2]))
+                for i in range(min(n.value, cap))]
 
     def take_gradient_sum(self):
         """Process-local exact gradient sum (no collective), closes the round:
@@ -324,6 +335,17 @@ class Engine:
         _check(self.lib.vnt_engine_regroup(self.h, rank, world_size,
                                            C.cast(nid, C.POINTER(C.c_uint8)) if nid else None,
                                            source_rank))
+
+    def regroup_ops(self, comm, source_rank: int = 0):
+        """Join a host-callback group (hostcomm.GlooGroup) and take the replica
+        state from its source_rank."""
+        self._comm_new = comm
+        _check(self.lib.vnt_engine_regroup_ops(self.h, C.cast(C.pointer(comm.ops), _vp),
+                                               source_rank))
+
+    def set_membership(self, member: bool, source_pool_rank: int = 0):
+        """Elastic resize inside the process pool (collective over the pool)."""
+        _check(self.lib.vnt_engine_set_membership(self.h, 1 if member else 0, source_pool_rank))
 
     def timings(self) -> dict:
         t = StepTimings()

@@ -31,6 +31,8 @@
 #include "common.cuh"
 #include "kernels_simt.cuh"
 #include "kernels_node.cuh"
+#include "kernels_shard.cuh"
+#include "comm.cuh"
 
 using namespace vntb;
 
@@ -44,6 +46,7 @@ int set_error(int code, const std::string& msg) {
 }
 
 constexpr int kScaleTargetBits = 40;   // |sum| of the largest element ~ 2^40 after scaling
+constexpr int kMaxRanks = 64;          // ranks of a sharded group (reduce-scatter overhang bound)
 constexpr int kLimBits = 50;           // per-node partial bound for up to 2^12 partials
 constexpr int kMaxPartialsLog2 = 21;   // beyond 2^21 partials the bound drops under the scale target
 constexpr int kLossRescale = 16;       // loss quantum step on a loss-range redo
@@ -76,7 +79,13 @@ struct vnt_engine {
   std::vector<uint64_t> woff, boff, wtoff;
   std::vector<int> tc_layer;   // 1: layer runs on tcgen05 tiles
   vnt_engine_options opt{};
-  ncclComm_t comm = nullptr;
+  // Process groups: `pool` spans every process the job started (resize
+  // migration runs over it); `comm` is the group that trains — the pool
+  // itself, or a split of it after a resize left some processes idle — and
+  // is null for a single process without a group.
+  std::unique_ptr<vntb::CommGroup> pool;
+  std::unique_ptr<vntb::CommGroup> active;   // owned split of the pool (when not the pool)
+  vntb::CommGroup* comm = nullptr;
   // Per-layer gradient all-reduce overlapped with the rest of the backward:
   // layer l's slice of G is reduced on comm_stream as soon as its dW/db are
   // final, while the compute stream continues (VNT_COMM_OVERLAP=0 disables).
@@ -85,7 +94,22 @@ struct vnt_engine {
   std::vector<cudaEvent_t> layer_ev;   // per layer: its dW/db done (compute stream)
   cudaEvent_t comm_ev = nullptr;       // comm_stream caught up
   int gemm_sms = 0;                    // CTAs the backward GEMMs may occupy
-  std::vector<uint64_t> comm_log;      // (G offset, count) of every gradient all-reduce
+  std::vector<uint64_t> comm_log;      // (op, G offset, count) of every collective of a step
+  // Sharded update (comm && layered path): layer l's gradient
+  // slice is reduce-scattered into Gs, this rank updates its 1/G of the
+  // parameters, and the new fp32 weights are all-gathered (deferred to the
+  // next step's forward, layer by layer) and expanded into W / Wᵀ / twins.
+  bool shard = false;
+  std::vector<uint64_t> sh_c, sh_lo, sh_hi, sh_soff, sh_aoff;   // per layer
+  long long* Gs = nullptr;        // reduced chunks, sum_l c_l
+  float* ag_send = nullptr;       // this rank's new fp32 weights, sum_l c_l
+  float* ag_recv = nullptr;       // gathered slices, sum_l G c_l
+  bool master_valid = true;       // w64 / v64 hold every element (not only this rank's)
+  bool ag_pending = false;        // ag_send holds weights not yet gathered
+  std::vector<char> ag_wait;      // per layer: gathered, not yet expanded
+  std::vector<cudaEvent_t> ag_ev; // per layer: its all-gather done (comm stream)
+  cudaEvent_t ag_fork = nullptr;
+  long long* d_word = nullptr;    // 8 scratch words (count agreement)
   cudaStream_t stream = nullptr;
   int sm_count = 0;
 
@@ -94,7 +118,9 @@ struct vnt_engine {
   double* v64 = nullptr;
   float* w32 = nullptr;
   float* wt32 = nullptr;
-  long long* G = nullptr;   // P + ntail
+  long long* G = nullptr;   // P, a zero gap (reduce-scatter overhang), then the tail
+  long long* tail = nullptr;   // G + tail_off: loss, examples, flags, then max|g| per tensor
+  uint64_t tail_off = 0;
   size_t ntail = 0;
   unsigned long long* gmax = nullptr;
   double* gout = nullptr;
@@ -206,7 +232,7 @@ struct vnt_engine {
     std::vector<int32_t> devs;
     uint64_t rows = 0;
     bool valid = false;
-    GraphEntry* ge[2][2] = {};
+    GraphEntry* ge[2][2][2] = {};
   } memo;
 
   vnt_step_timings timings{};
@@ -287,8 +313,9 @@ void drop_graphs(vnt_engine* e) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   e->graph_cache.clear();
   e->memo.valid = false;
-  for (auto& row : e->memo.ge)
-    for (auto& g : row) g = nullptr;
+  for (auto& plane : e->memo.ge)
+    for (auto& row : plane)
+      for (auto& g : row) g = nullptr;
 }
 
 // Stage this step's kernel parameters (scales, 1/B, lr, momentum) for the device.
@@ -458,7 +485,7 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
 
 // Tail and the per-tensor max|g| words sit back to back after G: one memset, one readback.
 void tail_reset(vnt_engine* e) {
-  VNT_CUDA(cudaMemsetAsync(e->G + e->P, 0, (e->ntail + ntensors(e)) * sizeof(long long), e->stream));
+  VNT_CUDA(cudaMemsetAsync(e->tail, 0, (e->ntail + ntensors(e)) * sizeof(long long), e->stream));
 }
 
 void split_into(vnt_engine* e, const float* x, float* hi, float* lo, size_t n) {
@@ -697,6 +724,8 @@ void combine_stats(vnt_engine* e, const std::vector<StatsLaunch>& stats, cudaStr
 void backup_stats(vnt_engine* e, cudaStream_t s);
 void layer_collective(vnt_engine* e, int l);
 void join_stats(vnt_engine* e);
+void issue_pending_gathers(vnt_engine* e);
+void await_layer_weights(vnt_engine* e, int l);
 
 // Input statistics of a pass depend on x only: observe_batch per node then the
 // Chan combine into each device lineage in ascending node id
@@ -738,7 +767,7 @@ void step_prologue(vnt_engine* e, const Pass& p, bool stage) {
   const unsigned slices = stage ? (unsigned)std::min<uint64_t>(
       64, ceil_div(maxrows * (e->widths[0] + e->widths[e->L]) * sizeof(double), 16384)) : 4;
   k_step_prologue<<<dim3(stage ? (unsigned)nn : 16u, slices), 256, 0, e->stream>>>(
-      e->m_sp, e->d_sp, e->G, e->P + e->ntail + ntensors(e), stage ? 1 : 0, e->xin, e->yin, row0,
+      e->m_sp, e->d_sp, e->G, e->tail_off + e->ntail + ntensors(e), stage ? 1 : 0, e->xin, e->yin, row0,
       row0 + nn, row0 + 3 * nn, (int)e->widths[0], (int)e->widths[e->L]);
   VNT_LAUNCH_CHECK();
   e->launches++;
@@ -790,7 +819,7 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   a.sp = e->d_sp;
   a.lim = pow2f(e->lim_bits);
   a.G = e->G;
-  a.tail = e->G + e->P;
+  a.tail = e->tail;
   a.examples = (long long)p.rows;
   const size_t base = ((size_t)a.rc * node_row_floats(e) + node_wt_floats(e) + 8 + 3) & ~(size_t)3;
   a.part_off = (int)base;
@@ -886,6 +915,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
   for (int l = 0; l < L; ++l) {
     const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
     const bool last = (l == L - 1);
+    await_layer_weights(e, l);   // sharded update: this layer's gathered weights
     const float* W = e->w32 + e->woff[l];
     const float* b = e->w32 + e->boff[l];
     prof_begin(e);
@@ -926,7 +956,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
   {
     const unsigned warps_per_block = 8;
     k_loss<<<(unsigned)ceil_div(p.rows, warps_per_block), warps_per_block * 32, 0, s>>>(
-        e->logits, e->yin, rows, (int)out, e->loss, e->D[L], e->DT[L], ldT, tcol, e->G + e->P,
+        e->logits, e->yin, rows, (int)out, e->loss, e->D[L], e->DT[L], ldT, tcol, e->tail,
         dts(L), e->d_sp);
     VNT_LAUNCH_CHECK();
     e->launches++;
@@ -943,13 +973,13 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       tc_weight_grad(e, l, p, col0, nrows, 1.f, lim, first_write, tw);
     } else if (out_l <= 32) {
       dispatch_skinny<DwSkinny>(out_l, s, e->X[l], in_l, e->D[l + 1], out_l, row0, nrows, (int)nn,
-                                sp_scale(e, tw), lim, e->G + e->woff[l], e->G + e->P, tw);
+                                sp_scale(e, tw), lim, e->G + e->woff[l], e->tail, tw);
       VNT_LAUNCH_CHECK();
       e->launches++;
     } else {
       dim3 grid((unsigned)ceil_div(out_l, 64), (unsigned)ceil_div(in_l, 64), (unsigned)nn);
       k_dw_ffma<<<grid, 256, 0, s>>>(e->XT[l], e->DT[l + 1], ldT, in_l, out_l, col0, nrows,
-                                     sp_scale(e, tw), lim, e->G + e->woff[l], e->G + e->P, tw);
+                                     sp_scale(e, tw), lim, e->G + e->woff[l], e->tail, tw);
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
@@ -957,7 +987,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     {
       dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
       k_db<<<grid, 128, 0, s>>>(e->D[l + 1], out_l, row0, nrows, sp_scale(e, tb), lim,
-                                e->G + e->boff[l], e->G + e->P, tb);
+                                e->G + e->boff[l], e->tail, tb);
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
@@ -1034,16 +1064,25 @@ void backup_stats(vnt_engine* e, cudaStream_t s) {
   e->stats_backed = true;
 }
 
+// Collective log (vnt_engine_comm_log): every rank of a group must issue the
+// identical sequence, so tests compare these across rank layouts.
+enum : uint64_t {
+  kLogAllReduce = 1, kLogReduceScatter = 2, kLogAllGather = 3, kLogMax = 4, kLogCount = 5,
+  kLogBroadcast = 6, kLogSend = 7, kLogRecv = 8
+};
+void log_comm(vnt_engine* e, uint64_t op, uint64_t off, uint64_t n) {
+  e->comm_log.insert(e->comm_log.end(), {op, off, n});
+  if (e->comm_log.size() > 6144) e->comm_log.erase(e->comm_log.begin(), e->comm_log.begin() + 3072);
+}
+
 // Sum of a host count over the process group (blocking; first round only).
 uint64_t global_count(vnt_engine* e, uint64_t local) {
-  long long* d = (long long*)dalloc(sizeof(long long));
   long long v = (long long)local;
-  VNT_CUDA(cudaMemcpyAsync(d, &v, sizeof v, cudaMemcpyHostToDevice, e->stream));
-  const ncclResult_t r = ncclAllReduce(d, d, 1, ncclInt64, ncclSum, e->comm, e->stream);
-  if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
-  VNT_CUDA(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, e->stream));
+  VNT_CUDA(cudaMemcpyAsync(e->d_word, &v, sizeof v, cudaMemcpyHostToDevice, e->stream));
+  e->comm->allreduce_sum_i64(e->d_word, 1, e->stream);
+  log_comm(e, kLogCount, 0, 1);
+  VNT_CUDA(cudaMemcpyAsync(&v, e->d_word, sizeof v, cudaMemcpyDeviceToHost, e->stream));
   VNT_CUDA(cudaStreamSynchronize(e->stream));
-  cudaFree(d);
   return (uint64_t)v;
 }
 
@@ -1067,6 +1106,7 @@ void restore_stats(vnt_engine* e) {
 
 void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, const double* y,
                 bool on_device, bool do_stats, bool layer_comm = false) {
+  issue_pending_gathers(e);   // weights of the last sharded update, awaited per layer
   auto& passes = plan_for(e, local);
   std::vector<std::vector<StatsLaunch>> stats(passes.size());
   if (do_stats) {
@@ -1096,48 +1136,120 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
   }
 }
 
-constexpr int kCommSms = 16;   // SMs left to NCCL while the backward GEMMs run
+constexpr int kCommSms = 16;   // SMs left to NCCL while GEMMs run beside its kernels
 
 bool overlap_wanted() {
   return !(getenv("VNT_COMM_OVERLAP") && getenv("VNT_COMM_OVERLAP")[0] == '0');
 }
 
-// NCCL group of (opt.rank, opt.world_size); with overlap its kernels are capped
-// at kCommSms CTAs so they fit beside the backward GEMMs.
-void comm_init(vnt_engine* e, const ncclUniqueId& id) {
-  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-  if (overlap_wanted()) cfg.maxCTAs = kCommSms;
-  const ncclResult_t r = ncclCommInitRankConfig(&e->comm, e->opt.world_size, id, e->opt.rank, &cfg);
-  if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+bool shard_wanted() { return !(getenv("VNT_SHARD") && getenv("VNT_SHARD")[0] == '0'); }
+
+void free_shards(vnt_engine* e) {
+  for (void* p : {(void*)e->Gs, (void*)e->ag_send, (void*)e->ag_recv})
+    if (p) cudaFree(p);
+  e->Gs = nullptr;
+  e->ag_send = nullptr;
+  e->ag_recv = nullptr;
+  e->shard = false;
+  e->ag_pending = false;
+  e->ag_wait.assign(e->L, 0);
 }
 
-// With an NCCL group, overlap the per-layer reductions with the backward; the
-// backward GEMMs then leave kCommSms SMs to the NCCL kernels beside them.
-void setup_comm_overlap(vnt_engine* e) {
-  e->gemm_sms = e->sm_count;
-  e->comm_overlap = e->comm && overlap_wanted();
-  if (!e->comm_overlap) return;
-  if (!e->comm_stream) {   // idempotent (regroup calls it again)
-    VNT_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
-    e->layer_ev.assign(e->L, nullptr);
-    for (auto& ev : e->layer_ev) VNT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    VNT_CUDA(cudaEventCreateWithFlags(&e->comm_ev, cudaEventDisableTiming));
+// This rank's fp32 chunk of every layer slice, from the current fp64 master
+// (what the next all-gather sends when no update has happened since).
+void refill_ag_send(vnt_engine* e) {
+  for (int l = 0; l < e->L; ++l) {
+    const long long n = (long long)(e->sh_hi[l] - e->sh_lo[l]);
+    if (n <= 0) continue;
+    k_f64_to_f32<<<(unsigned)std::min<long long>(ceil_div((uint64_t)n, 256), 1024), 256, 0, e->stream>>>(
+        e->w64 + e->woff[l] + e->sh_lo[l], e->ag_send + e->sh_soff[l], n);
+    VNT_LAUNCH_CHECK();
   }
-  e->gemm_sms = std::max(2, (e->sm_count - kCommSms) & ~1);   // even: CTA pairs
+}
+
+// Shard layout of the current group: layer slice n_l = in*out + out, chunk
+// c_l = ceil(n_l / G) rounded up to 32 words, rank r owns [r c_l, (r+1) c_l).
+void setup_shards(vnt_engine* e) {
+  free_shards(e);
+  if (!e->comm || e->node_path || !shard_wanted()) return;
+  const uint64_t S = (uint64_t)e->comm->size(), r = (uint64_t)e->comm->rank();
+  if (S > (uint64_t)kMaxRanks) throw EngineError(VNT_ERR_CONFIG, "sharded update supports up to 64 ranks");
+  e->sh_c.assign(e->L, 0);
+  e->sh_lo.assign(e->L, 0);
+  e->sh_hi.assign(e->L, 0);
+  e->sh_soff.assign(e->L, 0);
+  e->sh_aoff.assign(e->L, 0);
+  uint64_t soff = 0, aoff = 0;
+  for (int l = 0; l < e->L; ++l) {
+    const uint64_t n = e->widths[l] * e->widths[l + 1] + e->widths[l + 1];
+    const uint64_t c = round_up(ceil_div(n, S), 32);
+    e->sh_c[l] = c;
+    e->sh_lo[l] = std::min(r * c, n);
+    e->sh_hi[l] = std::min((r + 1) * c, n);
+    e->sh_soff[l] = soff;
+    e->sh_aoff[l] = aoff;
+    soff += c;
+    aoff += S * c;
+  }
+  e->Gs = (long long*)dalloc(soff * sizeof(long long));
+  e->ag_send = (float*)dalloc(soff * sizeof(float));
+  VNT_CUDA(cudaMemset(e->ag_send, 0, soff * sizeof(float)));
+  e->ag_recv = (float*)dalloc(aoff * sizeof(float));
+  if (e->ag_ev.empty()) {
+    e->ag_ev.assign(e->L, nullptr);
+    for (auto& ev : e->ag_ev) VNT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    VNT_CUDA(cudaEventCreateWithFlags(&e->ag_fork, cudaEventDisableTiming));
+  }
+  e->shard = true;
+  refill_ag_send(e);
+}
+
+// With a stream-ordered group (NCCL), overlap the per-layer reductions with
+// the backward (and the deferred weight gathers with the forward) on a comm
+// stream; GEMMs then leave kCommSms SMs to the NCCL kernels beside them.
+// Host-callback groups run every collective in line.
+void setup_comm(vnt_engine* e) {
+  drop_graphs(e);
+  e->gemm_sms = e->sm_count;
+  e->comm_overlap = e->comm && e->comm->on_stream() && overlap_wanted();
+  if (e->comm_overlap) {
+    if (!e->comm_stream) {   // idempotent (regroup calls it again)
+      VNT_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
+      e->layer_ev.assign(e->L, nullptr);
+      for (auto& ev : e->layer_ev) VNT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      VNT_CUDA(cudaEventCreateWithFlags(&e->comm_ev, cudaEventDisableTiming));
+    }
+    e->gemm_sms = std::max(2, (e->sm_count - kCommSms) & ~1);   // even: CTA pairs
+  }
+  setup_shards(e);
 }
 
 void allreduce(vnt_engine* e, long long* p, size_t n, cudaStream_t s) {
-  e->comm_log.push_back((uint64_t)(p - e->G));   // every rank must log the same sequence
-  e->comm_log.push_back((uint64_t)n);
-  if (e->comm_log.size() > 4096) e->comm_log.erase(e->comm_log.begin(), e->comm_log.begin() + 2048);
-  const ncclResult_t r = ncclAllReduce(p, p, n, ncclInt64, ncclSum, e->comm, s);
-  if (r != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(r));
+  log_comm(e, kLogAllReduce, (uint64_t)(p - e->G), (uint64_t)n);
+  e->comm->allreduce_sum_i64(p, n, s);
 }
 
-void collective(vnt_engine* e) {
-  // Exact int64 sum over processes; associative, so any NCCL algorithm or
-  // topology gives the same bits.
-  if (e->comm) allreduce(e, e->G, e->P + e->ntail, e->stream);
+// Layer l's slice of G -> this rank's reduced chunk in Gs.  The send range
+// G * c_l may run past the slice (into the next layer's final sums or the
+// zero gap before the tail); those words land beyond n_l and are ignored.
+void reduce_scatter_layer(vnt_engine* e, int l, cudaStream_t s) {
+  log_comm(e, kLogReduceScatter, e->woff[l], e->sh_c[l]);
+  e->comm->reduce_scatter_sum_i64(e->G + e->woff[l], e->Gs + e->sh_soff[l], e->sh_c[l], s);
+}
+
+// The step's gradient reduction, in line on the compute stream: per layer
+// (reduce-scatter, sharded update) then the tail, or one all-reduce of G.
+// `full`: the whole mean gradient is wanted on every rank (sync_gradients).
+void collective(vnt_engine* e, bool full = false) {
+  if (!e->comm) return;
+  if (e->shard && !full) {
+    for (int l = e->L - 1; l >= 0; --l) reduce_scatter_layer(e, l, e->stream);
+    allreduce(e, e->tail, e->ntail, e->stream);
+    return;
+  }
+  // Exact int64 sum over processes; associative, so any algorithm or topology
+  // gives the same bits.
+  allreduce(e, e->G, e->tail_off + e->ntail, e->stream);
 }
 
 // Overlapped variant, issued identically (same calls, same order) on every
@@ -1146,6 +1258,10 @@ void collective(vnt_engine* e) {
 void layer_collective(vnt_engine* e, int l) {
   VNT_CUDA(cudaEventRecord(e->layer_ev[l], e->stream));
   VNT_CUDA(cudaStreamWaitEvent(e->comm_stream, e->layer_ev[l], 0));
+  if (e->shard) {
+    reduce_scatter_layer(e, l, e->comm_stream);
+    return;
+  }
   const uint64_t n = e->widths[l] * e->widths[l + 1] + e->widths[l + 1];   // W then b, contiguous
   allreduce(e, e->G + e->woff[l], n, e->comm_stream);
 }
@@ -1154,13 +1270,137 @@ void layer_collective(vnt_engine* e, int l) {
 void finish_layer_collectives(vnt_engine* e) {
   VNT_CUDA(cudaEventRecord(e->layer_ev[0], e->stream));
   VNT_CUDA(cudaStreamWaitEvent(e->comm_stream, e->layer_ev[0], 0));
-  allreduce(e, e->G + e->P, e->ntail, e->comm_stream);
+  allreduce(e, e->tail, e->ntail, e->comm_stream);
   VNT_CUDA(cudaEventRecord(e->comm_ev, e->comm_stream));
   VNT_CUDA(cudaStreamWaitEvent(e->stream, e->comm_ev, 0));
 }
 
+// Start the all-gathers of the weights the last sharded update produced
+// (layer 0 first, so the forward can begin while the rest arrive).
+void issue_pending_gathers(vnt_engine* e) {
+  if (!e->shard || !e->ag_pending) return;
+  cudaStream_t cs = e->comm_overlap ? e->comm_stream : e->stream;
+  if (e->comm_overlap) {   // ag_send was written on the compute stream
+    VNT_CUDA(cudaEventRecord(e->ag_fork, e->stream));
+    VNT_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ag_fork, 0));
+  }
+  for (int l = 0; l < e->L; ++l) {
+    log_comm(e, kLogAllGather, e->woff[l], e->sh_c[l]);
+    e->comm->allgather(e->ag_send + e->sh_soff[l], e->ag_recv + e->sh_aoff[l], e->sh_c[l] * sizeof(float), cs);
+    if (e->comm_overlap) VNT_CUDA(cudaEventRecord(e->ag_ev[l], cs));
+  }
+  e->ag_wait.assign(e->L, 1);
+  e->ag_pending = false;
+}
+
+// Before layer l's fp32 weights are read: wait for its gather and expand it
+// into the copies the kernels read (same outputs as launch_sgd's unsharded path).
+void await_layer_weights(vnt_engine* e, int l) {
+  if (!e->shard || !e->ag_wait[l]) return;
+  cudaStream_t s = e->stream;
+  if (e->comm_overlap) VNT_CUDA(cudaStreamWaitEvent(s, e->ag_ev[l], 0));
+  const float* src = e->ag_recv + e->sh_aoff[l];
+  const int rows = (int)e->widths[l], cols = (int)e->widths[l + 1];
+  const bool twins_only = e->split && e->tc_layer[l];
+  const uint64_t wo = e->woff[l], to = e->wtoff[l], bo = e->boff[l];
+  dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+  k_expand_weight<<<grid, block, 0, s>>>(src, rows, cols, twins_only ? nullptr : e->w32 + wo,
+                                         e->split ? e->w32h + wo : nullptr, e->split ? e->w32l + wo : nullptr,
+                                         twins_only ? nullptr : e->wt32 + to,
+                                         e->split ? e->wt32h + to : nullptr, e->split ? e->wt32l + to : nullptr);
+  VNT_LAUNCH_CHECK();
+  k_expand_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, s>>>(src + (size_t)rows * cols, cols, e->w32 + bo,
+                                                             e->split ? e->w32h + bo : nullptr,
+                                                             e->split ? e->w32l + bo : nullptr);
+  VNT_LAUNCH_CHECK();
+  e->launches += 2;
+  e->ag_wait[l] = 0;
+}
+
+// Every fp32 weight current (before an unsharded update, a regroup, ...).
+void flush_gathers(vnt_engine* e) {
+  issue_pending_gathers(e);
+  for (int l = 0; l < e->L; ++l) await_layer_weights(e, l);
+}
+
+// Every rank's fp64 master (and momentum) complete: all-gather the shards
+// (get_params, regroup, unsharded updates).  Blocking; not on the hot path.
+void gather_master(vnt_engine* e) {
+  if (!e->shard || e->master_valid) return;
+  const uint64_t S = (uint64_t)e->comm->size();
+  uint64_t cmax = 0;
+  for (int l = 0; l < e->L; ++l) cmax = std::max(cmax, e->sh_c[l]);
+  double* send = (double*)dalloc(cmax * sizeof(double));
+  double* recv = (double*)dalloc(S * cmax * sizeof(double));
+  for (double* m : {e->w64, e->v64}) {
+    if (!m) continue;
+    for (int l = 0; l < e->L; ++l) {
+      const uint64_t n = e->widths[l] * e->widths[l + 1] + e->widths[l + 1];
+      const uint64_t c = e->sh_c[l], own = e->sh_hi[l] - e->sh_lo[l];
+      VNT_CUDA(cudaMemsetAsync(send, 0, c * sizeof(double), e->stream));
+      if (own)
+        VNT_CUDA(cudaMemcpyAsync(send, m + e->woff[l] + e->sh_lo[l], own * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, e->stream));
+      log_comm(e, kLogAllGather, e->woff[l], c);
+      e->comm->allgather(send, recv, c * sizeof(double), e->stream);
+      VNT_CUDA(cudaMemcpyAsync(m + e->woff[l], recv, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                               e->stream));
+    }
+  }
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  cudaFree(send);
+  cudaFree(recv);
+  e->master_valid = true;
+}
+
+// Sharded update: this rank's chunk of every layer, then the per-tensor
+// max|g| (the next step's scales) is max-reduced over the group.
+void launch_sgd_shard(vnt_engine* e) {
+  cudaStream_t s = e->stream;
+  for (int l = 0; l < e->L; ++l) {
+    ShardSgdArgs a{};
+    a.Gs = e->Gs + e->sh_soff[l];
+    a.w64 = e->w64 + e->woff[l];
+    a.v64 = e->v64 ? e->v64 + e->woff[l] : nullptr;
+    a.out32 = e->ag_send + e->sh_soff[l];
+    a.gmax = e->gmax + 2 * l;
+    a.tail = e->tail;
+    a.ntail_flags = (int)ntensors(e);
+    a.sp = e->d_sp;
+    a.tw = 2 * l;
+    a.lo = (long long)e->sh_lo[l];
+    a.hi = (long long)e->sh_hi[l];
+    a.nw = (long long)(e->widths[l] * e->widths[l + 1]);
+    const uint64_t n = std::max<uint64_t>(1, e->sh_hi[l] - e->sh_lo[l]);
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(n, 256 * 4), (uint64_t)e->sm_count * 8);
+    if (a.v64) k_sgd_shard<true><<<grid, 256, 0, s>>>(a);
+    else k_sgd_shard<false><<<grid, 256, 0, s>>>(a);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+  }
+  log_comm(e, kLogMax, (uint64_t)(reinterpret_cast<long long*>(e->gmax) - e->G), ntensors(e));
+  e->comm->allreduce_max_u64(e->gmax, ntensors(e), s);
+  e->ag_pending = true;
+  e->master_valid = false;
+}
+
+// Copy this rank's chunks out of an all-reduced G (the unsharded
+// sync_gradients path) so a sharded update can follow.
+void load_shards_from_full(vnt_engine* e) {
+  for (int l = 0; l < e->L; ++l) {
+    const uint64_t own = e->sh_hi[l] - e->sh_lo[l];
+    if (own)
+      VNT_CUDA(cudaMemcpyAsync(e->Gs + e->sh_soff[l], e->G + e->woff[l] + e->sh_lo[l],
+                               own * sizeof(long long), cudaMemcpyDeviceToDevice, e->stream));
+  }
+}
+
 // lr, 1/B (virtual_exec.cpp:165), momentum and 2^-s come from the step params.
 void launch_sgd(vnt_engine* e) {
+  if (e->shard) {
+    launch_sgd_shard(e);
+    return;
+  }
   cudaStream_t s = e->stream;
   if (e->node_path) {   // all tensors in one launch, row-major fp32 copies only
     SgdMulti m{};
@@ -1175,7 +1415,7 @@ void launch_sgd(vnt_engine* e) {
       a.w32 = e->w32 + off;
       a.gout = e->gout ? e->gout + off : nullptr;
       a.gmax = e->gmax + t;
-      a.tail = e->G + e->P;
+      a.tail = e->tail;
       a.ntail_flags = (int)ntensors(e);
       a.sp = e->d_sp;
       a.tensor = t;
@@ -1215,7 +1455,7 @@ void launch_sgd(vnt_engine* e) {
       }
       a.gout = e->gout ? e->gout + off : nullptr;
       a.gmax = e->gmax + t;
-      a.tail = e->G + e->P;
+      a.tail = e->tail;
       a.ntail_flags = (int)ntensors(e);
       a.sp = e->d_sp;
       a.tensor = t;
@@ -1260,7 +1500,7 @@ void join_stats(vnt_engine* e) {
 void enqueue_readback(vnt_engine* e, bool with_gmax) {
   join_stats(e);   // the step ends here: its statistics branch must have finished
   cudaStream_t s = e->stream;
-  k_copy_words<<<1, 64, 0, s>>>(reinterpret_cast<const unsigned long long*>(e->G + e->P),
+  k_copy_words<<<1, 64, 0, s>>>(reinterpret_cast<const unsigned long long*>(e->tail),
                                 reinterpret_cast<unsigned long long*>(e->m_tail),
                                 (int)(e->ntail + (with_gmax ? ntensors(e) : 0)));
   VNT_LAUNCH_CHECK();
@@ -1309,7 +1549,7 @@ __global__ void k_tail_add(long long* tail, int slot, long long v) { tail[slot] 
 void add_examples_tail(vnt_engine* e) {
   const long long rest = (long long)e->acc_examples - (long long)e->tail_examples;
   if (rest == 0) return;
-  k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailExamples, rest);
+  k_tail_add<<<1, 1, 0, e->stream>>>(e->tail, kTailExamples, rest);
   VNT_LAUNCH_CHECK();
   e->launches++;
   e->tail_examples = e->acc_examples;
@@ -1393,14 +1633,17 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
         if (graph_stage) launch_stage_rows(e, *graph_stage);
         begin_round_device(e);
       }
+      const bool overlap = e->comm && e->comm_overlap && !e->node_path;
+      issue_pending_gathers(e);
       if (passes.size() == 1) {
-        run_pass(e, passes[0], stats, true);
+        run_pass(e, passes[0], stats, true, overlap);
         e->acc_started = true;
         e->acc_examples += passes[0].rows;
       }
       add_examples_tail(e);
       if (events) VNT_CUDA(cudaEventRecord(e->ev[2], e->stream));
-      collective(e);
+      if (overlap) finish_layer_collectives(e);
+      else collective(e);
       if (events) VNT_CUDA(cudaEventRecord(e->ev[3], e->stream));
       launch_sgd(e);
       if (events) VNT_CUDA(cudaEventRecord(e->ev[4], e->stream));
@@ -1414,7 +1657,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
     Readback rb;
     const std::vector<Pass>* passes = local.empty() ? nullptr : &plan_for(e, local);
     const bool single = passes && passes->size() == 1;
-    if (single && attempt == 0 && e->graphs && !e->comm) {
+    if (single && attempt == 0 && e->graphs && (!e->comm || e->comm->on_stream())) {
       // Graph path: host prep outside, the whole device step as one graph launch.
       const Pass& p = (*passes)[0];
       ensure_combine(e, p.nodes.size());
@@ -1442,13 +1685,15 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
         e->memo.devs.assign(node_device, node_device + total_nodes);
         e->memo.rows = batch_rows;
         e->memo.valid = true;
-        for (auto& row : e->memo.ge)
-          for (auto& g : row) g = nullptr;
+        for (auto& plane : e->memo.ge)
+          for (auto& row : plane)
+            for (auto& g : row) g = nullptr;
       }
-      vnt_engine::GraphEntry*& slot = e->memo.ge[e->cur & 1][stage_in_graph ? 1 : 0];
+      const int gathers = (e->shard && e->ag_pending) ? 1 : 0;
+      vnt_engine::GraphEntry*& slot = e->memo.ge[e->cur & 1][stage_in_graph ? 1 : 0][gathers];
       if (!slot) {
         std::vector<int64_t> key = {(int64_t)e->opt.resident_rows, -1, e->cur,
-                                    stage_in_graph ? 1 : 0, (int64_t)total_nodes};
+                                    stage_in_graph ? 1 : 0, (int64_t)total_nodes, gathers};
         for (const auto& n : local) {
           key.push_back(n.node);
           key.push_back(n.dev);
@@ -1482,6 +1727,11 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
         } else {
           e->acc_started = true;
           e->acc_examples = p.rows;
+          if (e->shard) {   // host state the captured gathers / sharded update leave
+            e->ag_pending = true;
+            e->ag_wait.assign(e->L, 0);
+            e->master_valid = false;
+          }
           e->launches += ge.launches;
           e->prof_n = ge.prof_n;
           e->prof_flops = ge.prof_flops;
@@ -1506,7 +1756,9 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       if (!local.empty()) accumulate(e, local, x, y, on_device, attempt == 0, overlap);
       add_examples_tail(e);
       if (local.empty()) {
-        // This process hosts no node this step: contribute zeros.
+        // This process hosts no node this step: the same collectives as every
+        // other rank (the weight gathers, then the reductions) with zeros.
+        flush_gathers(e);
         VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
         if (overlap)
           for (int l = e->L - 1; l >= 0; --l) layer_collective(e, l);
@@ -1717,9 +1969,15 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
       e->wt32l = (float*)dalloc(toff * sizeof(float));
     }
     e->ntail = kTailOverflow + ntensors(e.get());
-    e->G = (long long*)dalloc((e->P + e->ntail + ntensors(e.get())) * sizeof(long long));
-    VNT_CUDA(cudaMemset(e->G, 0, (e->P + e->ntail + ntensors(e.get())) * sizeof(long long)));
-    e->gmax = reinterpret_cast<unsigned long long*>(e->G + e->P + e->ntail);
+    // zero gap after P: a sharded reduce-scatter of the last layer reads up to
+    // 32 words per rank past its slice (kMaxRanks ranks)
+    e->tail_off = round_up(e->P, 32) + 32 * kMaxRanks;
+    const uint64_t gwords = e->tail_off + e->ntail + ntensors(e.get());
+    e->G = (long long*)dalloc(gwords * sizeof(long long));
+    VNT_CUDA(cudaMemset(e->G, 0, gwords * sizeof(long long)));
+    e->tail = e->G + e->tail_off;
+    e->gmax = reinterpret_cast<unsigned long long*>(e->tail + e->ntail);
+    e->d_word = (long long*)dalloc(8 * sizeof(long long));
     if (e->node_path) {
       e->wpad = (float*)dalloc(node_wt_floats(e.get()) * sizeof(float));
       VNT_CUDA(cudaMemset(e->wpad, 0, node_wt_floats(e.get()) * sizeof(float)));
@@ -1741,18 +1999,29 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     // collective code paths (including the overlapped per-layer reduction) run
     // and can be tested on one GPU.
     const bool force = getenv("VNT_FORCE_COMM") && getenv("VNT_FORCE_COMM")[0] == '1';
-    if (e->opt.world_size > 1 || force) {
+    if (options->comm_ops) {
+      if (options->comm_ops->size < 1 || options->comm_ops->rank < 0 ||
+          options->comm_ops->rank >= options->comm_ops->size)
+        throw EngineError(VNT_ERR_CONFIG, "comm_ops: bad rank/size");
+      e->pool = std::make_unique<vntb::HostGroup>(*options->comm_ops);
+    } else if (e->opt.world_size > 1 || force) {
       ncclUniqueId id;
       if (e->opt.world_size > 1) {
         if (!options->nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
         std::memcpy(&id, options->nccl_id, sizeof id);
       } else {
-        const ncclResult_t g = ncclGetUniqueId(&id);
-        if (g != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(g));
+        vntb::nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
       }
-      comm_init(e.get(), id);
+      e->pool = std::make_unique<vntb::NcclGroup>(id, e->opt.rank, e->opt.world_size,
+                                                  overlap_wanted() ? kCommSms : 0);
     }
-    setup_comm_overlap(e.get());
+    e->comm = e->pool.get();
+    if (e->comm) {
+      e->opt.rank = e->comm->rank();
+      e->opt.world_size = e->comm->size();
+    }
+    e->opt.comm_ops = nullptr;
+    setup_comm(e.get());
     *out = e.release();
     return VNT_OK;
   });
@@ -1762,7 +2031,14 @@ void vnt_engine_destroy(vnt_engine* e) {
   if (!e) return;
   cudaSetDevice(e->opt.cuda_device);
   cudaStreamSynchronize(e->stream);
-  if (e->comm) ncclCommDestroy(e->comm);
+  if (e->comm_stream) cudaStreamSynchronize(e->comm_stream);
+  e->comm = nullptr;
+  e->active.reset();
+  e->pool.reset();
+  free_shards(e);
+  for (auto& ev : e->ag_ev) cudaEventDestroy(ev);
+  if (e->ag_fork) cudaEventDestroy(e->ag_fork);
+  if (e->d_word) cudaFree(e->d_word);
   tc_destroy(e);
   for (auto& kv : e->plans)
     for (auto& p : kv.second) cudaFree(p.d_meta);
@@ -1824,23 +2100,78 @@ void vnt_engine_destroy(vnt_engine* e) {
 uint64_t vnt_engine_param_count(const vnt_engine* e) { return e ? e->P : 0; }
 uint32_t vnt_engine_tensor_count(const vnt_engine* e) { return e ? ntensors(e) : 0; }
 
+}  // extern "C"
+
+namespace {
+// fp64 master -> every fp32 copy the kernels read; a pending sharded gather
+// is superseded (the master is complete on this rank).
+void refresh_from_master(vnt_engine* e) {
+  for (int l = 0; l < e->L; ++l) {
+    const int rows = (int)e->widths[l], cols = (int)e->widths[l + 1];
+    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+    k_refresh_weight<<<grid, block, 0, e->stream>>>(e->w64 + e->woff[l], e->w32 + e->woff[l],
+                                                    e->wt32 + e->wtoff[l], rows, cols);
+    VNT_LAUNCH_CHECK();
+    k_refresh_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, e->stream>>>(
+        e->w64 + e->boff[l], e->w32 + e->boff[l], (size_t)cols);
+    VNT_LAUNCH_CHECK();
+  }
+  split_weights(e);
+  e->master_valid = true;
+  if (e->shard) {
+    e->ag_pending = false;
+    e->ag_wait.assign(e->L, 0);
+    refill_ag_send(e);
+  }
+}
+// Before the process group changes: complete master and fp32 copies on this
+// rank, streams idle, graphs and the open round dropped, the old group closed.
+void quiesce_for_regroup(vnt_engine* e) {
+  if (e->comm) {
+    gather_master(e);
+    flush_gathers(e);
+  }
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->comm_stream) VNT_CUDA(cudaStreamSynchronize(e->comm_stream));
+  drop_graphs(e);
+  reset_acc(e);
+  e->comm = nullptr;
+  e->active.reset();
+  e->pool.reset();
+  free_shards(e);
+}
+
+// Replica state from `root` of group g: fp64 master, momentum and the
+// fixed-point scale history + loss quantum (numerical state).
+void broadcast_replica(vnt_engine* e, vntb::CommGroup* g, int root) {
+  g->broadcast(e->w64, e->P * sizeof(double), root, e->stream);
+  if (e->v64) g->broadcast(e->v64, e->P * sizeof(double), root, e->stream);
+  std::vector<int32_t> sc(e->scales);
+  sc.push_back(e->scales_init ? 1 : 0);
+  sc.push_back(e->loss_bits);
+  int32_t* d_sc = (int32_t*)dalloc(sc.size() * sizeof(int32_t));
+  VNT_CUDA(cudaMemcpyAsync(d_sc, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, e->stream));
+  g->broadcast(d_sc, sc.size() * sizeof(int32_t), root, e->stream);
+  VNT_CUDA(cudaMemcpyAsync(sc.data(), d_sc, sc.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  cudaFree(d_sc);
+  e->loss_bits = sc.back();
+  sc.pop_back();
+  e->scales_init = sc.back() != 0;
+  sc.pop_back();
+  e->scales.assign(sc.begin(), sc.end());
+}
+}  // namespace
+
+extern "C" {
+
 int vnt_engine_set_params(vnt_engine* e, const double* params, uint64_t n) {
   return guarded([&] {
     if (n != e->P) throw EngineError(VNT_ERR_SHAPE, "params layout does not match model layout");
     bind(e);
     VNT_CUDA(cudaMemcpyAsync(e->w64, params, n * sizeof(double), cudaMemcpyHostToDevice, e->stream));
-    for (int l = 0; l < e->L; ++l) {
-      const int rows = (int)e->widths[l], cols = (int)e->widths[l + 1];
-      dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
-      k_refresh_weight<<<grid, block, 0, e->stream>>>(e->w64 + e->woff[l], e->w32 + e->woff[l],
-                                                      e->wt32 + e->wtoff[l], rows, cols);
-      VNT_LAUNCH_CHECK();
-      k_refresh_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, e->stream>>>(
-          e->w64 + e->boff[l], e->w32 + e->boff[l], (size_t)cols);
-      VNT_LAUNCH_CHECK();
-    }
     if (e->v64) VNT_CUDA(cudaMemsetAsync(e->v64, 0, e->P * sizeof(double), e->stream));
-    split_weights(e);
+    refresh_from_master(e);
     VNT_CUDA(cudaStreamSynchronize(e->stream));
     return VNT_OK;
   });
@@ -1850,6 +2181,7 @@ int vnt_engine_get_params(vnt_engine* e, double* params, uint64_t n) {
   return guarded([&] {
     if (n != e->P) throw EngineError(VNT_ERR_SHAPE, "params layout does not match model layout");
     bind(e);
+    gather_master(e);
     VNT_CUDA(cudaMemcpyAsync(params, e->w64, n * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     VNT_CUDA(cudaStreamSynchronize(e->stream));
     return VNT_OK;
@@ -1936,17 +2268,18 @@ int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum, uint64_t
         if (!e->scales_init && e->comm) hint = std::max<uint64_t>(1, global_count(e, 0));
       }
       begin_round(e, hint);
+      flush_gathers(e);   // the gathers every rank with nodes issued in device_step
       VNT_CUDA(cudaMemsetAsync(e->G, 0, e->P * sizeof(long long), e->stream));
       e->acc_started = true;
     }
     add_examples_tail(e);
     if (e->acc_partials) {
-      k_tail_add<<<1, 1, 0, e->stream>>>(e->G + e->P, kTailPartials, (long long)e->acc_partials);
+      k_tail_add<<<1, 1, 0, e->stream>>>(e->tail, kTailPartials, (long long)e->acc_partials);
       VNT_LAUNCH_CHECK();
     }
     e->acc_examples = 0;
     e->tail_examples = 0;
-    collective(e);
+    collective(e, true);   // the full mean gradient on every rank (sync_gradients)
     Readback rb = read_tail(e, false);
     if (rb.nonfinite) {
       reset_acc(e);
@@ -2045,6 +2378,7 @@ int vnt_engine_sgd_apply(vnt_engine* e, double lr) {
     if (!e->synced) throw EngineError(VNT_ERR_CONFIG, "sgd_apply: call vnt_engine_sync first");
     const uint64_t examples = (uint64_t)e->h_tail[kTailExamples];
     upload_step_params(e, lr, 1.0 / (double)examples);
+    if (e->shard) load_shards_from_full(e);
     launch_sgd(e);
     read_tail(e, true);
     update_scales(e, examples);
@@ -2153,56 +2487,73 @@ int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const ui
     if (world_size < 1 || rank < 0 || rank >= world_size || source_rank < 0 ||
         source_rank >= world_size)
       throw EngineError(VNT_ERR_CONFIG, "bad rank/world_size/source_rank");
-    VNT_CUDA(cudaStreamSynchronize(e->stream));
-    if (e->comm_stream) VNT_CUDA(cudaStreamSynchronize(e->comm_stream));
-    if (e->comm) {
-      ncclCommDestroy(e->comm);
-      e->comm = nullptr;
-    }
-    drop_graphs(e);
-    reset_acc(e);
+    quiesce_for_regroup(e);
     e->opt.rank = rank;
     e->opt.world_size = world_size;
-    if (world_size == 1) {
-      setup_comm_overlap(e);
-      return VNT_OK;
+    if (world_size > 1) {
+      if (!nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof id);
+      e->pool = std::make_unique<vntb::NcclGroup>(id, rank, world_size, overlap_wanted() ? kCommSms : 0);
+      e->comm = e->pool.get();
+      broadcast_replica(e, e->comm, source_rank);
     }
-    if (!nccl_id) throw EngineError(VNT_ERR_CONFIG, "world_size > 1 needs nccl_id");
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof id);
-    comm_init(e, id);
-    setup_comm_overlap(e);
-    // Replica state from the source rank: fp64 master, momentum, fixed-point
-    // scale history (part of the numerical state).
-    auto bcast = [&](void* p, size_t n, ncclDataType_t t) {
-      const ncclResult_t rr = ncclBroadcast(p, p, n, t, source_rank, e->comm, e->stream);
-      if (rr != ncclSuccess) throw EngineError(VNT_ERR_NCCL, ncclGetErrorString(rr));
-    };
-    bcast(e->w64, e->P, ncclFloat64);
-    if (e->v64) bcast(e->v64, e->P, ncclFloat64);
-    int32_t* d_sc = (int32_t*)dalloc(ntensors(e) * sizeof(int32_t) + sizeof(int32_t));
-    std::vector<int32_t> sc(e->scales);
-    sc.push_back(e->scales_init ? 1 : 0);
-    VNT_CUDA(cudaMemcpyAsync(d_sc, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
-                             e->stream));
-    bcast(d_sc, sc.size(), ncclInt32);
-    VNT_CUDA(cudaMemcpyAsync(sc.data(), d_sc, sc.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                             e->stream));
+    setup_comm(e);
+    refresh_from_master(e);
     VNT_CUDA(cudaStreamSynchronize(e->stream));
-    cudaFree(d_sc);
-    e->scales.assign(sc.begin(), sc.end() - 1);
-    e->scales_init = sc.back() != 0;
-    for (int l = 0; l < e->L; ++l) {
-      const int rows = (int)e->widths[l], cols = (int)e->widths[l + 1];
-      dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
-      k_refresh_weight<<<grid, block, 0, e->stream>>>(e->w64 + e->woff[l], e->w32 + e->woff[l],
-                                                      e->wt32 + e->wtoff[l], rows, cols);
-      VNT_LAUNCH_CHECK();
-      k_refresh_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, e->stream>>>(
-          e->w64 + e->boff[l], e->w32 + e->boff[l], (size_t)cols);
-      VNT_LAUNCH_CHECK();
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_regroup_ops(vnt_engine* e, const vnt_comm_ops* ops, int32_t source_rank) {
+  return guarded([&] {
+    bind(e);
+    if (!ops || ops->size < 1 || ops->rank < 0 || ops->rank >= ops->size || source_rank < 0 ||
+        source_rank >= ops->size)
+      throw EngineError(VNT_ERR_CONFIG, "bad comm_ops/source_rank");
+    quiesce_for_regroup(e);
+    e->pool = std::make_unique<vntb::HostGroup>(*ops);
+    e->comm = e->pool.get();
+    e->opt.rank = ops->rank;
+    e->opt.world_size = ops->size;
+    broadcast_replica(e, e->comm, source_rank);
+    setup_comm(e);
+    refresh_from_master(e);
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_set_membership(vnt_engine* e, int32_t member, int32_t source_pool_rank) {
+  return guarded([&] {
+    bind(e);
+    if (!e->pool) throw EngineError(VNT_ERR_CONFIG, "set_membership: the engine has no process group");
+    if (source_pool_rank < 0 || source_pool_rank >= e->pool->size())
+      throw EngineError(VNT_ERR_CONFIG, "set_membership: bad source rank");
+    // A member before the change holds a complete replica; the source must be one.
+    if (e->comm) {
+      gather_master(e);
+      flush_gathers(e);
     }
-    split_weights(e);
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->comm_stream) VNT_CUDA(cudaStreamSynchronize(e->comm_stream));
+    drop_graphs(e);
+    reset_acc(e);
+    e->comm = nullptr;
+    e->active.reset();
+    free_shards(e);
+    std::unique_ptr<vntb::CommGroup> sub = e->pool->split(member ? 0 : -1, e->pool->rank());
+    log_comm(e, kLogBroadcast, 0, e->P);
+    broadcast_replica(e, e->pool.get(), source_pool_rank);
+    if (member) {
+      if (!sub) throw EngineError(VNT_ERR_NCCL, "set_membership: split returned no group");
+      e->active = std::move(sub);
+      e->comm = e->active.get();
+      e->opt.rank = e->comm->rank();
+      e->opt.world_size = e->comm->size();
+    }
+    setup_comm(e);
+    refresh_from_master(e);
     VNT_CUDA(cudaStreamSynchronize(e->stream));
     return VNT_OK;
   });
@@ -2210,12 +2561,10 @@ int vnt_engine_regroup(vnt_engine* e, int32_t rank, int32_t world_size, const ui
 
 int vnt_engine_comm_log(vnt_engine* e, uint64_t* out, uint32_t cap, uint32_t* count) {
   return guarded([&] {
-    const uint32_t n = (uint32_t)(e->comm_log.size() / 2);
+    const uint32_t n = (uint32_t)(e->comm_log.size() / 3);
     if (count) *count = n;
-    for (uint32_t i = 0; out && i < std::min(n, cap); ++i) {
-      out[2 * i] = e->comm_log[2 * i];
-      out[2 * i + 1] = e->comm_log[2 * i + 1];
-    }
+    for (uint32_t i = 0; out && i < std::min(n, cap); ++i)
+      for (int k = 0; k < 3; ++k) out[3 * i + k] = e->comm_log[3 * i + k];
     e->comm_log.clear();
     return VNT_OK;
   });

@@ -741,7 +741,7 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const 
   ep.first = first ? 1 : 0;
   ep.scale = scale;
   ep.lim = lim;
-  ep.tail = e->G + e->P;
+  ep.tail = e->tail;
   ep.tensor = tensor;
   tc_launch<kTcDw>(e, pair, a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep);
 }

@@ -254,13 +254,17 @@ def test_prefetch_is_bit_identical(port, monkeypatch, graphs, mode):
     assert np.array_equal(a.get_params(), b.get_params())
 
 
-@pytest.mark.parametrize("overlap,w,mode", [("1", [128, 256, 256, 10], "auto"),
-                                            ("0", [128, 256, 256, 10], "auto"),
-                                            ("1", [64, 96, 48, 10], "ffma")])
-def test_collective_paths_bit_identical(port, monkeypatch, overlap, w, mode):
+@pytest.mark.parametrize("overlap,shard,w,mode", [("1", "1", [128, 256, 256, 10], "auto"),
+                                                  ("0", "1", [128, 256, 256, 10], "auto"),
+                                                  ("1", "0", [128, 256, 256, 10], "auto"),
+                                                  ("0", "0", [128, 256, 256, 10], "auto"),
+                                                  ("1", "1", [64, 96, 48, 10], "ffma")])
+def test_collective_paths_bit_identical(port, monkeypatch, overlap, shard, w, mode):
     """VNT_FORCE_COMM=1 gives the engine a one-rank NCCL group, so the collective
-    code runs on one GPU: the single reduction (VNT_COMM_OVERLAP=0) and the
-    per-layer reductions overlapped with the backward on a comm stream (default)
+    code runs on one GPU: the sharded update (reduce-scatter, 1/G update,
+    deferred weight all-gather; default) or the all-reduce + full update
+    (VNT_SHARD=0), each in line (VNT_COMM_OVERLAP=0) or overlapped with the
+    backward / next forward on a comm stream and captured in the step graph,
     must leave every bit of the trajectory unchanged, for any pass grouping."""
     sizes, dev = vnt().uniform_mapping(256, 8, 1)
 
@@ -268,7 +272,7 @@ def test_collective_paths_bit_identical(port, monkeypatch, overlap, w, mode):
         e = make_engine(w, "relu", "softmax-cross-entropy", 4, port, gemm_mode=mode,
                         resident_rows=rr)
         losses = []
-        for s in range(3):
+        for s in range(5):   # steps 2.. replay the captured graph
             x, y = port.synth_batch(4, 2048, w[0], w[-1], s * 256, 256)
             losses.append(e.train_step(x, y, sizes, dev, 0.02)[0])
         return e.get_params(), losses
@@ -276,6 +280,7 @@ def test_collective_paths_bit_identical(port, monkeypatch, overlap, w, mode):
     want = trajectory(0)
     monkeypatch.setenv("VNT_FORCE_COMM", "1")
     monkeypatch.setenv("VNT_COMM_OVERLAP", overlap)
+    monkeypatch.setenv("VNT_SHARD", shard)
     for rr in (0, 96):
         got = trajectory(rr)
         assert got[1] == want[1]
@@ -374,15 +379,17 @@ def test_collective_sequence_node_path(port, monkeypatch):
         e.comm_log()
         e.train_step(x, y, sizes, np.array(node_device, np.int32), 0.02)
         logs.append(e.comm_log())
-    assert len(logs[0]) == 1 and logs[0][0][0] == 0
+    assert len(logs[0]) == 1 and logs[0][0][:2] == ("allreduce", 0)
     assert logs[1] == logs[0] and logs[2] == logs[0]
 
 
 def test_collective_sequence_is_rank_independent(port, monkeypatch):
-    """Every rank must issue the same all-reduces in the same order (NCCL
-    matches collectives by order): a process with all nodes, one with none
-    (it reduces zeros), and one whose nodes need three passes all log the same
-    (offset, count) sequence — per layer L-1..0 overlapped, then the tail."""
+    """Every rank must issue the same collectives in the same order (NCCL
+    matches them by order): a process with all nodes, one with none (it
+    reduces zeros), and one whose nodes need three passes all log the same
+    sequence — sharded update: per layer L-1..0 reduce-scatter (overlapped with
+    the backward), the tail all-reduce, the max|g| all-reduce; from the second
+    step on, first the weight all-gathers of layers 0..L-1."""
     monkeypatch.setenv("VNT_FORCE_COMM", "1")
     w = [128, 256, 256, 10]
     sizes, _ = vnt().uniform_mapping(256, 8, 1)
@@ -393,15 +400,20 @@ def test_collective_sequence_is_rank_independent(port, monkeypatch):
                         resident_rows=rr)
         e.comm_log()   # creation-time traffic, if any
         e.train_step(x, y, sizes, np.array(node_device, np.int32), 0.02)
-        logs.append(e.comm_log())
-    P = vnt().param_count(w)
+        first = e.comm_log()
+        e.train_step(x, y, sizes, np.array(node_device, np.int32), 0.02)
+        logs.append((first, e.comm_log()))
     L = len(w) - 1
     offs, p = [], 0
     for l in range(L):
-        offs.append((p, w[l] * w[l + 1] + w[l + 1]))
-        p += w[l] * w[l + 1] + w[l + 1]
-    want = list(reversed(offs)) + [(P, logs[0][-1][1])]
-    assert logs[0] == want
+        n = w[l] * w[l + 1] + w[l + 1]
+        offs.append((p, (n + 31) // 32 * 32))   # one rank: chunk = slice rounded to 32
+        p += n
+    rs = [("reduce_scatter", o, c) for o, c in reversed(offs)]
+    first, second = logs[0]
+    assert first[:L] == rs
+    assert [op for op, _, _ in first[L:]] == ["allreduce", "max"]
+    assert second == [("allgather", o, c) for o, c in offs] + first
     assert logs[1] == logs[0] and logs[2] == logs[0]
 
 
