@@ -248,6 +248,10 @@ int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out);
  * offset = position in the parameter layout (gradient buffer words).  Every
  * rank of a group must issue the identical sequence; clears the log. */
 int vnt_engine_comm_log(vnt_engine* e, uint64_t* out, uint32_t cap, uint32_t* count);
+/* Diagnostics (tests): hidden activations X[layer] (rows x width, fp32) of
+ * the last pass, e.g. to resolve relu masks at near-zero pre-activations when
+ * comparing with an fp64 reference.  Layered path only. */
+int vnt_engine_debug_activation(vnt_engine* e, int32_t layer, float* out, uint64_t rows);
 /* The CUDA stream the engine launches on (cudaStream_t as void*). */
 void* vnt_engine_stream(vnt_engine* e);
 /* Scratch device allocation owned by the engine (bench/test staging). */

@@ -312,6 +312,169 @@ int vo_forward_backward(const uint64_t* w, uint32_t nw, int act, int loss,
   return 0;
 }
 
+int vo_forward_backward_wide_masked(const uint64_t* w, uint32_t nw, int act, int loss,
+                                    const double* params, const double* x, const double* y,
+                                    uint64_t count, const float* const* act_ext, double tau,
+                                    double* grads, double* loss_out, uint64_t* n_amb,
+                                    uint64_t* n_conf);
+
+/* Wide-model variant of vo_forward_backward (same per-example arithmetic,
+ * model.cpp:270-338, without materialising the P-sized per-example gradient):
+ * per-example activations and deltas are kept (examples in parallel), then
+ * each gradient element sum_r a_r[i] d_r[o] over examples ascending is
+ * accumulated with Neumaier compensation — within an ulp or two of the exactly
+ * rounded sum the reference's ExactVectorAccumulator produces (tests pin it
+ * to vo_forward_backward on small models) — and scaled by 1/count. */
+int vo_forward_backward_wide(const uint64_t* w, uint32_t nw, int act, int loss,
+                             const double* params, const double* x, const double* y,
+                             uint64_t count, double* grads, double* loss_out) {
+  return vo_forward_backward_wide_masked(w, nw, act, loss, params, x, y, count, NULL, 0.0, grads,
+                                         loss_out, NULL, NULL);
+}
+
+/* relu only: where |z| <= tau * max_o |z| for a hidden unit of an example
+ * (an fp32 computation cannot resolve the sign there), relu' is taken from
+ * the caller's activations act_ext[l][r * w[l] + o] > 0 instead of z > 0
+ * (counted in *n_amb); elsewhere a disagreement between the two signs is
+ * counted in *n_conf. */
+int vo_forward_backward_wide_masked(const uint64_t* w, uint32_t nw, int act, int loss,
+                                    const double* params, const double* x, const double* y,
+                                    uint64_t count, const float* const* act_ext, double tau,
+                                    double* grads, double* loss_out, uint64_t* n_amb,
+                                    uint64_t* n_conf) {
+  const uint32_t L = nw - 1;
+  uint64_t sw = 0, woff[64], boff[64], off = 0;
+  if (L > 63 || count == 0) return 1;
+  for (uint32_t l = 0; l < L; ++l) {
+    woff[l] = off;
+    off += w[l] * w[l + 1];
+    boff[l] = off;
+    off += w[l + 1];
+  }
+  for (uint32_t l = 0; l <= L; ++l) sw += w[l];
+  /* per example: a[0..L] (layer inputs / outputs) and d[1..L] (dLoss/dz) */
+  double* A = (double*)malloc(sizeof(double) * sw * count);
+  double* D = (double*)malloc(sizeof(double) * sw * count);
+  double* EL = (double*)malloc(sizeof(double) * count);
+  unsigned char* MK = (unsigned char*)calloc(sw * count, 1);   /* relu' per hidden unit */
+  uint64_t amb = 0, conf = 0;
+  uint64_t aoff[65];
+  aoff[0] = 0;
+  for (uint32_t l = 0; l < L; ++l) aoff[l + 1] = aoff[l] + w[l];
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : amb, conf)
+  for (uint64_t r = 0; r < count; ++r) {
+    double* a = A + r * sw;
+    unsigned char* mk = MK + r * sw;
+    double* d = D + r * sw;
+    double* pre = (double*)malloc(sizeof(double) * sw);
+    memcpy(a, x + r * w[0], sizeof(double) * w[0]);
+    for (uint32_t l = 0; l < L; ++l) {
+      const uint64_t in = w[l], out = w[l + 1];
+      const double* W = params + woff[l];
+      double* z = pre + aoff[l + 1];
+      for (uint64_t o = 0; o < out; ++o) z[o] = params[boff[l] + o];
+      for (uint64_t i = 0; i < in; ++i) {   /* i ascending per output, as the reference */
+        const double ai = a[aoff[l] + i];
+        const double* Wr = W + i * out;
+        for (uint64_t o = 0; o < out; ++o) z[o] += ai * Wr[o];
+      }
+      double zmax = 0.0;
+      for (uint64_t o = 0; o < out; ++o) zmax = fabs(z[o]) > zmax ? fabs(z[o]) : zmax;
+      for (uint64_t o = 0; o < out; ++o) {
+        if (l + 1 == L) {
+          a[aoff[l + 1] + o] = z[o];
+          continue;
+        }
+        a[aoff[l + 1] + o] = activate(act, z[o]);
+        mk[aoff[l + 1] + o] = z[o] > 0.0;
+        if (act == 0 && act_ext && act_ext[l + 1]) {
+          const int on = act_ext[l + 1][r * out + o] > 0.0f;
+          if (fabs(z[o]) <= tau * zmax) {
+            amb += on != (z[o] > 0.0);
+            mk[aoff[l + 1] + o] = (unsigned char)on;
+            a[aoff[l + 1] + o] = on ? fabs(z[o]) : 0.0;
+          } else {
+            conf += on != (z[o] > 0.0);
+          }
+        }
+      }
+    }
+    const uint64_t ow = w[L];
+    const double* oa = a + aoff[L];
+    double* dl = d + aoff[L];
+    double lo = 0.0;
+    if (loss == 0) {
+      for (uint64_t o = 0; o < ow; ++o) {
+        const double df = oa[o] - y[r * ow + o];
+        lo += df * df;
+        dl[o] = 2.0 * df / (double)ow;
+      }
+      lo /= (double)ow;
+    } else {
+      double mx = oa[0];
+      for (uint64_t o = 1; o < ow; ++o) mx = oa[o] > mx ? oa[o] : mx;
+      double norm = 0.0;
+      for (uint64_t o = 0; o < ow; ++o) {
+        dl[o] = exp(oa[o] - mx);
+        norm += dl[o];
+      }
+      const double lognorm = log(norm);
+      for (uint64_t o = 0; o < ow; ++o) {
+        dl[o] /= norm;
+        lo -= y[r * ow + o] * (oa[o] - mx - lognorm);
+        dl[o] = dl[o] - y[r * ow + o];
+      }
+    }
+    EL[r] = lo;
+    for (uint32_t l = L - 1; l >= 1; --l) {
+      const uint64_t in = w[l], out = w[l + 1];
+      const double* W = params + woff[l];
+      const double* dn = d + aoff[l + 1];
+      for (uint64_t i = 0; i < in; ++i) {
+        double acc = 0.0;
+        const double* Wr = W + i * out;
+        for (uint64_t o = 0; o < out; ++o) acc += Wr[o] * dn[o];
+        d[aoff[l] + i] = act == 0 ? (mk[aoff[l] + i] ? acc : 0.0)
+                                  : acc * activate_grad(act, pre[aoff[l] + i]);
+      }
+    }
+    free(pre);
+  }
+  const double inv = 1.0 / (double)count;
+  for (uint32_t l = 0; l < L; ++l) {
+    const uint64_t in = w[l], out = w[l + 1];
+#pragma omp parallel for schedule(static)
+    for (uint64_t i = 0; i <= in; ++i) {   /* i == in: the bias */
+      double* s = (double*)calloc(out, sizeof(double));
+      double* c = (double*)calloc(out, sizeof(double));
+      for (uint64_t r = 0; r < count; ++r) {
+        const double ai = i < in ? A[r * sw + aoff[l] + i] : 1.0;
+        const double* dn = D + r * sw + aoff[l + 1];
+        for (uint64_t o = 0; o < out; ++o) {
+          const double v = ai * dn[o], t = s[o] + v;
+          c[o] += fabs(s[o]) >= fabs(v) ? (s[o] - t) + v : (v - t) + s[o];
+          s[o] = t;
+        }
+      }
+      double* g = grads + (i < in ? woff[l] + i * out : boff[l]);
+      for (uint64_t o = 0; o < out; ++o) g[o] = (s[o] + c[o]) * inv;
+      free(s);
+      free(c);
+    }
+  }
+  esum ls = {0, 0, NULL};
+  for (uint64_t r = 0; r < count; ++r) esum_add(&ls, EL[r]);
+  *loss_out = esum_total(&ls) * inv;
+  free(ls.p);
+  free(A);
+  free(D);
+  free(EL);
+  free(MK);
+  if (n_amb) *n_amb = amb;
+  if (n_conf) *n_conf = conf;
+  return 0;
+}
+
 void vo_sgd_momentum(double* w, double* v, const double* g, uint64_t n, double lr, double mu) {
   for (uint64_t i = 0; i < n; ++i) {
     v[i] = mu * v[i] + g[i];

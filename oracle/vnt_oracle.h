@@ -36,6 +36,21 @@ int vo_forward_backward(const uint64_t* widths, uint32_t nw, int act, int loss,
                         const double* params, const double* x, const double* y,
                         uint64_t count, double* grads, double* loss_out);
 
+/* The same for wide models (examples in parallel, Neumaier-compensated sums
+ * instead of the exact expansion: within 1-2 ulp of vo_forward_backward). */
+int vo_forward_backward_wide(const uint64_t* widths, uint32_t nw, int act, int loss,
+                             const double* params, const double* x, const double* y,
+                             uint64_t count, double* grads, double* loss_out);
+/* relu: hidden units whose |z| <= tau * max|z| (sign not resolvable in fp32)
+ * take relu' from act_ext[l] (rows x w[l] activations of an fp32 run; NULL
+ * entries / act_ext NULL: none); n_amb counts units whose mask was taken
+ * over and differed, n_conf sign disagreements outside the band. */
+int vo_forward_backward_wide_masked(const uint64_t* widths, uint32_t nw, int act, int loss,
+                                    const double* params, const double* x, const double* y,
+                                    uint64_t count, const float* const* act_ext, double tau,
+                                    double* grads, double* loss_out, uint64_t* n_amb,
+                                    uint64_t* n_conf);
+
 /* runner.cpp:37-82 + virtual_exec.cpp:71-100,120-168,207-282: a Trainer with
  * `n_devices` devices "gpu0".."gpuN-1", uniform mapping, sequential data. */
 void* vo_trainer_create(const uint64_t* widths, uint32_t nw, int act, int loss,

@@ -114,6 +114,7 @@ def load_engine() -> C.CDLL:
         "vnt_engine_comm_log": (C.c_int, [_vp, _u64p, C.c_uint32, C.POINTER(C.c_uint32)]),
         "vnt_engine_regroup_ops": (C.c_int, [_vp, _vp, C.c_int32]),
         "vnt_engine_set_membership": (C.c_int, [_vp, C.c_int32, C.c_int32]),
+        "vnt_engine_debug_activation": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_float), C.c_uint64]),
         "vnt_engine_prefetch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _u64p, _i32p, C.c_uint32,
                                           C.c_int32]),
         "vnt_engine_regroup": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32]),
@@ -346,6 +347,13 @@ class Engine:
     def set_membership(self, member: bool, source_pool_rank: int = 0):
         """Elastic resize inside the process pool (collective over the pool)."""
         _check(self.lib.vnt_engine_set_membership(self.h, 1 if member else 0, source_pool_rank))
+
+    def debug_activation(self, layer: int, rows: int) -> np.ndarray:
+        """Hidden activations X[layer] of the last pass (diagnostics)."""
+        out = np.empty((rows, self.widths[layer]), np.float32)
+        _check(self.lib.vnt_engine_debug_activation(self.h, layer,
+                                                    out.ctypes.data_as(C.POINTER(C.c_float)), rows))
+        return out
 
     def timings(self) -> dict:
         t = StepTimings()

@@ -2559,6 +2559,26 @@ int vnt_engine_set_membership(vnt_engine* e, int32_t member, int32_t source_pool
   });
 }
 
+int vnt_engine_debug_activation(vnt_engine* e, int32_t layer, float* out, uint64_t rows) {
+  return guarded([&] {
+    bind(e);
+    if (layer < 1 || layer >= e->L) throw EngineError(VNT_ERR_CONFIG, "debug_activation: hidden layers only");
+    if (e->node_path) throw EngineError(VNT_ERR_CONFIG, "debug_activation: layered path only");
+    if (rows > e->cap_rows) throw EngineError(VNT_ERR_CONFIG, "debug_activation: more rows than staged");
+    const uint64_t n = rows * e->widths[layer];
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->X[layer] && !(e->Xh[layer] && e->act != VNT_ACT_TANH)) {
+      VNT_CUDA(cudaMemcpy(out, e->X[layer], n * sizeof(float), cudaMemcpyDeviceToHost));
+    } else {   // only the 3xTF32 twins were written: x = hi + lo exactly
+      std::vector<float> hi(n), lo(n);
+      VNT_CUDA(cudaMemcpy(hi.data(), e->Xh[layer], n * sizeof(float), cudaMemcpyDeviceToHost));
+      VNT_CUDA(cudaMemcpy(lo.data(), e->Xl[layer], n * sizeof(float), cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < n; ++i) out[i] = hi[i] + lo[i];
+    }
+    return VNT_OK;
+  });
+}
+
 int vnt_engine_comm_log(vnt_engine* e, uint64_t* out, uint32_t cap, uint32_t* count) {
   return guarded([&] {
     const uint32_t n = (uint32_t)(e->comm_log.size() / 3);

@@ -35,8 +35,20 @@ namespace tc {
 constexpr int BM = 128, BK = 32;
 // w0 TMA, w1 MMA, w2..w9 epilogue (w2 also allocates TMEM): 320 threads leave
 // the dW epilogue 204 registers for its 64 int64 accumulators (no spills).
-constexpr int kEpiWarp0 = 2;
+// Warp roles: warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator
+// (idle otherwise), warp 3 idle; warps 4..11 epilogue.  The first warpgroup
+// gives registers to the epilogue warpgroups (setmaxnreg), which hold the
+// promoted K-chunk sums (fwd / bwd) or the int64 node sums (dW) in registers.
+constexpr int kEpiWarp0 = 4;
 constexpr int kThreads = (kEpiWarp0 + 8) * 32;
+constexpr int kRegsLow = 56, kRegsEpi = 224;   // 4 x 32 x 56 + 8 x 32 x 224 <= 64K
+
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsLow));
+}
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
+}
 
 enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
 
@@ -105,7 +117,39 @@ struct EpiArgs {
   // tile raster: groups of group_m tile rows, column-major inside a group, so
   // the tiles resident at once share A and B panels in L2 (0/1: row-major)
   int group_m;
+  // fwd / bwd-data: K is accumulated in TMEM in chunks of kchunk columns
+  // (multiple of BK; 0 = all of K at once) and the chunk sums are added in
+  // fp32 registers in chunk order ("promotion").  tcgen05's TMEM accumulation
+  // loses precision over long K chains (scripts/ubench_tf32_precision.cu:
+  // 3xTF32 at K = 4096 is 3e-5 of max|D| in one chain, 1.2e-6 in 128-column
+  // chunks vs 2.3e-6 for an fp32 FMA chain).  The first chunk of a tile is
+  // kfirst long: while it runs, the epilogue of the previous tile (its
+  // output stores, bursty across all SMs) still holds the other buffer.
+  int kchunk;
+  int kfirst;
 };
+
+// K range [kb, kb + kl) of segment s: a virtual node (dW) or a K chunk (fwd/bwd).
+__device__ __forceinline__ void seg_range(int s, int nseg, const int* seg_k0, const int* seg_rows, int K,
+                                          int kchunk, int kfirst, int& kb, int& kl) {
+  if (nseg > 0) {
+    kb = seg_k0[s];
+    kl = (int)round_up(seg_rows[s], 32);
+  } else if (kchunk > 0) {
+    kb = s == 0 ? 0 : kfirst + (s - 1) * kchunk;
+    const int len = s == 0 ? kfirst : kchunk;
+    kl = K - kb < len ? K - kb : len;
+  } else {
+    kb = 0;
+    kl = K;
+  }
+}
+
+__host__ __device__ inline int seg_count(int nseg, int K, int kchunk, int kfirst) {
+  if (nseg > 0) return nseg;
+  if (kchunk <= 0 || K <= kfirst) return 1;
+  return 1 + (K - kfirst + kchunk - 1) / kchunk;
+}
 
 
 
@@ -235,6 +279,43 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
+// fwd / bwd epilogue, K-chunk promotion: fold a finished chunk of TMEM
+// columns [col0, col0 + 32 NB) of this warp's lanes into the register sums
+// (first: overwrite), or — on the last chunk — add the sums into TMEM
+// (sum + last chunk) for the regular epilogue, which reads the total from
+// there (holding the 128 sums through the epilogue would spill).  16 columns
+// per TMEM access.
+template <int NB>
+__device__ __forceinline__ void promote_chunk(uint32_t taddr, float (&pacc)[NB][32], bool first,
+                                              bool last) {
+#pragma unroll
+  for (int c = 0; c < 2 * NB; ++c) {
+    float v[16];
+    tmem_ld16(taddr + (uint32_t)(c * 16), v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float& a = pacc[c >> 1][(c & 1) * 16 + j];
+      if (last) v[j] = a + v[j];
+      else a = first ? v[j] : a + v[j];
+    }
+    if (last) tmem_st16(taddr + (uint32_t)(c * 16), v);
+  }
+  if (last) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // Persistent: CTA b processes tiles b, b + gridDim.x, ... (n fastest).  Per
 // tile, nseg == 0 means one segment covering K; otherwise segment s covers K
 // columns [seg_k0[s], seg_k0[s] + round_up(seg_rows[s], 32)) — one virtual node.
@@ -261,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int segs = nseg > 0 ? nseg : 1;
+  const int segs = seg_count(nseg, K, EPI == kTcDw ? 0 : ep.kchunk, ep.kfirst);
   const int tiles_n = (int)ceil_div(ep.N, BN);
   const int tiles_m = (int)ceil_div(ep.M, BM);
   const int tiles = tiles_m * tiles_n;
@@ -290,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    regs_dec();
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
@@ -301,8 +383,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_coords(tile, tiles_m, tiles_n, ep.group_m, tm, tn);
         const int m0 = tm * BM, n0 = tn * BN;
         for (int s = 0; s < segs; ++s) {
-          const int kb = nseg > 0 ? seg_k0[s] : 0;
-          const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
+          int kb, kl;
+          seg_range(s, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
           for (int k = 0; k < kl; k += BK) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             mbar_expect_tx(&full[stage], C::kStageBytes);
@@ -322,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       TC_PROBE_DONE(EPI, 0);
     }
   } else if (warp == 1) {
+    regs_dec();
     {
       constexpr uint32_t idesc = idesc_tf32(BM, BN);
       int stage = 0;
@@ -334,7 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           TC_PROBE_WAIT(mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(b * BN);
-          const int kl = nseg > 0 ? (int)round_up(seg_rows[s], 32) : K;
+          int kb, kl;
+          seg_range(s, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
           for (int k = 0; k < kl; k += BK) {
 #ifdef VNT_TC_PROBE
             { const long long _t = clock64(); mbar_wait(&full[stage], phase);
@@ -368,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       TC_PROBE_DONE(EPI, 2);
     }
   } else if (warp >= kEpiWarp0) {
+    regs_inc();
     constexpr int COLS = BN / 2;          // columns per epilogue thread
     const int q = warp & 3;               // TMEM lane quarter this warp may access
     const int h = (warp - kEpiWarp0) >> 2;        // column half
@@ -386,7 +471,93 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < COLS; ++j) acc[j] = 0;
       }
-      for (int s = 0; s < segs; ++s, ++it) {
+      // fwd / bwd: 32 finished columns (tile column col) of this thread's row
+      auto finish32 = [&](float (&v)[32], int col) {
+        const int nb = n0 + col;
+        if (r >= ep.M) return;
+        const int tc = ep.tcol[r];
+        if (EPI == kTcBwd && nb + 32 <= ep.N) {
+          const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 xv = __ldg(xp + j / 4);
+            v[j] *= act_grad_from_out(ep.act, xv.x);
+            v[j + 1] *= act_grad_from_out(ep.act, xv.y);
+            v[j + 2] *= act_grad_from_out(ep.act, xv.z);
+            v[j + 3] *= act_grad_from_out(ep.act, xv.w);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = nb + j;
+            if (n < ep.N) {
+              if (EPI == kTcFwd)
+                v[j] = act_fwd(ep.act, v[j] + __ldg(ep.bias + n));
+              else
+                v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (nb + j < ep.N) {
+            const size_t o = (size_t)(nb + j) * ep.ldT + tc;
+            const float t = v[j] * tscale;
+            if (ep.outT) ep.outT[o] = t;
+            if (ep.outTh) {
+              const float th = tf32_rna(t);
+              ep.outTh[o] = th;
+              ep.outTl[o] = t - th;
+            }
+          }
+        if (ep.out) {   // null: only the 3xTF32 twins are consumed
+          float* orow = ep.out + (size_t)r * ep.ldo + nb;
+          if (nb + 32 <= ep.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nb + j < ep.N) orow[j] = v[j];
+          }
+        }
+        if (ep.outh) {
+          const size_t o = (size_t)r * ep.ldo + nb;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (nb + j >= ep.N) break;
+            float4 hv, lv;
+            hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
+            hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
+            hv.z = tf32_rna(v[j + 2]); lv.z = v[j + 2] - hv.z;
+            hv.w = tf32_rna(v[j + 3]); lv.w = v[j + 3] - hv.w;
+            *reinterpret_cast<float4*>(ep.outh + o + j) = hv;
+            *reinterpret_cast<float4*>(ep.outl + o + j) = lv;
+          }
+        }
+      };
+      int s0 = 0;
+      if constexpr (EPI != kTcDw) if (segs > 1) {
+        // K-chunk promotion: chunks 0..segs-2 fold into registers (buffer
+        // released at once); the sum is added into the last chunk's TMEM,
+        // which the regular epilogue below reads (same it).
+        float pacc[COLS / 32][32];
+        const uint32_t lane_col = ((uint32_t)(q * 32) << 16) + (uint32_t)(h * COLS);
+        for (int s = 0; s < segs; ++s, ++it) {
+          const int b = it & 1;
+          TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
+          tc_fence_after();
+          const bool last = s + 1 == segs;
+          promote_chunk<COLS / 32>(tmem + lane_col + (uint32_t)(b * BN), pacc, s == 0, last);
+          if (last) break;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        s0 = segs - 1;
+      }
+      for (int s = s0; s < segs; ++s, ++it) {
         const int b = it & 1;
         TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
         tc_fence_after();
@@ -406,78 +577,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else {
-        // one 32-column chunk per iteration, not unrolled: the unrolled
-        // epilogue overflowed the instruction cache (stall_no_inst at K = 784)
+          // one 32-column chunk per iteration, not unrolled: the unrolled
+          // epilogue overflowed the instruction cache (stall_no_inst at K = 784)
 #pragma unroll 1
-        for (int c = 0; c < COLS / 32; ++c) {
-          float v[32];
-          const int col = h * COLS + c * 32;
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
-          const int nb = n0 + col;
-          if (r < ep.M) {
-            const int tc = ep.tcol[r];
-            if (EPI == kTcBwd && nb + 32 <= ep.N) {
-              const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 xv = __ldg(xp + j / 4);
-                v[j] *= act_grad_from_out(ep.act, xv.x);
-                v[j + 1] *= act_grad_from_out(ep.act, xv.y);
-                v[j + 2] *= act_grad_from_out(ep.act, xv.z);
-                v[j + 3] *= act_grad_from_out(ep.act, xv.w);
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const int n = nb + j;
-                if (n < ep.N) {
-                  if (EPI == kTcFwd)
-                    v[j] = act_fwd(ep.act, v[j] + __ldg(ep.bias + n));
-                  else
-                    v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
-                }
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (nb + j < ep.N) {
-                const size_t o = (size_t)(nb + j) * ep.ldT + tc;
-                const float t = v[j] * tscale;
-                if (ep.outT) ep.outT[o] = t;
-                if (ep.outTh) {
-                  const float th = tf32_rna(t);
-                  ep.outTh[o] = th;
-                  ep.outTl[o] = t - th;
-                }
-              }
-            if (ep.out) {   // null: only the 3xTF32 twins are consumed
-              float* orow = ep.out + (size_t)r * ep.ldo + nb;
-              if (nb + 32 <= ep.N) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                  *reinterpret_cast<float4*>(orow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (nb + j < ep.N) orow[j] = v[j];
-              }
-            }
-            if (ep.outh) {
-              const size_t o = (size_t)r * ep.ldo + nb;
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                if (nb + j >= ep.N) break;
-                float4 hv, lv;
-                hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
-                hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
-                hv.z = tf32_rna(v[j + 2]); lv.z = v[j + 2] - hv.z;
-                hv.w = tf32_rna(v[j + 3]); lv.w = v[j + 3] - hv.w;
-                *reinterpret_cast<float4*>(ep.outh + o + j) = hv;
-                *reinterpret_cast<float4*>(ep.outl + o + j) = lv;
-              }
-            }
+          for (int c = 0; c < COLS / 32; ++c) {
+            float v[32];
+            const int col = h * COLS + c * 32;
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
+            finish32(v, col);
           }
-        }
         }
         tc_fence_before();
         __syncwarp();
@@ -511,6 +619,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       else if (!(amax < ep.lim))
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);
     }
+  } else {
+    regs_dec();   // warps 2, 3: the rest of the first warpgroup
   }
   tc_fence_before();
   __syncthreads();
@@ -635,10 +745,26 @@ OpMaps op_maps(const vnt_engine* e, const float* full, const float* hi, const fl
   return m;
 }
 
+// K chunk of the fwd / bwd-data promotion (EpiArgs::kchunk): 3xTF32 only —
+// a 1-pass TF32 GEMM is bounded by its operand rounding, not the chain.
+// VNT_TC_KCHUNK overrides (0 = one TMEM chain over all of K).
+int tc_kchunk(const vnt_engine* e) {
+  static const int env = getenv("VNT_TC_KCHUNK") ? atoi(getenv("VNT_TC_KCHUNK")) : -1;
+  if (env >= 0) return env == 0 ? 0 : (int)round_up((uint64_t)env, 32);
+  return e->split ? 256 : 0;
+}
+// First chunk of a tile (VNT_TC_KFIRST, default 256, multiple of 32).
+int tc_kfirst() {
+  static const int env = getenv("VNT_TC_KFIRST") ? atoi(getenv("VNT_TC_KFIRST")) : 256;
+  return std::max(32, (int)round_up((uint64_t)std::max(env, 1), 32));
+}
+
 template <int EPI>
 void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M, int N, int K,
                int nseg, const int* seg_k0, const int* seg_rows, vntb::tc::EpiArgs ep) {
   using namespace vntb::tc;
+  ep.kchunk = EPI == kTcDw ? 0 : tc_kchunk(e);
+  ep.kfirst = tc_kfirst();
   // forward GEMMs never share the GPU with the gradient reductions
   const int sms = EPI == kTcFwd ? e->sm_count : e->gemm_sms;
   ep.group_m = tc_group_m();

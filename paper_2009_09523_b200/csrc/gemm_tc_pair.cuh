@@ -119,7 +119,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int segs = nseg > 0 ? nseg : 1;   // dW: one K-chain per virtual node
+  // dW: one K-chain per virtual node; fwd / bwd: K chunks (EpiArgs::kchunk)
+  const int segs = seg_count(nseg, K, EPI == kTcDw ? 0 : ep.kchunk, ep.kfirst);
   const int tiles_n = (int)ceil_div(ep.N, BN);
   const int tiles_m = (int)ceil_div(ep.M, PM);
   const int tiles = tiles_m * tiles_n;
@@ -150,6 +151,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    regs_dec();
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
@@ -162,8 +164,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int m0 = tm * PM + (int)rank * BM;
         const int n0 = tn * BN + (int)rank * BNH;
         for (int sg = 0; sg < segs; ++sg) {
-          const int kb = nseg > 0 ? seg_k0[sg] : 0;
-          const int kl = nseg > 0 ? (int)round_up(seg_rows[sg], 32) : K;
+          int kb, kl;
+          seg_range(sg, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
           for (int k = 0; k < kl; k += BK) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
@@ -183,6 +185,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (rank == 0) TC_PROBE_DONE(EPI + 3, 0);
     }
   } else if (warp == 1) {
+    regs_dec();
     if (rank == 0) {
       constexpr uint32_t idesc = idesc_tf32(PM, BN);
       int stage = 0;
@@ -195,7 +198,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         TC_PROBE_WAIT(mbar_wait_cluster(&tempty[b], ((it >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * BN);
-        const int kl = nseg > 0 ? (int)round_up(seg_rows[sg], 32) : K;
+        int kb, kl;
+        seg_range(sg, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
         for (int k = 0; k < kl; k += BK) {
 #ifdef VNT_TC_PROBE
           { const long long _t = clock64(); mbar_wait(&full[stage], phase);
@@ -228,6 +232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       TC_PROBE_DONE(EPI + 3, 2);
     }
   } else if (warp >= kEpiWarp0) {
+    regs_inc();
     constexpr int COLS = BN / 2;
     const int q = warp & 3;
     const int h = (warp - kEpiWarp0) >> 2;
@@ -247,31 +252,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < COLS; ++j) acc[j] = 0;
       }
-      for (int sg = 0; sg < segs; ++sg, ++it) {
-      const int b = it & 1;
-      TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
-      tc_fence_after();
-      if constexpr (EPI == kTcDw) {
-        // per-node quantisation, as k_gemm_tc's dW epilogue (DESIGN.md §3)
-#pragma unroll
-        for (int c = 0; c < COLS / 16; ++c) {
-          float v[16];
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float x = v[j];
-            amax = fmax_nan(amax, fabsf(x));
-            acc[c * 16 + j] += __float2ll_rn(x);
-          }
-        }
-      } else {
-        // one 32-column chunk per iteration, not unrolled: the unrolled
-        // epilogue overflowed the instruction cache (stall_no_inst at K = 784)
-#pragma unroll 1
-      for (int c = 0; c < COLS / 32; ++c) {
-        float v[32];
-        const int col = h * COLS + c * 32;
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
+      // fwd / bwd: 32 finished columns (tile column col) of this thread's row ->
+      // bias + act (fwd) / f' (bwd), feature-major copies, row-major copies
+      // through the per-warp smem transpose tile.
+      auto finish32 = [&](float (&v)[32], int col) {
         const int nb = n0 + col;
         if constexpr (EPI == kTcFwd) {
           // bias: one coalesced load per warp, broadcast by shuffles
@@ -339,12 +323,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
         }
+      };
+      int sg0 = 0;
+      if constexpr (EPI != kTcDw) if (segs > 1) {
+        // K-chunk promotion (EpiArgs::kchunk): chunks 0..segs-2 fold into
+        // registers in chunk order (buffer released at once); the sum is
+        // added into the last chunk's TMEM, which the epilogue below reads.
+        float pacc[COLS / 32][32];
+        const uint32_t lane_col = ((uint32_t)(q * 32) << 16) + (uint32_t)(h * COLS);
+        for (int sg = 0; sg < segs; ++sg, ++it) {
+          const int b = it & 1;
+          TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
+          tc_fence_after();
+          const bool last = sg + 1 == segs;
+          promote_chunk<COLS / 32>(tmem + lane_col + (uint32_t)(b * BN), pacc, sg == 0, last);
+          if (last) break;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(&tempty[b]);
+        }
+        sg0 = segs - 1;
       }
+      for (int sg = sg0; sg < segs; ++sg, ++it) {
+      const int b = it & 1;
+      TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
+      tc_fence_after();
+      if constexpr (EPI == kTcDw) {
+        // per-node quantisation, as k_gemm_tc's dW epilogue (DESIGN.md §3)
+#pragma unroll
+        for (int c = 0; c < COLS / 16; ++c) {
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float x = v[j];
+            amax = fmax_nan(amax, fabsf(x));
+            acc[c * 16 + j] += __float2ll_rn(x);
+          }
+        }
+      } else {
+        // one 32-column chunk per iteration, not unrolled: the unrolled
+        // epilogue overflowed the instruction cache (stall_no_inst at K = 784)
+#pragma unroll 1
+        for (int c = 0; c < COLS / 32; ++c) {
+          float v[32];
+          const int col = h * COLS + c * 32;
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + col), v);
+          finish32(v, col);
+        }
       }
       tc_fence_before();
       if (EPI == kTcDw) {
         asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 epilogue warps of this CTA
-        if (warp == 4 && lane == 0) mbar_arrive_leader(&tempty[b]);
+        if (warp == kEpiWarp0 && lane == 0) mbar_arrive_leader(&tempty[b]);
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(&tempty[b]);
@@ -378,6 +409,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       else if (!(amax < ep.lim))
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailOverflow + ep.tensor]), 1ull);
     }
+  } else {
+    regs_dec();   // warps 2, 3: the rest of the first warpgroup
   }
   tc_fence_before();
   cluster_sync_all();

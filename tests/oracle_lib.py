@@ -115,6 +115,38 @@ class Oracle:
         assert rc == 0
         return g, lo.value
 
+    def forward_backward_wide(self, widths, act, loss, params, x, y, act_ext=None, tau=0.0,
+                              counts=False):
+        """vo_forward_backward_wide[_masked] (port only): the wide-model variant,
+        examples in parallel, compensated sums (pinned to forward_backward in
+        tests).  act_ext {layer: rows x width fp32 activations}: relu masks of
+        near-zero pre-activations (|z| <= tau max|z|) taken from them."""
+        assert self.kind == "port"
+        f = self.lib.vo_forward_backward_wide_masked
+        f.argtypes = self._fb.argtypes[:8] + [C.c_void_p, C.c_double, _f64p, _f64p,
+                                              C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        w, n = _widths(widths)
+        g = np.empty(self.param_count(widths), np.float64)
+        lo = C.c_double()
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        params = np.ascontiguousarray(params, np.float64)
+        keep, ptrs = [], None
+        if act_ext:
+            ptrs = (C.c_void_p * len(widths))()
+            for l, a in act_ext.items():
+                a = np.ascontiguousarray(a, np.float32)
+                keep.append(a)
+                ptrs[l] = a.ctypes.data
+        amb, conf = C.c_uint64(), C.c_uint64()
+        rc = f(w, n, ACT[act], LOSS[loss], _ptr(params), _ptr(x), _ptr(y), x.shape[0],
+               C.cast(ptrs, C.c_void_p) if ptrs is not None else None, tau, _ptr(g), C.byref(lo),
+               C.byref(amb), C.byref(conf))
+        assert rc == 0
+        if counts:
+            return g, lo.value, amb.value, conf.value
+        return g, lo.value
+
     def trainer(self, widths, act, loss, seed, global_batch, virtual_nodes, lr,
                 data_seed, dataset_size, n_devices, capacity=1 << 20, parallel=False,
                 shuffle_seed=None, prefetch=False):

@@ -106,3 +106,20 @@ def test_finite_differences(port):
                 fd = (port.forward_backward(w, act, loss, pp, x, y)[1]
                       - port.forward_backward(w, act, loss, pm, x, y)[1]) / (2 * h)
                 assert abs(fd - g[i]) <= 1e-6 * max(1.0, abs(g[i]))
+
+
+@pytest.mark.parametrize("widths,act,loss,B", [([64, 96, 48, 10], "relu", "softmax-cross-entropy", 64),
+                                               ([32, 64, 4], "tanh", "mse", 37),
+                                               ([784, 256, 10], "relu", "softmax-cross-entropy", 16)])
+def test_wide_oracle_pinned_to_exact_oracle(port, widths, act, loss, B):
+    """vo_forward_backward_wide (the checker of the headline-width GPU tests)
+    against the exactly rounded vo_forward_backward: same per-example
+    arithmetic, compensated instead of exact sums — loss bit-identical,
+    gradients within 4 ulp of the element's magnitude."""
+    p = port.init_params(widths, 5)
+    x, y = port.synth_batch(9, 1024, widths[0], widths[-1], 3, B)
+    g0, l0 = port.forward_backward(widths, act, loss, p, x, y)
+    g1, l1 = port.forward_backward_wide(widths, act, loss, p, x, y)
+    assert l1 == l0
+    ulp = np.spacing(np.abs(g0)) + np.spacing(np.abs(g0).max()) * 1e-6
+    assert np.all(np.abs(g1 - g0) <= 4 * ulp)
