@@ -57,15 +57,14 @@ struct PassNode {
   int dev;           // local device index
   uint64_t rows;     // node size
   uint64_t src_row;  // first row in the source batch
-  uint64_t prow;     // first row in the pass
-  uint64_t pcol;     // first column in the padded feature-major buffers
+  uint64_t prow;     // first row in the pass (node rows padded to 8)
 };
 
 struct Pass {
   std::vector<PassNode> nodes;
-  uint64_t rows = 0;
-  uint64_t ldT = 0;
-  int* d_meta = nullptr;   // [tcol(rows) | row0(n) | rows(n) | col0(n) | src_row(n)]
+  uint64_t rows = 0;       // pass rows, pad rows included
+  uint64_t examples = 0;   // the nodes' rows (no padding)
+  int* d_meta = nullptr;   // [valid(rows) | row0(n) | rows(n) | row0(n) | src_row(n)]
 };
 
 }  // namespace
@@ -132,7 +131,7 @@ struct vnt_engine {
   uint64_t acc_partials = 0;           // per-node partials this process added in the round
 
   // pass buffers
-  uint64_t cap_rows = 0, cap_ldT = 0, cap_vns = 0;
+  uint64_t cap_rows = 0, cap_vns = 0;
   double* xin = nullptr;   // = xbuf[cur]: the staged batch the kernels read
   double* yin = nullptr;
   double* xbuf[2] = {nullptr, nullptr};   // double-buffered input staging
@@ -159,7 +158,7 @@ struct vnt_engine {
     bool on_device = false;
     bool valid = false;
   } pf_next;
-  std::vector<float*> X, XT, D, DT;
+  std::vector<float*> X, D;
   // 3xTF32 operand twins (hi = rna_tf32(x), lo = x - hi), only when split.
   bool split = false;
   // whole-node kernel for small all-FFMA models (kernels_node.cuh)
@@ -176,7 +175,7 @@ struct vnt_engine {
   uint64_t host_n = 0;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   uint64_t tail_examples = 0;          // examples node kernels already added to the tail
-  std::vector<float*> Xh, Xl, XTh, XTl, Dh, Dl, DTh, DTl;
+  std::vector<float*> Xh, Xl, Dh, Dl;
   float *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
   float* logits = nullptr;
   double* vn_mean = nullptr;
@@ -303,10 +302,6 @@ uint32_t ntensors(const vnt_engine* e) { return 2u * e->L; }
 float pow2f(int s) { return std::ldexp(1.0f, s); }
 
 const float* sp_scale(vnt_engine* e, int t) { return &e->d_sp->scale[t]; }
-// DT[l] is consumed by the dW of layer l-1; tcgen05 dW expects it pre-scaled by 2^s.
-const float* dts_ptr(vnt_engine* e, int l) {
-  return e->tc_layer[l - 1] ? &e->d_sp->dts[l] : nullptr;
-}
 
 void drop_graphs(vnt_engine* e) {
   for (auto& kv : e->graph_cache)
@@ -325,7 +320,6 @@ void fill_step_params(vnt_engine* e, double lr, double inv_b) {
     h.scale[t] = pow2f(e->scales[t]);
     h.inv_scale[t] = std::ldexp(1.0, -e->scales[t]);
   }
-  for (int l = 1; l <= e->L; ++l) h.dts[l] = e->tc_layer[l - 1] ? pow2f(e->scales[2 * (l - 1)]) : 1.f;
   h.lr = lr;
   h.mu = e->opt.momentum;
   h.inv_b = inv_b;
@@ -354,11 +348,10 @@ int initial_scale(uint64_t batch) {
   return kScaleTargetBits - (int)std::ceil(std::log2((double)std::max<uint64_t>(batch, 1)));
 }
 
-void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
+void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t vns) {
   const int L = e->L;
-  if (rows <= e->cap_rows && ldT <= e->cap_ldT && vns <= e->cap_vns) return;
+  if (rows <= e->cap_rows && vns <= e->cap_vns) return;
   rows = std::max(rows, e->cap_rows);
-  ldT = std::max(ldT, e->cap_ldT);
   vns = std::max(vns, e->cap_vns);
   VNT_CUDA(cudaStreamSynchronize(e->stream));
   if (e->copy_stream) VNT_CUDA(cudaStreamSynchronize(e->copy_stream));
@@ -378,8 +371,7 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
   fre(e->logits);
   fre(e->vn_mean);
   fre(e->vn_m2);
-  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT, &e->Xh, &e->Xl, &e->XTh, &e->XTl, &e->Dh, &e->Dl,
-                  &e->DTh, &e->DTl})
+  for (auto* v : {&e->X, &e->D, &e->Xh, &e->Xl, &e->Dh, &e->Dl})
     for (auto*& p : *v) fre(p);
   const uint64_t in = e->widths[0], out = e->widths[L];
   for (int b = 0; b < 2; ++b) {
@@ -391,38 +383,23 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t ldT, uint64_t vns) {
   e->logits = (float*)dalloc(rows * out * sizeof(float));
   e->vn_mean = (double*)dalloc(vns * in * sizeof(double));
   e->vn_m2 = (double*)dalloc(vns * in * sizeof(double));
-  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT, &e->Xh, &e->Xl, &e->XTh, &e->XTl, &e->Dh, &e->Dl,
-                  &e->DTh, &e->DTl})
-    v->assign(L + 1, nullptr);
+  for (auto* v : {&e->X, &e->D, &e->Xh, &e->Xl, &e->Dh, &e->Dl}) v->assign(L + 1, nullptr);
   for (int l = 0; l <= L; ++l) {
     const uint64_t w = e->widths[l];
-    if (l < L) {
-      e->X[l] = (float*)dalloc(rows * w * sizeof(float));
-      e->XT[l] = (float*)dalloc(w * ldT * sizeof(float));
-      VNT_CUDA(cudaMemset(e->XT[l], 0, w * ldT * sizeof(float)));   // padding stays zero
-    }
-    if (l > 0) {
-      e->D[l] = (float*)dalloc(rows * w * sizeof(float));
-      e->DT[l] = (float*)dalloc(w * ldT * sizeof(float));
-      VNT_CUDA(cudaMemset(e->DT[l], 0, w * ldT * sizeof(float)));
-    }
+    if (l < L) e->X[l] = (float*)dalloc(rows * w * sizeof(float));
+    if (l > 0) e->D[l] = (float*)dalloc(rows * w * sizeof(float));
     if (e->split) {
-      if (l < L && e->tc_layer[l]) {   // operands of layer l: X[l] (fwd), XT[l] (dW)
+      if (l < L && e->tc_layer[l]) {   // operands of layer l: X[l] (fwd; dW, MN-major)
         e->Xh[l] = (float*)dalloc(rows * w * sizeof(float));
         e->Xl[l] = (float*)dalloc(rows * w * sizeof(float));
-        e->XTh[l] = (float*)dalloc(w * ldT * sizeof(float));
-        e->XTl[l] = (float*)dalloc(w * ldT * sizeof(float));
       }
-      if (l > 0 && e->tc_layer[l - 1]) {   // D[l] (bwd-data of l-1), DT[l] (dW of l-1)
+      if (l > 0 && e->tc_layer[l - 1]) {   // D[l] (bwd-data of l-1; dW of l-1, MN-major)
         e->Dh[l] = (float*)dalloc(rows * w * sizeof(float));
         e->Dl[l] = (float*)dalloc(rows * w * sizeof(float));
-        e->DTh[l] = (float*)dalloc(w * ldT * sizeof(float));
-        e->DTl[l] = (float*)dalloc(w * ldT * sizeof(float));
       }
     }
   }
   e->cap_rows = rows;
-  e->cap_ldT = ldT;
   e->cap_vns = vns;
 }
 
@@ -454,27 +431,26 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
   const uint64_t budget = e->opt.resident_rows ? e->opt.resident_rows : ~0ull;
   Pass cur;
   for (const auto& n : local) {
-    if (!cur.nodes.empty() && cur.rows + n.rows > budget) {
+    if (!cur.nodes.empty() && cur.examples + n.rows > budget) {
       passes.push_back(cur);
       cur = Pass{};
     }
     PassNode pn = n;
     pn.prow = cur.rows;
-    pn.pcol = cur.ldT;
-    cur.rows += n.rows;
-    cur.ldT += round_up(n.rows, 32);
+    cur.rows += round_up(n.rows, 8);   // a node's dW K-chain runs in whole k8 steps
+    cur.examples += n.rows;
     cur.nodes.push_back(pn);
   }
   if (!cur.nodes.empty()) passes.push_back(cur);
   for (auto& p : passes) {
     const size_t nn = p.nodes.size();
-    std::vector<int> meta(p.rows + 4 * nn);
+    std::vector<int> meta(p.rows + 4 * nn, 0);
     for (size_t k = 0; k < nn; ++k) {
       const auto& pn = p.nodes[k];
-      for (uint64_t r = 0; r < pn.rows; ++r) meta[pn.prow + r] = (int)(pn.pcol + r);
+      for (uint64_t r = 0; r < pn.rows; ++r) meta[pn.prow + r] = 1;   // pad rows stay 0
       meta[p.rows + k] = (int)pn.prow;
       meta[p.rows + nn + k] = (int)pn.rows;
-      meta[p.rows + 2 * nn + k] = (int)pn.pcol;
+      meta[p.rows + 2 * nn + k] = (int)pn.prow;
       meta[p.rows + 3 * nn + k] = (int)pn.src_row;
     }
     p.d_meta = (int*)dalloc(meta.size() * sizeof(int));
@@ -519,23 +495,21 @@ void dispatch_skinny(int no, A&&... a) {
 template <int NO>
 struct FwdSkinny {
   static void run(cudaStream_t s, const float* X, int K, const float* WT, int no, const float* b,
-                  int rows, int act, int last, float* out, float* outT, int ldT, const int* tcol) {
+                  int rows, int act, int last, float* out) {
     k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8 * skinny_rows<NO>()), 256, 0, s>>>(
-        X, K, WT, no, b, rows, act, last, out, outT, ldT, tcol);
+        X, K, WT, no, b, rows, act, last, out);
   }
 };
 template <int NO>
 struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
-                  int act, const float* Xprev, float* Dout, float* DT, int ldT, const int* tcol,
-                  const float* tscale, float* Dh, float* Dl, float* DTh, float* DTl) {
+                  int act, const float* Xprev, float* Dout, float* Dh, float* Dl) {
     static const int chunks = [] {   // 32-row chunks per CTA (VNT_BWD_SKINNY_CHUNKS)
       const char* v = getenv("VNT_BWD_SKINNY_CHUNKS");
       return v ? std::max(1, atoi(v)) : 4;
     }();
     dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32 * chunks)), block(32, 8);
-    k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, DT, ldT, tcol,
-                                            tscale, Dh, Dl, DTh, DTl, chunks);
+    k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, Dh, Dl, chunks);
   }
 };
 template <int NO>
@@ -640,9 +614,9 @@ void start_prefetch(vnt_engine* e, const double* x, const double* y, uint64_t ba
   auto& passes = plan_for(e, local);
   if (passes.size() != 1) return;
   const Pass& p = passes[0];
-  const bool fits = p.rows <= e->cap_rows && p.ldT <= e->cap_ldT && p.nodes.size() <= e->cap_vns;
+  const bool fits = p.rows <= e->cap_rows && p.nodes.size() <= e->cap_vns;
   if (!fits && !may_grow) return;   // never reallocate under a running step
-  ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
+  ensure_capacity(e, p.rows, p.nodes.size());
   const int b = 1 - e->cur;
   stage_inputs_to(e, p, x, y, on_device, e->xbuf[b], e->ybuf[b], e->copy_stream);
   VNT_CUDA(cudaEventRecord(e->pf_event, e->copy_stream));
@@ -820,7 +794,7 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   a.lim = pow2f(e->lim_bits);
   a.G = e->G;
   a.tail = e->tail;
-  a.examples = (long long)p.rows;
+  a.examples = (long long)p.examples;
   const size_t base = ((size_t)a.rc * node_row_floats(e) + node_wt_floats(e) + 8 + 3) & ~(size_t)3;
   a.part_off = (int)base;
   const size_t smem = (base + (CL > 1 ? (size_t)a.nstrips * kNodeOC : 0)) * sizeof(float);
@@ -858,7 +832,7 @@ void run_node_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>*
   }
   VNT_LAUNCH_CHECK();
   e->launches++;
-  e->tail_examples += p.rows;
+  e->tail_examples += p.examples;
   // Nothing in the step reads the lineage statistics: join the branch only
   // before xin is restaged or the step's control words are read (join_stats).
   if (stats) e->stats_join_pending = true;
@@ -874,35 +848,18 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     return;
   }
   const int L = e->L;
-  const uint64_t in = e->widths[0], out = e->widths[L];
+  const uint64_t out = e->widths[L];
   const size_t nn = p.nodes.size();
   cudaStream_t s = e->stream;
-  // The tcgen05 dW reads each node's columns padded to 32: keep the padding zero
-  // (a previous pass with another layout may have written there).
-  bool padded = false;
-  for (const auto& pn : p.nodes) padded |= (pn.rows % 32) != 0;
-  if (padded) {
-    for (int l = 0; l < L; ++l) {
-      if (!e->tc_layer[l]) continue;
-      // the dW reads the 3xTF32 twins when they exist, the plain copies otherwise
-      for (float* t : {e->XT[l], e->XTh[l], e->XTl[l]})
-        if (t) VNT_CUDA(cudaMemsetAsync(t, 0, e->widths[l] * p.ldT * sizeof(float), s));
-      for (float* t : {e->DT[l + 1], e->DTh[l + 1], e->DTl[l + 1]})
-        if (t) VNT_CUDA(cudaMemsetAsync(t, 0, e->widths[l + 1] * p.ldT * sizeof(float), s));
-    }
-  }
-  const int* tcol = p.d_meta;
+  const int* valid = p.d_meta;
   const int* row0 = p.d_meta + p.rows;
   const int* nrows = row0 + nn;
-  const int* col0 = nrows + nn;
-  const int rows = (int)p.rows, ldT = (int)p.ldT;
+  const int rows = (int)p.rows;
   {
-    dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(p.rows, 32)), block(32, 8);
     // A 3xTF32 first layer reads only the twins (allocated iff it is one).
     const bool twins = e->Xh[0] != nullptr;
-    k_ingest<<<grid, block, 0, s>>>(e->xin, twins ? nullptr : e->X[0], twins ? nullptr : e->XT[0],
-                                    e->Xh[0], e->Xl[0], e->XTh[0], e->XTl[0], tcol, rows, (int)in,
-                                    ldT);
+    k_ingest<<<(unsigned)p.rows, 128, 0, s>>>(e->xin, twins ? nullptr : e->X[0], e->Xh[0], e->Xl[0], valid,
+                                              (int)e->widths[0]);
     VNT_LAUNCH_CHECK();
     e->launches++;
   }
@@ -920,48 +877,37 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     const float* b = e->w32 + e->boff[l];
     prof_begin(e);
     if (e->tc_layer[l]) {
-      tc_forward(e, l, rows, ldT, tcol, last);
+      tc_forward(e, l, rows, last);
     } else if (N <= 32) {
       dispatch_skinny<FwdSkinny>(N, s, e->X[l], K, e->wt32 + e->wtoff[l], N, b, rows, e->act,
-                                 last ? 1 : 0,
-                                 last ? e->logits : e->X[l + 1], last ? nullptr : e->XT[l + 1],
-                                 ldT, tcol);
+                                 last ? 1 : 0, last ? e->logits : e->X[l + 1]);
       VNT_LAUNCH_CHECK();
       e->launches++;
     } else {
       dim3 grid((unsigned)ceil_div(N, 64), (unsigned)ceil_div(p.rows, 64));
       if (last) {
         k_gemm_ffma<kEpiLogits><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
-                                                     e->logits, N, nullptr, 0, nullptr, nullptr, 0,
-                                                     nullptr);
+                                                     e->logits, N, nullptr, 0);
       } else {
         k_gemm_ffma<kEpiHidden><<<grid, 256, 0, s>>>(e->X[l], K, W, N, rows, N, K, b, e->act,
-                                                     e->X[l + 1], N, e->XT[l + 1], ldT, tcol,
-                                                     nullptr, 0, nullptr);
+                                                     e->X[l + 1], N, nullptr, 0);
       }
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
     prof_end(e, 2.0 * rows * (double)K * N);
-    if (!last && !e->tc_layer[l]) {   // tcgen05 epilogues write the twins themselves
+    if (!last && !e->tc_layer[l])   // tcgen05 epilogues write the twins themselves
       split_into(e, e->X[l + 1], e->Xh[l + 1], e->Xl[l + 1], p.rows * (uint64_t)N);
-      split_into(e, e->XT[l + 1], e->XTh[l + 1], e->XTl[l + 1], (uint64_t)N * p.ldT);
-    }
   }
   VNT_CUDA(cudaEventRecord(e->ev[1], s));
-  // Feature-major delta copies DT[l] feed the dW of layer l-1; for tcgen05
-  // layers they carry that dW's 2^s quantisation scale (exact power of two).
-  auto dts = [&](int l) { return dts_ptr(e, l); };
-  // Loss + output delta (model.cpp:289-315).
+  // Loss + output delta (model.cpp:289-315); pad rows get zero deltas.
   {
     const unsigned warps_per_block = 8;
     k_loss<<<(unsigned)ceil_div(p.rows, warps_per_block), warps_per_block * 32, 0, s>>>(
-        e->logits, e->yin, rows, (int)out, e->loss, e->D[L], e->DT[L], ldT, tcol, e->tail,
-        dts(L), e->d_sp);
+        e->logits, e->yin, rows, (int)out, e->loss, e->D[L], valid, e->tail, e->d_sp);
     VNT_LAUNCH_CHECK();
     e->launches++;
     split_into(e, e->D[L], e->Dh[L], e->Dl[L], p.rows * out);
-    split_into(e, e->DT[L], e->DTh[L], e->DTl[L], out * p.ldT);
   }
   // Backward (model.cpp:317-338): dW/db per node into the exact sum, then delta.
   const float lim = pow2f(e->lim_bits);
@@ -970,7 +916,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     const int tw = 2 * l, tb = 2 * l + 1;
     prof_begin(e);
     if (e->tc_layer[l]) {
-      tc_weight_grad(e, l, p, col0, nrows, 1.f, lim, first_write, tw);
+      tc_weight_grad(e, l, p, row0, nrows, sp_scale(e, tw), lim, first_write, tw);
     } else if (out_l <= 32) {
       dispatch_skinny<DwSkinny>(out_l, s, e->X[l], in_l, e->D[l + 1], out_l, row0, nrows, (int)nn,
                                 sp_scale(e, tw), lim, e->G + e->woff[l], e->tail, tw);
@@ -978,8 +924,8 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       e->launches++;
     } else {
       dim3 grid((unsigned)ceil_div(out_l, 64), (unsigned)ceil_div(in_l, 64), (unsigned)nn);
-      k_dw_ffma<<<grid, 256, 0, s>>>(e->XT[l], e->DT[l + 1], ldT, in_l, out_l, col0, nrows,
-                                     sp_scale(e, tw), lim, e->G + e->woff[l], e->tail, tw);
+      k_dw_ffma<<<grid, 256, 0, s>>>(e->X[l], e->D[l + 1], in_l, out_l, row0, nrows, sp_scale(e, tw), lim,
+                                     e->G + e->woff[l], e->tail, tw);
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
@@ -995,28 +941,24 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     if (l > 0) {
       prof_begin(e);
       if (e->tc_layer[l]) {
-        tc_backward_data(e, l, rows, ldT, tcol, dts(l));
+        tc_backward_data(e, l, rows);
       } else if (out_l <= 32) {
-        // D[l] stays plain for k_db; DT[l] feeds only the (twin-reading) dW of l-1
+        // D[l] stays plain for k_db; its twins feed a tcgen05 bwd-data / dW of l-1
         dispatch_skinny<BwdSkinny>(out_l, s, e->D[l + 1], e->w32 + e->woff[l], out_l, in_l, rows,
-                                   e->act, e->X[l], e->D[l], e->DTh[l] ? nullptr : e->DT[l], ldT,
-                                   tcol, dts(l), e->Dh[l], e->Dl[l], e->DTh[l], e->DTl[l]);
+                                   e->act, e->X[l], e->D[l], e->Dh[l], e->Dl[l]);
         VNT_LAUNCH_CHECK();
         e->launches++;
       } else {
         const float* WT = e->wt32 + e->wtoff[l];
         dim3 grid((unsigned)ceil_div(in_l, 64), (unsigned)ceil_div(p.rows, 64));
         k_gemm_ffma<kEpiBwd><<<grid, 256, 0, s>>>(e->D[l + 1], out_l, WT, in_l, rows, in_l, out_l,
-                                                  nullptr, e->act, e->D[l], in_l, e->DT[l], ldT,
-                                                  tcol, e->X[l], in_l, dts(l));
+                                                  nullptr, e->act, e->D[l], in_l, e->X[l], in_l);
         VNT_LAUNCH_CHECK();
         e->launches++;
       }
       prof_end(e, 2.0 * rows * (double)in_l * out_l);
-      if (!e->tc_layer[l] && out_l > 32) {   // tcgen05 and skinny kernels write twins
+      if (!e->tc_layer[l] && out_l > 32)   // tcgen05 and skinny kernels write twins
         split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l);
-        split_into(e, e->DT[l], e->DTh[l], e->DTl[l], (uint64_t)in_l * p.ldT);
-      }
     }
   }
   if (stats) VNT_CUDA(cudaStreamWaitEvent(e->stream, e->join_ev, 0));
@@ -1118,7 +1060,7 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
   }
   for (size_t i = 0; i < passes.size(); ++i) {
     const auto& p = passes[i];
-    ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
+    ensure_capacity(e, p.rows, p.nodes.size());
     join_stats(e);   // the previous pass's statistics still read xin
     // A prefetched batch is consumed on the first attempt only (on a rescale
     // retry the prefetch slot already holds the next batch).
@@ -1131,7 +1073,7 @@ void accumulate(vnt_engine* e, std::vector<PassNode>& local, const double* x, co
     run_pass(e, p, do_stats ? &stats[i] : nullptr, !e->acc_started,
              layer_comm && i + 1 == passes.size());
     e->acc_started = true;
-    e->acc_examples += p.rows;
+    e->acc_examples += p.examples;
     e->acc_partials += p.nodes.size();
   }
 }
@@ -1579,7 +1521,7 @@ std::vector<PassNode> local_nodes(vnt_engine* e, const uint64_t* node_sizes,
         throw EngineError(VNT_ERR_CAPACITY, "virtual node " + std::to_string(n) + " (" +
                                                 std::to_string(node_sizes[n]) +
                                                 " examples) exceeds memory capacity of device");
-      local.push_back(PassNode{(int)n, d, node_sizes[n], off, 0, 0});
+      local.push_back(PassNode{(int)n, d, node_sizes[n], off, 0});
     }
     off += node_sizes[n];
   }
@@ -1638,7 +1580,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       if (passes.size() == 1) {
         run_pass(e, passes[0], stats, true, overlap);
         e->acc_started = true;
-        e->acc_examples += passes[0].rows;
+        e->acc_examples += passes[0].examples;
       }
       add_examples_tail(e);
       if (events) VNT_CUDA(cudaEventRecord(e->ev[2], e->stream));
@@ -1661,7 +1603,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       // Graph path: host prep outside, the whole device step as one graph launch.
       const Pass& p = (*passes)[0];
       ensure_combine(e, p.nodes.size());
-      ensure_capacity(e, p.rows, p.ldT, p.nodes.size());
+      ensure_capacity(e, p.rows, p.nodes.size());
       size_t off = 0;
       const std::vector<StatsLaunch> stats = prep_stats(e, p, off);
       hc.mark();   // 2: plan, capacity, stats prep
@@ -1726,7 +1668,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
           ge.prof_flops.assign(e->prof_flops.end() - (long)(ge.prof_n / 2), e->prof_flops.end());
         } else {
           e->acc_started = true;
-          e->acc_examples = p.rows;
+          e->acc_examples = p.examples;
           if (e->shard) {   // host state the captured gathers / sharded update leave
             e->ag_pending = true;
             e->ag_wait.assign(e->L, 0);
@@ -2045,7 +1987,7 @@ void vnt_engine_destroy(vnt_engine* e) {
   for (auto* p : e->scratch) cudaFree(p);
   for (void* p : {(void*)e->w32h, (void*)e->w32l, (void*)e->wt32h, (void*)e->wt32l})
     if (p) cudaFree(p);
-  for (auto* v : {&e->Xh, &e->Xl, &e->XTh, &e->XTl, &e->Dh, &e->Dl, &e->DTh, &e->DTl})
+  for (auto* v : {&e->Xh, &e->Xl, &e->Dh, &e->Dl})
     for (auto* p : *v)
       if (p) cudaFree(p);
   for (void* p : {(void*)e->w64, (void*)e->v64, (void*)e->w32, (void*)e->wt32, (void*)e->G,
@@ -2053,7 +1995,7 @@ void vnt_engine_destroy(vnt_engine* e) {
                   (void*)e->xbuf[1], (void*)e->ybuf[1], (void*)e->logits,
                   (void*)e->vn_mean, (void*)e->vn_m2})
     if (p) cudaFree(p);
-  for (auto* v : {&e->X, &e->XT, &e->D, &e->DT})
+  for (auto* v : {&e->X, &e->D})
     for (auto* p : *v)
       if (p) cudaFree(p);
   for (auto& d : e->devs) {
@@ -2226,7 +2168,7 @@ int vnt_engine_device_step(vnt_engine* e, int32_t device, const double* x, const
       if (node_sizes[k] > e->devs[device].capacity)
         throw EngineError(VNT_ERR_CAPACITY, "micro-batch of " + std::to_string(node_sizes[k]) +
                                                 " examples exceeds memory capacity of device");
-      local.push_back(PassNode{(int)k, device, node_sizes[k], off, 0, 0});
+      local.push_back(PassNode{(int)k, device, node_sizes[k], off, 0});
       off += node_sizes[k];
       m.waves += 1;
       m.examples += node_sizes[k];

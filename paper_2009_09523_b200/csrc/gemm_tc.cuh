@@ -99,19 +99,18 @@ struct EpiArgs {
   int act;
   float* out;
   int ldo;
-  float* outT;
-  int ldT;
-  const int* tcol;
   const float* Xprev;
   int ldx;
-  const float* tscale_p;  // scale of the feature-major copy (DT: 2^s of the next dW); null = 1
-  // 3xTF32 operand twins of out / outT for the next tcgen05 consumer (or nullptr)
-  float *outh, *outl, *outTh, *outTl;
-  // dW
+  // 3xTF32 operand twins of out for the next tcgen05 consumer (or nullptr)
+  float *outh, *outl;
+  // dW: per-node partial g -> rint(g * 2^s) (scale_p: 2^s of the tensor, read
+  // per CTA from the step parameters), |g 2^s| < lim
   long long* G;
   int ldg;
   int first;
-  float scale, lim;
+  const float* scale_p;
+  float lim;
+  int mn3;   // dW operand maps are 3-D (bit 0: A, bit 1: B), see make_map_mn3
   long long* tail;
   int tensor;
   // tile raster: groups of group_m tile rows, column-major inside a group, so
@@ -129,12 +128,13 @@ struct EpiArgs {
   int kfirst;
 };
 
-// K range [kb, kb + kl) of segment s: a virtual node (dW) or a K chunk (fwd/bwd).
+// K range [kb, kb + kl) of segment s: a virtual node's rows rounded up to 8
+// (dW; pad rows carry zero deltas) or a K chunk (fwd/bwd).
 __device__ __forceinline__ void seg_range(int s, int nseg, const int* seg_k0, const int* seg_rows, int K,
                                           int kchunk, int kfirst, int& kb, int& kl) {
   if (nseg > 0) {
     kb = seg_k0[s];
-    kl = (int)round_up(seg_rows[s], 32);
+    kl = (int)round_up(seg_rows[s], 8);
   } else if (kchunk > 0) {
     kb = s == 0 ? 0 : kfirst + (s - 1) * kchunk;
     const int len = s == 0 ? kfirst : kchunk;
@@ -189,6 +189,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// 3-D box {32 features, rows, feature groups} of an MN-major operand map
+// (make_map_mn3): all 32-feature groups of a tile in one instruction.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"((uint64_t)tm), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
                                             int c1) {
   asm volatile(
@@ -216,10 +227,27 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: kind::tf32, D fp32, A/B tf32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: kind::tf32, D fp32, A/B tf32, K-major (fwd /
+// bwd-data) or MN-major (dW: bits 15/16; both operands are the row-major
+// activations / deltas themselves, K = rows).
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool mn_major = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (mn_major ? (3u << 15) : 0u) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// MN-major tf32 operand: the only smem layout tcgen05 takes for it is the
+// 128-B swizzle with 32-B atomicity (layout type SWIZZLE_128B_BASE32B; what a
+// TMA box with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B lands in): rows of 128 B
+// (32 features), 4-row atoms of 512 B (SBO), the 32-feature groups of an
+// operand tile kMnGroupBytes apart (LBO).  A k8 MMA step = 8 rows = 1024 B.
+constexpr uint32_t kMnGroupBytes = 32 * 32 * 4;   // one TMA box: 32 rows x 128 B
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(kMnGroupBytes >> 4) << 16;   // LBO: next 32-feature group
+  d |= (uint64_t)(512 >> 4) << 32;             // SBO: next 4-row atom
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;                      // SWIZZLE_128B_BASE32B
+  return d;
 }
 
 // The MMA role runs on a whole warp with warp-uniform operands; one elected
@@ -388,11 +416,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kl; k += BK) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             mbar_expect_tx(&full[stage], C::kStageBytes);
-            tma_load_2d(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
-            tma_load_2d(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
-            if (SPLIT == 3) {
-              tma_load_2d(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
-              tma_load_2d(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
+            if constexpr (EPI == kTcDw) {
+              // MN-major: 32 rows of the row-major X / D per stage, 32-feature
+              // groups kMnGroupBytes apart — one 3-D box per operand when the
+              // width is a multiple of 32 (ep.mn3 bit 0: A, bit 1: B), else
+              // one 2-D box per group (zero fill past the width)
+              if (ep.mn3 & 1) {
+                tma_load_3d(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / 32);
+                if (SPLIT == 3) tma_load_3d(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / 32);
+              } else {
+#pragma unroll
+                for (int g = 0; g < BM / 32; ++g) {
+                  tma_load_2d(sA + stage * C::kBytesA + g * kMnGroupBytes, &tmA, &full[stage], m0 + 32 * g, kb + k);
+                  if (SPLIT == 3)
+                    tma_load_2d(sAl + stage * C::kBytesA + g * kMnGroupBytes, &tmAl, &full[stage], m0 + 32 * g,
+                                kb + k);
+                }
+              }
+              if (ep.mn3 & 2) {
+                tma_load_3d(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / 32);
+                if (SPLIT == 3) tma_load_3d(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / 32);
+              } else {
+#pragma unroll
+                for (int g = 0; g < BN / 32; ++g) {
+                  tma_load_2d(sB + stage * C::kBytesB + g * kMnGroupBytes, &tmB, &full[stage], n0 + 32 * g, kb + k);
+                  if (SPLIT == 3)
+                    tma_load_2d(sBl + stage * C::kBytesB + g * kMnGroupBytes, &tmBl, &full[stage], n0 + 32 * g,
+                                kb + k);
+                }
+              }
+            } else {
+              tma_load_2d(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
+              tma_load_2d(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
+              if (SPLIT == 3) {
+                tma_load_2d(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
+                tma_load_2d(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
+              }
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -406,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     regs_dec();
     {
-      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, EPI == kTcDw);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;  // global (tile, segment) counter
@@ -427,13 +486,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full[stage], phase);
 #endif
             tc_fence_after();
-            const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
-            const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
-            const uint64_t ald = sdesc_sw128(su32(sAl + stage * C::kBytesA));
-            const uint64_t bld = sdesc_sw128(su32(sBl + stage * C::kBytesB));
+            constexpr bool mn = EPI == kTcDw;
+            const uint64_t ad = mn ? sdesc_sw128_mn(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
+            const uint64_t bd = mn ? sdesc_sw128_mn(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
+            const uint64_t ald = mn ? sdesc_sw128_mn(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
+            const uint64_t bld = mn ? sdesc_sw128_mn(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
+            // dW: a node's K-chain is its rows rounded up to 8 (k8 steps past
+            // that are rows of the next node: skipped); a k8 step is one
+            // 1024-B atom (MN-major), 32 B inside the atom (K-major)
+            const int ksteps = mn ? min(BK, kl - k) / 8 : BK / 8;
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t o = (uint64_t)(kk * 2);
+              if (kk >= ksteps) break;
+              const uint64_t o = (uint64_t)(mn ? kk * 64 : kk * 2);
               mma_tf32(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
               if (SPLIT == 3) {
                 mma_tf32(d, ad + o, bld + o, idesc, 1u);
@@ -457,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;               // TMEM lane quarter this warp may access
     const int h = (warp - kEpiWarp0) >> 2;        // column half
     const int row = q * 32 + lane;        // tile row == TMEM lane
-    const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
+    const float dscale = EPI == kTcDw ? *ep.scale_p : 1.f;   // dW: 2^s of the tensor
     uint32_t it = 0;
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     TC_PROBE_DECL;
@@ -475,7 +540,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto finish32 = [&](float (&v)[32], int col) {
         const int nb = n0 + col;
         if (r >= ep.M) return;
-        const int tc = ep.tcol[r];
         if (EPI == kTcBwd && nb + 32 <= ep.N) {
           const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
 #pragma unroll
@@ -498,18 +562,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (nb + j < ep.N) {
-            const size_t o = (size_t)(nb + j) * ep.ldT + tc;
-            const float t = v[j] * tscale;
-            if (ep.outT) ep.outT[o] = t;
-            if (ep.outTh) {
-              const float th = tf32_rna(t);
-              ep.outTh[o] = th;
-              ep.outTl[o] = t - th;
-            }
-          }
         if (ep.out) {   // null: only the 3xTF32 twins are consumed
           float* orow = ep.out + (size_t)r * ep.ldo + nb;
           if (nb + 32 <= ep.N) {
@@ -571,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float x = v[j];
+              const float x = v[j] * dscale;   // exact: power of two
               amax = fmax_nan(amax, fabsf(x));
               acc[c * 16 + j] += __float2ll_rn(x);
             }
@@ -654,7 +706,8 @@ inline EncodeTiledFn encode_fn() {
 // K-major fp32 operand [rows][K] with leading dimension ld (elements); box
 // 32 (K, 128 B) x box_rows, 128B swizzle, zero fill out of bounds.
 inline CUtensorMap make_map(const float* base, uint64_t rows, uint64_t K, uint64_t ld,
-                            uint32_t box_rows) {
+                            uint32_t box_rows,
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {K, rows};
   const cuuint64_t strides[1] = {ld * sizeof(float)};
@@ -662,9 +715,28 @@ inline CUtensorMap make_map(const float* base, uint64_t rows, uint64_t K, uint64
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw EngineError(9, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+// MN-major dW operand [rows][F] (features contiguous, F % 32 == 0) as a 3-D
+// tensor {32 features, rows, F / 32 groups}: a box {32, 32, box_groups} puts
+// the groups kMnGroupBytes apart in smem, the layout the MMA descriptor
+// expects, in one TMA instruction.
+inline CUtensorMap make_map_mn3(const float* base, uint64_t rows, uint64_t F, uint64_t ld,
+                                uint32_t box_groups) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {32, rows, F / 32};
+  const cuuint64_t strides[2] = {ld * sizeof(float), 32 * sizeof(float)};
+  const cuuint32_t box[3] = {32, 32, box_groups};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw EngineError(9, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
   return m;
 }
 
@@ -704,6 +776,12 @@ bool tc_use_pair() {
 // kernel).  Per SM the pair reads half of B and writes half of B's
 // stages into smem; with the whole-warp MMA issue it beats the single-CTA dW
 // on cfg3 (profiles/r01_summary.md).
+// 3-D TMA maps for the MN-major dW operands (VNT_TC_MN3=0: one 2-D box per group).
+bool tc_mn3() {
+  static const bool on = !(getenv("VNT_TC_MN3") && getenv("VNT_TC_MN3")[0] == '0');
+  return on;
+}
+
 bool tc_dw_pair() {
   static const bool on = !(getenv("VNT_TC_DW_PAIR") && getenv("VNT_TC_DW_PAIR")[0] == '0');
   return on;
@@ -731,15 +809,25 @@ struct OpMaps {
   CUtensorMap hi, lo;
 };
 
+// mn_major: the dW operands (X / D rows as K, features contiguous) in the
+// 32-B-atom 128-B swizzle tcgen05 requires for MN-major tf32; mn3_groups > 0:
+// as 3-D maps loading that many 32-feature groups per box (width % 32 == 0).
 OpMaps op_maps(const vnt_engine* e, const float* full, const float* hi, const float* lo,
-               uint64_t rows, uint64_t K, uint64_t ld, uint32_t box) {
+               uint64_t rows, uint64_t K, uint64_t ld, uint32_t box, bool mn_major = false,
+               uint32_t mn3_groups = 0) {
   using namespace vntb::tc;
+  const CUtensorMapSwizzle swz = mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   OpMaps m;
+  if (mn3_groups) {
+    m.hi = make_map_mn3(e->split ? hi : full, rows, K, ld, mn3_groups);
+    m.lo = e->split ? make_map_mn3(lo, rows, K, ld, mn3_groups) : m.hi;
+    return m;
+  }
   if (e->split) {
-    m.hi = make_map(hi, rows, K, ld, box);
-    m.lo = make_map(lo, rows, K, ld, box);
+    m.hi = make_map(hi, rows, K, ld, box, swz);
+    m.lo = make_map(lo, rows, K, ld, box, swz);
   } else {
-    m.hi = make_map(full, rows, K, ld, box);
+    m.hi = make_map(full, rows, K, ld, box, swz);
     m.lo = m.hi;
   }
   return m;
@@ -751,11 +839,15 @@ OpMaps op_maps(const vnt_engine* e, const float* full, const float* hi, const fl
 int tc_kchunk(const vnt_engine* e) {
   static const int env = getenv("VNT_TC_KCHUNK") ? atoi(getenv("VNT_TC_KCHUNK")) : -1;
   if (env >= 0) return env == 0 ? 0 : (int)round_up((uint64_t)env, 32);
-  return e->split ? 256 : 0;
+  return e->split ? 128 : 0;
 }
-// First chunk of a tile (VNT_TC_KFIRST, default 256, multiple of 32).
+// First chunk of a tile (VNT_TC_KFIRST, default 512, multiple of 32): it runs
+// while the previous tile's epilogue still holds the other TMEM buffer.
+// Measured at cfg3 (scripts/sweep_kchunk.py): 512/128 keeps the headline
+// gradient within 1e-5 of max of the fp64 reference at 3 % below no
+// promotion (which is 1.3e-4 off).
 int tc_kfirst() {
-  static const int env = getenv("VNT_TC_KFIRST") ? atoi(getenv("VNT_TC_KFIRST")) : 256;
+  static const int env = getenv("VNT_TC_KFIRST") ? atoi(getenv("VNT_TC_KFIRST")) : 512;
   return std::max(32, (int)round_up((uint64_t)std::max(env, 1), 32));
 }
 
@@ -788,7 +880,7 @@ void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M
   e->launches++;
 }
 
-void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool last) {
+void tc_forward(vnt_engine* e, int l, int rows, bool last) {
   using namespace vntb::tc;
   const int K = (int)e->widths[l], N = (int)e->widths[l + 1];
   if (last) throw vntb::EngineError(1, "tcgen05 path does not produce logits");
@@ -802,26 +894,19 @@ void tc_forward(vnt_engine* e, int l, int rows, int ldT, const int* tcol, bool l
   ep.N = N;
   ep.bias = e->w32 + e->boff[l];
   ep.act = e->act;
-  // Plain X / Xᵀ only when a consumer reads them: a 3xTF32 layer l+1 reads the
+  // Plain X only when a consumer reads it: a 3xTF32 layer l+1 reads the
   // twins, and its bwd-data takes relu' from the hi twin (sign of hi == sign of
   // x); tanh' needs the full value, so tanh keeps the plain X.
   const bool twins = e->Xh[l + 1] != nullptr;
   ep.out = twins && e->act != VNT_ACT_TANH ? nullptr : e->X[l + 1];
   ep.ldo = N;
-  ep.outT = twins ? nullptr : e->XT[l + 1];
-  ep.ldT = ldT;
-  ep.tcol = tcol;
-  ep.tscale_p = nullptr;
   // twins are allocated only when the consuming layer l+1 runs on tcgen05 in 3xTF32
   ep.outh = e->Xh[l + 1];
   ep.outl = e->Xl[l + 1];
-  ep.outTh = e->XTh[l + 1];
-  ep.outTl = e->XTl[l + 1];
   tc_launch<kTcFwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
-void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol,
-                      const float* tscale) {
+void tc_backward_data(vnt_engine* e, int l, int rows) {
   using namespace vntb::tc;
   const int N = (int)e->widths[l], K = (int)e->widths[l + 1];
   const bool pair = tc_use_pair();
@@ -835,41 +920,41 @@ void tc_backward_data(vnt_engine* e, int l, int rows, int ldT, const int* tcol,
   ep.act = e->act;
   ep.out = e->D[l];          // k_db reads the plain delta
   ep.ldo = N;
-  ep.outT = e->DTh[l] ? nullptr : e->DT[l];   // a 3xTF32 dW reads only the twins
-  ep.ldT = ldT;
-  ep.tcol = tcol;
   // relu' / identity' from the hi twin when the plain X was not written (above)
   ep.Xprev = (e->Xh[l] && e->act != VNT_ACT_TANH) ? e->Xh[l] : e->X[l];
   ep.ldx = N;
-  ep.tscale_p = tscale;
   ep.outh = e->Dh[l];
   ep.outl = e->Dl[l];
-  ep.outTh = e->DTh[l];
-  ep.outTl = e->DTl[l];
   tc_launch<kTcBwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
-void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* col0, const int* nrows,
-                    float scale, float lim, bool first, int tensor) {
+// Per-node dW: A = X[l] (rows x in), B = D[l+1] (rows x out), both read as
+// MN-major operands (boxes of 32 features x 32 rows), K = a node's rows.
+void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* row0, const int* nrows,
+                    const float* scale_p, float lim, bool first, int tensor) {
   using namespace vntb::tc;
   const int M = (int)e->widths[l], N = (int)e->widths[l + 1];
-  const uint64_t ldT = p.ldT;
   // CTA pairs (256x128, B's smem traffic per SM halved), see tc_dw_pair().
   const bool pair = tc_use_pair() && tc_dw_pair();
-  const uint32_t bn = pair ? PairCfg<kTcDw, 3>::BNH : TileCfg<kTcDw>::BN;
-  const OpMaps a = op_maps(e, e->XT[l], e->XTh[l], e->XTl[l], M, ldT, ldT, BM);
-  const OpMaps b = op_maps(e, e->DT[l + 1], e->DTh[l + 1], e->DTl[l + 1], N, ldT, ldT, bn);
+  const uint64_t rows = p.rows;
+  // 3-D maps (one TMA per operand and stage) where the width allows
+  const bool a3 = M % 32 == 0 && tc_mn3(), b3 = N % 32 == 0 && tc_mn3();
+  const uint32_t bgroups = (pair ? PairCfg<kTcDw, 3>::BNH : TileCfg<kTcDw>::BN) / 32;
+  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, M, M, 32, true, a3 ? BM / 32 : 0);
+  const OpMaps b = op_maps(e, e->D[l + 1], e->Dh[l + 1], e->Dl[l + 1], rows, N, N, 32, true,
+                           b3 ? bgroups : 0);
   EpiArgs ep{};
+  ep.mn3 = (a3 ? 1 : 0) | (b3 ? 2 : 0);
   ep.M = M;
   ep.N = N;
   ep.G = e->G + e->woff[l];
   ep.ldg = N;
   ep.first = first ? 1 : 0;
-  ep.scale = scale;
+  ep.scale_p = scale_p;
   ep.lim = lim;
   ep.tail = e->tail;
   ep.tensor = tensor;
-  tc_launch<kTcDw>(e, pair, a, b, M, N, (int)ldT, (int)p.nodes.size(), col0, nrows, ep);
+  tc_launch<kTcDw>(e, pair, a, b, M, N, (int)rows, (int)p.nodes.size(), row0, nrows, ep);
 }
 
 }  // namespace

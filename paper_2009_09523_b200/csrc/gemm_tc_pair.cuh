@@ -73,6 +73,15 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* t
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* tm, uint64_t* bar,
+                                                 int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"((uint64_t)tm), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // Whole-warp callers, one elected lane issues (see mma_tf32).
 __device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                               uint32_t accumulate) {
@@ -169,11 +178,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kl; k += BK) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
-            tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
-            tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
-            if (SPLIT == 3) {
-              tma_load_2d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
-              tma_load_2d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
+            if constexpr (EPI == kTcDw) {
+              // MN-major: 32 rows of the row-major X / D per stage (see k_gemm_tc)
+              if (ep.mn3 & 1) {
+                tma_load_3d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / 32);
+                if (SPLIT == 3) tma_load_3d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / 32);
+              } else {
+#pragma unroll
+                for (int g = 0; g < BM / 32; ++g) {
+                  tma_load_2d_pair(sA + stage * C::kBytesA + g * kMnGroupBytes, &tmA, &full[stage], m0 + 32 * g,
+                                   kb + k);
+                  if (SPLIT == 3)
+                    tma_load_2d_pair(sAl + stage * C::kBytesA + g * kMnGroupBytes, &tmAl, &full[stage], m0 + 32 * g,
+                                     kb + k);
+                }
+              }
+              if (ep.mn3 & 2) {
+                tma_load_3d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / 32);
+                if (SPLIT == 3) tma_load_3d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / 32);
+              } else {
+#pragma unroll
+                for (int g = 0; g < BNH / 32; ++g) {
+                  tma_load_2d_pair(sB + stage * C::kBytesB + g * kMnGroupBytes, &tmB, &full[stage], n0 + 32 * g,
+                                   kb + k);
+                  if (SPLIT == 3)
+                    tma_load_2d_pair(sBl + stage * C::kBytesB + g * kMnGroupBytes, &tmBl, &full[stage], n0 + 32 * g,
+                                     kb + k);
+                }
+              }
+            } else {
+              tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
+              tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
+              if (SPLIT == 3) {
+                tma_load_2d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
+                tma_load_2d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
+              }
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -187,7 +226,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     regs_dec();
     if (rank == 0) {
-      constexpr uint32_t idesc = idesc_tf32(PM, BN);
+      constexpr uint32_t idesc = idesc_tf32(PM, BN, EPI == kTcDw);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;
@@ -208,13 +247,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], phase);
 #endif
           tc_fence_after();
-          const uint64_t ad = sdesc_sw128(su32(sA + stage * C::kBytesA));
-          const uint64_t bd = sdesc_sw128(su32(sB + stage * C::kBytesB));
-          const uint64_t ald = sdesc_sw128(su32(sAl + stage * C::kBytesA));
-          const uint64_t bld = sdesc_sw128(su32(sBl + stage * C::kBytesB));
+          constexpr bool mn = EPI == kTcDw;
+          const uint64_t ad = mn ? sdesc_sw128_mn(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
+          const uint64_t bd = mn ? sdesc_sw128_mn(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
+          const uint64_t ald = mn ? sdesc_sw128_mn(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
+          const uint64_t bld = mn ? sdesc_sw128_mn(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
+          const int ksteps = mn ? min(BK, kl - k) / 8 : BK / 8;   // dW: node rows rounded to 8
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t o = (uint64_t)(kk * 2);
+            if (kk >= ksteps) break;
+            const uint64_t o = (uint64_t)(mn ? kk * 64 : kk * 2);
             mma_tf32_pair(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
             if (SPLIT == 3) {
               mma_tf32_pair(d, ad + o, bld + o, idesc, 1u);
@@ -237,7 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int h = (warp - kEpiWarp0) >> 2;
     const int row = q * 32 + lane;
-    const float tscale = (EPI != kTcDw && ep.tscale_p) ? *ep.tscale_p : 1.f;
+    const float dscale = EPI == kTcDw ? *ep.scale_p : 1.f;   // dW: 2^s of the tensor
     uint32_t it = 0;
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     TC_PROBE_DECL;
@@ -246,7 +288,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile, tiles_m, tiles_n, ep.group_m, tm, tn);
       const int m0 = tm * PM + (int)rank * BM, n0 = tn * BN;
       const int r = m0 + row;
-      const int tc = (EPI != kTcDw && r < ep.M) ? ep.tcol[r] : 0;
       long long acc[EPI == kTcDw ? COLS : 1];
       if (EPI == kTcDw) {
 #pragma unroll
@@ -284,19 +325,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (n < ep.N) v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
             }
           }
-          // feature-major copies: lanes are consecutive rows -> 128 B per store
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (nb + j < ep.N) {
-              const size_t o = (size_t)(nb + j) * ep.ldT + tc;
-              const float t = v[j] * tscale;
-              if (ep.outT) ep.outT[o] = t;
-              if (ep.outTh) {
-                const float th = tf32_rna(t);
-                ep.outTh[o] = th;
-                ep.outTl[o] = t - th;
-              }
-            }
         }
         // row-major copies: transpose the warp's 32x32 block through smem so
         // every store writes 128 contiguous bytes of one row (a per-thread
@@ -356,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const float x = v[j];
+            const float x = v[j] * dscale;   // exact: power of two
             amax = fmax_nan(amax, fabsf(x));
             acc[c * 16 + j] += __float2ll_rn(x);
           }

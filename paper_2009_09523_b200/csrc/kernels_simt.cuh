@@ -1,13 +1,14 @@
 // FFMA / memory-bound kernels of the virtual-node step (sm_100a).
 //
-// Layout in HBM: for a pass of `rows` examples (virtual nodes
+// Layout in HBM: for a pass of `rows` rows (virtual nodes
 // concatenated in ascending node id, exactly the contiguous slices of
-// virtual_exec.cpp:221-238):
+// virtual_exec.cpp:221-238, each node's rows padded to a multiple of 8 with
+// pad rows; valid[r] = 0 marks them):
 //   X[l]  fp32 [rows][w_l]      activations (X[0] = input), row-major
-//   XT[l] fp32 [w_l][ldT]       the same, feature-major; node k occupies columns
-//                               [col0_k, col0_k + rows_k), padded to 32 with zeros
-//   D[l]  fp32 [rows][w_l]      dLoss/dZ_l (l = 1..L); DT[l] feature-major
-//   G     int64 [P + tail]      fixed-point gradient sum (exact, order-free)
+//   D[l]  fp32 [rows][w_l]      dLoss/dZ_l (l = 1..L), zero on pad rows
+//   G     int64 [P + gap + tail] fixed-point gradient sum (exact, order-free)
+// The per-node dW GEMMs read X and D as they are (K = rows: MN-major tcgen05
+// operands), so no feature-major copies exist.
 #pragma once
 
 #include "common.cuh"
@@ -36,7 +37,6 @@ enum : int {
 constexpr int kMaxLayers = 64;
 struct StepParams {
   float scale[2 * kMaxLayers];       // 2^s_t: per-node partial quantisation multiplier
-  float dts[kMaxLayers + 1];         // DT[l] copy scale (2^s of the dW consuming it, or 1)
   double inv_scale[2 * kMaxLayers];  // 2^-s_t
   double lr, mu, inv_b;
   double loss_scale;                 // 2^b: per-row loss quantum 2^-b
@@ -53,34 +53,32 @@ __device__ __forceinline__ void put_twins(float* hi, float* lo, size_t idx, floa
   lo[idx] = v - h;
 }
 
-// fp64 batch rows -> fp32 X0 (row-major) and XT0 (feature-major, padded per
-// node); X0/XT0 may be null when only the 3xTF32 twins are consumed.
-__global__ void k_ingest(const double* __restrict__ x, float* __restrict__ X0,
-                         float* __restrict__ XT0, float* __restrict__ X0h, float* __restrict__ X0l,
-                         float* __restrict__ XT0h, float* __restrict__ XT0l,
-                         const int* __restrict__ tcol, int rows, int in, int ldT) {
-  __shared__ float tile[32][33];
-  const int r0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int k = ty; k < 32; k += 8) {
-    const int r = r0 + k, j = j0 + tx;
-    float v = 0.f;
-    if (r < rows && j < in) {
-      v = __double2float_rn(x[(size_t)r * in + j]);
-      const size_t idx = (size_t)r * in + j;
-      if (X0) X0[idx] = v;
-      if (X0h) put_twins(X0h, X0l, idx, v);
+// fp64 batch rows -> fp32 X0 and/or its 3xTF32 twins (X0 null when only the
+// twins are consumed); pad rows (valid[r] == 0) become zeros.  One block per
+// row, two elements per thread and iteration.
+__global__ void __launch_bounds__(128) k_ingest(const double* __restrict__ x, float* __restrict__ X0,
+                                                float* __restrict__ X0h, float* __restrict__ X0l,
+                                                const int* __restrict__ valid, int in) {
+  const int r = blockIdx.x;
+  const bool ok = valid[r] != 0;
+  const double* xr = x + (size_t)r * in;
+  const size_t base = (size_t)r * in;
+  if ((in & 1) == 0) {
+    for (int j = 2 * threadIdx.x; j < in; j += 2 * blockDim.x) {
+      double2 d = ok ? __ldg(reinterpret_cast<const double2*>(xr + j)) : make_double2(0.0, 0.0);
+      const float2 v = make_float2(__double2float_rn(d.x), __double2float_rn(d.y));
+      if (X0) *reinterpret_cast<float2*>(X0 + base + j) = v;
+      if (X0h) {
+        const float2 h = make_float2(tf32_rna(v.x), tf32_rna(v.y));
+        *reinterpret_cast<float2*>(X0h + base + j) = h;
+        *reinterpret_cast<float2*>(X0l + base + j) = make_float2(v.x - h.x, v.y - h.y);
+      }
     }
-    tile[k][tx] = v;
-  }
-  __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int j = j0 + k, r = r0 + tx;
-    if (r < rows && j < in) {
-      const size_t o = (size_t)j * ldT + tcol[r];
-      const float v = tile[tx][k];
-      if (XT0) XT0[o] = v;
-      if (XT0h) put_twins(XT0h, XT0l, o, v);
+  } else {
+    for (int j = threadIdx.x; j < in; j += blockDim.x) {
+      const float v = ok ? __double2float_rn(xr[j]) : 0.f;
+      if (X0) X0[base + j] = v;
+      if (X0h) put_twins(X0h, X0l, base + j, v);
     }
   }
 }
@@ -291,10 +289,8 @@ template <int EPI>
 __global__ void __launch_bounds__(256) k_gemm_ffma(
     const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb, int M, int N,
     int K, const float* __restrict__ bias, int act, float* __restrict__ out, int ldo,
-    float* __restrict__ outT, int ldT, const int* __restrict__ tcol,
-    const float* __restrict__ Xprev, int ldx, const float* __restrict__ tscale_p) {
+    const float* __restrict__ Xprev, int ldx) {
   __shared__ __align__(16) float As[16][64 + 4];
-  const float tscale = tscale_p ? *tscale_p : 1.f;
   __shared__ __align__(16) float Bs[16][64 + 4];
   const int t = threadIdx.x;
   const int tx = t % 16, ty = t / 16;
@@ -336,7 +332,6 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
   for (int i = 0; i < 4; ++i) {
     const int r = m0 + ty * 4 + i;
     if (r >= M) continue;
-    const int tc = (EPI != kEpiLogits) ? tcol[r] : 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx * 4 + j;
@@ -348,7 +343,6 @@ __global__ void __launch_bounds__(256) k_gemm_ffma(
         v = v * act_grad_from_out(act, Xprev[(size_t)r * ldx + n]);
       }
       out[(size_t)r * ldo + n] = v;
-      if (EPI != kEpiLogits) outT[(size_t)n * ldT + tc] = v * tscale;
     }
   }
 }
@@ -376,28 +370,26 @@ __device__ __forceinline__ bool row_loss_q(double loss, const StepParams* sp, lo
 // model.cpp:289-315, one warp per row, fp64 from fp32 logits.  Row loss is
 // quantised at 2^-32 and summed exactly (int64 atomics: order-free).
 __global__ void k_loss(const float* __restrict__ logits, const double* __restrict__ y, int rows,
-                       int outw, int loss_kind, float* __restrict__ D, float* __restrict__ DT,
-                       int ldT, const int* __restrict__ tcol, long long* __restrict__ tail,
-                       const float* __restrict__ tscale_p, const StepParams* __restrict__ sp) {
-  const float tscale = tscale_p ? *tscale_p : 1.f;
+                       int outw, int loss_kind, float* __restrict__ D,
+                       const int* __restrict__ valid, long long* __restrict__ tail,
+                       const StepParams* __restrict__ sp) {
   __shared__ unsigned long long block_loss;   // exact int64 sum of this block's rows
   if (threadIdx.x == 0) block_loss = 0;
   __syncthreads();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int r = warp;
-  if (warp < rows) {
+  if (warp < rows && !valid[r]) {   // pad row: zero delta, no loss
+    for (int o = lane; o < outw; o += 32) D[(size_t)r * outw + o] = 0.f;
+  } else if (warp < rows) {
     const float* z = logits + (size_t)r * outw;
     const double* yr = y + (size_t)r * outw;
-    const int tc = tcol[r];
     double loss = 0.0;
     if (loss_kind == 0) {
       for (int o = lane; o < outw; o += 32) {
         const double d = (double)z[o] - yr[o];
         loss += d * d;
-        const float dl = (float)(2.0 * d / (double)outw);
-        D[(size_t)r * outw + o] = dl;
-        DT[(size_t)o * ldT + tc] = dl * tscale;
+        D[(size_t)r * outw + o] = (float)(2.0 * d / (double)outw);
       }
 #pragma unroll
       for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
@@ -415,9 +407,7 @@ __global__ void k_loss(const float* __restrict__ logits, const double* __restric
       for (int o = lane; o < outw; o += 32) {
         const double zm = (double)z[o] - mx;
         loss -= yr[o] * (zm - lognorm);
-        const float dl = (float)(exp(zm) / norm - yr[o]);
-        D[(size_t)r * outw + o] = dl;
-        DT[(size_t)o * ldT + tc] = dl * tscale;
+        D[(size_t)r * outw + o] = (float)(exp(zm) / norm - yr[o]);
       }
 #pragma unroll
       for (int s = 16; s; s >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, s);
@@ -453,18 +443,18 @@ __device__ __forceinline__ long long quantise(float g, float scale, float lim,
 // ascending); blockIdx.z = node.  Quantised per node and added with exact
 // int64 atomics into the zeroed weight slice of G (order-free).
 __global__ void __launch_bounds__(256) k_dw_ffma(
-    const float* __restrict__ XT, const float* __restrict__ DT, int ldT, int in, int out,
-    const int* __restrict__ vn_col0, const int* __restrict__ vn_rows,
+    const float* __restrict__ X, const float* __restrict__ D, int in, int out,
+    const int* __restrict__ vn_row0, const int* __restrict__ vn_rows,
     const float* __restrict__ scale_p, float lim, long long* __restrict__ G,
     long long* __restrict__ tail, int tensor) {
   __shared__ __align__(16) float As[16][64 + 4];
-  const float scale = *scale_p;
   __shared__ __align__(16) float Bs[16][64 + 4];
+  const float scale = *scale_p;
   const int t = threadIdx.x;
   const int tx = t % 16, ty = t / 16;
   const int i0 = blockIdx.y * 64, o0 = blockIdx.x * 64;
   const int v = blockIdx.z;
-  const int c0 = vn_col0[v], n = vn_rows[v];
+  const int r0 = vn_row0[v], n = vn_rows[v];
   float g[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -472,12 +462,13 @@ __global__ void __launch_bounds__(256) k_dw_ffma(
     for (int j = 0; j < 4; ++j) g[i][j] = 0.f;
   for (int k0 = 0; k0 < n; k0 += 16) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < 4; ++e) {   // rows of X / D, features contiguous across lanes
       const int idx = t + e * 256;
-      const int mm = idx / 16, kk = idx % 16;
+      const int mm = idx % 64, kk = idx / 64;
       const bool kin = (k0 + kk) < n;
-      As[kk][mm] = (kin && i0 + mm < in) ? XT[(size_t)(i0 + mm) * ldT + c0 + k0 + kk] : 0.f;
-      Bs[kk][mm] = (kin && o0 + mm < out) ? DT[(size_t)(o0 + mm) * ldT + c0 + k0 + kk] : 0.f;
+      const size_t r = (size_t)(r0 + k0 + kk);
+      As[kk][mm] = (kin && i0 + mm < in) ? X[r * in + i0 + mm] : 0.f;
+      Bs[kk][mm] = (kin && o0 + mm < out) ? D[r * out + o0 + mm] : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -544,9 +535,7 @@ template <int NO>
 __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X, int K,
                                                     const float* __restrict__ WT, int no,
                                                     const float* __restrict__ bias, int rows,
-                                                    int act, int last, float* __restrict__ out,
-                                                    float* __restrict__ outT, int ldT,
-                                                    const int* __restrict__ tcol) {
+                                                    int act, int last, float* __restrict__ out) {
   // A warp owns R rows so each W value read serves all of them; W^T is staged
   // through shared memory in k-chunks ([o][k], conflict-free).  Per (row, o)
   // the partial sums run lane-strided over k in ascending order and meet in a
@@ -610,33 +599,24 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
       v += bias[lane];
       if (!last) v = act_fwd(act, v);
       out[(size_t)row * no + lane] = v;
-      if (!last) outT[(size_t)lane * ldT + tcol[row]] = v;
     }
   }
 }
 
 // bwd-data through a skinny layer: D[r][i] = (sum_o Dn[r][o] W[i][o]) f'(X[r][i]),
-// o ascending; 32x32 (row, i) tiles, transposed copy through smem.
+// o ascending; 32 features x chunks*32 rows per block (the row block's Dn
+// rows staged in smem), D and its 3xTF32 twins written row-major.
 template <int NO>
 __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn,
                                                     const float* __restrict__ W, int no, int in,
                                                     int rows, int act,
                                                     const float* __restrict__ Xprev,
                                                     float* __restrict__ Dout,
-                                                    float* __restrict__ DT, int ldT,
-                                                    const int* __restrict__ tcol,
-                                                    const float* __restrict__ tscale_p,
                                                     float* __restrict__ Dh, float* __restrict__ Dl,
-                                                    float* __restrict__ DTh,
-                                                    float* __restrict__ DTl, int chunks) {
-  const float tscale = tscale_p ? *tscale_p : 1.f;
-  // 32 features x chunks*32 rows per block, o ascending per output;
-  // transposed copy through smem.
-  __shared__ float tile[32][33];
+                                                    int chunks) {
   __shared__ float dn[32][NO];
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
-  const int i0 = blockIdx.x * 32;
-  const int i = i0 + tx;
+  const int i = blockIdx.x * 32 + tx;
   float w[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) w[o] = (i < in && o < no) ? W[(size_t)i * no + o] : 0.f;
@@ -649,28 +629,18 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
       dn[rr][o] = (r0 + rr < rows && o < no) ? Dn[(size_t)(r0 + rr) * no + o] : 0.f;
     }
     __syncthreads();
+    if (i >= in) continue;
+#pragma unroll 4
     for (int k = ty; k < 32; k += 8) {
       const int r = r0 + k;
+      if (r >= rows) break;
       float acc = 0.f;
 #pragma unroll
       for (int o = 0; o < NO; ++o) acc = fmaf(dn[k][o], w[o], acc);
-      float v = 0.f;
-      if (r < rows && i < in) {
-        v = acc * act_grad_from_out(act, Xprev[(size_t)r * in + i]);
-        Dout[(size_t)r * in + i] = v;
-        if (Dh) put_twins(Dh, Dl, (size_t)r * in + i, v);
-      }
-      tile[k][tx] = v;
-    }
-    __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-      const int ii = i0 + k, r = r0 + tx;
-      if (r < rows && ii < in) {
-        const size_t o = (size_t)ii * ldT + tcol[r];
-        const float t = tile[tx][k] * tscale;
-        if (DT) DT[o] = t;
-        if (DTh) put_twins(DTh, DTl, o, t);
-      }
+      const size_t idx = (size_t)r * in + i;
+      const float v = acc * act_grad_from_out(act, Xprev[idx]);
+      if (Dout) Dout[idx] = v;
+      if (Dh) put_twins(Dh, Dl, idx, v);
     }
   }
 }

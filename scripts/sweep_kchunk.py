@@ -15,8 +15,8 @@ for spec in sys.argv[1:]:
     d = json.loads(out.strip().splitlines()[-1])
     diag = subprocess.run([sys.executable, "scripts/diag_headline.py", "auto"], env=env, capture_output=True,
                           text=True, timeout=600).stdout
-    devs = [float(m) for m in re.findall(r"dev ([0-9.e+-]+)", diag)]
+    devs = [float(m) for m in re.findall(r"max dev ([0-9.e+-]+)", diag)] or [float("nan")]
     loss = re.search(r"loss ([0-9.]+) ([0-9.]+)", diag)
     print(f"kfirst {kf:>5} kchunk {kc:>4}: {d['value']:.4g} samples/s, {d['ms_per_step']:.3f} ms/step, "
-          f"frac {d['roofline']['frac']:.3f} | max grad dev {max(devs):.2e} of max, "
+          f"frac {d['roofline']['frac']:.3f} | grad dev (masks resolved) {max(devs):.2e} of max, "
           f"loss {loss.group(1)} vs {loss.group(2)}", flush=True)

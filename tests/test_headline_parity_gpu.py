@@ -4,8 +4,9 @@ oracle (model.cpp:238-360 restated as vo_forward_backward_wide, pinned to the
 exactly rounded oracle in tests/test_oracle.py).
 
 The dense layers run as 3xTF32 tcgen05 GEMMs with K = 4096 (forward,
-bwd-data; accumulated in TMEM in 128-column chunks added in fp32 registers)
-and per-node dW K-chains of 8 (cfg3-like) or 256 rows (cfg4-like).
+bwd-data; accumulated in TMEM in K chunks of 512 then 128 columns, added in
+fp32 registers) and per-node dW K-chains of 8 (cfg3-like) or 256 rows
+(cfg4-like) read as MN-major operands straight from the row-major activations.
 
 Stated tolerances (fp32-grade arithmetic against fp64):
   * mean gradient: max |g - g_ref| <= 2e-5 * max |g_ref|, per tensor
