@@ -492,12 +492,37 @@ void dispatch_skinny(int no, A&&... a) {
   else F<32>::run(a...);
 }
 
+// W^T of a skinny layer fits in shared memory: the persistent resident-W kernel.
+constexpr size_t kSkinnyResidentSmem = 200 * 1024;
 template <int NO>
 struct FwdSkinny {
-  static void run(cudaStream_t s, const float* X, int K, const float* WT, int no, const float* b,
+  static void run(cudaStream_t s, int sms, const float* X, int K, const float* WT, int no, const float* b,
                   int rows, int act, int last, float* out) {
+    const size_t smem = (size_t)no * K * sizeof(float);
+    if (K % 4 == 0 && smem <= kSkinnyResidentSmem) {
+      static bool attr = false;
+      if (!attr) {
+        VNT_CUDA(cudaFuncSetAttribute(k_fwd_skinny_res<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSkinnyResidentSmem));
+        attr = true;
+      }
+      const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(sms, ceil_div(rows, 32)));
+      k_fwd_skinny_res<NO><<<grid, 1024, smem, s>>>(X, K, WT, no, b, rows, act, last, out);
+      return;
+    }
     k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8 * skinny_rows<NO>()), 256, 0, s>>>(
         X, K, WT, no, b, rows, act, last, out);
+  }
+};
+template <int NO>
+struct BackSkinny {
+  static void run(cudaStream_t s, const float* X, const float* Dn, const float* W, int in, int no, int act,
+                  const int* row0, const int* nrows, int nn, float* Dout, float* Dh, float* Dl,
+                  const float* scale_w, long long* Gw, int tw, const float* scale_b, long long* Gb, int tb,
+                  float lim, long long* tail) {
+    dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
+    k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, Dh, Dl, scale_w, Gw, tw,
+                                               scale_b, Gb, tb, lim, tail);
   }
 };
 template <int NO>
@@ -879,7 +904,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     if (e->tc_layer[l]) {
       tc_forward(e, l, rows, last);
     } else if (N <= 32) {
-      dispatch_skinny<FwdSkinny>(N, s, e->X[l], K, e->wt32 + e->wtoff[l], N, b, rows, e->act,
+      dispatch_skinny<FwdSkinny>(N, s, e->sm_count, e->X[l], K, e->wt32 + e->wtoff[l], N, b, rows, e->act,
                                  last ? 1 : 0, last ? e->logits : e->X[l + 1]);
       VNT_LAUNCH_CHECK();
       e->launches++;
@@ -911,17 +936,26 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
   }
   // Backward (model.cpp:317-338): dW/db per node into the exact sum, then delta.
   const float lim = pow2f(e->lim_bits);
+  int db_done = -1;   // a fused skinny backward already produced this layer's db
   for (int l = L - 1; l >= 0; --l) {
     const int in_l = (int)e->widths[l], out_l = (int)e->widths[l + 1];
     const int tw = 2 * l, tb = 2 * l + 1;
+    const bool skinny = !e->tc_layer[l] && out_l <= 32;
     prof_begin(e);
     if (e->tc_layer[l]) {
       tc_weight_grad(e, l, p, row0, nrows, sp_scale(e, tw), lim, first_write, tw);
-    } else if (out_l <= 32) {
-      dispatch_skinny<DwSkinny>(out_l, s, e->X[l], in_l, e->D[l + 1], out_l, row0, nrows, (int)nn,
-                                sp_scale(e, tw), lim, e->G + e->woff[l], e->tail, tw);
+    } else if (skinny) {
+      // dW_l, D[l] (twins, plain only when a non-tcgen05 consumer needs it) and
+      // the db of layer l-1 in one pass over X[l] (k_skinny_backward)
+      const bool data = l > 0;
+      dispatch_skinny<BackSkinny>(out_l, s, e->X[l], e->D[l + 1], e->w32 + e->woff[l], in_l, out_l, e->act,
+                                  row0, nrows, (int)nn, data && !e->Dh[l] ? e->D[l] : nullptr,
+                                  data ? e->Dh[l] : nullptr, data ? e->Dl[l] : nullptr, sp_scale(e, tw),
+                                  e->G + e->woff[l], tw, data ? sp_scale(e, tb - 2) : nullptr,
+                                  data ? e->G + e->boff[l - 1] : nullptr, tb - 2, lim, e->tail);
       VNT_LAUNCH_CHECK();
       e->launches++;
+      if (data) db_done = l - 1;
     } else {
       dim3 grid((unsigned)ceil_div(out_l, 64), (unsigned)ceil_div(in_l, 64), (unsigned)nn);
       k_dw_ffma<<<grid, 256, 0, s>>>(e->X[l], e->D[l + 1], in_l, out_l, row0, nrows, sp_scale(e, tw), lim,
@@ -930,7 +964,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       e->launches++;
     }
     prof_end(e, 2.0 * rows * (double)in_l * out_l);
-    {
+    if (db_done != l) {
       dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
       k_db<<<grid, 128, 0, s>>>(e->D[l + 1], out_l, row0, nrows, sp_scale(e, tb), lim,
                                 e->G + e->boff[l], e->tail, tb);
@@ -938,16 +972,10 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       e->launches++;
     }
     if (layer_comm) layer_collective(e, l);   // layer l's gradient is final in this process
-    if (l > 0) {
+    if (l > 0 && !skinny) {
       prof_begin(e);
       if (e->tc_layer[l]) {
         tc_backward_data(e, l, rows);
-      } else if (out_l <= 32) {
-        // D[l] stays plain for k_db; its twins feed a tcgen05 bwd-data / dW of l-1
-        dispatch_skinny<BwdSkinny>(out_l, s, e->D[l + 1], e->w32 + e->woff[l], out_l, in_l, rows,
-                                   e->act, e->X[l], e->D[l], e->Dh[l], e->Dl[l]);
-        VNT_LAUNCH_CHECK();
-        e->launches++;
       } else {
         const float* WT = e->wt32 + e->wtoff[l];
         dim3 grid((unsigned)ceil_div(in_l, 64), (unsigned)ceil_div(p.rows, 64));
@@ -957,7 +985,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
         e->launches++;
       }
       prof_end(e, 2.0 * rows * (double)in_l * out_l);
-      if (!e->tc_layer[l] && out_l > 32)   // tcgen05 and skinny kernels write twins
+      if (!e->tc_layer[l])   // tcgen05 epilogues write the twins themselves
         split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l);
     }
   }

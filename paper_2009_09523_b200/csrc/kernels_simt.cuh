@@ -706,6 +706,156 @@ __global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __
   }
 }
 
+// Forward of a skinny layer with all of W^T ([no][K], K % 4 == 0) resident in
+// shared memory: a persistent grid, one warp per row at a time, float4 loads
+// of the row (4 in flight per lane); per output the lane-strided partial sums
+// run over k ascending, then a fixed xor tree, so every output depends only on
+// its row.
+template <int NO>
+__global__ void __launch_bounds__(1024) k_fwd_skinny_res(const float* __restrict__ X, int K,
+                                                         const float* __restrict__ WT, int no,
+                                                         const float* __restrict__ bias, int rows,
+                                                         int act, int last, float* __restrict__ out) {
+  extern __shared__ float4 wsm[];
+  const int K4 = K >> 2;
+  for (int i = threadIdx.x; i < no * K4; i += blockDim.x) wsm[i] = __ldg(reinterpret_cast<const float4*>(WT) + i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+    const float4* xr = reinterpret_cast<const float4*>(X + (size_t)r * K);
+    float acc[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) acc[o] = 0.f;
+    auto fold = [&](const float4& xv, int k4) {
+#pragma unroll
+      for (int o = 0; o < NO; ++o)
+        if (o < no) {
+          const float4 w = wsm[o * K4 + k4];
+          acc[o] = fmaf(xv.x, w.x, acc[o]);
+          acc[o] = fmaf(xv.y, w.y, acc[o]);
+          acc[o] = fmaf(xv.z, w.z, acc[o]);
+          acc[o] = fmaf(xv.w, w.w, acc[o]);
+        }
+    };
+    int k4 = lane;
+    for (; k4 + 96 < K4; k4 += 128) {   // k ascending per lane: k4, +32, +64, +96
+      float4 xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = __ldg(xr + k4 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) fold(xv[u], k4 + 32 * u);
+    }
+    for (; k4 < K4; k4 += 32) fold(__ldg(xr + k4), k4);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+#pragma unroll
+      for (int sft = 16; sft; sft >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], sft);
+    }
+    float v = 0.f;
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+      if (o == lane) v = acc[o];
+    if (lane < no) {
+      v += bias[lane];
+      if (!last) v = act_fwd(act, v);
+      out[(size_t)r * no + lane] = v;
+    }
+  }
+}
+
+// Backward through a skinny layer l (no <= 32 outputs) for one virtual node and
+// a slab of 128 input features per block (thread = feature i), over the
+// node's rows in order — one read of X[l] for three results:
+//   dW_l[i][o]  = sum_r X[r][i] Dn[r][o]             (fmaf chain, rows ascending)
+//   D[l][r][i]  = (sum_o Dn[r][o] W[i][o]) f'(X[r][i]) (o ascending)
+//   db_{l-1}[i] = sum_r D[l][r][i]                    (rows ascending)
+// the same operation orders as k_dw_skinny, k_bwd_skinny and k_db.  Node
+// partials are quantised and added into G with int64 atomics (exact).  D[l]
+// is written as the 3xTF32 twins and/or plain (each nullable); Gb == nullptr
+// (l == 0): no bwd-data / db.
+template <int NO>
+__global__ void __launch_bounds__(128) k_skinny_backward(
+    const float* __restrict__ X, const float* __restrict__ Dn, const float* __restrict__ W, int in, int no,
+    int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, float* __restrict__ Dout,
+    float* __restrict__ Dh, float* __restrict__ Dl, const float* __restrict__ scale_w, long long* __restrict__ Gw,
+    int tw, const float* __restrict__ scale_b, long long* __restrict__ Gb, int tb, float lim,
+    long long* __restrict__ tail) {
+  static_assert(NO % 4 == 0, "dn rows are read as float4");
+  __shared__ __align__(16) float dn[64][NO];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  const int r0 = vn_row0[v], n = vn_rows[v];
+  const bool data = Gb != nullptr;
+  float w[NO], g[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    w[o] = (data && i < in && o < no) ? __ldg(W + (size_t)i * no + o) : 0.f;
+    g[o] = 0.f;
+  }
+  float db = 0.f;
+  for (int c = 0; c < n; c += 64) {
+    const int cn = min(64, n - c);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cn * NO; k += blockDim.x)
+      dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
+    __syncthreads();
+    if (i >= in) continue;
+    const float* xp = X + (size_t)(r0 + c) * in + i;
+    for (int rr = 0; rr < cn; rr += 8) {
+      float a[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = rr + j < cn ? __ldg(xp + (size_t)(rr + j) * in) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (rr + j >= cn) break;
+        const float4* d4 = reinterpret_cast<const float4*>(&dn[rr + j][0]);
+        float acc = 0.f;
+#pragma unroll
+        for (int o = 0; o < NO; o += 4) {
+          const float4 d = d4[o / 4];
+          g[o] = fmaf(a[j], d.x, g[o]);
+          g[o + 1] = fmaf(a[j], d.y, g[o + 1]);
+          g[o + 2] = fmaf(a[j], d.z, g[o + 2]);
+          g[o + 3] = fmaf(a[j], d.w, g[o + 3]);
+          acc = fmaf(d.x, w[o], acc);
+          acc = fmaf(d.y, w[o + 1], acc);
+          acc = fmaf(d.z, w[o + 2], acc);
+          acc = fmaf(d.w, w[o + 3], acc);
+        }
+        if (data) {
+          const float dv = acc * act_grad_from_out(act, a[j]);
+          const size_t idx = (size_t)(r0 + c + rr + j) * in + i;
+          if (Dout) Dout[idx] = dv;
+          if (Dh) put_twins(Dh, Dl, idx, dv);
+          db += dv;
+        }
+      }
+    }
+  }
+  if (i >= in) return;
+  if (data)   // the node's pad rows (up to a multiple of 8) carry zero deltas
+    for (int r = n; r < ((n + 7) & ~7); ++r) {
+      const size_t idx = (size_t)(r0 + r) * in + i;
+      if (Dout) Dout[idx] = 0.f;
+      if (Dh) {
+        Dh[idx] = 0.f;
+        Dl[idx] = 0.f;
+      }
+    }
+  const float sw = *scale_w;
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    if (o >= no) break;
+    const long long q = quantise(g[o], sw, lim, tail, tw);
+    if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&Gw[(size_t)i * no + o]), (unsigned long long)q);
+  }
+  if (data) {
+    const long long q = quantise(db, *scale_b, lim, tail, tb);
+    if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&Gb[i]), (unsigned long long)q);
+  }
+}
+
 // -------------------------------------------------------------------- SGD
 // sync_gradients' rounding + x(1/B) (virtual_exec.cpp:169-174) and
 // sgd_apply (model.cpp:364-374) fused: g = double(S) * 2^-s * (1/B);
