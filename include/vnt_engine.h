@@ -236,6 +236,25 @@ int vnt_engine_regroup_ops(vnt_engine* e, const vnt_comm_ops* ops, int32_t sourc
  * from pool rank source_pool_rank (a member of the previous training group). */
 int vnt_engine_set_membership(vnt_engine* e, int32_t member, int32_t source_pool_rank);
 
+/* Elastic resize of this process's logical devices (elastic.cpp:106-245 on
+ * the GPU): first the merges, in order — merges[2k] (old index, a removed
+ * lineage) is combined into merges[2k+1] (old index, a survivor) as
+ * LayerStats::combine (model.cpp:123-139); then new device i takes old
+ * lineage src[i] (a survivor's own, or a copy of a survivor's post-merge
+ * lineage for an added device; -1: empty).  Capacities are set afterwards
+ * with vnt_engine_set_device_capacity. */
+int vnt_engine_remap_devices(vnt_engine* e, uint32_t new_count, const int32_t* src,
+                             uint32_t n_merges, const int32_t* merges);
+/* Cross-process lineage moves over the process pool (a removed device's
+ * statistics to its survivor, a survivor's to an added device): the sender
+ * ships (count, mean, m2) of its local device; the receiver combines it into
+ * (merge != 0) or overwrites (seed) its local device.  Pairs must be issued
+ * in the same order on every process. */
+int vnt_engine_send_lineage(vnt_engine* e, int32_t device, int32_t peer);
+int vnt_engine_recv_lineage(vnt_engine* e, int32_t peer, int32_t device, int32_t merge);
+/* This process's rank / size in the process pool (0 / 1 without a group). */
+int vnt_engine_pool_rank(const vnt_engine* e, int32_t* rank, int32_t* size);
+
 /* Forget the scale history: the next step uses the deterministic initial scale
  * 40 - ceil(log2 B) (stateless callers, e.g. vnt::train_step on a World). */
 int vnt_engine_reset_scales(vnt_engine* e);

@@ -40,6 +40,15 @@ typedef struct vnt_runner_config { /* RunnerConfig, runner.hpp:19-33 */
   int32_t prefetch;
   int32_t gemm_mode; /* VNT_GEMM_* */
   double momentum;
+  /* B200 extensions: one process per GPU (every process passes the same
+   * config; devices are placed round-robin by ascending id).  comm_ops: a
+   * host-callback group; else world_size > 1 needs the 128-byte nccl_id. */
+  const vnt_comm_ops* comm_ops;
+  const uint8_t* nccl_id;
+  int32_t rank;
+  int32_t world_size;
+  int32_t cuda_device;
+  uint64_t resident_rows;
 } vnt_runner_config;
 
 const char* vnt_host_last_error(void);
@@ -47,12 +56,14 @@ const char* vnt_host_last_error(void);
 int vnt_trainer_create(const vnt_runner_config* config, vnt_trainer** out);
 void vnt_trainer_destroy(vnt_trainer* t);
 uint64_t vnt_trainer_param_count(const vnt_trainer* t);
-/* StepMetrics: loss and per-device metrics in ascending device id (up to cap). */
+/* StepMetrics: loss and the metrics of this process's devices in ascending
+ * device id (up to cap).  A process hosting no device returns loss NaN. */
 int vnt_trainer_step(vnt_trainer* t, double* loss, vnt_device_metrics* per_device, uint32_t cap);
 int vnt_trainer_params(vnt_trainer* t, double* out, uint64_t n);
 int vnt_trainer_resize(vnt_trainer* t, const vnt_device_spec* devices, uint32_t n);
 uint32_t vnt_trainer_device_count(const vnt_trainer* t);
-/* Input statistics of the idx-th worker (ascending id): count, mean[in], m2[in]. */
+/* Input statistics of this process's idx-th worker (ascending id): count,
+ * mean[in], m2[in].  vnt_trainer_device_count: this process's workers. */
 int vnt_trainer_input_stats(vnt_trainer* t, uint32_t idx, double* count, double* mean, double* m2);
 
 /* Host-only (no GPU): SynthDataset::sequential_batch and Model::init_params. */

@@ -364,9 +364,115 @@ class Engine:
         return int(self.lib.vnt_engine_stream(self.h) or 0)
 
 
+class _DevSpec(C.Structure):
+    _fields_ = [("device_id", C.c_char_p), ("device_type", C.c_char_p), ("memory_capacity", C.c_uint64)]
+
+
+class _RunnerCfg(C.Structure):   # vnt_runner_config (include/vnt_trainer.h)
+    _fields_ = [("layer_widths", C.POINTER(C.c_uint64)), ("num_widths", C.c_uint32),
+                ("activation", C.c_int32), ("loss", C.c_int32), ("seed", C.c_uint64),
+                ("global_batch", C.c_uint64), ("virtual_nodes", C.c_uint64), ("lr", C.c_double),
+                ("data_seed", C.c_uint64), ("dataset_size", C.c_uint64),
+                ("shuffle_epochs", C.c_int32), ("shuffle_seed", C.c_uint64),
+                ("devices", C.POINTER(_DevSpec)), ("num_devices", C.c_uint32),
+                ("parallel_devices", C.c_int32), ("prefetch", C.c_int32), ("gemm_mode", C.c_int32),
+                ("momentum", C.c_double), ("comm_ops", C.c_void_p), ("nccl_id", C.POINTER(C.c_uint8)),
+                ("rank", C.c_int32), ("world_size", C.c_int32), ("cuda_device", C.c_int32),
+                ("resident_rows", C.c_uint64)]
+
+
+_host_lib = None
+
+
+def load_host():
+    """libvnt.so: the C++ drop-in vnt:: API and its C-ABI (include/vnt_trainer.h)."""
+    global _host_lib
+    if _host_lib is None:
+        load_engine()
+        if not HOST_SO.exists():
+            raise ImportError(f"{HOST_SO} missing: run __graft_entry__.build()")
+        _host_lib = C.CDLL(str(HOST_SO))
+        _host_lib.vnt_host_last_error.restype = C.c_char_p
+        _host_lib.vnt_trainer_param_count.restype = C.c_uint64
+        _host_lib.vnt_trainer_device_count.restype = C.c_uint32
+    return _host_lib
+
+
+def _hcheck(rc: int):
+    if rc != VNT_OK:
+        raise VntError(rc, load_host().vnt_host_last_error().decode(errors="replace"))
+
+
+class Trainer:
+    """The drop-in vnt::Trainer (RunnerConfig / step / resize / params / world)
+    through its C-ABI.  devices: [(device_id, memory_capacity)] or a count
+    ("gpu0".. names).  comm: a hostcomm.GlooGroup for one process per rank."""
+
+    def __init__(self, widths, activation, loss, seed, global_batch, virtual_nodes, lr, data_seed,
+                 dataset_size, devices, shuffle_seed=None, prefetch=False, gemm_mode="auto",
+                 momentum=0.0, comm=None, resident_rows=0, cuda_device=0):
+        self.lib = load_host()
+        self.widths = [int(w) for w in widths]
+        self._w = (C.c_uint64 * len(self.widths))(*self.widths)
+        self._devs = self._dev_array(devices)
+        self._comm = comm
+        cfg = _RunnerCfg(self._w, len(self.widths), ACTIVATIONS[activation], LOSSES[loss], seed,
+                         global_batch, virtual_nodes, lr, data_seed, dataset_size,
+                         0 if shuffle_seed is None else 1, shuffle_seed or 0, self._devs, len(self._devs),
+                         0, 1 if prefetch else 0, GEMM_MODES[gemm_mode], momentum,
+                         C.cast(C.pointer(comm.ops), C.c_void_p) if comm is not None else None, None,
+                         comm.rank if comm is not None else 0, comm.size if comm is not None else 1,
+                         cuda_device, resident_rows)
+        h = C.c_void_p()
+        _hcheck(self.lib.vnt_trainer_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.P = int(self.lib.vnt_trainer_param_count(h))
+
+    @staticmethod
+    def _dev_array(devices):
+        if isinstance(devices, int):
+            devices = [(f"gpu{i}", 1 << 20) for i in range(devices)]
+        arr = (_DevSpec * len(devices))()
+        for i, (name, cap) in enumerate(devices):
+            arr[i] = _DevSpec(name.encode(), b"B200", cap)
+        return arr
+
+    def step(self) -> float:
+        lo = C.c_double()
+        _hcheck(self.lib.vnt_trainer_step(self.h, C.byref(lo), None, 0))
+        return lo.value
+
+    def resize(self, devices):
+        arr = self._dev_array(devices)
+        _hcheck(self.lib.vnt_trainer_resize(self.h, arr, len(arr)))
+
+    def params(self) -> np.ndarray:
+        p = np.empty(self.P)
+        _hcheck(self.lib.vnt_trainer_params(self.h, p.ctypes.data_as(_f64p), self.P))
+        return p
+
+    def local_device_count(self) -> int:
+        return int(self.lib.vnt_trainer_device_count(self.h))
+
+    def input_stats(self, idx):
+        cnt = C.c_double()
+        mean = np.empty(self.widths[0])
+        m2 = np.empty(self.widths[0])
+        _hcheck(self.lib.vnt_trainer_input_stats(self.h, idx, C.byref(cnt), mean.ctypes.data_as(_f64p),
+                                                 m2.ctypes.data_as(_f64p)))
+        return cnt.value, mean, m2
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vnt_trainer_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
 def param_count(widths) -> int:
     return sum(widths[i] * widths[i + 1] + widths[i + 1] for i in range(len(widths) - 1))
 
 
-__all__ = ["Engine", "VntError", "uniform_mapping", "param_count", "load_engine",
-           "ENGINE_SO", "HOST_SO"]
+__all__ = ["Engine", "Trainer", "VntError", "uniform_mapping", "param_count", "load_engine",
+           "load_host", "ENGINE_SO", "HOST_SO"]

@@ -2178,6 +2178,166 @@ int vnt_engine_add_device(vnt_engine* e, uint64_t capacity, int32_t* out_index) 
 }
 
 int vnt_engine_device_count(const vnt_engine* e) { return e ? (int)e->devs.size() : 0; }
+}  // extern "C"
+
+namespace {
+vnt_engine::LDev new_lineage(vnt_engine* e, uint64_t capacity) {
+  vnt_engine::LDev d;
+  d.capacity = capacity;
+  const uint64_t in = e->widths[0];
+  d.mean = (double*)dalloc(in * sizeof(double));
+  d.m2 = (double*)dalloc(in * sizeof(double));
+  d.mean_bak = (double*)dalloc(in * sizeof(double));
+  d.m2_bak = (double*)dalloc(in * sizeof(double));
+  VNT_CUDA(cudaMemset(d.mean, 0, in * sizeof(double)));
+  VNT_CUDA(cudaMemset(d.m2, 0, in * sizeof(double)));
+  return d;
+}
+
+void free_lineage(vnt_engine::LDev& d) {
+  for (double* p : {d.mean, d.m2, d.mean_bak, d.m2_bak})
+    if (p) cudaFree(p);
+  d = vnt_engine::LDev{};
+}
+
+// LayerStats::combine(other) of lineage `a` with (count_b, mean_b, m2_b) on the
+// device (model.cpp:123-139; the same factors and kernel as the per-node
+// combine of a step, so the operation order is the reference's).
+void combine_lineage(vnt_engine* e, vnt_engine::LDev& a, double count_b, const double* mean_b,
+                     const double* m2_b) {
+  if (count_b == 0) return;
+  CombineStep st{0, 0, 0.0, 0.0};
+  if (a.count == 0) {
+    st.copy = 1;
+    a.count = count_b;
+  } else {
+    const double n = a.count + count_b;
+    st.f1 = a.count * count_b / n;
+    st.f2 = count_b / n;
+    a.count = n;
+  }
+  CombineStep* d_st = (CombineStep*)dalloc(sizeof st);
+  VNT_CUDA(cudaMemcpyAsync(d_st, &st, sizeof st, cudaMemcpyHostToDevice, e->stream));
+  const uint64_t in = e->widths[0];
+  k_stats_combine<<<(unsigned)ceil_div(in, 128), 128, 0, e->stream>>>(a.mean, a.m2, (int)in, mean_b, m2_b, d_st, 1);
+  VNT_LAUNCH_CHECK();
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  cudaFree(d_st);
+}
+
+// Lineage wire format over the process pool: [count | mean[in] | m2[in]] fp64.
+double* lineage_packet(vnt_engine* e, uint64_t& words) {
+  words = 1 + 2 * e->widths[0];
+  return (double*)dalloc(words * sizeof(double));
+}
+
+void quiesce_local(vnt_engine* e) {
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->aux_stream) VNT_CUDA(cudaStreamSynchronize(e->aux_stream));
+  e->stats_join_pending = false;
+  e->pf.valid = false;
+  drop_graphs(e);
+  reset_acc(e);
+}
+}  // namespace
+
+extern "C" {
+
+int vnt_engine_remap_devices(vnt_engine* e, uint32_t new_count, const int32_t* src, uint32_t n_merges,
+                             const int32_t* merges) {
+  return guarded([&] {
+    bind(e);
+    const int old = (int)e->devs.size();
+    for (uint32_t k = 0; k < n_merges; ++k) {
+      const int from = merges[2 * k], to = merges[2 * k + 1];
+      if (from < 0 || from >= old || to < 0 || to >= old || from == to)
+        throw EngineError(VNT_ERR_MIGRATION, "remap_devices: bad merge pair");
+    }
+    for (uint32_t i = 0; i < new_count; ++i)
+      if (src[i] < -1 || src[i] >= old) throw EngineError(VNT_ERR_MIGRATION, "remap_devices: bad source");
+    quiesce_local(e);
+    // merges first, in order (migrate_state: removed lineages into survivors)
+    for (uint32_t k = 0; k < n_merges; ++k) {
+      auto& from = e->devs[merges[2 * k]];
+      combine_lineage(e, e->devs[merges[2 * k + 1]], from.count, from.mean, from.m2);
+    }
+    // then the new list: its own lineage (a survivor), a copy of a survivor's
+    // post-merge lineage (an added device), or empty (src -1)
+    const uint64_t in = e->widths[0];
+    std::vector<vnt_engine::LDev> next;
+    for (uint32_t i = 0; i < new_count; ++i) {
+      vnt_engine::LDev d = new_lineage(e, src[i] >= 0 ? e->devs[src[i]].capacity : 1);
+      if (src[i] >= 0) {
+        const auto& s0 = e->devs[src[i]];
+        d.count = s0.count;
+        VNT_CUDA(cudaMemcpyAsync(d.mean, s0.mean, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+        VNT_CUDA(cudaMemcpyAsync(d.m2, s0.m2, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+      }
+      next.push_back(d);
+    }
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    for (auto& d : e->devs) free_lineage(d);
+    e->devs = std::move(next);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_send_lineage(vnt_engine* e, int32_t device, int32_t peer) {
+  return guarded([&] {
+    bind(e);
+    if (!e->pool) throw EngineError(VNT_ERR_CONFIG, "send_lineage: the engine has no process group");
+    if (device < 0 || device >= (int32_t)e->devs.size()) throw EngineError(VNT_ERR_CONFIG, "unknown device");
+    quiesce_local(e);
+    uint64_t words = 0;
+    double* pk = lineage_packet(e, words);
+    const auto& d = e->devs[device];
+    const uint64_t in = e->widths[0];
+    VNT_CUDA(cudaMemcpyAsync(pk, &d.count, sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    VNT_CUDA(cudaMemcpyAsync(pk + 1, d.mean, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    VNT_CUDA(cudaMemcpyAsync(pk + 1 + in, d.m2, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    log_comm(e, kLogSend, (uint64_t)peer, words);
+    e->pool->send(pk, words * sizeof(double), peer, e->stream);
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    cudaFree(pk);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_recv_lineage(vnt_engine* e, int32_t peer, int32_t device, int32_t merge) {
+  return guarded([&] {
+    bind(e);
+    if (!e->pool) throw EngineError(VNT_ERR_CONFIG, "recv_lineage: the engine has no process group");
+    if (device < 0 || device >= (int32_t)e->devs.size()) throw EngineError(VNT_ERR_CONFIG, "unknown device");
+    quiesce_local(e);
+    uint64_t words = 0;
+    double* pk = lineage_packet(e, words);
+    log_comm(e, kLogRecv, (uint64_t)peer, words);
+    e->pool->recv(pk, words * sizeof(double), peer, e->stream);
+    double count = 0;
+    VNT_CUDA(cudaMemcpyAsync(&count, pk, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    VNT_CUDA(cudaStreamSynchronize(e->stream));
+    const uint64_t in = e->widths[0];
+    auto& d = e->devs[device];
+    if (merge) {
+      combine_lineage(e, d, count, pk + 1, pk + 1 + in);
+    } else {   // seed: the device starts as a copy of the sender's lineage
+      d.count = count;
+      VNT_CUDA(cudaMemcpyAsync(d.mean, pk + 1, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+      VNT_CUDA(cudaMemcpyAsync(d.m2, pk + 1 + in, in * sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+      VNT_CUDA(cudaStreamSynchronize(e->stream));
+    }
+    cudaFree(pk);
+    return VNT_OK;
+  });
+}
+
+int vnt_engine_pool_rank(const vnt_engine* e, int32_t* rank, int32_t* size) {
+  if (!e) return VNT_ERR_CONFIG;
+  if (rank) *rank = e->pool ? e->pool->rank() : 0;
+  if (size) *size = e->pool ? e->pool->size() : 1;
+  return VNT_OK;
+}
+
 
 int vnt_engine_device_step(vnt_engine* e, int32_t device, const double* x, const double* y,
                            const uint64_t* node_sizes, uint32_t num_nodes,

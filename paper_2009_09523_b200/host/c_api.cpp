@@ -78,6 +78,12 @@ int vnt_trainer_create(const vnt_runner_config* c, vnt_trainer** out) {
     rc.prefetch = c->prefetch != 0;
     rc.gemm_mode = c->gemm_mode;
     rc.momentum = c->momentum;
+    rc.comm_ops = c->comm_ops;
+    if (c->nccl_id) rc.nccl_id.assign(c->nccl_id, c->nccl_id + 128);
+    rc.rank = c->rank;
+    rc.world_size = c->world_size < 1 ? 1 : c->world_size;
+    rc.cuda_device = c->cuda_device;
+    rc.resident_rows = c->resident_rows;
     auto t = std::make_unique<vnt_trainer>();
     t->t = std::make_unique<vnt::Trainer>(rc);
     *out = t.release();

@@ -17,6 +17,9 @@ struct GpuModel {
 
   // Makes at least n logical devices exist with the given capacities.
   void ensure_devices(const std::vector<std::size_t>& capacities);
+  // Skipped when the engine already holds exactly these values (the last
+  // upload or download): the reference API passes params by value on every
+  // call, the engine keeps them resident.
   void upload_params(const std::vector<double>& values);
   std::vector<double> download_params();
   void set_stats(int dev, const StatefulKernelState& k);
@@ -24,6 +27,8 @@ struct GpuModel {
 
   std::mutex mu;
   vnt_engine* eng = nullptr;
+  std::vector<double> resident;   // host copy of the engine's parameters (if known)
+  bool resident_valid = false;
   std::size_t in_width = 0;
   int ndev = 0;
 };

@@ -23,9 +23,51 @@ SCEN = {
 }
 
 
+RESIZES = {2: ["gpu0", "gpu1"], 4: ["gpu0", "gpu1", "gpu5"]}   # step -> device ids
+
+
+def trainer_run(model, rank, world, out):
+    """The C++ drop-in Trainer (vnt_trainer C-ABI) on every process: 4 devices,
+    resized to 2 (with 3 processes one goes idle) and then to 3 with a new id."""
+    import paper_2009_09523_b200 as vnt
+    comm = None
+    if world > 1:
+        from paper_2009_09523_b200 import hostcomm
+        comm = hostcomm.world_group()
+    widths, act, loss, B, V, steps, mode = SCEN[model]
+    t = vnt.Trainer(widths, act, loss, 3, B, V, 0.05, 7, 4096, [(f"gpu{i}", 1 << 20) for i in range(4)],
+                    gemm_mode=mode, comm=comm)
+    losses = []
+    for s in range(6):
+        if s in RESIZES:
+            t.resize([(d, 1 << 20) for d in RESIZES[s]])
+        losses.append(t.step())
+    params = t.params()
+    stats = {}
+    for i in range(t.local_device_count()):
+        stats[i] = t.input_stats(i)
+    np.savez(out, losses=np.array(losses), params=params,
+             counts=np.array([stats[i][0] for i in sorted(stats)]),
+             means=np.array([stats[i][1] for i in sorted(stats)]) if stats else np.zeros((0, widths[0])),
+             m2s=np.array([stats[i][2] for i in sorted(stats)]) if stats else np.zeros((0, widths[0])),
+             log=np.array([]))
+    t.close()
+
+
 def main():
     scenario, out = sys.argv[1], sys.argv[2]
     kind, _, model = scenario.partition(":")
+    if kind == "trainer":
+        rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        trainer_run(model, rank, world, out)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     import paper_2009_09523_b200 as vnt
     comm = None

@@ -67,28 +67,6 @@ def test_cpp_dropin_suite_on_gpu():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-class _Dev(C.Structure):
-    _fields_ = [("device_id", C.c_char_p), ("device_type", C.c_char_p), ("memory_capacity", C.c_uint64)]
-
-
-class _Cfg(C.Structure):
-    _fields_ = [("layer_widths", C.POINTER(C.c_uint64)), ("num_widths", C.c_uint32),
-                ("activation", C.c_int32), ("loss", C.c_int32), ("seed", C.c_uint64),
-                ("global_batch", C.c_uint64), ("virtual_nodes", C.c_uint64), ("lr", C.c_double),
-                ("data_seed", C.c_uint64), ("dataset_size", C.c_uint64),
-                ("shuffle_epochs", C.c_int32), ("shuffle_seed", C.c_uint64),
-                ("devices", C.POINTER(_Dev)), ("num_devices", C.c_uint32),
-                ("parallel_devices", C.c_int32), ("prefetch", C.c_int32), ("gemm_mode", C.c_int32),
-                ("momentum", C.c_double)]
-
-
-def _devs(n):
-    arr = (_Dev * n)()
-    for i in range(n):
-        arr[i] = _Dev(f"gpu{i}".encode(), b"B200", 1 << 20)
-    return arr
-
-
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", ["headline", "cfg1", "shuffled"])
 def test_dropin_trainer_matches_reference_trainer(port, ref, case):
@@ -105,36 +83,26 @@ def test_dropin_trainer_matches_reference_trainer(port, ref, case):
         w, act, loss, seed, B, V, lr, ds, n, G, steps = [4, 16, 4], 1, 0, 11, 64, 8, 0.05, 11, 256, 8, 30
     else:
         w, act, loss, seed, B, V, lr, ds, n, G, steps = [784, 16, 10], 1, 1, 11, 256, 16, 0.05, 11, 60000, 1, 10
-    wa = (C.c_uint64 * len(w))(*w)
-    devs = _devs(G)
-    cfg = _Cfg(wa, len(w), act, loss, seed, B, V, lr, ds, n, int(shuffle), 7 if shuffle else 0,
-               devs, G, 0, int(shuffle), 1, 0.0)
-    h = C.c_void_p()
-    assert lib.vnt_trainer_create(C.byref(cfg), C.byref(h)) == 0, lib.vnt_host_last_error()
+    import paper_2009_09523_b200 as vnt
+    mine = vnt.Trainer(w, ["relu", "tanh", "identity"][act], ["mse", "softmax-cross-entropy"][loss], seed,
+                       B, V, lr, ds, n, G, shuffle_seed=7 if shuffle else None, prefetch=shuffle)
     extra = dict(shuffle_seed=7, prefetch=True) if shuffle else {}
     t = o.trainer(w, ["relu", "tanh", "identity"][act], ["mse", "softmax-cross-entropy"][loss], seed,
                   B, V, lr, ds, n, G, **extra)
-    lo = C.c_double()
     for s in range(steps):
         if case != "cfg1" and s in (10, 20):
             k = 4 if s == 10 else 8
-            assert lib.vnt_trainer_resize(h, _devs(k), k) == 0, lib.vnt_host_last_error()
+            mine.resize(k)
             t.resize(k)
-        assert lib.vnt_trainer_step(h, C.byref(lo), None, 0) == 0, lib.vnt_host_last_error()
+        got = mine.step()
         want = t.step()
-        assert abs(lo.value - want) <= 2e-5 * abs(want), (s, lo.value, want)
-    P = port.param_count(w)
-    p = np.empty(P)
-    assert lib.vnt_trainer_params(h, p.ctypes.data_as(C.POINTER(C.c_double)), P) == 0
-    assert np.abs(p - t.params()).max() <= 2e-5
+        assert abs(got - want) <= 2e-5 * abs(want), (s, got, want)
+    assert np.abs(mine.params() - t.params()).max() <= 2e-5
     # Input statistics are fp64 in the reference's op order: bit-identical,
-    # including lineages merged/seeded by the resizes.
+    # including lineages merged/seeded by the resizes (moved on the GPU).
+    assert mine.local_device_count() == G
     for i in range(G):
-        cnt = C.c_double()
-        mean = np.empty(w[0])
-        m2 = np.empty(w[0])
-        assert lib.vnt_trainer_input_stats(h, i, C.byref(cnt), mean.ctypes.data_as(C.POINTER(C.c_double)),
-                                           m2.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        cnt, mean, m2 = mine.input_stats(i)
         c2, mean2, m22 = t.input_stats(i)
-        assert cnt.value == c2 and np.array_equal(mean, mean2) and np.array_equal(m2, m22)
-    lib.vnt_trainer_destroy(h)
+        assert cnt == c2 and np.array_equal(mean, mean2) and np.array_equal(m2, m22)
+    mine.close()

@@ -81,33 +81,24 @@ def test_cfg4_fullsize_memory_bounded_passes():
 
 def test_cfg5_resize_8_4_8_transparent():
     """config 5 shape: cfg2 ([784,16,10], B=256, V=16) with resize 8->4 at step 10 and
-    4->8 at step 20 over 30 steps, through the drop-in Trainer (vnt_trainer.h)."""
+    4->8 at step 20 over 30 steps, through the drop-in Trainer (vnt_trainer.h);
+    the lineages move on the GPU (vnt_engine_remap_devices)."""
     import paper_2009_09523_b200 as vnt
-    from test_dropin import _Cfg, _devs, _host
-    lib = _host()
-    w = [784, 16, 10]
-    wa = (C.c_uint64 * 3)(*w)
 
     def run(schedule):
-        devs = _devs(8)
-        cfg = _Cfg(wa, 3, 1, 1, 11, 256, 16, 0.05, 11, 60000, 0, 0, devs, 8, 0, 0, 0, 0.0)
-        h = C.c_void_p()
-        assert lib.vnt_trainer_create(C.byref(cfg), C.byref(h)) == 0
-        lo = C.c_double()
+        t = vnt.Trainer([784, 16, 10], "tanh", "softmax-cross-entropy", 11, 256, 16, 0.05, 11, 60000, 8)
         losses = []
         for s in range(30):
             if s in schedule:
-                k = schedule[s]
-                assert lib.vnt_trainer_resize(h, _devs(k), k) == 0
-            assert lib.vnt_trainer_step(h, C.byref(lo), None, 0) == 0
-            losses.append(lo.value)
-        P = vnt.param_count(w)
-        p = np.empty(P)
-        assert lib.vnt_trainer_params(h, p.ctypes.data_as(C.POINTER(C.c_double)), P) == 0
-        lib.vnt_trainer_destroy(h)
-        return p, losses
+                t.resize(schedule[s])
+            losses.append(t.step())
+        p = t.params()
+        stats = [t.input_stats(i) for i in range(t.local_device_count())]
+        t.close()
+        return p, losses, stats
 
-    p0, l0 = run({})
-    p1, l1 = run({10: 4, 20: 8})
+    p0, l0, s0 = run({})
+    p1, l1, s1 = run({10: 4, 20: 8})
     assert l0 == l1
     assert np.array_equal(p0, p1)
+    assert len(s0) == len(s1) == 8

@@ -89,3 +89,24 @@ def test_resize_by_pool_membership(tmp_path):
         assert np.array_equal(g["params"], ref["params"]), r
         mask = ~np.isnan(g["losses"])
         assert np.array_equal(g["losses"][mask], ref["losses"][mask]), r
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_trainer_processes_with_resize(tmp_path, world):
+    """The C++ drop-in Trainer with one process per rank (round-robin device
+    placement) through resizes 4 -> 2 -> 3 devices (a new id; with 3
+    processes one idles and rejoins): parameters and every device's input
+    statistics bitwise equal to the single-process Trainer's."""
+    ref = launch("trainer:wide", 1, tmp_path)[0]
+    got = launch("trainer:wide", world, tmp_path)
+    final = ["gpu0", "gpu1", "gpu5"]                 # ascending ids after the last resize
+    placed = {"gpu0": 0, "gpu1": 1, "gpu2": 2 % world, "gpu3": 3 % world, "gpu5": 4 % world}
+    for r, g in enumerate(got):
+        mine = [final.index(d) for d in final if placed[d] == r]
+        mask = ~np.isnan(g["losses"])
+        assert np.array_equal(g["losses"][mask], ref["losses"][mask]), r
+        if mine:   # trains at the end: holds the current replica
+            assert mask[-1] and np.array_equal(g["params"], ref["params"]), r
+        assert list(g["counts"]) == [ref["counts"][i] for i in mine], r
+        for k, i in enumerate(mine):
+            assert np.array_equal(g["means"][k], ref["means"][i]) and np.array_equal(g["m2s"][k], ref["m2s"][i])
