@@ -105,7 +105,7 @@ typedef struct vnt_engine_options {
   const uint8_t* nccl_id;  /* 128-byte ncclUniqueId from rank 0, NULL if world 1   */
   int32_t gemm_mode;       /* VNT_GEMM_*                                           */
   double momentum;         /* 0: plain SGD exactly as the reference                */
-  uint64_t resident_rows;  /* rows kept resident per pass on the GPU (0: all)      */
+  uint64_t resident_rows;  /* rows resident per pass (0: what 85 % of free HBM holds) */
   const vnt_comm_ops* comm_ops; /* host-callback group instead of NCCL (NULL: NCCL) */
 } vnt_engine_options;
 
@@ -130,6 +130,7 @@ typedef struct vnt_step_timings { /* device time of the last train step, ms (CUD
   float gemm_ms;
   uint32_t gemm_launches;
   double gemm_flops;
+  uint32_t passes;         /* passes of resident nodes the step ran (this process) */
 } vnt_step_timings;
 
 const char* vnt_last_error(void);

@@ -59,7 +59,8 @@ class StepTimings(C.Structure):
     _fields_ = [("total_ms", C.c_float), ("forward_ms", C.c_float), ("backward_ms", C.c_float),
                 ("sync_ms", C.c_float), ("update_ms", C.c_float),
                 ("kernel_launches", C.c_uint32), ("rescale_retries", C.c_uint32),
-                ("gemm_ms", C.c_float), ("gemm_launches", C.c_uint32), ("gemm_flops", C.c_double)]
+                ("gemm_ms", C.c_float), ("gemm_launches", C.c_uint32), ("gemm_flops", C.c_double),
+                ("passes", C.c_uint32)]
 
     def as_dict(self):
         return {k: (float(getattr(self, k)) if t in (C.c_float, C.c_double) else int(getattr(self, k)))

@@ -414,7 +414,33 @@ void ensure_combine(vnt_engine* e, size_t n) {
   e->combine_cap = n;
 }
 
-// Group local nodes (ascending id) into passes that fit resident_rows.
+// Device bytes per pass row (the buffers ensure_capacity allocates).
+uint64_t pass_row_bytes(const vnt_engine* e) {
+  const uint64_t in = e->widths[0], out = e->widths[e->L];
+  uint64_t b = 2 * (in + out) * sizeof(double) + out * sizeof(float);   // staging x2, logits
+  for (int l = 0; l <= e->L; ++l) {
+    const uint64_t w = e->widths[l] * sizeof(float);
+    if (l < e->L) b += w * (e->split && e->tc_layer[l] ? 3 : 1);            // X (+ twins)
+    if (l > 0) b += w * (e->split && e->tc_layer[l - 1] ? 3 : 1);           // D (+ twins)
+  }
+  return b;
+}
+
+// Rows of one pass when the caller set no resident_rows: as many as 85 % of
+// the free HBM holds (counting the pass buffers already allocated).  A node's
+// own size is bounded by its device's memory_capacity (CapacityError), as in
+// the reference's device_step; how many nodes are resident together is the
+// B200's memory, not the model's.
+uint64_t hbm_row_budget(vnt_engine* e) {
+  size_t free_b = 0, total_b = 0;
+  VNT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t row = pass_row_bytes(e);
+  const double usable = 0.85 * ((double)free_b + (double)(e->cap_rows * row));
+  return std::max<uint64_t>(1, (uint64_t)(usable / (double)row));
+}
+
+// Group local nodes (ascending id) into passes that fit the resident-row budget
+// (vnt_engine_options::resident_rows, else hbm_row_budget).
 std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
   std::vector<int64_t> key;
   key.reserve(local.size() * 4 + 1);
@@ -428,7 +454,7 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
   auto it = e->plans.find(key);
   if (it != e->plans.end()) return it->second;
   std::vector<Pass> passes;
-  const uint64_t budget = e->opt.resident_rows ? e->opt.resident_rows : ~0ull;
+  const uint64_t budget = e->opt.resident_rows ? e->opt.resident_rows : hbm_row_budget(e);
   Pass cur;
   for (const auto& n : local) {
     if (!cur.nodes.empty() && cur.examples + n.rows > budget) {
@@ -1782,6 +1808,7 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
   (void)cudaGetLastError();
   e->timings.kernel_launches = e->launches;
   e->timings.rescale_retries = retries;
+  e->timings.passes = local.empty() ? 0u : (uint32_t)plan_for(e, local).size();
   prof_collect(e);
   if (per_dev) {
     for (size_t d = 0; d < e->devs.size(); ++d) {

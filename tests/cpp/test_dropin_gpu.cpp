@@ -149,6 +149,31 @@ static RunnerConfig toy_config(std::size_t devices) {
   return c;
 }
 
+TEST_CASE("a train_step loop over a World is the Trainer's trajectory bit for bit") {
+  // runner.cpp:75-82: Trainer::step is train_step on the Trainer's World; the
+  // World carries the fixed-point scale history (WorkerState::scales).
+  const RunnerConfig cfg = toy_config(4);
+  Trainer trainer(cfg);
+  Model model(cfg.model);
+  World world = make_world(model, cfg.devices);
+  const auto mapping = make_uniform_mapping(cfg.global_batch, cfg.virtual_nodes, cfg.devices);
+  const SynthDataset data(cfg.data_seed, cfg.dataset_size, 3, 2);
+  for (std::uint64_t s = 0; s < 8; ++s) {
+    const Batch b = data.sequential_batch((s * cfg.global_batch) % cfg.dataset_size, cfg.global_batch);
+    const StepMetrics a = train_step(model, world, mapping, b, cfg.lr, {s, false});
+    const StepMetrics t = trainer.step();
+    CHECK(a.loss == t.loss);
+    CHECK(world.workers[0].params.bitwise_equal(trainer.params()));
+    CHECK(world.workers[0].scales.size() == 4);
+  }
+  // and the World-level migrate_state carries the scales through a resize
+  InMemoryTransport tr;
+  const auto plan = elastic::plan_resize(mapping, gpus(6));
+  const World next = elastic::migrate_state(plan, world, tr);
+  CHECK(next.workers.size() == 6);
+  for (const auto& w : next.workers) CHECK(w.scales == world.workers[0].scales);
+}
+
 TEST_CASE("resize schedule does not perturb the training trajectory") {
   const auto rep = elastic::resized_training_equivalence_harness(
       toy_config(8), {{2, gpus(4)}, {4, gpus(8)}}, 6);
