@@ -77,6 +77,9 @@ struct vnt_engine {
   uint64_t P = 0;
   std::vector<uint64_t> woff, boff, wtoff;
   std::vector<int> tc_layer;   // 1: layer runs on tcgen05 tiles
+  uint64_t ld0 = 0;             // row stride of X[0] (and twins): the input width, rounded
+                                // up to 32 when layer 0 runs on tcgen05 (3-D TMA boxes of
+                                // its MN-major dW operand); pad columns stay zero
   vnt_engine_options opt{};
   // Process groups: `pool` spans every process the job started (resize
   // migration runs over it); `comm` is the group that trains — the pool
@@ -386,12 +389,20 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t vns) {
   for (auto* v : {&e->X, &e->D, &e->Xh, &e->Xl, &e->Dh, &e->Dl}) v->assign(L + 1, nullptr);
   for (int l = 0; l <= L; ++l) {
     const uint64_t w = e->widths[l];
-    if (l < L) e->X[l] = (float*)dalloc(rows * w * sizeof(float));
+    const uint64_t wx = l == 0 ? e->ld0 : w;   // X row stride
+    if (l < L) {
+      e->X[l] = (float*)dalloc(rows * wx * sizeof(float));
+      if (wx != w) VNT_CUDA(cudaMemset(e->X[l], 0, rows * wx * sizeof(float)));
+    }
     if (l > 0) e->D[l] = (float*)dalloc(rows * w * sizeof(float));
     if (e->split) {
       if (l < L && e->tc_layer[l]) {   // operands of layer l: X[l] (fwd; dW, MN-major)
-        e->Xh[l] = (float*)dalloc(rows * w * sizeof(float));
-        e->Xl[l] = (float*)dalloc(rows * w * sizeof(float));
+        e->Xh[l] = (float*)dalloc(rows * wx * sizeof(float));
+        e->Xl[l] = (float*)dalloc(rows * wx * sizeof(float));
+        if (wx != w) {
+          VNT_CUDA(cudaMemset(e->Xh[l], 0, rows * wx * sizeof(float)));
+          VNT_CUDA(cudaMemset(e->Xl[l], 0, rows * wx * sizeof(float)));
+        }
       }
       if (l > 0 && e->tc_layer[l - 1]) {   // D[l] (bwd-data of l-1; dW of l-1, MN-major)
         e->Dh[l] = (float*)dalloc(rows * w * sizeof(float));
@@ -420,7 +431,8 @@ uint64_t pass_row_bytes(const vnt_engine* e) {
   uint64_t b = 2 * (in + out) * sizeof(double) + out * sizeof(float);   // staging x2, logits
   for (int l = 0; l <= e->L; ++l) {
     const uint64_t w = e->widths[l] * sizeof(float);
-    if (l < e->L) b += w * (e->split && e->tc_layer[l] ? 3 : 1);            // X (+ twins)
+    const uint64_t wx = (l == 0 ? e->ld0 : e->widths[l]) * sizeof(float);
+    if (l < e->L) b += wx * (e->split && e->tc_layer[l] ? 3 : 1);           // X (+ twins)
     if (l > 0) b += w * (e->split && e->tc_layer[l - 1] ? 3 : 1);           // D (+ twins)
   }
   return b;
@@ -910,7 +922,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     // A 3xTF32 first layer reads only the twins (allocated iff it is one).
     const bool twins = e->Xh[0] != nullptr;
     k_ingest<<<(unsigned)p.rows, 128, 0, s>>>(e->xin, twins ? nullptr : e->X[0], e->Xh[0], e->Xl[0], valid,
-                                              (int)e->widths[0]);
+                                              (int)e->widths[0], (int)e->ld0);
     VNT_LAUNCH_CHECK();
     e->launches++;
   }
@@ -1907,6 +1919,7 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
       e->tc_layer.push_back(tc_layer_eligible(e->opt.gemm_mode, e->widths[l], e->widths[l + 1]));
     }
     e->P = off;
+    e->ld0 = e->tc_layer[0] ? round_up(e->widths[0], 32) : e->widths[0];
     {
       // Chosen from the widths alone, so every run of a model takes the same path.
       bool any_tc = false;

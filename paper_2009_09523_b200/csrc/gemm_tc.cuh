@@ -886,7 +886,8 @@ void tc_forward(vnt_engine* e, int l, int rows, bool last) {
   if (last) throw vntb::EngineError(1, "tcgen05 path does not produce logits");
   const bool pair = tc_use_pair();
   const uint32_t bn = pair ? PairCfg<kTcFwd>::BNH : TileCfg<kTcFwd>::BN;
-  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, K, K, BM);
+  const uint64_t lda = l == 0 ? e->ld0 : (uint64_t)K;
+  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, K, lda, BM);
   const uint64_t wo = e->wtoff[l];
   const OpMaps b = op_maps(e, e->wt32 + wo, e->wt32h + wo, e->wt32l + wo, N, K, K, bn);
   EpiArgs ep{};
@@ -938,9 +939,13 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* row0, const 
   const bool pair = tc_use_pair() && tc_dw_pair();
   const uint64_t rows = p.rows;
   // 3-D maps (one TMA per operand and stage) where the width allows
-  const bool a3 = M % 32 == 0 && tc_mn3(), b3 = N % 32 == 0 && tc_mn3();
+  // X[0] rows are padded to a multiple of 32 (ld0, zero pad columns): the 3-D
+  // box covers the last partial feature group from the pad
+  const uint64_t lda = l == 0 ? e->ld0 : (uint64_t)M;
+  const bool a3 = lda % 32 == 0 && tc_mn3(), b3 = N % 32 == 0 && tc_mn3();
   const uint32_t bgroups = (pair ? PairCfg<kTcDw, 3>::BNH : TileCfg<kTcDw>::BN) / 32;
-  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, M, M, 32, true, a3 ? BM / 32 : 0);
+  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, a3 ? lda : (uint64_t)M, lda, 32, true,
+                           a3 ? BM / 32 : 0);
   const OpMaps b = op_maps(e, e->D[l + 1], e->Dh[l + 1], e->Dl[l + 1], rows, N, N, 32, true,
                            b3 ? bgroups : 0);
   EpiArgs ep{};

@@ -54,15 +54,15 @@ __device__ __forceinline__ void put_twins(float* hi, float* lo, size_t idx, floa
 }
 
 // fp64 batch rows -> fp32 X0 and/or its 3xTF32 twins (X0 null when only the
-// twins are consumed); pad rows (valid[r] == 0) become zeros.  One block per
-// row, two elements per thread and iteration.
+// twins are consumed), row stride ld; pad rows (valid[r] == 0) become zeros.
+// One block per row, two elements per thread and iteration.
 __global__ void __launch_bounds__(128) k_ingest(const double* __restrict__ x, float* __restrict__ X0,
                                                 float* __restrict__ X0h, float* __restrict__ X0l,
-                                                const int* __restrict__ valid, int in) {
+                                                const int* __restrict__ valid, int in, int ld) {
   const int r = blockIdx.x;
   const bool ok = valid[r] != 0;
   const double* xr = x + (size_t)r * in;
-  const size_t base = (size_t)r * in;
+  const size_t base = (size_t)r * ld;   // ld >= in: the pad columns stay zero
   if ((in & 1) == 0) {
     for (int j = 2 * threadIdx.x; j < in; j += 2 * blockDim.x) {
       double2 d = ok ? __ldg(reinterpret_cast<const double2*>(xr + j)) : make_double2(0.0, 0.0);
