@@ -1004,8 +1004,10 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     prof_end(e, 2.0 * rows * (double)in_l * out_l);
     if (db_done != l) {
       dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
-      k_db<<<grid, 128, 0, s>>>(e->D[l + 1], out_l, row0, nrows, sp_scale(e, tb), lim,
-                                e->G + e->boff[l], e->tail, tb);
+      // a tcgen05 bwd-data leaves D only as its twins (hi + lo is exact)
+      const bool twins_only = l + 1 < L && e->tc_layer[l + 1] && e->Dh[l + 1];
+      k_db<<<grid, 128, 0, s>>>(twins_only ? e->Dh[l + 1] : e->D[l + 1], twins_only ? e->Dl[l + 1] : nullptr,
+                                out_l, row0, nrows, sp_scale(e, tb), lim, e->G + e->boff[l], e->tail, tb);
       VNT_LAUNCH_CHECK();
       e->launches++;
     }

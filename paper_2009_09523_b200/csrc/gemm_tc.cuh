@@ -919,7 +919,9 @@ void tc_backward_data(vnt_engine* e, int l, int rows) {
   ep.M = rows;
   ep.N = N;
   ep.act = e->act;
-  ep.out = e->D[l];          // k_db reads the plain delta
+  // k_db and a non-tcgen05 layer l-1 read the plain delta; with twins (a
+  // tcgen05 layer l-1 in 3xTF32) k_db sums hi + lo instead
+  ep.out = e->Dh[l] ? nullptr : e->D[l];
   ep.ldo = N;
   // relu' / identity' from the hi twin when the plain X was not written (above)
   ep.Xprev = (e->Xh[l] && e->act != VNT_ACT_TANH) ? e->Xh[l] : e->X[l];

@@ -502,9 +502,11 @@ __global__ void __launch_bounds__(256) k_dw_ffma(
 // Per-node bias gradient (model.cpp:322: gb = delta): column sums of D over
 // the node's rows, fp32 in row order, quantised per node; one CTA column per
 // node, exact int64 atomics (order-free) into the zeroed bias slice of G.
-__global__ void k_db(const float* __restrict__ D, int out, const int* __restrict__ vn_row0,
-                     const int* __restrict__ vn_rows, const float* __restrict__ scale_p, float lim,
-                     long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
+__global__ void k_db(const float* __restrict__ D, const float* __restrict__ Dlo, int out,
+                     const int* __restrict__ vn_row0, const int* __restrict__ vn_rows,
+                     const float* __restrict__ scale_p, float lim, long long* __restrict__ G,
+                     long long* __restrict__ tail, int tensor) {
+  // Dlo != nullptr: D is given as its 3xTF32 twins (hi + lo == D exactly)
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
   if (o >= out) return;
@@ -512,15 +514,20 @@ __global__ void k_db(const float* __restrict__ D, int out, const int* __restrict
   const float scale = *scale_p;
   float g = 0.f;
   const float* d = D + (size_t)r0 * out + o;
+  const float* dl = Dlo ? Dlo + (size_t)r0 * out + o : nullptr;
   int r = 0;
   for (; r + 8 <= n; r += 8) {   // 8 loads in flight, adds still in row order
     float t[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) t[j] = __ldg(d + (size_t)(r + j) * out);
+    if (dl) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] += __ldg(dl + (size_t)(r + j) * out);
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) g += t[j];
   }
-  for (; r < n; ++r) g += __ldg(d + (size_t)r * out);
+  for (; r < n; ++r) g += __ldg(d + (size_t)r * out) + (dl ? __ldg(dl + (size_t)r * out) : 0.f);
   const long long q = quantise(g, scale, lim, tail, tensor);
   if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&G[o]), (unsigned long long)q);
 }
