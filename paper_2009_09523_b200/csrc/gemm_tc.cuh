@@ -857,8 +857,10 @@ void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M
   using namespace vntb::tc;
   ep.kchunk = EPI == kTcDw ? 0 : tc_kchunk(e);
   ep.kfirst = tc_kfirst();
-  // forward GEMMs never share the GPU with the gradient reductions
-  const int sms = EPI == kTcFwd ? e->sm_count : e->gemm_sms;
+  // The backward GEMMs share the GPU with the per-layer gradient reductions,
+  // and with a sharded update the forward ones with the weight all-gathers:
+  // they leave kCommSms SMs to the NCCL kernels (gemm_sms).
+  const int sms = (EPI == kTcFwd && !e->shard) ? e->sm_count : e->gemm_sms;
   ep.group_m = tc_group_m();
   // CTA-pair kernels for all three GEMMs in both modes
   if (pair) {
