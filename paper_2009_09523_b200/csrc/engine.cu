@@ -526,6 +526,7 @@ template <template <int> class F, class... A>
 void dispatch_skinny(int no, A&&... a) {
   if (no <= 4) F<4>::run(a...);
   else if (no <= 8) F<8>::run(a...);
+  else if (no <= 12) F<12>::run(a...);
   else if (no <= 16) F<16>::run(a...);
   else F<32>::run(a...);
 }
@@ -544,8 +545,8 @@ struct FwdSkinny {
                                       (int)kSkinnyResidentSmem));
         attr = true;
       }
-      const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(sms, ceil_div(rows, 32)));
-      k_fwd_skinny_res<NO><<<grid, 1024, smem, s>>>(X, K, WT, no, b, rows, act, last, out);
+      const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(sms, ceil_div(rows, 64)));
+      k_fwd_skinny_res<NO><<<grid, 512, smem, s>>>(X, K, WT, no, b, rows, act, last, out);
       return;
     }
     k_fwd_skinny<NO><<<(unsigned)ceil_div(rows, 8 * skinny_rows<NO>()), 256, 0, s>>>(

@@ -714,59 +714,79 @@ __global__ void k_dw_skinny(const float* __restrict__ X, int in, const float* __
 }
 
 // Forward of a skinny layer with all of W^T ([no][K], K % 4 == 0) resident in
-// shared memory: a persistent grid, one warp per row at a time, float4 loads
-// of the row (4 in flight per lane); per output the lane-strided partial sums
-// run over k ascending, then a fixed xor tree, so every output depends only on
-// its row.
+// shared memory: a persistent grid; a warp takes 4 rows at a time so every W
+// value read from smem serves 4 rows (smem bandwidth, not HBM, bound the
+// one-row version), float4 loads of the rows (2 per row in flight per lane);
+// per (row, output) the lane-strided partial sums run over k ascending, then a
+// fixed xor tree, so every output depends only on its row.
 template <int NO>
-__global__ void __launch_bounds__(1024) k_fwd_skinny_res(const float* __restrict__ X, int K,
-                                                         const float* __restrict__ WT, int no,
-                                                         const float* __restrict__ bias, int rows,
-                                                         int act, int last, float* __restrict__ out) {
+__global__ void __launch_bounds__(512) k_fwd_skinny_res(const float* __restrict__ X, int K,
+                                                        const float* __restrict__ WT, int no,
+                                                        const float* __restrict__ bias, int rows,
+                                                        int act, int last, float* __restrict__ out) {
+  constexpr int R = 4;
   extern __shared__ float4 wsm[];
   const int K4 = K >> 2;
   for (int i = threadIdx.x; i < no * K4; i += blockDim.x) wsm[i] = __ldg(reinterpret_cast<const float4*>(WT) + i);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
-    const float4* xr = reinterpret_cast<const float4*>(X + (size_t)r * K);
-    float acc[NO];
+  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * R; r0 < rows; r0 += nw * R) {
+    const float4* xr[R];
 #pragma unroll
-    for (int o = 0; o < NO; ++o) acc[o] = 0.f;
-    auto fold = [&](const float4& xv, int k4) {
+    for (int q = 0; q < R; ++q) xr[q] = reinterpret_cast<const float4*>(X + (size_t)min(r0 + q, rows - 1) * K);
+    float acc[R][NO];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+      for (int o = 0; o < NO; ++o) acc[q][o] = 0.f;
+    auto fold = [&](const float4 (&xv)[R], int k4) {
 #pragma unroll
       for (int o = 0; o < NO; ++o)
         if (o < no) {
           const float4 w = wsm[o * K4 + k4];
-          acc[o] = fmaf(xv.x, w.x, acc[o]);
-          acc[o] = fmaf(xv.y, w.y, acc[o]);
-          acc[o] = fmaf(xv.z, w.z, acc[o]);
-          acc[o] = fmaf(xv.w, w.w, acc[o]);
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            acc[q][o] = fmaf(xv[q].x, w.x, acc[q][o]);
+            acc[q][o] = fmaf(xv[q].y, w.y, acc[q][o]);
+            acc[q][o] = fmaf(xv[q].z, w.z, acc[q][o]);
+            acc[q][o] = fmaf(xv[q].w, w.w, acc[q][o]);
+          }
         }
     };
     int k4 = lane;
-    for (; k4 + 96 < K4; k4 += 128) {   // k ascending per lane: k4, +32, +64, +96
-      float4 xv[4];
+    for (; k4 + 32 < K4; k4 += 64) {   // k ascending per lane: k4, k4 + 32
+      float4 xa[R], xb[R];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = __ldg(xr + k4 + 32 * u);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) fold(xv[u], k4 + 32 * u);
+      for (int q = 0; q < R; ++q) {
+        xa[q] = __ldg(xr[q] + k4);
+        xb[q] = __ldg(xr[q] + k4 + 32);
+      }
+      fold(xa, k4);
+      fold(xb, k4 + 32);
     }
-    for (; k4 < K4; k4 += 32) fold(__ldg(xr + k4), k4);
+    for (; k4 < K4; k4 += 32) {
+      float4 xa[R];
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
-#pragma unroll
-      for (int sft = 16; sft; sft >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], sft);
+      for (int q = 0; q < R; ++q) xa[q] = __ldg(xr[q] + k4);
+      fold(xa, k4);
     }
-    float v = 0.f;
 #pragma unroll
-    for (int o = 0; o < NO; ++o)
-      if (o == lane) v = acc[o];
-    if (lane < no) {
-      v += bias[lane];
-      if (!last) v = act_fwd(act, v);
-      out[(size_t)r * no + lane] = v;
+    for (int q = 0; q < R; ++q) {
+#pragma unroll
+      for (int o = 0; o < NO; ++o) {
+#pragma unroll
+        for (int sft = 16; sft; sft >>= 1) acc[q][o] += __shfl_xor_sync(0xffffffffu, acc[q][o], sft);
+      }
+      float v = 0.f;
+#pragma unroll
+      for (int o = 0; o < NO; ++o)
+        if (o == lane) v = acc[q][o];
+      if (lane < no && r0 + q < rows) {
+        v += bias[lane];
+        if (!last) v = act_fwd(act, v);
+        out[(size_t)(r0 + q) * no + lane] = v;
+      }
     }
   }
 }
