@@ -179,6 +179,9 @@ struct vnt_engine {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   uint64_t tail_examples = 0;          // examples node kernels already added to the tail
   std::vector<float*> Xh, Xl, Dh, Dl;
+  // relu' of X[l] as bits [rows][mask_ld(l)] when both the producing forward
+  // and the consuming bwd-data of X[l] run on tcgen05 (relu_mask(l))
+  std::vector<uint32_t*> Mk;
   float *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
   float* logits = nullptr;
   double* vn_mean = nullptr;
@@ -247,6 +250,13 @@ struct vnt_engine {
   uint32_t launches = 0;
   std::vector<void*> scratch;
 };
+
+// X[l] gets a relu bit mask: written by a tcgen05 forward of layer l-1, read
+// by the tcgen05 bwd-data of layer l.
+bool relu_mask(const vnt_engine* e, int l) {
+  return e->act == VNT_ACT_RELU && l >= 1 && l < e->L && e->tc_layer[l] && e->tc_layer[l - 1];
+}
+uint64_t mask_ld(const vnt_engine* e, int l) { return round_up(ceil_div(e->widths[l], 32), 4); }
 
 #include "gemm_tc.cuh"
 
@@ -376,6 +386,7 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t vns) {
   fre(e->vn_m2);
   for (auto* v : {&e->X, &e->D, &e->Xh, &e->Xl, &e->Dh, &e->Dl})
     for (auto*& p : *v) fre(p);
+  for (auto*& p : e->Mk) fre(p);
   const uint64_t in = e->widths[0], out = e->widths[L];
   for (int b = 0; b < 2; ++b) {
     e->xbuf[b] = (double*)dalloc(rows * in * sizeof(double));
@@ -387,6 +398,9 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t vns) {
   e->vn_mean = (double*)dalloc(vns * in * sizeof(double));
   e->vn_m2 = (double*)dalloc(vns * in * sizeof(double));
   for (auto* v : {&e->X, &e->D, &e->Xh, &e->Xl, &e->Dh, &e->Dl}) v->assign(L + 1, nullptr);
+  e->Mk.assign(L + 1, nullptr);
+  for (int l = 1; l < L; ++l)
+    if (relu_mask(e, l)) e->Mk[l] = (uint32_t*)dalloc(rows * mask_ld(e, l) * sizeof(uint32_t));
   for (int l = 0; l <= L; ++l) {
     const uint64_t w = e->widths[l];
     const uint64_t wx = l == 0 ? e->ld0 : w;   // X row stride
@@ -434,6 +448,7 @@ uint64_t pass_row_bytes(const vnt_engine* e) {
     const uint64_t wx = (l == 0 ? e->ld0 : e->widths[l]) * sizeof(float);
     if (l < e->L) b += wx * (e->split && e->tc_layer[l] ? 3 : 1);           // X (+ twins)
     if (l > 0) b += w * (e->split && e->tc_layer[l - 1] ? 3 : 1);           // D (+ twins)
+    if (relu_mask(e, l)) b += mask_ld(e, l) * sizeof(uint32_t);
   }
   return b;
 }
@@ -2069,6 +2084,8 @@ void vnt_engine_destroy(vnt_engine* e) {
   for (auto* v : {&e->X, &e->D})
     for (auto* p : *v)
       if (p) cudaFree(p);
+  for (auto* p : e->Mk)
+    if (p) cudaFree(p);
   for (auto& d : e->devs) {
     cudaFree(d.mean);
     cudaFree(d.m2);

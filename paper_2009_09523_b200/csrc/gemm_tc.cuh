@@ -101,6 +101,12 @@ struct EpiArgs {
   int ldo;
   const float* Xprev;
   int ldx;
+  // relu: f'(X) as a bit mask, [rows][ldm] words (bit j of word w = column
+  // 32 w + j > 0) — written by the producing forward, read by the bwd-data
+  // (the fp32 Xprev read in the final epilogue stalled the next tile's MMAs)
+  uint32_t* mask_out;
+  const uint32_t* mask_in;
+  int ldm;
   // 3xTF32 operand twins of out for the next tcgen05 consumer (or nullptr)
   float *outh, *outl;
   // dW: per-node partial g -> rint(g * 2^s) (scale_p: 2^s of the tensor, read
@@ -540,7 +546,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto finish32 = [&](float (&v)[32], int col) {
         const int nb = n0 + col;
         if (r >= ep.M) return;
-        if (EPI == kTcBwd && nb + 32 <= ep.N) {
+        if (EPI == kTcBwd && ep.mask_in) {
+          const uint32_t m = __ldg(ep.mask_in + (size_t)r * ep.ldm + nb / 32);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= ((m >> j) & 1u) ? 1.f : 0.f;   // relu' (model.cpp:336)
+        } else if (EPI == kTcBwd && nb + 32 <= ep.N) {
           const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -561,6 +571,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 v[j] *= act_grad_from_out(ep.act, ep.Xprev[(size_t)r * ep.ldx + n]);
             }
           }
+        }
+        if (EPI == kTcFwd && ep.mask_out) {
+          uint32_t m = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) m |= (nb + j < ep.N && v[j] > 0.f ? 1u : 0u) << j;
+          ep.mask_out[(size_t)r * ep.ldm + nb / 32] = m;
         }
         if (ep.out) {   // null: only the 3xTF32 twins are consumed
           float* orow = ep.out + (size_t)r * ep.ldo + nb;
@@ -906,6 +922,8 @@ void tc_forward(vnt_engine* e, int l, int rows, bool last) {
   // twins are allocated only when the consuming layer l+1 runs on tcgen05 in 3xTF32
   ep.outh = e->Xh[l + 1];
   ep.outl = e->Xl[l + 1];
+  ep.mask_out = e->Mk[l + 1];   // relu' bits for the tcgen05 bwd-data of layer l+1
+  ep.ldm = e->Mk[l + 1] ? (int)mask_ld(e, l + 1) : 0;
   tc_launch<kTcFwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
@@ -930,6 +948,8 @@ void tc_backward_data(vnt_engine* e, int l, int rows) {
   ep.ldx = N;
   ep.outh = e->Dh[l];
   ep.outl = e->Dl[l];
+  ep.mask_in = e->Mk[l];
+  ep.ldm = e->Mk[l] ? (int)mask_ld(e, l) : 0;
   tc_launch<kTcBwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 

@@ -293,6 +293,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < COLS; ++j) acc[j] = 0;
       }
+      // bwd-data with a relu mask: this thread's 128 mask bits, loaded before
+      // the K chunks so the final epilogue never waits on memory
+      unsigned long long mk01 = 0, mk23 = 0;
+      if constexpr (EPI == kTcBwd) {
+        if (ep.mask_in && r < ep.M) {
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(ep.mask_in + (size_t)r * ep.ldm + (n0 + h * COLS) / 32));
+          mk01 = (unsigned long long)w.x | ((unsigned long long)w.y << 32);
+          mk23 = (unsigned long long)w.z | ((unsigned long long)w.w << 32);
+        }
+      }
       // fwd / bwd: 32 finished columns (tile column col) of this thread's row ->
       // bias + act (fwd) / f' (bwd), feature-major copies, row-major copies
       // through the per-warp smem transpose tile.
@@ -307,8 +317,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (nb + j < ep.N) v[j] = act_fwd(ep.act, v[j] + bj);
           }
         }
+        if constexpr (EPI == kTcFwd) {
+          if (ep.mask_out && r < ep.M) {
+            uint32_t m = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) m |= (nb + j < ep.N && v[j] > 0.f ? 1u : 0u) << j;
+            ep.mask_out[(size_t)r * ep.ldm + nb / 32] = m;
+          }
+        }
         if (r < ep.M) {
-          if (EPI == kTcBwd && nb + 32 <= ep.N) {
+          if (EPI == kTcBwd && ep.mask_in) {
+            const int c = (col - h * COLS) >> 5;
+            const uint32_t m = (uint32_t)(((c & 2) ? mk23 : mk01) >> (32 * (c & 1)));
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= ((m >> j) & 1u) ? 1.f : 0.f;   // relu' (model.cpp:336)
+          } else if (EPI == kTcBwd && nb + 32 <= ep.N) {
             const float4* xp = reinterpret_cast<const float4*>(ep.Xprev + (size_t)r * ep.ldx + nb);
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {

@@ -21,7 +21,9 @@ PKG = ROOT / "paper_2009_09523_b200"
 
 from paper_2009_09523_b200 import build as b  # noqa: E402
 
-subprocess.check_call([b.NVCC, *b.ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-DVNT_TC_PROBE",
+import os  # noqa: E402
+extra = os.environ.get("VNT_EXTRA_DEFS", "").split()   # e.g. "-DVNT_EXP_X" for experiments
+subprocess.check_call([b.NVCC, *b.ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-DVNT_TC_PROBE", *extra,
                        "-shared", "-o", str(PKG / "libvnt_engine.so"), str(PKG / "csrc" / "engine.cu"),
                        *b.nccl_flags(), "-lcuda"])
 
