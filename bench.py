@@ -138,7 +138,7 @@ def headline_parity(vnt, work):
     return {"grad_dev_of_max": worst, "loss_rel_dev": abs(ls / ex - l_ref) / abs(l_ref),
             "tolerance": {"grad_dev_of_max": 2e-5, "loss_rel_dev": 2e-6},
             "relu_masks_resolved": flips, "mask_conflicts": conflicts,
-            "sample": f"B={B}, V={V}, widths {w}, gemm_mode auto (3xTF32); reference: fp64 C port"}
+            "sample": f"B={B}, V={V}, widths {w}, gemm_mode auto (split-fp16 tcgen05); reference: fp64 C port"}
 
 
 class ClockSampler:
@@ -486,28 +486,45 @@ def run_ours(args, work):
         line["gpu_launches_note"] = "timed region ran as CUDA-graph replays (one graph per step)"
     if gemm_n and gemm_ms > 0:
         achieved = gemm_fl / (gemm_ms / 1e3) / 1e12
-        # TF32 tensor peak is not in MEASURED_PEAKS.json: half the measured bf16 dense rate
-        # (tf32 kind runs at 1/2 the f16 rate; 1.1 vs 2.25 PF nominal).
         mode = args.gemm_mode
-        if mode == "auto":
-            mode = "3xtf32"   # VNT_GEMM_AUTO = tcgen05 3xTF32 for wide layers (vnt_engine.h)
+        if mode in ("auto", "3xtf32"):
+            mode = "3xf16"   # VNT_GEMM_AUTO = tcgen05 split-fp16 for wide layers (vnt_engine.h)
+        alt = None
         if mode == "ffma":
             peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
             peak_note = "fp32 FFMA peak 148 SM x 128 FMA/clk x 2 x sm_max_mhz"
+        elif mode == "3xf16":
+            # kind::f16 runs at the bf16 rate: the driver's measured bf16 dense
+            # burst (MEASURED_PEAKS.json) / 3 for the three MMA passes
+            # (hi*hi + hi*lo + lo*hi).  Beside it: the sustained figure (the GEMMs
+            # run inside a long step), the clock-level ceiling at the median SM
+            # clock of the timed region (148 SM x 8192 f16 flop/clk,
+            # scripts/ubench_mma_rate.cu) and the nominal 2.25 PF.
+            peak = peaks["bf16_tflops"] / 3
+            peak_note = f"bf16/f16 dense burst {peaks['bf16_tflops']:.1f} TFLOP/s ({peak_src}) / 3 MMA passes"
+            sm_mhz = (line.get("clocks") or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+            alt = {}
+            if peaks.get("bf16_tflops_sustained"):
+                sus = peaks["bf16_tflops_sustained"] / 3
+                alt["bf16_sustained"] = {"peak": sus, "frac": achieved / sus,
+                                         "source": f"bf16 dense sustained ({peak_src}) / 3"}
+            ck = 148 * 8192 * sm_mhz * 1e6 / 1e12 / 3
+            alt["clock_level"] = {"peak": ck, "frac": achieved / ck,
+                                  "source": f"148 SM x 8192 f16 flop/clk x median SM clock {sm_mhz:.0f} MHz"
+                                            " of the timed region / 3"}
+            alt["nominal"] = {"peak": 2250.0 / 3, "frac": achieved / (2250.0 / 3),
+                              "source": "2.25 PFLOP/s dense f16 nominal / 3"}
         else:
-            # Measured here: cuBLAS TF32 8192^3 held for 3 s on this GPU (no TF32
-            # figure in MEASURED_PEAKS.json); /3 for the 3xTF32 passes.  The
-            # figure derived from the driver's bf16 burst (bf16/2) is beside it.
-            # MEASURED_PEAKS.json has no TF32 figure: the denominator is the
-            # documented fallback, 1.1 PFLOP/s dense TF32 (B200_PROFILING.md),
-            # /3 for the 3xTF32 passes.  Beside it: the clock-level ceiling at
+            # 1-pass TF32.  MEASURED_PEAKS.json has no TF32 figure: the
+            # denominator is the documented fallback, 1.1 PFLOP/s dense TF32
+            # (B200_PROFILING.md).  Beside it: the clock-level ceiling at
             # the median SM clock of the timed region (148 SM x 4096 TF32
             # flop/clk, scripts/ubench_mma.cu), cuBLAS TF32 measured here, and
             # the driver's bf16 burst / 2.
-            passes = 3 if mode == "3xtf32" else 1
+            passes = 1
             peak = 1100.0 / passes
             peak_note = ("TF32 dense 1.1 PFLOP/s (fallback, B200_PROFILING.md; no TF32 figure in "
-                         "MEASURED_PEAKS.json)" + (", /3 for the 3xTF32 passes" if passes == 3 else ""))
+                         "MEASURED_PEAKS.json)")
             tf32_meas = measure_tf32_peak()
             sm_mhz = (line.get("clocks") or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
             clock_peak = 148 * 4096 * sm_mhz * 1e6 / 1e12 / passes
@@ -519,7 +536,7 @@ def run_ours(args, work):
             "gemm_share_of_step": (gemm_ms / args.steps) / ms_per_step,
             "algorithmic_flops_per_step": flops_step,
             "gemm_launches_per_step": gemm_n / args.steps,
-            "alt_peaks": None if mode == "ffma" else {
+            "alt_peaks": alt if mode != "tf32" else {
                 "clock_level": {"peak": clock_peak, "frac": achieved / clock_peak,
                                 "source": f"148 SM x 4096 TF32 flop/clk x median SM clock {sm_mhz:.0f} MHz"
                                           " of the timed region" + (", /3" if passes == 3 else "")},
@@ -531,10 +548,8 @@ def run_ours(args, work):
         }
         # DRAM bytes per GEMM launch from the committed `ncu --set full` capture of
         # this workload and mode (profiles/), next to the algorithmic operand bytes.
-        prof = ROOT / "profiles" / "r02_ncu_gemm_3xtf32.json"
-        if not prof.exists():
-            prof = ROOT / "profiles" / "r01_ncu_gemm_3xtf32.json"
-        if prof.exists() and args.workload == "cfg3" and args.gemm_mode in ("auto", "3xtf32"):
+        prof = ROOT / "profiles" / "r02_ncu_gemm_3xf16.json"
+        if prof.exists() and args.workload == "cfg3" and args.gemm_mode in ("auto", "3xf16", "3xtf32"):
             pj = json.loads(prof.read_text())
             line["roofline"]["traffic"] = pj["mean_dram_bytes_per_gemm_launch"]
             line["roofline"]["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write)"
@@ -672,7 +687,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--gemm-mode", default="auto", choices=["auto", "ffma", "tf32", "3xtf32"])
+    ap.add_argument("--gemm-mode", default="auto", choices=["auto", "ffma", "tf32", "3xf16", "3xtf32"])
     ap.add_argument("--resident-rows", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true",

@@ -57,10 +57,12 @@ extern "C" {
 
 /* GEMM arithmetic for the dense layers.  Selection depends on layer widths
  * only (never on rows), so it is identical on every rank. */
-#define VNT_GEMM_AUTO 0        /* = VNT_GEMM_3XTF32 for wide layers, FFMA fp32 otherwise    */
+#define VNT_GEMM_AUTO 0        /* = VNT_GEMM_3XF16 for wide layers, FFMA fp32 otherwise     */
 #define VNT_GEMM_FFMA 1        /* fp32 FFMA everywhere (exact fp32 products)          */
 #define VNT_GEMM_TF32 2        /* tcgen05 kind::tf32, 1 pass                         */
-#define VNT_GEMM_3XTF32 3      /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi          */
+#define VNT_GEMM_3XF16 3       /* tcgen05 kind::f16 on split-fp16 operands             */
+                               /* (x 2^s = hi + lo, hi*hi + hi*lo + lo*hi, 22 bits)     */
+#define VNT_GEMM_3XTF32 VNT_GEMM_3XF16   /* round-1 name of the split mode           */
 
 typedef struct vnt_engine vnt_engine;
 
@@ -211,12 +213,16 @@ int vnt_engine_get_input_stats(vnt_engine* e, int32_t device, double* count, dou
 int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count,
                                const double* mean, const double* m2);
 
-/* Fixed-point scale state (part of the numerical state: migrated on resize).
- * Scales set here are authoritative: the first round does not replace them
- * with its batch-size estimate. */
+/* Scale state (part of the numerical state: migrated on resize).  n =
+ * vnt_engine_tensor_count: the fixed-point scales 2^s per gradient tensor;
+ * n = vnt_engine_scale_count: followed by the split-fp16 operand exponents
+ * sigma (VNT_GEMM_3XF16), the full state a bitwise-continued trajectory
+ * needs.  Scales set here are authoritative: the first round does not
+ * replace them with its batch-size estimate. */
 int vnt_engine_get_scales(vnt_engine* e, int32_t* scales, uint32_t n);
 int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n);
 uint32_t vnt_engine_tensor_count(const vnt_engine* e);
+uint32_t vnt_engine_scale_count(const vnt_engine* e);
 /* Elastic resize across processes (elastic.cpp:106-245 at the process level):
  * join a new NCCL group (world_size, rank, 128-byte id from its rank 0) and
  * take the replica state — fp64 parameters, momentum and the fixed-point
@@ -269,8 +275,10 @@ int vnt_engine_last_timings(vnt_engine* e, vnt_step_timings* out);
  * rank of a group must issue the identical sequence; clears the log. */
 int vnt_engine_comm_log(vnt_engine* e, uint64_t* out, uint32_t cap, uint32_t* count);
 /* Diagnostics (tests): hidden activations X[layer] (rows x width, fp32) of
- * the last pass, e.g. to resolve relu masks at near-zero pre-activations when
- * comparing with an fp64 reference.  Layered path only. */
+ * the last pass, its nodes' rows in order (pad rows dropped), e.g. to resolve
+ * relu masks at near-zero pre-activations when comparing with an fp64
+ * reference; (hi + lo) 2^-sigma when only split-fp16 twins exist.  Layered
+ * path only. */
 int vnt_engine_debug_activation(vnt_engine* e, int32_t layer, float* out, uint64_t rows);
 /* The CUDA stream the engine launches on (cudaStream_t as void*). */
 void* vnt_engine_stream(vnt_engine* e);

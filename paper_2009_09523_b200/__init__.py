@@ -20,7 +20,7 @@ HOST_SO = PKG / "libvnt.so"
 
 ACTIVATIONS = {"relu": 0, "tanh": 1, "identity": 2}
 LOSSES = {"mse": 0, "softmax-cross-entropy": 1}
-GEMM_MODES = {"auto": 0, "ffma": 1, "tf32": 2, "3xtf32": 3}
+GEMM_MODES = {"auto": 0, "ffma": 1, "tf32": 2, "3xf16": 3, "3xtf32": 3}   # 3xtf32: round-1 name
 
 VNT_OK = 0
 ERRORS = {1: "Error", 2: "ConfigError", 3: "CapacityError", 6: "ShapeError",
@@ -91,6 +91,7 @@ def load_engine() -> C.CDLL:
         "vnt_engine_destroy": (None, [_vp]),
         "vnt_engine_param_count": (C.c_uint64, [_vp]),
         "vnt_engine_tensor_count": (C.c_uint32, [_vp]),
+        "vnt_engine_scale_count": (C.c_uint32, [_vp]),
         "vnt_engine_set_params": (C.c_int, [_vp, _f64p, C.c_uint64]),
         "vnt_engine_get_params": (C.c_int, [_vp, _f64p, C.c_uint64]),
         "vnt_engine_add_device": (C.c_int, [_vp, C.c_uint64, _i32p]),
@@ -322,9 +323,12 @@ class Engine:
         mean, m2 = _f64(mean), _f64(m2)
         _check(self.lib.vnt_engine_set_input_stats(self.h, device, count, _fp(mean), _fp(m2)))
 
-    def scales(self) -> np.ndarray:
-        out = np.empty(self.ntensors, np.int32)
-        _check(self.lib.vnt_engine_get_scales(self.h, out.ctypes.data_as(_i32p), self.ntensors))
+    def scales(self, full: bool = False) -> np.ndarray:
+        """Fixed-point scale exponents per gradient tensor; full=True appends the
+        split-fp16 operand exponents (vnt_engine_scale_count)."""
+        n = int(self.lib.vnt_engine_scale_count(self.h)) if full else self.ntensors
+        out = np.empty(n, np.int32)
+        _check(self.lib.vnt_engine_get_scales(self.h, out.ctypes.data_as(_i32p), n))
         return out
 
     def set_scales(self, s):

@@ -1,6 +1,7 @@
 // Shared helpers for the B200 virtual-node engine.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,6 +28,9 @@ struct EngineError : std::runtime_error {
 #define VNT_LAUNCH_CHECK() VNT_CUDA(cudaGetLastError())
 
 constexpr int kLossScaleBits = 32;   // default per-row loss quantisation 2^32 (exact int64 sum)
+// A virtual node's rows are padded to a multiple of this in a pass (zero
+// deltas): its dW K-chain runs in whole k16 steps of kind::f16 (k8 of tf32).
+constexpr int kNodeRowPad = 16;
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
@@ -35,6 +39,14 @@ inline int ceil_log2(uint64_t n) {
   int k = 0;
   while (k < 63 && (1ull << k) < n) ++k;
   return k;
+}
+
+// max with NaN propagation (max.NaN.f32): one instruction tracks both a
+// range check and a non-finite check.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
 }
 
 // Activation codes follow model.hpp:20 (relu, tanh, identity).

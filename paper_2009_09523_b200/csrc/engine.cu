@@ -178,11 +178,19 @@ struct vnt_engine {
   uint64_t host_n = 0;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   uint64_t tail_examples = 0;          // examples node kernels already added to the tail
-  std::vector<float*> Xh, Xl, Dh, Dl;
+  std::vector<__half*> Xh, Xl, Dh, Dl;
   // relu' of X[l] as bits [rows][mask_ld(l)] when both the producing forward
   // and the consuming bwd-data of X[l] run on tcgen05 (relu_mask(l))
   std::vector<uint32_t*> Mk;
-  float *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
+  __half *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
+  // split-fp16 operand scales: sigma per operand tensor (X[l] at l, D[l] at
+  // L+1+l, all weights at 2L+2), chosen from the previous step's global max|x|
+  // (h16max: one word per operand after gmax, max-reduced across ranks)
+  std::vector<int> h16_sig;
+  std::vector<int> h16_sig_step;   // the scales the last step ran with
+  std::vector<std::pair<uint64_t, uint64_t>> last_rows;   // (pass row, rows) per node of the last pass
+  unsigned long long* h16max = nullptr;
+  unsigned long long* h_h16max = nullptr;
   float* logits = nullptr;
   double* vn_mean = nullptr;
   double* vn_m2 = nullptr;
@@ -257,6 +265,25 @@ bool relu_mask(const vnt_engine* e, int l) {
   return e->act == VNT_ACT_RELU && l >= 1 && l < e->L && e->tc_layer[l] && e->tc_layer[l - 1];
 }
 uint64_t mask_ld(const vnt_engine* e, int l) { return round_up(ceil_div(e->widths[l], 32), 4); }
+
+// Split-fp16 operand ids (StepParams::h16_mul / h16_inv, h16max).
+int h16_op_x(const vnt_engine*, int l) { return l; }
+int h16_op_d(const vnt_engine* e, int l) { return e->L + 1 + l; }
+int h16_op_w(const vnt_engine* e) { return 2 * e->L + 2; }
+int h16_nops(const vnt_engine* e) { return 2 * e->L + 3; }
+const float* h16_inv(vnt_engine* e, int op) { return &e->d_sp->h16_inv[op]; }
+// Twins of operand `op` with its scale, max word and range flag (kTailH16:
+// the step is redone; kTailH16W for the weight twins an update writes for
+// the next step).
+vntb::Twin16 twin_of(vnt_engine* e, __half* hi, __half* lo, int op, int flag = vntb::kTailH16) {
+  vntb::Twin16 t{};
+  t.hi = hi;
+  t.lo = lo;
+  t.mul = &e->d_sp->h16_mul[op];
+  t.amax = e->h16max + op;
+  t.flag = e->tail + flag;
+  return t;
+}
 
 #include "gemm_tc.cuh"
 
@@ -338,6 +365,11 @@ void fill_step_params(vnt_engine* e, double lr, double inv_b) {
   h.inv_b = inv_b;
   h.loss_scale = std::ldexp(1.0, e->loss_bits);
   h.loss_lim = std::ldexp(1.0, 62) / e->loss_rows;
+  e->h16_sig_step = e->h16_sig;
+  for (size_t op = 0; op < e->h16_sig.size(); ++op) {
+    h.h16_mul[op] = std::ldexp(1.f, e->h16_sig[op]);
+    h.h16_inv[op] = std::ldexp(1.f, -e->h16_sig[op]);
+  }
 }
 
 // Pinned h_sp -> d_sp on the stream (a kernel reading mapped host memory, so it
@@ -384,7 +416,9 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t vns) {
   fre(e->logits);
   fre(e->vn_mean);
   fre(e->vn_m2);
-  for (auto* v : {&e->X, &e->D, &e->Xh, &e->Xl, &e->Dh, &e->Dl})
+  for (auto* v : {&e->X, &e->D})
+    for (auto*& p : *v) fre(p);
+  for (auto* v : {&e->Xh, &e->Xl, &e->Dh, &e->Dl})
     for (auto*& p : *v) fre(p);
   for (auto*& p : e->Mk) fre(p);
   const uint64_t in = e->widths[0], out = e->widths[L];
@@ -397,7 +431,8 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t vns) {
   e->logits = (float*)dalloc(rows * out * sizeof(float));
   e->vn_mean = (double*)dalloc(vns * in * sizeof(double));
   e->vn_m2 = (double*)dalloc(vns * in * sizeof(double));
-  for (auto* v : {&e->X, &e->D, &e->Xh, &e->Xl, &e->Dh, &e->Dl}) v->assign(L + 1, nullptr);
+  for (auto* v : {&e->X, &e->D}) v->assign(L + 1, nullptr);
+  for (auto* v : {&e->Xh, &e->Xl, &e->Dh, &e->Dl}) v->assign(L + 1, nullptr);
   e->Mk.assign(L + 1, nullptr);
   for (int l = 1; l < L; ++l)
     if (relu_mask(e, l)) e->Mk[l] = (uint32_t*)dalloc(rows * mask_ld(e, l) * sizeof(uint32_t));
@@ -411,16 +446,16 @@ void ensure_capacity(vnt_engine* e, uint64_t rows, uint64_t vns) {
     if (l > 0) e->D[l] = (float*)dalloc(rows * w * sizeof(float));
     if (e->split) {
       if (l < L && e->tc_layer[l]) {   // operands of layer l: X[l] (fwd; dW, MN-major)
-        e->Xh[l] = (float*)dalloc(rows * wx * sizeof(float));
-        e->Xl[l] = (float*)dalloc(rows * wx * sizeof(float));
+        e->Xh[l] = (__half*)dalloc(rows * wx * sizeof(__half));
+        e->Xl[l] = (__half*)dalloc(rows * wx * sizeof(__half));
         if (wx != w) {
-          VNT_CUDA(cudaMemset(e->Xh[l], 0, rows * wx * sizeof(float)));
-          VNT_CUDA(cudaMemset(e->Xl[l], 0, rows * wx * sizeof(float)));
+          VNT_CUDA(cudaMemset(e->Xh[l], 0, rows * wx * sizeof(__half)));
+          VNT_CUDA(cudaMemset(e->Xl[l], 0, rows * wx * sizeof(__half)));
         }
       }
       if (l > 0 && e->tc_layer[l - 1]) {   // D[l] (bwd-data of l-1; dW of l-1, MN-major)
-        e->Dh[l] = (float*)dalloc(rows * w * sizeof(float));
-        e->Dl[l] = (float*)dalloc(rows * w * sizeof(float));
+        e->Dh[l] = (__half*)dalloc(rows * w * sizeof(__half));
+        e->Dl[l] = (__half*)dalloc(rows * w * sizeof(__half));
       }
     }
   }
@@ -446,8 +481,8 @@ uint64_t pass_row_bytes(const vnt_engine* e) {
   for (int l = 0; l <= e->L; ++l) {
     const uint64_t w = e->widths[l] * sizeof(float);
     const uint64_t wx = (l == 0 ? e->ld0 : e->widths[l]) * sizeof(float);
-    if (l < e->L) b += wx * (e->split && e->tc_layer[l] ? 3 : 1);           // X (+ twins)
-    if (l > 0) b += w * (e->split && e->tc_layer[l - 1] ? 3 : 1);           // D (+ twins)
+    if (l < e->L) b += wx * (e->split && e->tc_layer[l] ? 2 : 1);           // X (+ fp16 twins)
+    if (l > 0) b += w * (e->split && e->tc_layer[l - 1] ? 2 : 1);           // D (+ fp16 twins)
     if (relu_mask(e, l)) b += mask_ld(e, l) * sizeof(uint32_t);
   }
   return b;
@@ -490,7 +525,7 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
     }
     PassNode pn = n;
     pn.prow = cur.rows;
-    cur.rows += round_up(n.rows, 8);   // a node's dW K-chain runs in whole k8 steps
+    cur.rows += round_up(n.rows, kNodeRowPad);   // a node's dW K-chain runs in whole MMA K steps
     cur.examples += n.rows;
     cur.nodes.push_back(pn);
   }
@@ -513,27 +548,79 @@ std::vector<Pass>& plan_for(vnt_engine* e, const std::vector<PassNode>& local) {
 }
 
 // Tail and the per-tensor max|g| words sit back to back after G: one memset, one readback.
+// Words zeroed per step after G: tail, per-tensor max|g|, split-fp16 maxima.
+size_t tail_words(const vnt_engine* e) { return e->ntail + ntensors(e) + (size_t)h16_nops(e); }
+
 void tail_reset(vnt_engine* e) {
-  VNT_CUDA(cudaMemsetAsync(e->tail, 0, (e->ntail + ntensors(e)) * sizeof(long long), e->stream));
+  VNT_CUDA(cudaMemsetAsync(e->tail, 0, tail_words(e) * sizeof(long long), e->stream));
 }
 
-void split_into(vnt_engine* e, const float* x, float* hi, float* lo, size_t n) {
+void split_into(vnt_engine* e, const float* x, __half* hi, __half* lo, size_t n, int op,
+                int flag = vntb::kTailH16) {
   if (!e->split || !hi) return;
-  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(n / 4 + 1, 256), 148 * 16);
-  k_split<<<blocks, 256, 0, e->stream>>>(x, hi, lo, n);
+  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(n, 256 * 4), 148 * 16);
+  k_split16<<<blocks, 256, 0, e->stream>>>(x, twin_of(e, hi, lo, op, flag), n);
   VNT_LAUNCH_CHECK();
   e->launches++;
 }
 
 void node_pad(vnt_engine* e);
 
+// Target of every split-fp16 scale: max|x| 2^sigma in [2^12, 2^13).
+int h16_sigma_for(float m) { return 12 - (int)std::floor(std::log2((double)m)); }
+
+// max |w| over the weight matrices (fp32 copies), host side.
+__global__ void k_absmax(const float* __restrict__ x, size_t n, unsigned long long* out) {
+  float m = 0.f;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x)
+    m = vntb::fmax_nan(m, fabsf(x[k]));
+  const unsigned b = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(out, (unsigned long long)b);
+}
+
+// Weight twins from the fp32 copies (set_params, resize, a re-split): sigma_W
+// from the current max|w| first (the only operand whose max is known before
+// its twins are written).
+void resplit_weight_twins(vnt_engine* e);
 void split_weights(vnt_engine* e) {
   if (e->node_path) node_pad(e);
   if (!e->split) return;
-  split_into(e, e->w32, e->w32h, e->w32l, e->P);
-  uint64_t tot = 0;
-  for (int l = 0; l < e->L; ++l) tot += e->widths[l] * e->widths[l + 1];
-  split_into(e, e->wt32, e->wt32h, e->wt32l, tot);
+  const int op = h16_op_w(e);
+  VNT_CUDA(cudaMemsetAsync(e->d_word, 0, sizeof(long long), e->stream));
+  for (int l = 0; l < e->L; ++l) {
+    if (!e->tc_layer[l]) continue;
+    const size_t n = e->widths[l] * e->widths[l + 1];
+    k_absmax<<<(unsigned)std::min<size_t>(ceil_div(n, 256 * 8), 1024), 256, 0, e->stream>>>(
+        e->w32 + e->woff[l], n, reinterpret_cast<unsigned long long*>(e->d_word));
+    VNT_LAUNCH_CHECK();
+  }
+  unsigned long long bits = 0;
+  VNT_CUDA(cudaMemcpyAsync(&bits, e->d_word, sizeof bits, cudaMemcpyDeviceToHost, e->stream));
+  VNT_CUDA(cudaStreamSynchronize(e->stream));
+  float m;
+  const uint32_t b32 = (uint32_t)bits;
+  std::memcpy(&m, &b32, sizeof m);
+  if (!std::isfinite(m)) throw EngineError(VNT_ERR_NONFINITE, "non-finite weight");
+  // the same band rule as h16_retune: sigma_W is a function of the weights'
+  // history, not of when the twins were last re-split (refresh, regroup)
+  const double x = std::ldexp((double)m, e->h16_sig[op]);
+  if (m > 0.f && !(x >= 1024.0 && x < 16384.0)) e->h16_sig[op] = h16_sigma_for(m);
+  e->h_sp->h16_mul[op] = std::ldexp(1.f, e->h16_sig[op]);
+  e->h_sp->h16_inv[op] = std::ldexp(1.f, -e->h16_sig[op]);
+  copy_step_params(e);
+  resplit_weight_twins(e);
+}
+
+// Weight twins of the tcgen05 layers from the fp32 copies at the current sigma_W.
+void resplit_weight_twins(vnt_engine* e) {
+  const int op = h16_op_w(e);
+  for (int l = 0; l < e->L; ++l) {
+    if (!e->tc_layer[l]) continue;
+    const size_t n = e->widths[l] * e->widths[l + 1];
+    split_into(e, e->w32 + e->woff[l], e->w32h + e->woff[l], e->w32l + e->woff[l], n, op, vntb::kTailH16W);
+    split_into(e, e->wt32 + e->wtoff[l], e->wt32h + e->wtoff[l], e->wt32l + e->wtoff[l], n, op,
+               vntb::kTailH16W);
+  }
 }
 
 // Skinny-layer (out <= 32) kernels: NO is the compile-time bound.
@@ -571,24 +658,24 @@ struct FwdSkinny {
 template <int NO>
 struct BackSkinny {
   static void run(cudaStream_t s, const float* X, const float* Dn, const float* W, int in, int no, int act,
-                  const int* row0, const int* nrows, int nn, float* Dout, float* Dh, float* Dl,
+                  const int* row0, const int* nrows, int nn, float* Dout, vntb::Twin16 twins,
                   const float* scale_w, long long* Gw, int tw, const float* scale_b, long long* Gb, int tb,
                   float lim, long long* tail) {
     dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
-    k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, Dh, Dl, scale_w, Gw, tw,
-                                               scale_b, Gb, tb, lim, tail);
+    k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, twins, scale_w, Gw,
+                                               tw, scale_b, Gb, tb, lim, tail);
   }
 };
 template <int NO>
 struct BwdSkinny {
   static void run(cudaStream_t s, const float* Dn, const float* W, int no, int in, int rows,
-                  int act, const float* Xprev, float* Dout, float* Dh, float* Dl) {
+                  int act, const float* Xprev, float* Dout, vntb::Twin16 twins) {
     static const int chunks = [] {   // 32-row chunks per CTA (VNT_BWD_SKINNY_CHUNKS)
       const char* v = getenv("VNT_BWD_SKINNY_CHUNKS");
       return v ? std::max(1, atoi(v)) : 4;
     }();
     dim3 grid((unsigned)ceil_div(in, 32), (unsigned)ceil_div(rows, 32 * chunks)), block(32, 8);
-    k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, Dh, Dl, chunks);
+    k_bwd_skinny<NO><<<grid, block, 0, s>>>(Dn, W, no, in, rows, act, Xprev, Dout, twins, chunks);
   }
 };
 template <int NO>
@@ -820,7 +907,7 @@ void step_prologue(vnt_engine* e, const Pass& p, bool stage) {
   const unsigned slices = stage ? (unsigned)std::min<uint64_t>(
       64, ceil_div(maxrows * (e->widths[0] + e->widths[e->L]) * sizeof(double), 16384)) : 4;
   k_step_prologue<<<dim3(stage ? (unsigned)nn : 16u, slices), 256, 0, e->stream>>>(
-      e->m_sp, e->d_sp, e->G, e->tail_off + e->ntail + ntensors(e), stage ? 1 : 0, e->xin, e->yin, row0,
+      e->m_sp, e->d_sp, e->G, e->tail_off + tail_words(e), stage ? 1 : 0, e->xin, e->yin, row0,
       row0 + nn, row0 + 3 * nn, (int)e->widths[0], (int)e->widths[e->L]);
   VNT_LAUNCH_CHECK();
   e->launches++;
@@ -930,14 +1017,17 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
   const uint64_t out = e->widths[L];
   const size_t nn = p.nodes.size();
   cudaStream_t s = e->stream;
+  e->last_rows.clear();
+  for (const auto& n : p.nodes) e->last_rows.emplace_back(n.prow, n.rows);
   const int* valid = p.d_meta;
   const int* row0 = p.d_meta + p.rows;
   const int* nrows = row0 + nn;
   const int rows = (int)p.rows;
   {
-    // A 3xTF32 first layer reads only the twins (allocated iff it is one).
+    // A split-fp16 first layer reads only the twins (allocated iff it is one).
     const bool twins = e->Xh[0] != nullptr;
-    k_ingest<<<(unsigned)p.rows, 128, 0, s>>>(e->xin, twins ? nullptr : e->X[0], e->Xh[0], e->Xl[0], valid,
+    const vntb::Twin16 tw = twins ? twin_of(e, e->Xh[0], e->Xl[0], h16_op_x(e, 0)) : vntb::Twin16{};
+    k_ingest<<<(unsigned)p.rows, 128, 0, s>>>(e->xin, twins ? nullptr : e->X[0], tw, valid,
                                               (int)e->widths[0], (int)e->ld0);
     VNT_LAUNCH_CHECK();
     e->launches++;
@@ -976,7 +1066,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     }
     prof_end(e, 2.0 * rows * (double)K * N);
     if (!last && !e->tc_layer[l])   // tcgen05 epilogues write the twins themselves
-      split_into(e, e->X[l + 1], e->Xh[l + 1], e->Xl[l + 1], p.rows * (uint64_t)N);
+      split_into(e, e->X[l + 1], e->Xh[l + 1], e->Xl[l + 1], p.rows * (uint64_t)N, h16_op_x(e, l + 1));
   }
   VNT_CUDA(cudaEventRecord(e->ev[1], s));
   // Loss + output delta (model.cpp:289-315); pad rows get zero deltas.
@@ -986,7 +1076,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
         e->logits, e->yin, rows, (int)out, e->loss, e->D[L], valid, e->tail, e->d_sp);
     VNT_LAUNCH_CHECK();
     e->launches++;
-    split_into(e, e->D[L], e->Dh[L], e->Dl[L], p.rows * out);
+    split_into(e, e->D[L], e->Dh[L], e->Dl[L], p.rows * out, h16_op_d(e, L));
   }
   // Backward (model.cpp:317-338): dW/db per node into the exact sum, then delta.
   const float lim = pow2f(e->lim_bits);
@@ -1004,7 +1094,9 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       const bool data = l > 0;
       dispatch_skinny<BackSkinny>(out_l, s, e->X[l], e->D[l + 1], e->w32 + e->woff[l], in_l, out_l, e->act,
                                   row0, nrows, (int)nn, data && !e->Dh[l] ? e->D[l] : nullptr,
-                                  data ? e->Dh[l] : nullptr, data ? e->Dl[l] : nullptr, sp_scale(e, tw),
+                                  data && e->Dh[l] ? twin_of(e, e->Dh[l], e->Dl[l], h16_op_d(e, l))
+                                                   : vntb::Twin16{},
+                                  sp_scale(e, tw),
                                   e->G + e->woff[l], tw, data ? sp_scale(e, tb - 2) : nullptr,
                                   data ? e->G + e->boff[l - 1] : nullptr, tb - 2, lim, e->tail);
       VNT_LAUNCH_CHECK();
@@ -1020,9 +1112,11 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     prof_end(e, 2.0 * rows * (double)in_l * out_l);
     if (db_done != l) {
       dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
-      // a tcgen05 bwd-data leaves D only as its twins (hi + lo is exact)
+      // a tcgen05 bwd-data leaves D only as its split-fp16 twins
       const bool twins_only = l + 1 < L && e->tc_layer[l + 1] && e->Dh[l + 1];
-      k_db<<<grid, 128, 0, s>>>(twins_only ? e->Dh[l + 1] : e->D[l + 1], twins_only ? e->Dl[l + 1] : nullptr,
+      k_db<<<grid, 128, 0, s>>>(e->D[l + 1], twins_only ? e->Dh[l + 1] : nullptr,
+                                twins_only ? e->Dl[l + 1] : nullptr,
+                                twins_only ? h16_inv(e, h16_op_d(e, l + 1)) : nullptr,
                                 out_l, row0, nrows, sp_scale(e, tb), lim, e->G + e->boff[l], e->tail, tb);
       VNT_LAUNCH_CHECK();
       e->launches++;
@@ -1042,7 +1136,7 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
       }
       prof_end(e, 2.0 * rows * (double)in_l * out_l);
       if (!e->tc_layer[l])   // tcgen05 epilogues write the twins themselves
-        split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l);
+        split_into(e, e->D[l], e->Dh[l], e->Dl[l], p.rows * (uint64_t)in_l, h16_op_d(e, l));
     }
   }
   if (stats) VNT_CUDA(cudaStreamWaitEvent(e->stream, e->join_ev, 0));
@@ -1278,6 +1372,20 @@ void collective(vnt_engine* e, bool full = false) {
   allreduce(e, e->G, e->tail_off + e->ntail, e->stream);
 }
 
+// The split-fp16 operand maxima of this step over the group (the next step's
+// scales, h16_retune, must be the same on every rank).
+bool h16_reduced(const vnt_engine* e) {
+  if (!e->split || e->node_path) return false;
+  for (int l = 0; l < e->L; ++l)
+    if (e->tc_layer[l]) return true;
+  return false;
+}
+void h16_reduce(vnt_engine* e) {
+  if (!e->comm || !h16_reduced(e)) return;
+  log_comm(e, kLogMax, (uint64_t)(reinterpret_cast<long long*>(e->h16max) - e->G), h16_nops(e));
+  e->comm->allreduce_max_u64(e->h16max, h16_nops(e), e->stream);
+}
+
 // Overlapped variant, issued identically (same calls, same order) on every
 // rank: layer l's G slice once its dW/db are final, from the compute stream's
 // point of view (run_pass records layer_ev[l] after them).
@@ -1330,14 +1438,13 @@ void await_layer_weights(vnt_engine* e, int l) {
   const bool twins_only = e->split && e->tc_layer[l];
   const uint64_t wo = e->woff[l], to = e->wtoff[l], bo = e->boff[l];
   dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32)), block(32, 8);
+  // the twins feed this step: their range flag is the redo slot kTailH16
+  const vntb::Twin16 tw = twins_only ? twin_of(e, e->w32h + wo, e->w32l + wo, h16_op_w(e)) : vntb::Twin16{};
   k_expand_weight<<<grid, block, 0, s>>>(src, rows, cols, twins_only ? nullptr : e->w32 + wo,
-                                         e->split ? e->w32h + wo : nullptr, e->split ? e->w32l + wo : nullptr,
-                                         twins_only ? nullptr : e->wt32 + to,
-                                         e->split ? e->wt32h + to : nullptr, e->split ? e->wt32l + to : nullptr);
+                                         twins_only ? nullptr : e->wt32 + to, tw,
+                                         twins_only ? e->wt32h + to : nullptr, twins_only ? e->wt32l + to : nullptr);
   VNT_LAUNCH_CHECK();
-  k_expand_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, s>>>(src + (size_t)rows * cols, cols, e->w32 + bo,
-                                                             e->split ? e->w32h + bo : nullptr,
-                                                             e->split ? e->w32l + bo : nullptr);
+  k_expand_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, s>>>(src + (size_t)rows * cols, cols, e->w32 + bo);
   VNT_LAUNCH_CHECK();
   e->launches += 2;
   e->ag_wait[l] = 0;
@@ -1381,10 +1488,13 @@ void gather_master(vnt_engine* e) {
 
 // Sharded update: this rank's chunk of every layer, then the per-tensor
 // max|g| (the next step's scales) is max-reduced over the group.
-void launch_sgd_shard(vnt_engine* e) {
+void launch_sgd_shard(vnt_engine* e, bool reduce_h16) {
   cudaStream_t s = e->stream;
+  if (reduce_h16) h16_reduce(e);   // the update's range check reads the group's maxima
   for (int l = 0; l < e->L; ++l) {
     ShardSgdArgs a{};
+    a.h16max = e->h16max;
+    a.h16n = h16_reduced(e) ? h16_nops(e) : 0;
     a.Gs = e->Gs + e->sh_soff[l];
     a.w64 = e->w64 + e->woff[l];
     a.v64 = e->v64 ? e->v64 + e->woff[l] : nullptr;
@@ -1422,11 +1532,14 @@ void load_shards_from_full(vnt_engine* e) {
 }
 
 // lr, 1/B (virtual_exec.cpp:165), momentum and 2^-s come from the step params.
-void launch_sgd(vnt_engine* e) {
+// reduce_h16: max-reduce the split-fp16 operand maxima first (every path
+// except an sgd_apply after vnt_engine_sync, which already did).
+void launch_sgd(vnt_engine* e, bool reduce_h16 = true) {
   if (e->shard) {
-    launch_sgd_shard(e);
+    launch_sgd_shard(e, reduce_h16);
     return;
   }
+  if (reduce_h16) h16_reduce(e);
   cudaStream_t s = e->stream;
   if (e->node_path) {   // all tensors in one launch, row-major fp32 copies only
     SgdMulti m{};
@@ -1469,21 +1582,25 @@ void launch_sgd(vnt_engine* e) {
       a.w64 = e->w64 + off;
       a.v64 = e->v64 ? e->v64 + off : nullptr;
       a.G = e->G + off;
-      // a 3xTF32 layer's weight GEMMs read only the twins
+      // a split-fp16 layer's weight GEMMs read only the twins (written for
+      // the next step: their range flag is kTailH16W, not a redo of this one)
       const bool twins_only = part == 0 && e->split && e->tc_layer[l];
       a.w32 = twins_only ? nullptr : e->w32 + off;
       a.wt32 = (part || twins_only) ? nullptr : e->wt32 + e->wtoff[l];
-      if (e->split) {
+      if (twins_only) {
         a.w32h = e->w32h + off;
         a.w32l = e->w32l + off;
-        a.wt32h = part ? nullptr : e->wt32h + e->wtoff[l];
-        a.wt32l = part ? nullptr : e->wt32l + e->wtoff[l];
+        a.wt32h = e->wt32h + e->wtoff[l];
+        a.wt32l = e->wt32l + e->wtoff[l];
+        a.wtw = twin_of(e, a.w32h, a.w32l, h16_op_w(e), vntb::kTailH16W);
       }
       a.gout = e->gout ? e->gout + off : nullptr;
       a.gmax = e->gmax + t;
       a.tail = e->tail;
       a.ntail_flags = (int)ntensors(e);
       a.sp = e->d_sp;
+      a.h16max = e->h16max;
+      a.h16n = h16_reduced(e) ? h16_nops(e) : 0;
       a.tensor = t;
       if (part == 0) {
         a.rows = (int)e->widths[l];
@@ -1513,6 +1630,7 @@ struct Readback {
   uint64_t partials;
   bool nonfinite;
   bool loss_range;             // a row loss outside the int64 range at this quantum
+  bool h16_range;              // a split-fp16 operand of this step left its range (redo)
   std::vector<int> overflow;   // tensor ids
 };
 
@@ -1528,7 +1646,7 @@ void enqueue_readback(vnt_engine* e, bool with_gmax) {
   cudaStream_t s = e->stream;
   k_copy_words<<<1, 64, 0, s>>>(reinterpret_cast<const unsigned long long*>(e->tail),
                                 reinterpret_cast<unsigned long long*>(e->m_tail),
-                                (int)(e->ntail + (with_gmax ? ntensors(e) : 0)));
+                                (int)(with_gmax || e->split ? tail_words(e) : e->ntail));
   VNT_LAUNCH_CHECK();
 }
 
@@ -1539,6 +1657,7 @@ Readback parse_readback(vnt_engine* e) {
   r.partials = (uint64_t)e->h_tail[kTailPartials];
   r.nonfinite = e->h_tail[kTailNonfinite] != 0;
   r.loss_range = e->h_tail[kTailLossRange] != 0;
+  r.h16_range = e->split && e->h_tail[kTailH16] != 0;
   for (uint32_t t = 0; t < ntensors(e); ++t)
     if (e->h_tail[kTailOverflow + t]) r.overflow.push_back((int)t);
   return r;
@@ -1556,6 +1675,42 @@ void relax_loss_bits(vnt_engine* e, double mean_loss) {
   if (e->loss_bits >= kLossScaleBits) return;
   if (std::fabs(mean_loss) * std::ldexp(1.0, kLossScaleBits + 8) < std::ldexp(1.0, 62) / e->loss_rows)
     e->loss_bits = kLossScaleBits;
+}
+
+void refresh_from_master(vnt_engine* e);
+
+// Split-fp16 scales for the next step (or the redo) from this step's max|x|
+// per operand — max-reduced over the group, so identical on every rank.  An
+// operand whose max|x| 2^sigma left [2^10, 2^14) is re-targeted to [2^12,
+// 2^13) (h16_sigma_for).  The weight twins the update just wrote (unsharded)
+// are re-split from the fp64 master at the new sigma; sharded, the next
+// weight expansion reads it.  Returns false if some operand max is not finite.
+struct H16Review {
+  bool finite = true;   // every operand max finite
+  bool under = false;   // some max|x| 2^sigma < kH16Under: the device skipped the update
+};
+H16Review h16_retune(vnt_engine* e) {
+  H16Review r;
+  if (!e->split) return r;
+  bool resplit = false;
+  for (int op = 0; op < h16_nops(e); ++op) {
+    const uint32_t b = (uint32_t)e->h_h16max[op];
+    if (b == 0) continue;
+    float m;
+    std::memcpy(&m, &b, sizeof m);
+    if (!std::isfinite(m)) {
+      r.finite = false;
+      continue;
+    }
+    const double x = std::ldexp((double)m, e->h16_sig[op]);
+    // the device-side test of block_poisoned (StepParams mul < 2^100)
+    if (h16_reduced(e) && x < vntb::kH16Under && e->h16_sig[op] < vntb::kH16SigMax) r.under = true;
+    if (x >= 1024.0 && x < 16384.0) continue;
+    e->h16_sig[op] = std::min(h16_sigma_for(m), vntb::kH16SigMax);
+    if (op == h16_op_w(e)) resplit = !e->shard;
+  }
+  if (resplit && r.finite) refresh_from_master(e);
+  return r;
 }
 
 void update_scales(vnt_engine* e, uint64_t batch) {
@@ -1798,18 +1953,23 @@ int train_step_impl(vnt_engine* e, const double* x, const double* y, uint64_t ba
       start_queued_prefetch(e);   // overlaps the next batch's H2D with this step
       rb = read_tail(e, true);
     }
-    if (rb.nonfinite || !rb.overflow.empty()) {
+    if (rb.nonfinite || !rb.overflow.empty() || rb.h16_range) {
       e->prof_n = 0;
       e->prof_flops.clear();
     }
-    if (rb.nonfinite) {
+    // an fp16 operand out of range (inf twins) also poisons what follows it:
+    // redo at the retuned scales before judging the non-finite flag
+    const H16Review h16 = h16_retune(e);
+    if (rb.nonfinite && !(rb.h16_range && h16.finite)) {
       restore_stats(e);
       reset_acc(e);
       throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
     }
-    if (!rb.overflow.empty() || rb.loss_range) {
-      for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
-      if (rb.loss_range) e->loss_bits -= kLossRescale;
+    if (!rb.overflow.empty() || rb.loss_range || rb.h16_range || h16.under) {
+      if (!rb.h16_range && !h16.under) {
+        for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
+        if (rb.loss_range) e->loss_bits -= kLossRescale;
+      }
       ++retries;
       reset_acc(e);
       if (retries > 8) throw EngineError(VNT_ERR_RESCALE, "fixed-point range could not be found");
@@ -1937,7 +2097,10 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
       e->tc_layer.push_back(tc_layer_eligible(e->opt.gemm_mode, e->widths[l], e->widths[l + 1]));
     }
     e->P = off;
-    e->ld0 = e->tc_layer[0] ? round_up(e->widths[0], 32) : e->widths[0];
+    // X[0] row stride: a whole number of 128-B MN-major groups for the dW
+    // operand when layer 0 runs on tcgen05 (64 fp16 / 32 fp32 features)
+    const bool split_mode = e->opt.gemm_mode == VNT_GEMM_3XF16 || e->opt.gemm_mode == VNT_GEMM_AUTO;
+    e->ld0 = e->tc_layer[0] ? round_up(e->widths[0], split_mode ? 64 : 32) : e->widths[0];
     {
       // Chosen from the widths alone, so every run of a model takes the same path.
       bool any_tc = false;
@@ -1989,29 +2152,39 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     VNT_CUDA(cudaMemset(e->w32, 0, e->P * sizeof(float)));
     e->wt32 = (float*)dalloc(toff * sizeof(float));
     VNT_CUDA(cudaMemset(e->wt32, 0, toff * sizeof(float)));
-    e->split = e->opt.gemm_mode == VNT_GEMM_3XTF32 || e->opt.gemm_mode == VNT_GEMM_AUTO;
+    e->split = split_mode;
     if (e->split) {
-      e->w32h = (float*)dalloc(e->P * sizeof(float));
-      e->w32l = (float*)dalloc(e->P * sizeof(float));
-      e->wt32h = (float*)dalloc(toff * sizeof(float));
-      e->wt32l = (float*)dalloc(toff * sizeof(float));
+      e->w32h = (__half*)dalloc(e->P * sizeof(__half));
+      e->w32l = (__half*)dalloc(e->P * sizeof(__half));
+      e->wt32h = (__half*)dalloc(toff * sizeof(__half));
+      e->wt32l = (__half*)dalloc(toff * sizeof(__half));
+    }
+    // split-fp16 scales before any history: activations |x| < 2^7, deltas
+    // |d| < 2^5 (larger values flag kTailH16 and the step is redone at the
+    // measured range); the weights' from their values (split_weights)
+    e->h16_sig.assign(h16_nops(e.get()), 0);
+    for (int l = 0; l <= e->L; ++l) {
+      e->h16_sig[h16_op_x(e.get(), l)] = 8;
+      e->h16_sig[h16_op_d(e.get(), l)] = 10;
     }
     e->ntail = kTailOverflow + ntensors(e.get());
     // zero gap after P: a sharded reduce-scatter of the last layer reads up to
     // 32 words per rank past its slice (kMaxRanks ranks)
     e->tail_off = round_up(e->P, 32) + 32 * kMaxRanks;
-    const uint64_t gwords = e->tail_off + e->ntail + ntensors(e.get());
+    const uint64_t gwords = e->tail_off + tail_words(e.get());
     e->G = (long long*)dalloc(gwords * sizeof(long long));
     VNT_CUDA(cudaMemset(e->G, 0, gwords * sizeof(long long)));
     e->tail = e->G + e->tail_off;
     e->gmax = reinterpret_cast<unsigned long long*>(e->tail + e->ntail);
+    e->h16max = e->gmax + ntensors(e.get());
     e->d_word = (long long*)dalloc(8 * sizeof(long long));
     if (e->node_path) {
       e->wpad = (float*)dalloc(node_wt_floats(e.get()) * sizeof(float));
       VNT_CUDA(cudaMemset(e->wpad, 0, node_wt_floats(e.get()) * sizeof(float)));
     }
-    VNT_CUDA(cudaMallocHost(&e->h_tail, (e->ntail + ntensors(e.get())) * sizeof(long long)));
+    VNT_CUDA(cudaMallocHost(&e->h_tail, tail_words(e.get()) * sizeof(long long)));
     e->h_gmax = reinterpret_cast<unsigned long long*>(e->h_tail + e->ntail);
+    e->h_h16max = e->h_gmax + ntensors(e.get());
     VNT_CUDA(cudaHostGetDevicePointer((void**)&e->m_tail, e->h_tail, 0));
     e->scales.assign(ntensors(e.get()), 0);
     if (e->L > vntb::kMaxLayers) throw EngineError(VNT_ERR_CONFIG, "too many layers (max 64)");
@@ -2177,6 +2350,7 @@ void broadcast_replica(vnt_engine* e, vntb::CommGroup* g, int root) {
   g->broadcast(e->w64, e->P * sizeof(double), root, e->stream);
   if (e->v64) g->broadcast(e->v64, e->P * sizeof(double), root, e->stream);
   std::vector<int32_t> sc(e->scales);
+  sc.insert(sc.end(), e->h16_sig.begin(), e->h16_sig.end());
   sc.push_back(e->scales_init ? 1 : 0);
   sc.push_back(e->loss_bits);
   int32_t* d_sc = (int32_t*)dalloc(sc.size() * sizeof(int32_t));
@@ -2189,7 +2363,8 @@ void broadcast_replica(vnt_engine* e, vntb::CommGroup* g, int root) {
   sc.pop_back();
   e->scales_init = sc.back() != 0;
   sc.pop_back();
-  e->scales.assign(sc.begin(), sc.end());
+  e->scales.assign(sc.begin(), sc.begin() + ntensors(e));
+  e->h16_sig.assign(sc.begin() + ntensors(e), sc.end());
 }
 }  // namespace
 
@@ -2470,10 +2645,17 @@ int vnt_engine_sync(vnt_engine* e, double* mean_grad, double* loss_sum, uint64_t
     e->acc_examples = 0;
     e->tail_examples = 0;
     collective(e, true);   // the full mean gradient on every rank (sync_gradients)
+    h16_reduce(e);
     Readback rb = read_tail(e, false);
-    if (rb.nonfinite) {
+    const H16Review h16 = h16_retune(e);
+    if (rb.nonfinite && !(rb.h16_range && h16.finite)) {
       reset_acc(e);
       throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
+    }
+    if (rb.h16_range || h16.under) {
+      restore_stats(e);
+      reset_acc(e);
+      throw EngineError(VNT_ERR_RESCALE, "fp16 operand range exceeded; scale lowered, redo the step");
     }
     if (rb.partials > (1ull << (62 - e->lim_bits))) {
       reset_acc(e);
@@ -2520,10 +2702,16 @@ int vnt_engine_take_gradient_sum(vnt_engine* e, double* sum, double* loss_sum,
     if (!e->acc_started) throw EngineError(VNT_ERR_CONFIG, "no gradients accumulated");
     add_examples_tail(e);
     Readback rb = read_tail(e, false);
-    if (rb.nonfinite) {
+    const H16Review h16 = h16_retune(e);
+    if (rb.nonfinite && !(rb.h16_range && h16.finite)) {
       restore_stats(e);
       reset_acc(e);
       throw EngineError(VNT_ERR_NONFINITE, "ExactAccumulator: non-finite value");
+    }
+    if (rb.h16_range || h16.under) {
+      restore_stats(e);
+      reset_acc(e);
+      throw EngineError(VNT_ERR_RESCALE, "fp16 operand range exceeded; scale lowered, redo the step");
     }
     if (!rb.overflow.empty() || rb.loss_range) {
       for (int t : rb.overflow) e->scales[t] -= kRescaleStep;
@@ -2569,8 +2757,9 @@ int vnt_engine_sgd_apply(vnt_engine* e, double lr) {
     const uint64_t examples = (uint64_t)e->h_tail[kTailExamples];
     upload_step_params(e, lr, 1.0 / (double)examples);
     if (e->shard) load_shards_from_full(e);
-    launch_sgd(e);
+    launch_sgd(e, false);   // vnt_engine_sync reduced the operand maxima
     read_tail(e, true);
+    h16_retune(e);   // the weight twins this update wrote
     update_scales(e, examples);
     reset_acc(e);
     return VNT_OK;
@@ -2653,19 +2842,40 @@ int vnt_engine_set_input_stats(vnt_engine* e, int32_t device, double count, cons
   });
 }
 
+uint32_t scale_count(const vnt_engine* e) {
+  return ntensors(e) + (h16_reduced(e) ? (uint32_t)h16_nops(e) : 0u);
+}
+
+uint32_t vnt_engine_scale_count(const vnt_engine* e) { return e ? scale_count(e) : 0; }
+
 int vnt_engine_get_scales(vnt_engine* e, int32_t* scales, uint32_t n) {
   return guarded([&] {
-    if (n != ntensors(e)) throw EngineError(VNT_ERR_SHAPE, "scale count mismatch");
+    if (n != ntensors(e) && n != scale_count(e)) throw EngineError(VNT_ERR_SHAPE, "scale count mismatch");
     std::copy(e->scales.begin(), e->scales.end(), scales);
+    if (n > ntensors(e)) std::copy(e->h16_sig.begin(), e->h16_sig.end(), scales + ntensors(e));
     return VNT_OK;
   });
 }
 
 int vnt_engine_set_scales(vnt_engine* e, const int32_t* scales, uint32_t n) {
   return guarded([&] {
-    if (n != ntensors(e)) throw EngineError(VNT_ERR_SHAPE, "scale count mismatch");
-    e->scales.assign(scales, scales + n);
+    if (n != ntensors(e) && n != scale_count(e)) throw EngineError(VNT_ERR_SHAPE, "scale count mismatch");
+    e->scales.assign(scales, scales + ntensors(e));
     e->scales_init = true;   // explicit scales are not replaced by the first-round estimate
+    if (n > ntensors(e)) {
+      const bool w_changed = e->h16_sig[h16_op_w(e)] != scales[ntensors(e) + h16_op_w(e)];
+      e->h16_sig.assign(scales + ntensors(e), scales + n);
+      if (w_changed) {   // the weight twins follow their scale
+        e->h_sp->h16_mul[h16_op_w(e)] = std::ldexp(1.f, e->h16_sig[h16_op_w(e)]);
+        e->h_sp->h16_inv[h16_op_w(e)] = std::ldexp(1.f, -e->h16_sig[h16_op_w(e)]);
+        copy_step_params(e);
+        if (!e->shard || e->master_valid) {
+          refresh_from_master(e);
+        } else if (!e->ag_pending) {   // re-expand the gathered fp32 weights (ag_recv)
+          e->ag_wait.assign(e->L, 1);
+        }
+      }
+    }
     return VNT_OK;
   });
 }
@@ -2755,16 +2965,27 @@ int vnt_engine_debug_activation(vnt_engine* e, int32_t layer, float* out, uint64
     if (layer < 1 || layer >= e->L) throw EngineError(VNT_ERR_CONFIG, "debug_activation: hidden layers only");
     if (e->node_path) throw EngineError(VNT_ERR_CONFIG, "debug_activation: layered path only");
     if (rows > e->cap_rows) throw EngineError(VNT_ERR_CONFIG, "debug_activation: more rows than staged");
-    const uint64_t n = rows * e->widths[layer];
+    const uint64_t w = e->widths[layer];
+    uint64_t prows = 0;   // pass rows up to the last node (pad rows included)
+    for (const auto& pr : e->last_rows) prows = std::max(prows, pr.first + pr.second);
+    const uint64_t n = prows * w;
     VNT_CUDA(cudaStreamSynchronize(e->stream));
-    if (e->X[layer] && !(e->Xh[layer] && e->act != VNT_ACT_TANH)) {
-      VNT_CUDA(cudaMemcpy(out, e->X[layer], n * sizeof(float), cudaMemcpyDeviceToHost));
-    } else {   // only the 3xTF32 twins were written: x = hi + lo exactly
-      std::vector<float> hi(n), lo(n);
-      VNT_CUDA(cudaMemcpy(hi.data(), e->Xh[layer], n * sizeof(float), cudaMemcpyDeviceToHost));
-      VNT_CUDA(cudaMemcpy(lo.data(), e->Xl[layer], n * sizeof(float), cudaMemcpyDeviceToHost));
-      for (uint64_t i = 0; i < n; ++i) out[i] = hi[i] + lo[i];
+    std::vector<float> pass(n);
+    const bool twins_only = e->Xh[layer] && e->Mk[layer] && e->tc_layer[layer - 1];
+    if (!twins_only) {
+      VNT_CUDA(cudaMemcpy(pass.data(), e->X[layer], n * sizeof(float), cudaMemcpyDeviceToHost));
+    } else {   // only the split-fp16 twins were written: x ~= (hi + lo) 2^-sigma (22 bits)
+      std::vector<__half> hi(n), lo(n);
+      VNT_CUDA(cudaMemcpy(hi.data(), e->Xh[layer], n * sizeof(__half), cudaMemcpyDeviceToHost));
+      VNT_CUDA(cudaMemcpy(lo.data(), e->Xl[layer], n * sizeof(__half), cudaMemcpyDeviceToHost));
+      const float inv = std::ldexp(1.f, -e->h16_sig_step[h16_op_x(e, layer)]);
+      for (uint64_t i = 0; i < n; ++i) pass[i] = (__half2float(hi[i]) + __half2float(lo[i])) * inv;
     }
+    // the nodes' rows in order, without the pad rows
+    uint64_t r = 0;
+    for (const auto& pr : e->last_rows)
+      for (uint64_t k = 0; k < pr.second && r < rows; ++k, ++r)
+        std::memcpy(out + r * w, pass.data() + (pr.first + k) * w, w * sizeof(float));
     return VNT_OK;
   });
 }

@@ -12,7 +12,11 @@
 // CTA-pair kernels are in gemm_tc_pair.cuh.  Warp roles: w0 TMA producer (one
 // lane), w1 MMA issuer (the whole warp runs the loop, one elected lane issues
 // tcgen05.mma.kind::tf32; accumulators in TMEM), w2 TMEM allocator, w2..w9
-// epilogue (tcgen05.ld, 32x32b).  Smem operand tiles are 128B-swizzled
+// epilogue (tcgen05.ld, 32x32b).  Two operand formats (SPLIT): 1 = fp32
+// tensors read by kind::tf32 (one pass), 3 = split-fp16 twins (x 2^sigma =
+// hi + lo, kernels_simt.cuh) read by kind::f16 as hi*hi + hi*lo + lo*hi; a
+// stage row is 128 B either way (32 tf32 or 64 fp16 K elements), so the
+// tiling, swizzles and barriers are shared.  Smem operand tiles are 128B-swizzled
 // K-major (TMA SWIZZLE_128B <-> UMMA SWIZZLE_128B descriptors); an mbarrier
 // ring feeds the MMA warp; two TMEM accumulators let the epilogue of segment s
 // overlap the MMAs of s+1.  Tiles are visited in groups of tile rows
@@ -32,7 +36,18 @@
 namespace vntb {
 namespace tc {
 
-constexpr int BM = 128, BK = 32;
+constexpr int BM = 128;
+
+// Operand format of a SPLIT: element bytes, K elements per 128-B stage row
+// (also the rows per stage and the features per 128-B group of the MN-major
+// dW operands) and K per MMA instruction.
+template <int SPLIT>
+struct Fmt {
+  static constexpr int EB = SPLIT == 3 ? 2 : 4;
+  static constexpr int BKE = 128 / EB;
+  static constexpr int KSTEP = 32 / EB;
+  static constexpr uint32_t kGroupBytes = BKE * 128;   // an MN-major 128-B group of BKE rows
+};
 // w0 TMA, w1 MMA, w2..w9 epilogue (w2 also allocates TMEM): 320 threads leave
 // the dW epilogue 204 registers for its 64 int64 accumulators (no spills).
 // Warp roles: warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator
@@ -79,8 +94,8 @@ __device__ unsigned long long g_tc_probe[6][8];
 template <int EPI, int SPLIT = 1>
 struct TileCfg {
   static constexpr int BN = EPI == kTcDw ? 128 : 256;
-  static constexpr int kBytesA = BM * BK * 4;
-  static constexpr int kBytesB = BN * BK * 4;
+  static constexpr int kBytesA = BM * 128;
+  static constexpr int kBytesB = BN * 128;
   static constexpr int kStageBytes = (SPLIT == 3 ? 2 : 1) * (kBytesA + kBytesB);
   static constexpr int STAGES_MAX = EPI == kTcDw ? 6 : 4;
   static constexpr int STAGES = (192 * 1024 / kStageBytes) < STAGES_MAX ? (192 * 1024 / kStageBytes)
@@ -89,8 +104,8 @@ struct TileCfg {
   static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256;
 };
 
-// 3xTF32: x = hi + lo with hi = rna_tf32(x) (cvt.rna.tf32.f32) and lo = x - hi
-// (exact); per k-step hi*hi + hi*lo + lo*hi accumulate into one TMEM tile.
+// Split-fp16: per k16 step hi*hi + hi*lo + lo*hi accumulate into one TMEM
+// tile; the epilogue multiplies by 2^-(sigma_A + sigma_B) (exact).
 
 struct EpiArgs {
   int M, N;
@@ -107,8 +122,11 @@ struct EpiArgs {
   uint32_t* mask_out;
   const uint32_t* mask_in;
   int ldm;
-  // 3xTF32 operand twins of out for the next tcgen05 consumer (or nullptr)
-  float *outh, *outl;
+  // split-fp16 twins of out for the next tcgen05 consumer (tw.hi nullptr: none)
+  Twin16 tw;
+  // split-fp16 operands: 2^-sigma of A and B (nullptr: fp32 operands)
+  const float* inv_a;
+  const float* inv_b;
   // dW: per-node partial g -> rint(g * 2^s) (scale_p: 2^s of the tensor, read
   // per CTA from the step parameters), |g 2^s| < lim
   long long* G;
@@ -123,7 +141,7 @@ struct EpiArgs {
   // the tiles resident at once share A and B panels in L2 (0/1: row-major)
   int group_m;
   // fwd / bwd-data: K is accumulated in TMEM in chunks of kchunk columns
-  // (multiple of BK; 0 = all of K at once) and the chunk sums are added in
+  // (multiple of Fmt::BKE; 0 = all of K at once) and the chunk sums are added in
   // fp32 registers in chunk order ("promotion").  tcgen05's TMEM accumulation
   // loses precision over long K chains (scripts/ubench_tf32_precision.cu:
   // 3xTF32 at K = 4096 is 3e-5 of max|D| in one chain, 1.2e-6 in 128-column
@@ -134,13 +152,13 @@ struct EpiArgs {
   int kfirst;
 };
 
-// K range [kb, kb + kl) of segment s: a virtual node's rows rounded up to 8
-// (dW; pad rows carry zero deltas) or a K chunk (fwd/bwd).
+// K range [kb, kb + kl) of segment s: a virtual node's rows rounded up to
+// kNodeRowPad (dW; pad rows carry zero deltas) or a K chunk (fwd/bwd).
 __device__ __forceinline__ void seg_range(int s, int nseg, const int* seg_k0, const int* seg_rows, int K,
                                           int kchunk, int kfirst, int& kb, int& kl) {
   if (nseg > 0) {
     kb = seg_k0[s];
-    kl = (int)round_up(seg_rows[s], 8);
+    kl = (int)round_up(seg_rows[s], kNodeRowPad);
   } else if (kchunk > 0) {
     kb = s == 0 ? 0 : kfirst + (s - 1) * kchunk;
     const int len = s == 0 ? kfirst : kchunk;
@@ -159,13 +177,6 @@ __host__ __device__ inline int seg_count(int nseg, int K, int kchunk, int kfirst
 
 
 
-// max with NaN propagation (max.NaN.f32): one instruction tracks both the
-// range check and the non-finite check of the per-node partials.
-__device__ __forceinline__ float fmax_nan(float a, float b) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-  return r;
-}
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -241,6 +252,24 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool mn_major = 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// MN-major fp16 operand (split-fp16 dW): the plain 128-B swizzle, rows of
+// 128 B (64 features), 8-row core groups 1024 B apart (SBO), the 64-feature
+// groups of an operand tile Fmt<3>::kGroupBytes apart (LBO).  A k16 MMA step =
+// 16 rows = 2048 B.
+__device__ __forceinline__ uint64_t sdesc_sw128_mn16(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(Fmt<3>::kGroupBytes >> 4) << 16;   // LBO: next 64-feature group
+  d |= (uint64_t)(1024 >> 4) << 32;                  // SBO: next 8-row core group
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, D fp32, A/B fp16.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool mn_major = false) {
+  return (1u << 4) | (mn_major ? (3u << 15) : 0u) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // MN-major tf32 operand: the only smem layout tcgen05 takes for it is the
 // 128-B swizzle with 32-B atomicity (layout type SWIZZLE_128B_BASE32B; what a
 // TMA box with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B lands in): rows of 128 B
@@ -268,6 +297,41 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uin
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int SPLIT>
+__device__ __forceinline__ void mma_op(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (SPLIT == 3) mma_f16(d, a, b, idesc, acc);
+  else mma_tf32(d, a, b, idesc, acc);
+}
+
+template <int SPLIT>
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr) {
+  if constexpr (SPLIT == 3) return sdesc_sw128_mn16(saddr);
+  else return sdesc_sw128_mn(saddr);
+}
+
+template <int SPLIT>
+__host__ __device__ constexpr uint32_t idesc_of(int M, int N, bool mn_major) {
+  return SPLIT == 3 ? idesc_f16(M, N, mn_major) : idesc_tf32(M, N, mn_major);
+}
+
+// Epilogue side of the split-fp16 outputs: this thread's max |x| (and the
+// range flag) into the twins' words, once per kernel (see twin_flush).
+__device__ __forceinline__ void tw_put(const Twin16& t, size_t o, float x, float mul, float& m) {
+  put16(t.hi, t.lo, o, x, mul);
+  m = fmax_nan(m, fabsf(x));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -362,7 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               int K, int nseg, const int* __restrict__ seg_k0, const int* __restrict__ seg_rows,
               EpiArgs ep) {
   using C = TileCfg<EPI, SPLIT>;
-  constexpr int BN = C::BN, STAGES = C::STAGES;
+  using F = Fmt<SPLIT>;
+  constexpr int BN = C::BN, STAGES = C::STAGES, BKE = F::BKE, GW = F::BKE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -419,35 +484,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < segs; ++s) {
           int kb, kl;
           seg_range(s, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
-          for (int k = 0; k < kl; k += BK) {
+          for (int k = 0; k < kl; k += BKE) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             mbar_expect_tx(&full[stage], C::kStageBytes);
             if constexpr (EPI == kTcDw) {
-              // MN-major: 32 rows of the row-major X / D per stage, 32-feature
-              // groups kMnGroupBytes apart — one 3-D box per operand when the
-              // width is a multiple of 32 (ep.mn3 bit 0: A, bit 1: B), else
-              // one 2-D box per group (zero fill past the width)
+              // MN-major: BKE rows of the row-major X / D per stage, GW-feature
+              // (128-B) groups F::kGroupBytes apart — one 3-D box per operand
+              // when the width is a multiple of GW (ep.mn3 bit 0: A, bit 1:
+              // B), else one 2-D box per group (zero fill past the width)
               if (ep.mn3 & 1) {
-                tma_load_3d(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / 32);
-                if (SPLIT == 3) tma_load_3d(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / 32);
+                tma_load_3d(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / GW);
+                if (SPLIT == 3) tma_load_3d(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / GW);
               } else {
 #pragma unroll
-                for (int g = 0; g < BM / 32; ++g) {
-                  tma_load_2d(sA + stage * C::kBytesA + g * kMnGroupBytes, &tmA, &full[stage], m0 + 32 * g, kb + k);
+                for (int g = 0; g < BM / GW; ++g) {
+                  tma_load_2d(sA + stage * C::kBytesA + g * F::kGroupBytes, &tmA, &full[stage], m0 + GW * g, kb + k);
                   if (SPLIT == 3)
-                    tma_load_2d(sAl + stage * C::kBytesA + g * kMnGroupBytes, &tmAl, &full[stage], m0 + 32 * g,
+                    tma_load_2d(sAl + stage * C::kBytesA + g * F::kGroupBytes, &tmAl, &full[stage], m0 + GW * g,
                                 kb + k);
                 }
               }
               if (ep.mn3 & 2) {
-                tma_load_3d(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / 32);
-                if (SPLIT == 3) tma_load_3d(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / 32);
+                tma_load_3d(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / GW);
+                if (SPLIT == 3) tma_load_3d(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / GW);
               } else {
 #pragma unroll
-                for (int g = 0; g < BN / 32; ++g) {
-                  tma_load_2d(sB + stage * C::kBytesB + g * kMnGroupBytes, &tmB, &full[stage], n0 + 32 * g, kb + k);
+                for (int g = 0; g < BN / GW; ++g) {
+                  tma_load_2d(sB + stage * C::kBytesB + g * F::kGroupBytes, &tmB, &full[stage], n0 + GW * g, kb + k);
                   if (SPLIT == 3)
-                    tma_load_2d(sBl + stage * C::kBytesB + g * kMnGroupBytes, &tmBl, &full[stage], n0 + 32 * g,
+                    tma_load_2d(sBl + stage * C::kBytesB + g * F::kGroupBytes, &tmBl, &full[stage], n0 + GW * g,
                                 kb + k);
                 }
               }
@@ -471,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     regs_dec();
     {
-      constexpr uint32_t idesc = idesc_tf32(BM, BN, EPI == kTcDw);
+      constexpr uint32_t idesc = idesc_of<SPLIT>(BM, BN, EPI == kTcDw);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;  // global (tile, segment) counter
@@ -484,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = tmem + (uint32_t)(b * BN);
           int kb, kl;
           seg_range(s, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
-          for (int k = 0; k < kl; k += BK) {
+          for (int k = 0; k < kl; k += BKE) {
 #ifdef VNT_TC_PROBE
             { const long long _t = clock64(); mbar_wait(&full[stage], phase);
               atomicAdd(&g_tc_probe[EPI][6], (unsigned long long)(clock64() - _t)); }
@@ -493,22 +558,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             tc_fence_after();
             constexpr bool mn = EPI == kTcDw;
-            const uint64_t ad = mn ? sdesc_sw128_mn(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
-            const uint64_t bd = mn ? sdesc_sw128_mn(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
-            const uint64_t ald = mn ? sdesc_sw128_mn(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
-            const uint64_t bld = mn ? sdesc_sw128_mn(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
-            // dW: a node's K-chain is its rows rounded up to 8 (k8 steps past
-            // that are rows of the next node: skipped); a k8 step is one
-            // 1024-B atom (MN-major), 32 B inside the atom (K-major)
-            const int ksteps = mn ? min(BK, kl - k) / 8 : BK / 8;
+            const uint64_t ad = mn ? sdesc_mn<SPLIT>(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
+            const uint64_t bd = mn ? sdesc_mn<SPLIT>(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
+            const uint64_t ald = mn ? sdesc_mn<SPLIT>(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
+            const uint64_t bld = mn ? sdesc_mn<SPLIT>(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
+            // dW: a node's K-chain is its rows rounded up to kNodeRowPad (K
+            // steps past that are rows of the next node: skipped); a K step
+            // is KSTEP 128-B rows (MN-major), 32 B inside the row (K-major)
+            constexpr int KS = F::KSTEP;
+            const int ksteps = mn ? min(BKE, kl - k) / KS : BKE / KS;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
+            for (int kk = 0; kk < BKE / KS; ++kk) {
               if (kk >= ksteps) break;
-              const uint64_t o = (uint64_t)(mn ? kk * 64 : kk * 2);
-              mma_tf32(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+              const uint64_t o = (uint64_t)(mn ? kk * KS * 8 : kk * 2);
+              mma_op<SPLIT>(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
               if (SPLIT == 3) {
-                mma_tf32(d, ad + o, bld + o, idesc, 1u);
-                mma_tf32(d, ald + o, bd + o, idesc, 1u);
+                mma_op<SPLIT>(d, ad + o, bld + o, idesc, 1u);
+                mma_op<SPLIT>(d, ald + o, bd + o, idesc, 1u);
               }
             }
             mma_commit(&empty[stage]);
@@ -528,7 +594,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;               // TMEM lane quarter this warp may access
     const int h = (warp - kEpiWarp0) >> 2;        // column half
     const int row = q * 32 + lane;        // tile row == TMEM lane
-    const float dscale = EPI == kTcDw ? *ep.scale_p : 1.f;   // dW: 2^s of the tensor
+    // split-fp16 operands: TMEM holds the sums at 2^(sigma_A + sigma_B)
+    const float unscale = ep.inv_a ? *ep.inv_a * *ep.inv_b : 1.f;
+    const float dscale = EPI == kTcDw ? *ep.scale_p * unscale : 1.f;   // dW: 2^s of the tensor
+    const float tmul = ep.tw.hi ? *ep.tw.mul : 1.f;
+    float tmax = 0.f;   // max |x| of the twins written
     uint32_t it = 0;
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     TC_PROBE_DECL;
@@ -546,6 +616,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto finish32 = [&](float (&v)[32], int col) {
         const int nb = n0 + col;
         if (r >= ep.M) return;
+        if constexpr (SPLIT == 3) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= unscale;
+        }
         if (EPI == kTcBwd && ep.mask_in) {
           const uint32_t m = __ldg(ep.mask_in + (size_t)r * ep.ldm + nb / 32);
 #pragma unroll
@@ -590,19 +664,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + j < ep.N) orow[j] = v[j];
           }
         }
-        if (ep.outh) {
+        if (ep.tw.hi) {
           const size_t o = (size_t)r * ep.ldo + nb;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            if (nb + j >= ep.N) break;
-            float4 hv, lv;
-            hv.x = tf32_rna(v[j]);     lv.x = v[j] - hv.x;
-            hv.y = tf32_rna(v[j + 1]); lv.y = v[j + 1] - hv.y;
-            hv.z = tf32_rna(v[j + 2]); lv.z = v[j + 2] - hv.z;
-            hv.w = tf32_rna(v[j + 3]); lv.w = v[j + 3] - hv.w;
-            *reinterpret_cast<float4*>(ep.outh + o + j) = hv;
-            *reinterpret_cast<float4*>(ep.outl + o + j) = lv;
-          }
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < ep.N) tw_put(ep.tw, o + j, v[j], tmul, tmax);
         }
       };
       int s0 = 0;
@@ -681,6 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef VNT_TC_PROBE
     if (warp == kEpiWarp0 && lane == 0) TC_PROBE_DONE(EPI, 4);
 #endif
+    if (EPI != kTcDw && ep.tw.hi) twin_flush(ep.tw, tmax, tmul);
     if (EPI == kTcDw) {
       if (!(amax <= 3.402823466e38f))   // NaN or inf: some partial was non-finite
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
@@ -719,17 +786,19 @@ inline EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// K-major fp32 operand [rows][K] with leading dimension ld (elements); box
-// 32 (K, 128 B) x box_rows, 128B swizzle, zero fill out of bounds.
-inline CUtensorMap make_map(const float* base, uint64_t rows, uint64_t K, uint64_t ld,
+// K-major operand [rows][K] (fp32, eb = 4, or fp16, eb = 2) with leading
+// dimension ld (elements); box 128 B of K x box_rows, 128B swizzle, zero fill
+// out of bounds.
+inline CUtensorMap make_map(const void* base, uint64_t rows, uint64_t K, uint64_t ld,
                             uint32_t box_rows,
-                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, int eb = 4) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {K, rows};
-  const cuuint64_t strides[1] = {ld * sizeof(float)};
-  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint64_t strides[1] = {ld * (uint64_t)eb};
+  const cuuint32_t box[2] = {(cuuint32_t)(128 / eb), box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides,
+  const CUresult r = encode_fn()(&m, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 2, (void*)base, dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -737,20 +806,24 @@ inline CUtensorMap make_map(const float* base, uint64_t rows, uint64_t K, uint64
   return m;
 }
 
-// MN-major dW operand [rows][F] (features contiguous, F % 32 == 0) as a 3-D
-// tensor {32 features, rows, F / 32 groups}: a box {32, 32, box_groups} puts
-// the groups kMnGroupBytes apart in smem, the layout the MMA descriptor
-// expects, in one TMA instruction.
-inline CUtensorMap make_map_mn3(const float* base, uint64_t rows, uint64_t F, uint64_t ld,
-                                uint32_t box_groups) {
+// MN-major dW operand [rows][F] (features contiguous, F a multiple of the
+// group width gw = 128 B / eb) as a 3-D tensor {gw features, rows, F / gw
+// groups}: a box {gw, gw rows, box_groups} puts the groups kGroupBytes apart
+// in smem, the layout the MMA descriptor expects, in one TMA instruction.
+// fp32: the 32-B-atom 128-B swizzle (tf32 MN-major); fp16: the plain one.
+inline CUtensorMap make_map_mn3(const void* base, uint64_t rows, uint64_t F, uint64_t ld,
+                                uint32_t box_groups, int eb = 4) {
   CUtensorMap m;
-  const cuuint64_t dims[3] = {32, rows, F / 32};
-  const cuuint64_t strides[2] = {ld * sizeof(float), 32 * sizeof(float)};
-  const cuuint32_t box[3] = {32, 32, box_groups};
+  const uint32_t gw = 128 / eb;
+  const cuuint64_t dims[3] = {gw, rows, F / gw};
+  const cuuint64_t strides[2] = {ld * (uint64_t)eb, (uint64_t)gw * eb};
+  const cuuint32_t box[3] = {gw, gw, box_groups};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides,
+  const CUresult r = encode_fn()(&m, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 3, (void*)base, dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 eb == 2 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw EngineError(9, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
   return m;
@@ -812,59 +885,66 @@ int tc_group_m() {
   return g;
 }
 
+// Split-fp16 operands need 16-byte row strides (widths % 8 == 0).
 bool tc_layer_eligible(int mode, uint64_t in, uint64_t out) {
   if (mode == VNT_GEMM_FFMA) return false;
-  return in >= 64 && out >= 64 && in % 4 == 0 && out % 4 == 0;
+  const uint64_t a = mode == VNT_GEMM_TF32 ? 4 : 8;
+  return in >= 64 && out >= 64 && in % a == 0 && out % a == 0;
 }
 
 void tc_init(vnt_engine*) {}
 void tc_destroy(vnt_engine*) {}
 
-// Operand maps: the fp32 tensor itself (1 pass) or its tf32 hi / lo twins (3 passes).
+// Operand maps: the fp32 tensor itself (1 pass, kind::tf32) or its split-fp16
+// hi / lo twins (3 passes, kind::f16).
 struct OpMaps {
   CUtensorMap hi, lo;
 };
 
 // mn_major: the dW operands (X / D rows as K, features contiguous) in the
-// 32-B-atom 128-B swizzle tcgen05 requires for MN-major tf32; mn3_groups > 0:
-// as 3-D maps loading that many 32-feature groups per box (width % 32 == 0).
-OpMaps op_maps(const vnt_engine* e, const float* full, const float* hi, const float* lo,
+// MN-major 128-B swizzle (32-B atoms for tf32); mn3_groups > 0: as 3-D maps
+// loading that many 128-B feature groups per box (width % group == 0).
+OpMaps op_maps(const vnt_engine* e, const float* full, const __half* hi, const __half* lo,
                uint64_t rows, uint64_t K, uint64_t ld, uint32_t box, bool mn_major = false,
                uint32_t mn3_groups = 0) {
   using namespace vntb::tc;
-  const CUtensorMapSwizzle swz = mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const int eb = e->split ? 2 : 4;
+  const CUtensorMapSwizzle swz =
+      mn_major && !e->split ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   OpMaps m;
   if (mn3_groups) {
-    m.hi = make_map_mn3(e->split ? hi : full, rows, K, ld, mn3_groups);
-    m.lo = e->split ? make_map_mn3(lo, rows, K, ld, mn3_groups) : m.hi;
+    m.hi = make_map_mn3(e->split ? (const void*)hi : (const void*)full, rows, K, ld, mn3_groups, eb);
+    m.lo = e->split ? make_map_mn3(lo, rows, K, ld, mn3_groups, eb) : m.hi;
     return m;
   }
   if (e->split) {
-    m.hi = make_map(hi, rows, K, ld, box, swz);
-    m.lo = make_map(lo, rows, K, ld, box, swz);
+    m.hi = make_map(hi, rows, K, ld, box, swz, eb);
+    m.lo = make_map(lo, rows, K, ld, box, swz, eb);
   } else {
-    m.hi = make_map(full, rows, K, ld, box, swz);
+    m.hi = make_map(full, rows, K, ld, box, swz, eb);
     m.lo = m.hi;
   }
   return m;
 }
 
-// K chunk of the fwd / bwd-data promotion (EpiArgs::kchunk): 3xTF32 only —
+// K elements per stage of the engine's operand format.
+int tc_bke(const vnt_engine* e) { return e->split ? vntb::tc::Fmt<3>::BKE : vntb::tc::Fmt<1>::BKE; }
+
+// K chunk of the fwd / bwd-data promotion (EpiArgs::kchunk): split-fp16 only —
 // a 1-pass TF32 GEMM is bounded by its operand rounding, not the chain.
-// VNT_TC_KCHUNK overrides (0 = one TMEM chain over all of K).
+// VNT_TC_KCHUNK overrides (0 = one TMEM chain over all of K); rounded to the
+// stage K.
 int tc_kchunk(const vnt_engine* e) {
   static const int env = getenv("VNT_TC_KCHUNK") ? atoi(getenv("VNT_TC_KCHUNK")) : -1;
-  if (env >= 0) return env == 0 ? 0 : (int)round_up((uint64_t)env, 32);
-  return e->split ? 128 : 0;
+  if (env >= 0) return env == 0 ? 0 : (int)round_up((uint64_t)env, tc_bke(e));
+  return e->split ? 256 : 0;
 }
-// First chunk of a tile (VNT_TC_KFIRST, default 512, multiple of 32): it runs
-// while the previous tile's epilogue still holds the other TMEM buffer.
-// Measured at cfg3 (scripts/sweep_kchunk.py): 512/128 keeps the headline
-// gradient within 1e-5 of max of the fp64 reference at 3 % below no
-// promotion (which is 1.3e-4 off).
-int tc_kfirst() {
+// First chunk of a tile (VNT_TC_KFIRST, default 512): it runs while the
+// previous tile's epilogue still holds the other TMEM buffer.  Measured at
+// cfg3 (scripts/sweep_kchunk.py, profiles/r02_summary.md).
+int tc_kfirst(const vnt_engine* e) {
   static const int env = getenv("VNT_TC_KFIRST") ? atoi(getenv("VNT_TC_KFIRST")) : 512;
-  return std::max(32, (int)round_up((uint64_t)std::max(env, 1), 32));
+  return std::max(tc_bke(e), (int)round_up((uint64_t)std::max(env, 1), tc_bke(e)));
 }
 
 template <int EPI>
@@ -872,7 +952,7 @@ void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M
                int nseg, const int* seg_k0, const int* seg_rows, vntb::tc::EpiArgs ep) {
   using namespace vntb::tc;
   ep.kchunk = EPI == kTcDw ? 0 : tc_kchunk(e);
-  ep.kfirst = tc_kfirst();
+  ep.kfirst = tc_kfirst(e);
   // The backward GEMMs share the GPU with the per-layer gradient reductions,
   // and with a sharded update the forward ones with the weight all-gathers:
   // they leave kCommSms SMs to the NCCL kernels (gemm_sms).
@@ -907,21 +987,25 @@ void tc_forward(vnt_engine* e, int l, int rows, bool last) {
   const uint64_t lda = l == 0 ? e->ld0 : (uint64_t)K;
   const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, K, lda, BM);
   const uint64_t wo = e->wtoff[l];
-  const OpMaps b = op_maps(e, e->wt32 + wo, e->wt32h + wo, e->wt32l + wo, N, K, K, bn);
+  const OpMaps b = op_maps(e, e->wt32 + wo, e->split ? e->wt32h + wo : nullptr,
+                           e->split ? e->wt32l + wo : nullptr, N, K, K, bn);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
   ep.bias = e->w32 + e->boff[l];
   ep.act = e->act;
-  // Plain X only when a consumer reads it: a 3xTF32 layer l+1 reads the
-  // twins, and its bwd-data takes relu' from the hi twin (sign of hi == sign of
-  // x); tanh' needs the full value, so tanh keeps the plain X.
+  if (e->split) {
+    ep.inv_a = h16_inv(e, h16_op_x(e, l));
+    ep.inv_b = h16_inv(e, h16_op_w(e));
+  }
+  // Plain X only when a consumer reads it: a split-fp16 layer l+1 reads the
+  // twins, and with relu its bwd-data takes f' from the mask bits; other
+  // activations keep the plain X for f'.
   const bool twins = e->Xh[l + 1] != nullptr;
-  ep.out = twins && e->act != VNT_ACT_TANH ? nullptr : e->X[l + 1];
+  ep.out = twins && e->Mk[l + 1] ? nullptr : e->X[l + 1];
   ep.ldo = N;
-  // twins are allocated only when the consuming layer l+1 runs on tcgen05 in 3xTF32
-  ep.outh = e->Xh[l + 1];
-  ep.outl = e->Xl[l + 1];
+  // twins are allocated only when the consuming layer l+1 runs on tcgen05 in split-fp16
+  if (twins) ep.tw = twin_of(e, e->Xh[l + 1], e->Xl[l + 1], h16_op_x(e, l + 1));
   ep.mask_out = e->Mk[l + 1];   // relu' bits for the tcgen05 bwd-data of layer l+1
   ep.ldm = e->Mk[l + 1] ? (int)mask_ld(e, l + 1) : 0;
   tc_launch<kTcFwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
@@ -934,27 +1018,31 @@ void tc_backward_data(vnt_engine* e, int l, int rows) {
   const uint32_t bn = pair ? PairCfg<kTcBwd>::BNH : TileCfg<kTcBwd>::BN;
   const OpMaps a = op_maps(e, e->D[l + 1], e->Dh[l + 1], e->Dl[l + 1], rows, K, K, BM);
   const uint64_t wo = e->woff[l];
-  const OpMaps b = op_maps(e, e->w32 + wo, e->w32h + wo, e->w32l + wo, N, K, K, bn);
+  const OpMaps b = op_maps(e, e->w32 + wo, e->split ? e->w32h + wo : nullptr,
+                           e->split ? e->w32l + wo : nullptr, N, K, K, bn);
   EpiArgs ep{};
   ep.M = rows;
   ep.N = N;
   ep.act = e->act;
+  if (e->split) {
+    ep.inv_a = h16_inv(e, h16_op_d(e, l + 1));
+    ep.inv_b = h16_inv(e, h16_op_w(e));
+  }
   // k_db and a non-tcgen05 layer l-1 read the plain delta; with twins (a
-  // tcgen05 layer l-1 in 3xTF32) k_db sums hi + lo instead
+  // split-fp16 layer l-1) k_db reads the twins instead
   ep.out = e->Dh[l] ? nullptr : e->D[l];
   ep.ldo = N;
-  // relu' / identity' from the hi twin when the plain X was not written (above)
-  ep.Xprev = (e->Xh[l] && e->act != VNT_ACT_TANH) ? e->Xh[l] : e->X[l];
+  ep.Xprev = e->X[l];   // f' when there is no relu mask
   ep.ldx = N;
-  ep.outh = e->Dh[l];
-  ep.outl = e->Dl[l];
+  if (e->Dh[l]) ep.tw = twin_of(e, e->Dh[l], e->Dl[l], h16_op_d(e, l));
   ep.mask_in = e->Mk[l];
   ep.ldm = e->Mk[l] ? (int)mask_ld(e, l) : 0;
   tc_launch<kTcBwd>(e, pair, a, b, rows, N, K, 0, nullptr, nullptr, ep);
 }
 
 // Per-node dW: A = X[l] (rows x in), B = D[l+1] (rows x out), both read as
-// MN-major operands (boxes of 32 features x 32 rows), K = a node's rows.
+// MN-major operands (boxes of one 128-B feature group x BKE rows), K = a
+// node's rows.
 void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* row0, const int* nrows,
                     const float* scale_p, float lim, bool first, int tensor) {
   using namespace vntb::tc;
@@ -962,15 +1050,16 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* row0, const 
   // CTA pairs (256x128, B's smem traffic per SM halved), see tc_dw_pair().
   const bool pair = tc_use_pair() && tc_dw_pair();
   const uint64_t rows = p.rows;
-  // 3-D maps (one TMA per operand and stage) where the width allows
-  // X[0] rows are padded to a multiple of 32 (ld0, zero pad columns): the 3-D
-  // box covers the last partial feature group from the pad
+  const uint32_t gw = (uint32_t)tc_bke(e);   // features per 128-B group
+  // 3-D maps (one TMA per operand and stage) where the width allows.
+  // X[0] rows are padded to a multiple of the group (ld0, zero pad columns):
+  // the 3-D box covers the last partial feature group from the pad
   const uint64_t lda = l == 0 ? e->ld0 : (uint64_t)M;
-  const bool a3 = lda % 32 == 0 && tc_mn3(), b3 = N % 32 == 0 && tc_mn3();
-  const uint32_t bgroups = (pair ? PairCfg<kTcDw, 3>::BNH : TileCfg<kTcDw>::BN) / 32;
-  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, a3 ? lda : (uint64_t)M, lda, 32, true,
-                           a3 ? BM / 32 : 0);
-  const OpMaps b = op_maps(e, e->D[l + 1], e->Dh[l + 1], e->Dl[l + 1], rows, N, N, 32, true,
+  const bool a3 = lda % gw == 0 && tc_mn3(), b3 = N % gw == 0 && tc_mn3();
+  const uint32_t bgroups = (pair ? PairCfg<kTcDw, 3>::BNH : TileCfg<kTcDw>::BN) / gw;
+  const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, a3 ? lda : (uint64_t)M, lda, gw, true,
+                           a3 ? BM / gw : 0);
+  const OpMaps b = op_maps(e, e->D[l + 1], e->Dh[l + 1], e->Dl[l + 1], rows, N, N, gw, true,
                            b3 ? bgroups : 0);
   EpiArgs ep{};
   ep.mn3 = (a3 ? 1 : 0) | (b3 ? 2 : 0);
@@ -983,6 +1072,10 @@ void tc_weight_grad(vnt_engine* e, int l, const Pass& p, const int* row0, const 
   ep.lim = lim;
   ep.tail = e->tail;
   ep.tensor = tensor;
+  if (e->split) {
+    ep.inv_a = h16_inv(e, h16_op_x(e, l));
+    ep.inv_b = h16_inv(e, h16_op_d(e, l + 1));
+  }
   tc_launch<kTcDw>(e, pair, a, b, M, N, (int)rows, (int)p.nodes.size(), row0, nrows, ep);
 }
 

@@ -17,8 +17,8 @@ template <int EPI, int SPLIT = 1>
 struct PairCfg {
   static constexpr int BN = EPI == kTcDw ? 128 : 256;
   static constexpr int BNH = BN / 2;
-  static constexpr int kBytesA = BM * BK * 4;
-  static constexpr int kBytesB = BNH * BK * 4;
+  static constexpr int kBytesA = BM * 128;
+  static constexpr int kBytesB = BNH * 128;
   static constexpr int kStageBytes = (SPLIT == 3 ? 2 : 1) * (kBytesA + kBytesB);
   static constexpr int STAGES = (192 * 1024 / kStageBytes) < 6 ? (192 * 1024 / kStageBytes) : 6;
   static constexpr int kTmemCols = 2 * BN;
@@ -82,6 +82,17 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* t
       : "memory");
 }
 
+__device__ __forceinline__ void mma_f16_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Whole-warp callers, one elected lane issues (see mma_tf32).
 __device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                               uint32_t accumulate) {
@@ -92,6 +103,12 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t a, uint64_t b
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+template <int SPLIT>
+__device__ __forceinline__ void mma_op_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (SPLIT == 3) mma_f16_pair(d, a, b, idesc, acc);
+  else mma_tf32_pair(d, a, b, idesc, acc);
 }
 
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
@@ -111,7 +128,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmBl, int K, int nseg,
                    const int* __restrict__ seg_k0, const int* __restrict__ seg_rows, EpiArgs ep) {
   using C = PairCfg<EPI, SPLIT>;
-  constexpr int BN = C::BN, BNH = C::BNH, STAGES = C::STAGES, PM = 2 * BM;
+  using F = Fmt<SPLIT>;
+  constexpr int BN = C::BN, BNH = C::BNH, STAGES = C::STAGES, PM = 2 * BM, BKE = F::BKE, GW = F::BKE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -175,35 +193,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int sg = 0; sg < segs; ++sg) {
           int kb, kl;
           seg_range(sg, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
-          for (int k = 0; k < kl; k += BK) {
+          for (int k = 0; k < kl; k += BKE) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
             if constexpr (EPI == kTcDw) {
-              // MN-major: 32 rows of the row-major X / D per stage (see k_gemm_tc)
+              // MN-major: BKE rows of the row-major X / D per stage (see k_gemm_tc)
               if (ep.mn3 & 1) {
-                tma_load_3d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / 32);
-                if (SPLIT == 3) tma_load_3d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / 32);
+                tma_load_3d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / GW);
+                if (SPLIT == 3) tma_load_3d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / GW);
               } else {
 #pragma unroll
-                for (int g = 0; g < BM / 32; ++g) {
-                  tma_load_2d_pair(sA + stage * C::kBytesA + g * kMnGroupBytes, &tmA, &full[stage], m0 + 32 * g,
+                for (int g = 0; g < BM / GW; ++g) {
+                  tma_load_2d_pair(sA + stage * C::kBytesA + g * F::kGroupBytes, &tmA, &full[stage], m0 + GW * g,
                                    kb + k);
                   if (SPLIT == 3)
-                    tma_load_2d_pair(sAl + stage * C::kBytesA + g * kMnGroupBytes, &tmAl, &full[stage], m0 + 32 * g,
-                                     kb + k);
+                    tma_load_2d_pair(sAl + stage * C::kBytesA + g * F::kGroupBytes, &tmAl, &full[stage],
+                                     m0 + GW * g, kb + k);
                 }
               }
               if (ep.mn3 & 2) {
-                tma_load_3d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / 32);
-                if (SPLIT == 3) tma_load_3d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / 32);
+                tma_load_3d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / GW);
+                if (SPLIT == 3) tma_load_3d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / GW);
               } else {
 #pragma unroll
-                for (int g = 0; g < BNH / 32; ++g) {
-                  tma_load_2d_pair(sB + stage * C::kBytesB + g * kMnGroupBytes, &tmB, &full[stage], n0 + 32 * g,
+                for (int g = 0; g < BNH / GW; ++g) {
+                  tma_load_2d_pair(sB + stage * C::kBytesB + g * F::kGroupBytes, &tmB, &full[stage], n0 + GW * g,
                                    kb + k);
                   if (SPLIT == 3)
-                    tma_load_2d_pair(sBl + stage * C::kBytesB + g * kMnGroupBytes, &tmBl, &full[stage], n0 + 32 * g,
-                                     kb + k);
+                    tma_load_2d_pair(sBl + stage * C::kBytesB + g * F::kGroupBytes, &tmBl, &full[stage],
+                                     n0 + GW * g, kb + k);
                 }
               }
             } else {
@@ -226,7 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     regs_dec();
     if (rank == 0) {
-      constexpr uint32_t idesc = idesc_tf32(PM, BN, EPI == kTcDw);
+      constexpr uint32_t idesc = idesc_of<SPLIT>(PM, BN, EPI == kTcDw);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;
@@ -239,7 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t d = tmem + (uint32_t)(b * BN);
         int kb, kl;
         seg_range(sg, nseg, seg_k0, seg_rows, K, ep.kchunk, ep.kfirst, kb, kl);
-        for (int k = 0; k < kl; k += BK) {
+        for (int k = 0; k < kl; k += BKE) {
 #ifdef VNT_TC_PROBE
           { const long long _t = clock64(); mbar_wait(&full[stage], phase);
             atomicAdd(&g_tc_probe[EPI + 3][6], (unsigned long long)(clock64() - _t)); }
@@ -248,19 +266,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
           tc_fence_after();
           constexpr bool mn = EPI == kTcDw;
-          const uint64_t ad = mn ? sdesc_sw128_mn(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
-          const uint64_t bd = mn ? sdesc_sw128_mn(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
-          const uint64_t ald = mn ? sdesc_sw128_mn(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
-          const uint64_t bld = mn ? sdesc_sw128_mn(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
-          const int ksteps = mn ? min(BK, kl - k) / 8 : BK / 8;   // dW: node rows rounded to 8
+          const uint64_t ad = mn ? sdesc_mn<SPLIT>(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
+          const uint64_t bd = mn ? sdesc_mn<SPLIT>(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
+          const uint64_t ald = mn ? sdesc_mn<SPLIT>(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
+          const uint64_t bld = mn ? sdesc_mn<SPLIT>(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
+          constexpr int KS = F::KSTEP;
+          const int ksteps = mn ? min(BKE, kl - k) / KS : BKE / KS;   // dW: node rows rounded to kNodeRowPad
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
+          for (int kk = 0; kk < BKE / KS; ++kk) {
             if (kk >= ksteps) break;
-            const uint64_t o = (uint64_t)(mn ? kk * 64 : kk * 2);
-            mma_tf32_pair(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            const uint64_t o = (uint64_t)(mn ? kk * KS * 8 : kk * 2);
+            mma_op_pair<SPLIT>(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
             if (SPLIT == 3) {
-              mma_tf32_pair(d, ad + o, bld + o, idesc, 1u);
-              mma_tf32_pair(d, ald + o, bd + o, idesc, 1u);
+              mma_op_pair<SPLIT>(d, ad + o, bld + o, idesc, 1u);
+              mma_op_pair<SPLIT>(d, ald + o, bd + o, idesc, 1u);
             }
           }
           mma_commit_pair(&empty[stage]);
@@ -279,7 +298,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int h = (warp - kEpiWarp0) >> 2;
     const int row = q * 32 + lane;
-    const float dscale = EPI == kTcDw ? *ep.scale_p : 1.f;   // dW: 2^s of the tensor
+    const float unscale = ep.inv_a ? *ep.inv_a * *ep.inv_b : 1.f;   // split-fp16: 2^-(sigma_A + sigma_B)
+    const float dscale = EPI == kTcDw ? *ep.scale_p * unscale : 1.f;   // dW: 2^s of the tensor
+    const float tmul = ep.tw.hi ? *ep.tw.mul : 1.f;
+    float tmax = 0.f;   // max |x| of the twins written
     uint32_t it = 0;
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     TC_PROBE_DECL;
@@ -308,6 +330,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // through the per-warp smem transpose tile.
       auto finish32 = [&](float (&v)[32], int col) {
         const int nb = n0 + col;
+        if constexpr (SPLIT == 3) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= unscale;
+        }
         if constexpr (EPI == kTcFwd) {
           // bias: one coalesced load per warp, broadcast by shuffles
           const float bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) : 0.f;
@@ -352,7 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // row-major copies: transpose the warp's 32x32 block through smem so
         // every store writes 128 contiguous bytes of one row (a per-thread
         // float4 row store touches 32 lines per instruction)
-        if (ep.out || ep.outh) {
+        if (ep.out || ep.tw.hi) {
           float* st = stile + (warp - kEpiWarp0) * (32 * 33);
 #pragma unroll
           for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
@@ -365,11 +391,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (rb + k < ep.M && n < ep.N) {
               const size_t o = (size_t)(rb + k) * ep.ldo + n;
               if (ep.out) ep.out[o] = x;
-              if (ep.outh) {
-                const float hx = tf32_rna(x);
-                ep.outh[o] = hx;
-                ep.outl[o] = x - hx;
-              }
+              if (ep.tw.hi) tw_put(ep.tw, o, x, tmul, tmax);
             }
           }
           __syncwarp();
@@ -454,6 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #ifdef VNT_TC_PROBE
     if (warp == kEpiWarp0 && lane == 0 && rank == 0) TC_PROBE_DONE(EPI + 3, 4);
 #endif
+    if (EPI != kTcDw && ep.tw.hi) twin_flush(ep.tw, tmax, tmul);
     if (EPI == kTcDw) {
       if (!(amax <= 3.402823466e38f))   // NaN or inf: some partial was non-finite
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);

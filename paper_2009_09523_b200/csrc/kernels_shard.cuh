@@ -24,6 +24,8 @@ struct ShardSgdArgs {
   const long long* tail;
   int ntail_flags;
   const StepParams* sp;
+  const unsigned long long* h16max;   // see SgdArgs
+  int h16n;
   int tw;                    // tensor id of the weight (bias = tw + 1)
   long long lo, hi;          // this rank's slice range
   long long nw;              // weight elements of the slice (in * out)
@@ -31,7 +33,7 @@ struct ShardSgdArgs {
 
 template <bool MOM>
 __global__ void __launch_bounds__(256) k_sgd_shard(ShardSgdArgs a) {
-  if (block_poisoned(a.tail, a.ntail_flags)) return;
+  if (block_poisoned(a.tail, a.ntail_flags, a.sp, a.h16max, a.h16n)) return;
   const double inv_b = a.sp->inv_b, lr = a.sp->lr, mu = a.sp->mu;
   const double isw = a.sp->inv_scale[a.tw], isb = a.sp->inv_scale[a.tw + 1];
   double mw = 0.0, mb = 0.0;
@@ -64,15 +66,17 @@ __global__ void k_f64_to_f32(const double* __restrict__ src, float* __restrict__
     dst[i] = __double2float_rn(src[i]);
 }
 
-// Gathered fp32 weight [rows][cols] -> row-major copy and twins, transposed
-// copy and twins (each output nullable), 32x32 tiles through smem.
+// Gathered fp32 weight [rows][cols] -> row-major copy and split-fp16 twins,
+// transposed copy and twins (each output nullable), 32x32 tiles through smem.
+// The twins' range flag is tw.flag (kTailH16: these twins feed this step).
 __global__ void k_expand_weight(const float* __restrict__ src, int rows, int cols,
-                                float* __restrict__ w32, float* __restrict__ w32h,
-                                float* __restrict__ w32l, float* __restrict__ wt32,
-                                float* __restrict__ wt32h, float* __restrict__ wt32l) {
+                                float* __restrict__ w32, float* __restrict__ wt32, Twin16 tw,
+                                __half* __restrict__ wt32h, __half* __restrict__ wt32l) {
   __shared__ float tile[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const float mul = tw.hi ? *tw.mul : 1.f;
+  float m = 0.f;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r = r0 + ty + 8 * k, c = c0 + tx;
@@ -81,14 +85,14 @@ __global__ void k_expand_weight(const float* __restrict__ src, int rows, int col
       const size_t idx = (size_t)r * cols + c;
       v = src[idx];
       if (w32) w32[idx] = v;
-      if (w32h) {
-        const float h = tf32_rna(v);
-        w32h[idx] = h;
-        w32l[idx] = v - h;
+      if (tw.hi) {
+        put16(tw.hi, tw.lo, idx, v, mul);
+        m = fmax_nan(m, fabsf(v));
       }
     }
     tile[ty + 8 * k][tx] = v;
   }
+  if (tw.hi) twin_flush(tw, m, mul);
   if (!wt32 && !wt32h) return;
   __syncthreads();
 #pragma unroll
@@ -98,26 +102,13 @@ __global__ void k_expand_weight(const float* __restrict__ src, int rows, int col
       const float v = tile[tx][ty + 8 * k];
       const size_t o = (size_t)c * rows + r;
       if (wt32) wt32[o] = v;
-      if (wt32h) {
-        const float h = tf32_rna(v);
-        wt32h[o] = h;
-        wt32l[o] = v - h;
-      }
+      if (wt32h) put16(wt32h, wt32l, o, v, mul);
     }
   }
 }
 
-__global__ void k_expand_vec(const float* __restrict__ src, int n, float* __restrict__ w32,
-                             float* __restrict__ w32h, float* __restrict__ w32l) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const float v = src[i];
-    w32[i] = v;
-    if (w32h) {
-      const float h = tf32_rna(v);
-      w32h[i] = h;
-      w32l[i] = v - h;
-    }
-  }
+__global__ void k_expand_vec(const float* __restrict__ src, int n, float* __restrict__ w32) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) w32[i] = src[i];
 }
 
 }  // namespace vntb

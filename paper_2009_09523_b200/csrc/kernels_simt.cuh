@@ -15,11 +15,50 @@
 
 namespace vntb {
 
-// 3xTF32 operand split: hi = rna_tf32(x) (cvt.rna.tf32.f32), lo = x - hi (exact).
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// Split-fp16 operands of the tcgen05 GEMMs (gemm mode 3XF16): an operand
+// tensor x is stored as two fp16 arrays with x 2^sigma ~= hi + lo,
+//   hi = fp16_rn(x 2^sigma),  lo = fp16_rn(x 2^sigma - hi)
+// (22 significant bits, the fp32 product hi*hi + hi*lo + lo*hi of two such
+// operands runs on kind::f16 at twice the kind::tf32 rate).  sigma is one
+// power of two per operand tensor, chosen each step from the previous step's
+// max|x| over all ranks so that max|x| 2^sigma sits in [2^12, 2^13)
+// (DESIGN.md §3): fp16 range limits then cost nothing — an element 2^-38 of
+// the tensor max still keeps its absolute error below 2^-25 2^-sigma.
+// Producers track max|x| (one atomicMax per warp) and flag |x 2^sigma| >=
+// kH16Lim in the tail (kTailH16: the step is redone at the new sigma, the
+// update is skipped on device).
+constexpr float kH16Lim = 32768.f;
+// max|x| 2^sigma below this (global max, sigma below kH16SigMax): the fp16
+// split would lose bits to subnormals; the update is skipped and the step
+// redone at the retuned sigma (a first step with far-off initial scales).
+constexpr float kH16Under = 0.25f;
+constexpr int kH16SigMax = 100;
+struct Twin16 {
+  __half* hi;
+  __half* lo;
+  const float* mul;            // 2^sigma of the operand (step parameters)
+  unsigned long long* amax;    // max |x| of the operand, fp32 bits
+  long long* flag;             // tail slot counting |x 2^sigma| >= kH16Lim
+};
+
+__device__ __forceinline__ void put16(__half* hi, __half* lo, size_t idx, float v, float mul) {
+  const float s = v * mul;   // exact: power of two
+  const __half h = __float2half_rn(s);
+  hi[idx] = h;
+  lo[idx] = __float2half_rn(s - __half2float(h));   // s - h exact in fp32
+}
+
+// max |x| of the calling lanes into t.amax (warp reduce, one atomic) and the
+// range flag; NaN propagates into the max (its bits order above inf).
+__device__ __forceinline__ void twin_flush(const Twin16& t, float m, float mul) {
+  const unsigned mask = __activemask();
+  const unsigned b = __reduce_max_sync(mask, __float_as_uint(m));
+  unsigned lane;
+  asm("mov.u32 %0, %%laneid;" : "=r"(lane));
+  if (b != 0u && lane == (unsigned)(__ffs(mask) - 1)) {
+    atomicMax(t.amax, (unsigned long long)b);
+    if (!(__uint_as_float(b) * mul < kH16Lim)) atomicAdd(reinterpret_cast<unsigned long long*>(t.flag), 1ull);
+  }
 }
 
 // Tail slots of the int64 accumulator (all summed exactly by the collective).
@@ -28,7 +67,9 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // per-node partials of a device_step round (int64 headroom check at sync).
 enum : int {
   kTailLoss = 0, kTailExamples = 1, kTailNonfinite = 2, kTailLossRange = 3, kTailPartials = 4,
-  kTailOverflow = 5
+  kTailH16 = 5,    // an fp16 operand of this step left its range (redo at a new sigma)
+  kTailH16W = 6,   // the weight twins written by this step's update left it (re-split)
+  kTailOverflow = 7
 };
 
 // Per-step values the kernels read from device memory (one small H2D copy per
@@ -37,6 +78,10 @@ enum : int {
 constexpr int kMaxLayers = 64;
 struct StepParams {
   float scale[2 * kMaxLayers];       // 2^s_t: per-node partial quantisation multiplier
+  // split-fp16 operand scales 2^sigma / 2^-sigma: X[l] at l, D[l] at L+1+l,
+  // the weights (all layers) at 2L+2 (h16_op_*)
+  float h16_mul[2 * kMaxLayers + 4];
+  float h16_inv[2 * kMaxLayers + 4];
   double inv_scale[2 * kMaxLayers];  // 2^-s_t
   double lr, mu, inv_b;
   double loss_scale;                 // 2^b: per-row loss quantum 2^-b
@@ -46,41 +91,43 @@ struct StepParams {
 };
 
 // ---------------------------------------------------------------- ingest
-// fp64 rows (reference Batch layout, data.hpp:14-31) -> fp32 X0 and XT0.
-__device__ __forceinline__ void put_twins(float* hi, float* lo, size_t idx, float v) {
-  const float h = tf32_rna(v);   // same split as k_split
-  hi[idx] = h;
-  lo[idx] = v - h;
-}
-
-// fp64 batch rows -> fp32 X0 and/or its 3xTF32 twins (X0 null when only the
-// twins are consumed), row stride ld; pad rows (valid[r] == 0) become zeros.
-// One block per row, two elements per thread and iteration.
+// fp64 batch rows (reference Batch layout, data.hpp:14-31) -> fp32 X0 and/or
+// its split-fp16 twins (X0 null when only the twins are consumed), row stride
+// ld; pad rows (valid[r] == 0) become zeros.  One block per row, two
+// elements per thread and iteration.
 __global__ void __launch_bounds__(128) k_ingest(const double* __restrict__ x, float* __restrict__ X0,
-                                                float* __restrict__ X0h, float* __restrict__ X0l,
-                                                const int* __restrict__ valid, int in, int ld) {
+                                                Twin16 tw, const int* __restrict__ valid, int in, int ld) {
   const int r = blockIdx.x;
   const bool ok = valid[r] != 0;
   const double* xr = x + (size_t)r * in;
   const size_t base = (size_t)r * ld;   // ld >= in: the pad columns stay zero
+  const float mul = tw.hi ? *tw.mul : 1.f;
+  float m = 0.f;
   if ((in & 1) == 0) {
     for (int j = 2 * threadIdx.x; j < in; j += 2 * blockDim.x) {
       double2 d = ok ? __ldg(reinterpret_cast<const double2*>(xr + j)) : make_double2(0.0, 0.0);
       const float2 v = make_float2(__double2float_rn(d.x), __double2float_rn(d.y));
       if (X0) *reinterpret_cast<float2*>(X0 + base + j) = v;
-      if (X0h) {
-        const float2 h = make_float2(tf32_rna(v.x), tf32_rna(v.y));
-        *reinterpret_cast<float2*>(X0h + base + j) = h;
-        *reinterpret_cast<float2*>(X0l + base + j) = make_float2(v.x - h.x, v.y - h.y);
+      if (tw.hi) {
+        const float2 s = make_float2(v.x * mul, v.y * mul);
+        const __half2 h = __floats2half2_rn(s.x, s.y);
+        const float2 hf = __half22float2(h);
+        *reinterpret_cast<__half2*>(tw.hi + base + j) = h;
+        *reinterpret_cast<__half2*>(tw.lo + base + j) = __floats2half2_rn(s.x - hf.x, s.y - hf.y);
+        m = fmax_nan(m, fmax_nan(fabsf(v.x), fabsf(v.y)));
       }
     }
   } else {
     for (int j = threadIdx.x; j < in; j += blockDim.x) {
       const float v = ok ? __double2float_rn(xr[j]) : 0.f;
       if (X0) X0[base + j] = v;
-      if (X0h) put_twins(X0h, X0l, base + j, v);
+      if (tw.hi) {
+        put16(tw.hi, tw.lo, base + j, v, mul);
+        m = fmax_nan(m, fabsf(v));
+      }
     }
   }
+  if (tw.hi) twin_flush(tw, m, mul);
 }
 
 // ------------------------------------------------------- small copies
@@ -502,32 +549,44 @@ __global__ void __launch_bounds__(256) k_dw_ffma(
 // Per-node bias gradient (model.cpp:322: gb = delta): column sums of D over
 // the node's rows, fp32 in row order, quantised per node; one CTA column per
 // node, exact int64 atomics (order-free) into the zeroed bias slice of G.
-__global__ void k_db(const float* __restrict__ D, const float* __restrict__ Dlo, int out,
+// D is either fp32 (Dh == nullptr) or given only as its split-fp16 twins:
+// d = (hi + lo) 2^-sigma (hi + lo exact in fp32, the scaling exact).
+__global__ void k_db(const float* __restrict__ D, const __half* __restrict__ Dh,
+                     const __half* __restrict__ Dl, const float* __restrict__ inv_p, int out,
                      const int* __restrict__ vn_row0, const int* __restrict__ vn_rows,
                      const float* __restrict__ scale_p, float lim, long long* __restrict__ G,
                      long long* __restrict__ tail, int tensor) {
-  // Dlo != nullptr: D is given as its 3xTF32 twins (hi + lo == D exactly)
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
   if (o >= out) return;
   const int r0 = vn_row0[v], n = vn_rows[v];
   const float scale = *scale_p;
   float g = 0.f;
-  const float* d = D + (size_t)r0 * out + o;
-  const float* dl = Dlo ? Dlo + (size_t)r0 * out + o : nullptr;
   int r = 0;
-  for (; r + 8 <= n; r += 8) {   // 8 loads in flight, adds still in row order
-    float t[8];
+  if (Dh) {
+    const float inv = *inv_p;
+    const __half* dh = Dh + (size_t)r0 * out + o;
+    const __half* dl = Dl + (size_t)r0 * out + o;
+    for (; r + 8 <= n; r += 8) {   // 8 loads in flight, adds still in row order
+      float t[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = __ldg(d + (size_t)(r + j) * out);
-    if (dl) {
+      for (int j = 0; j < 8; ++j)
+        t[j] = (__half2float(dh[(size_t)(r + j) * out]) + __half2float(dl[(size_t)(r + j) * out])) * inv;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) t[j] += __ldg(dl + (size_t)(r + j) * out);
+      for (int j = 0; j < 8; ++j) g += t[j];
     }
+    for (; r < n; ++r) g += (__half2float(dh[(size_t)r * out]) + __half2float(dl[(size_t)r * out])) * inv;
+  } else {
+    const float* d = D + (size_t)r0 * out + o;
+    for (; r + 8 <= n; r += 8) {
+      float t[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) g += t[j];
+      for (int j = 0; j < 8; ++j) t[j] = __ldg(d + (size_t)(r + j) * out);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g += t[j];
+    }
+    for (; r < n; ++r) g += __ldg(d + (size_t)r * out);
   }
-  for (; r < n; ++r) g += __ldg(d + (size_t)r * out) + (dl ? __ldg(dl + (size_t)r * out) : 0.f);
   const long long q = quantise(g, scale, lim, tail, tensor);
   if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&G[o]), (unsigned long long)q);
 }
@@ -612,15 +671,16 @@ __global__ void __launch_bounds__(256) k_fwd_skinny(const float* __restrict__ X,
 
 // bwd-data through a skinny layer: D[r][i] = (sum_o Dn[r][o] W[i][o]) f'(X[r][i]),
 // o ascending; 32 features x chunks*32 rows per block (the row block's Dn
-// rows staged in smem), D and its 3xTF32 twins written row-major.
+// rows staged in smem), D and/or its split-fp16 twins written row-major.
 template <int NO>
 __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn,
                                                     const float* __restrict__ W, int no, int in,
                                                     int rows, int act,
                                                     const float* __restrict__ Xprev,
-                                                    float* __restrict__ Dout,
-                                                    float* __restrict__ Dh, float* __restrict__ Dl,
+                                                    float* __restrict__ Dout, Twin16 tw,
                                                     int chunks) {
+  const float mul = tw.hi ? *tw.mul : 1.f;
+  float m = 0.f;
   __shared__ float dn[32][NO];
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
   const int i = blockIdx.x * 32 + tx;
@@ -647,9 +707,13 @@ __global__ void __launch_bounds__(256) k_bwd_skinny(const float* __restrict__ Dn
       const size_t idx = (size_t)r * in + i;
       const float v = acc * act_grad_from_out(act, Xprev[idx]);
       if (Dout) Dout[idx] = v;
-      if (Dh) put_twins(Dh, Dl, idx, v);
+      if (tw.hi) {
+        put16(tw.hi, tw.lo, idx, v, mul);
+        m = fmax_nan(m, fabsf(v));
+      }
     }
   }
+  if (tw.hi) twin_flush(tw, m, mul);
 }
 
 // Per-node dW of a skinny layer: thread per input feature i, NO accumulators,
@@ -799,13 +863,13 @@ __global__ void __launch_bounds__(512) k_fwd_skinny_res(const float* __restrict_
 //   db_{l-1}[i] = sum_r D[l][r][i]                    (rows ascending)
 // the same operation orders as k_dw_skinny, k_bwd_skinny and k_db.  Node
 // partials are quantised and added into G with int64 atomics (exact).  D[l]
-// is written as the 3xTF32 twins and/or plain (each nullable); Gb == nullptr
+// is written as the split-fp16 twins and/or plain (each nullable); Gb == nullptr
 // (l == 0): no bwd-data / db.
 template <int NO>
 __global__ void __launch_bounds__(128) k_skinny_backward(
     const float* __restrict__ X, const float* __restrict__ Dn, const float* __restrict__ W, int in, int no,
     int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, float* __restrict__ Dout,
-    float* __restrict__ Dh, float* __restrict__ Dl, const float* __restrict__ scale_w, long long* __restrict__ Gw,
+    Twin16 twd, const float* __restrict__ scale_w, long long* __restrict__ Gw,
     int tw, const float* __restrict__ scale_b, long long* __restrict__ Gb, int tb, float lim,
     long long* __restrict__ tail) {
   static_assert(NO % 4 == 0, "dn rows are read as float4");
@@ -814,6 +878,8 @@ __global__ void __launch_bounds__(128) k_skinny_backward(
   const int v = blockIdx.y;
   const int r0 = vn_row0[v], n = vn_rows[v];
   const bool data = Gb != nullptr;
+  const float mul = twd.hi ? *twd.mul : 1.f;
+  float m = 0.f;
   float w[NO], g[NO];
 #pragma unroll
   for (int o = 0; o < NO; ++o) {
@@ -854,20 +920,24 @@ __global__ void __launch_bounds__(128) k_skinny_backward(
           const float dv = acc * act_grad_from_out(act, a[j]);
           const size_t idx = (size_t)(r0 + c + rr + j) * in + i;
           if (Dout) Dout[idx] = dv;
-          if (Dh) put_twins(Dh, Dl, idx, dv);
+          if (twd.hi) {
+            put16(twd.hi, twd.lo, idx, dv, mul);
+            m = fmax_nan(m, fabsf(dv));
+          }
           db += dv;
         }
       }
     }
   }
+  if (twd.hi) twin_flush(twd, m, mul);
   if (i >= in) return;
-  if (data)   // the node's pad rows (up to a multiple of 8) carry zero deltas
-    for (int r = n; r < ((n + 7) & ~7); ++r) {
+  if (data)   // the node's pad rows (up to kNodeRowPad) carry zero deltas
+    for (int r = n; r < (int)round_up(n, kNodeRowPad); ++r) {
       const size_t idx = (size_t)(r0 + r) * in + i;
       if (Dout) Dout[idx] = 0.f;
-      if (Dh) {
-        Dh[idx] = 0.f;
-        Dl[idx] = 0.f;
+      if (twd.hi) {
+        twd.hi[idx] = __float2half_rn(0.f);
+        twd.lo[idx] = __float2half_rn(0.f);
       }
     }
   const float sw = *scale_w;
@@ -895,10 +965,13 @@ struct SgdArgs {
   const long long* G;   // exact gradient sum (same layout as params)
   float* w32;
   float* wt32;          // transposed copy (weights only) or nullptr
-  float *w32h, *w32l;   // 3xTF32 twins of w32 (or nullptr)
-  float *wt32h, *wt32l; // 3xTF32 twins of wt32 (or nullptr)
+  __half *w32h, *w32l;   // split-fp16 twins of w32 (or nullptr)
+  __half *wt32h, *wt32l; // split-fp16 twins of wt32 (or nullptr)
+  Twin16 wtw;            // the weights' scale, max and range slot (kTailH16W)
   double* gout;         // optional mean-gradient export
   unsigned long long* gmax;  // max |g| of this tensor (bit pattern of a positive double)
+  const unsigned long long* h16max;  // split-fp16 operand maxima of the step (global), h16n of them
+  int h16n;
   const long long* tail;
   int ntail_flags;
   const StepParams* sp; // 2^-s per tensor, 1/B (virtual_exec.cpp:165), lr, mu
@@ -908,13 +981,22 @@ struct SgdArgs {
   int rows, cols;       // tensor shape (bias: rows = 1)
 };
 
-// Block-wide: did the step hit a non-finite value or a fixed-point overflow?
-// One flag per thread (blockDim >= 1 + nflags), no serial chain of loads.
-__device__ __forceinline__ bool block_poisoned(const long long* tail, int nflags) {
+// Block-wide: did the step hit a non-finite value, a fixed-point overflow or
+// a split-fp16 operand out of its range (kTailH16, or a global max|x| 2^sigma
+// below kH16Under)?  One flag per thread, no serial chain of loads.
+__device__ __forceinline__ bool block_poisoned(const long long* tail, int nflags,
+                                               const StepParams* sp = nullptr,
+                                               const unsigned long long* h16max = nullptr, int h16n = 0) {
   const int t = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nt = blockDim.x * blockDim.y;
   bool bad = false;
-  if (t == 0) bad = tail[kTailNonfinite] != 0 || tail[kTailLossRange] != 0;
-  else if (t <= nflags) bad = tail[kTailOverflow + t - 1] != 0;
+  if (t == 0) bad = tail[kTailNonfinite] != 0 || tail[kTailLossRange] != 0 || tail[kTailH16] != 0;
+  for (int i = t; i < nflags; i += nt) bad |= tail[kTailOverflow + i] != 0;
+  for (int i = t; i < h16n; i += nt) {
+    const float m = __uint_as_float((uint32_t)h16max[i]);
+    const float mul = sp->h16_mul[i];
+    bad |= m > 0.f && m * mul < kH16Under && mul < 0x1p100f;
+  }
   return __syncthreads_or(bad);
 }
 
@@ -976,9 +1058,11 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
     w[k] = ok ? a.w64[idx] : 0.0;
     if constexpr (MOM) v[k] = ok ? a.v64[idx] : 0.0;
   }
-  if (block_poisoned(a.tail, a.ntail_flags)) return;
+  if (block_poisoned(a.tail, a.ntail_flags, a.sp, a.h16max, a.h16n)) return;
   const double inv_scale = a.sp->inv_scale[a.tensor], inv_b = a.sp->inv_b;
   const double lr = a.sp->lr, mu = a.sp->mu;
+  const float wmul = a.w32h ? *a.wtw.mul : 1.f;
+  float wm = 0.f;
   double mx = 0.0;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
@@ -996,14 +1080,14 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
       if constexpr (MOM) a.v64[idx] = u;
       if (a.w32) a.w32[idx] = w32;
       if (a.w32h) {
-        const float h = tf32_rna(w32);
-        a.w32h[idx] = h;
-        a.w32l[idx] = w32 - h;
+        put16(a.w32h, a.w32l, idx, w32, wmul);
+        wm = fmax_nan(wm, fabsf(w32));
       }
       if (a.gout) a.gout[idx] = g;
       mx = fmax(mx, fabs(g));
     }
   }
+  if (a.w32h) twin_flush(a.wtw, wm, wmul);
   block_max_to(a.gmax, mx);
   if (!a.wt32 && !a.wt32h) return;
   __syncthreads();
@@ -1020,18 +1104,14 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
         const float v = tile[h * 32 + tx][cc];
         const size_t o = (size_t)col * a.rows + r;
         if (a.wt32) a.wt32[o] = v;
-        if (a.wt32h) {
-          const float hv = tf32_rna(v);
-          a.wt32h[o] = hv;
-          a.wt32l[o] = v - hv;
-        }
+        if (a.wt32h) put16(a.wt32h, a.wt32l, o, v, wmul);
       }
     }
   }
 }
 
 __global__ void k_sgd_vec(SgdArgs a) {
-  if (block_poisoned(a.tail, a.ntail_flags)) return;
+  if (block_poisoned(a.tail, a.ntail_flags, a.sp, a.h16max, a.h16n)) return;
   const size_t n = (size_t)a.rows * a.cols;
   double mx = 0.0;
   for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
@@ -1039,11 +1119,6 @@ __global__ void k_sgd_vec(SgdArgs a) {
     float w32;
     mx = fmax(mx, sgd_one(a, k, w32));
     a.w32[k] = w32;
-    if (a.w32h) {
-      const float h = tf32_rna(w32);
-      a.w32h[k] = h;
-      a.w32l[k] = w32 - h;
-    }
   }
   block_max_to(a.gmax, mx);
 }
@@ -1080,26 +1155,18 @@ __global__ void k_refresh_vec(const double* __restrict__ w64, float* __restrict_
 }  // namespace vntb
 
 namespace vntb {
-__global__ void k_split(const float* __restrict__ x, float* __restrict__ hi,
-                        float* __restrict__ lo, size_t n) {
-  const size_t n4 = n / 4;
-  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n4;
+// fp32 tensor -> its split-fp16 twins (an FFMA-produced operand of a tcgen05
+// layer, the weights after set_params / a re-split).
+__global__ void k_split16(const float* __restrict__ x, Twin16 t, size_t n) {
+  const float mul = *t.mul;
+  float m = 0.f;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
        k += (size_t)gridDim.x * blockDim.x) {
-    const float4 v = reinterpret_cast<const float4*>(x)[k];
-    float4 h, l;
-    h.x = tf32_rna(v.x); l.x = v.x - h.x;
-    h.y = tf32_rna(v.y); l.y = v.y - h.y;
-    h.z = tf32_rna(v.z); l.z = v.z - h.z;
-    h.w = tf32_rna(v.w); l.w = v.w - h.w;
-    reinterpret_cast<float4*>(hi)[k] = h;
-    reinterpret_cast<float4*>(lo)[k] = l;
+    const float v = x[k];
+    put16(t.hi, t.lo, k, v, mul);
+    m = fmax_nan(m, fabsf(v));
   }
-  for (size_t k = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
-       k += (size_t)gridDim.x * blockDim.x) {
-    const float h = tf32_rna(x[k]);
-    hi[k] = h;
-    lo[k] = x[k] - h;
-  }
+  twin_flush(t, m, mul);
 }
 
 // sync_gradients export: mean = double(S) * 2^-s * (1/B) (virtual_exec.cpp:162-166).

@@ -194,7 +194,7 @@ const World& Trainer::world() const {
   if (!world_cache_) {
     World w;
     const std::size_t in = config_.model.input_width();
-    std::vector<std::int32_t> scales(vnt_engine_tensor_count(engine_));
+    std::vector<std::int32_t> scales(vnt_engine_scale_count(engine_));
     raise_status(vnt_engine_get_scales(engine_, scales.data(), (uint32_t)scales.size()), "Trainer::world");
     const auto mine = local_devices();
     for (std::size_t i = 0; i < mine.size(); ++i) {

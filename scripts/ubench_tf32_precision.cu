@@ -2,6 +2,9 @@
 // K chains?  One CTA computes D[128 x N] = A[128 x K] B[N x K]^T with
 //   mode 1: one pass (operands rounded to tf32 by the MMA)
 //   mode 3: 3xTF32 (hi*hi + hi*lo + lo*hi, hi = rna_tf32(x), lo = x - hi)
+//   mode 2: 2xFP16 on kind::f16 (hi*hi + hi*lo + lo*hi, hi = f16(x*2^s),
+//           lo = f16(x*2^s - hi); per-operand power-of-two scale, undone in
+//           the fp32 promotion)
 // accumulating in TMEM either over the whole K, or over chunks of KC and then
 // added into fp32 registers on the CUDA cores ("promotion").  Errors are
 // reported relative to sum_k |a_k b_k| and to max |D| against an fp64 host
@@ -15,6 +18,7 @@
 #include <cstdlib>
 #include <random>
 #include <vector>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1);} } while (0)
@@ -33,6 +37,11 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+// element (r, k) of a [rows x 64] K-major f16 tile with the 128-B swizzle
+__device__ __forceinline__ int swz16(int r, int k) { return r * 64 + ((((k >> 3) ^ (r & 7)) << 3) | (k & 7)); }
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -42,11 +51,13 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ int swz(int r, int k) { return r * 32 + ((((k >> 2) ^ (r & 7)) << 2) | (k & 3)); }
 
 __global__ void __launch_bounds__(128, 1) k_probe(const float* A, const float* B, int K, int passes, int KC,
-                                                  float* D) {
+                                                  float* D, float sa_s, float sb_s) {
   extern __shared__ uint8_t smem_raw[];
   float* base = (float*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   float* sa[2] = {base, base + M * KB};            // hi, lo
   float* sb[2] = {base + 2 * M * KB, base + 2 * M * KB + N * KB};
+  const bool h16 = passes == 2;
+  const int kb = h16 ? 2 * KB : KB;   // K elements per 128-B atom row
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -65,8 +76,26 @@ __global__ void __launch_bounds__(128, 1) k_probe(const float* A, const float* B
   float acc[N];   // thread = row (lane of TMEM), promoted sums
   for (int j = 0; j < N; ++j) acc[j] = 0.f;
   uint32_t phase = 0;
-  constexpr uint32_t idesc = idesc_tf32(M, N);
-  for (int k0 = 0; k0 < K; k0 += KB) {
+  const uint32_t idesc = h16 ? idesc_f16(M, N) : idesc_tf32(M, N);
+  for (int k0 = 0; k0 < K; k0 += kb) {
+    if (h16) {
+      __half* ha[2] = {(__half*)sa[0], (__half*)sa[1]};
+      __half* hb[2] = {(__half*)sb[0], (__half*)sb[1]};
+      for (int i = tid; i < M * kb; i += 128) {
+        const int r = i / kb, k = i % kb;
+        const float v = A[(size_t)r * K + k0 + k] * sa_s;
+        const __half h = __float2half_rn(v);
+        ha[0][swz16(r, k)] = h;
+        ha[1][swz16(r, k)] = __float2half_rn(v - __half2float(h));
+      }
+      for (int i = tid; i < N * kb; i += 128) {
+        const int r = i / kb, k = i % kb;
+        const float v = B[(size_t)r * K + k0 + k] * sb_s;
+        const __half h = __float2half_rn(v);
+        hb[0][swz16(r, k)] = h;
+        hb[1][swz16(r, k)] = __float2half_rn(v - __half2float(h));
+      }
+    } else {
     for (int i = tid; i < M * KB; i += 128) {
       const int r = i / KB, k = i % KB;
       const float v = A[(size_t)r * K + k0 + k];
@@ -81,6 +110,7 @@ __global__ void __launch_bounds__(128, 1) k_probe(const float* A, const float* B
       sb[0][swz(r, k)] = h;
       sb[1][swz(r, k)] = v - h;
     }
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     const bool first_of_chunk = (k0 % KC) == 0;
@@ -88,14 +118,19 @@ __global__ void __launch_bounds__(128, 1) k_probe(const float* A, const float* B
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int kk = 0; kk < KB / 8; ++kk) {
         const uint64_t o = (uint64_t)(kk * 2);   // 32 B per k8 step, in 16-B units
-        const int np = passes == 3 ? 3 : 1;
+        const int np = passes == 1 ? 1 : 3;
         for (int p = 0; p < np; ++p) {
           const int ia = (p == 2) ? 1 : 0, ib = (p == 1) ? 1 : 0;   // hh, hl, lh
           const uint64_t ad = sdesc_sw128(su32(sa[ia])) + o, bd = sdesc_sw128(su32(sb[ib])) + o;
           const uint32_t accum = (first_of_chunk && kk == 0 && p == 0) ? 0u : 1u;
-          asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
-                       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n}" ::"r"(tmem),
-                       "l"(ad), "l"(bd), "r"(idesc), "r"(accum) : "memory");
+          if (h16)
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}" ::"r"(tmem),
+                         "l"(ad), "l"(bd), "r"(idesc), "r"(accum) : "memory");
+          else
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n}" ::"r"(tmem),
+                         "l"(ad), "l"(bd), "r"(idesc), "r"(accum) : "memory");
         }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
@@ -103,7 +138,7 @@ __global__ void __launch_bounds__(128, 1) k_probe(const float* A, const float* B
     asm volatile("{\n\t.reg .pred p;\nW:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W;\n}" ::"r"(su32(&bar)), "r"(phase) : "memory");
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const bool last_of_chunk = ((k0 + KB) % KC) == 0 || k0 + KB >= K;
+    const bool last_of_chunk = ((k0 + kb) % KC) == 0 || k0 + kb >= K;
     if (last_of_chunk) {
       // drain the chunk's TMEM sum into registers (lane = row = tid)
       for (int j0 = 0; j0 < N; j0 += 8) {
@@ -119,7 +154,8 @@ __global__ void __launch_bounds__(128, 1) k_probe(const float* A, const float* B
     }
     __syncthreads();
   }
-  for (int j = 0; j < N; ++j) D[(size_t)tid * N + j] = acc[j];
+  const float unscale = 1.f / (sa_s * sb_s);
+  for (int j = 0; j < N; ++j) D[(size_t)tid * N + j] = acc[j] * unscale;
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
 }
@@ -127,10 +163,17 @@ __global__ void __launch_bounds__(128, 1) k_probe(const float* A, const float* B
 int main() {
   std::mt19937_64 rng(7);
   std::normal_distribution<float> nd(0.f, 1.f);
+  std::uniform_real_distribution<float> ud(0.f, 1.f);
+  for (int dist : {0, 1})
   for (int K : {256, 1024, 4096}) {
     std::vector<float> A((size_t)M * K), B((size_t)N * K);
-    for (auto& v : A) v = nd(rng);
-    for (auto& v : B) v = nd(rng) / std::sqrt((float)K);
+    // dist 0: normal; dist 1: relu-like A (half zeros) with magnitudes spread
+    // log-uniformly over 2^-20..2^4, B normal scaled by 1e-4 (a gradient)
+    for (auto& v : A) v = dist == 0 ? nd(rng) : (ud(rng) < 0.5f ? 0.f : std::exp2(-20.f + 24.f * ud(rng)));
+    for (auto& v : B) v = nd(rng) / std::sqrt((float)K) * (dist == 0 ? 1.f : 1e-4f);
+    float amax = 0, bmax = 0;
+    for (auto v : A) amax = std::max(amax, std::fabs(v));
+    for (auto v : B) bmax = std::max(bmax, std::fabs(v));
     std::vector<double> ref((size_t)M * N), mag((size_t)M * N);
     double dmax = 0;
     for (int i = 0; i < M; ++i)
@@ -158,13 +201,17 @@ int main() {
     CK(cudaMalloc(&dD, (size_t)M * N * 4));
     CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
-    printf("K=%d  fp32 FFMA chain: max err %.2e of max|D|\n", K, ffma_err);
-    for (int passes : {1, 3})
-      for (int KC : {K, 1024, 256, 128, 32}) {
-        if (KC > K) continue;
+    printf("dist %d K=%d  fp32 FFMA chain: max err %.2e of max|D|\n", dist, K, ffma_err);
+    for (int passes : {1, 3, 2})
+      for (int headroom : {4, 12})
+      for (int KC : {K, 1024, 256, 128, 64}) {
+        if (KC > K || (passes != 2 && headroom != 4)) continue;
+        // 2xFP16: scale so max|x| * s ~ 2^(15 - headroom)
+        const float sa_s = passes == 2 ? std::exp2(std::floor(15 - headroom - std::log2(amax))) : 1.f;
+        const float sb_s = passes == 2 ? std::exp2(std::floor(15 - headroom - std::log2(bmax))) : 1.f;
         const int smem = (2 * M * KB + 2 * N * KB) * 4 + 1024;
         CK(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k_probe<<<1, 128, smem>>>(dA, dB, K, passes, KC, dD);
+        k_probe<<<1, 128, smem>>>(dA, dB, K, passes, KC, dD, sa_s, sb_s);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
         std::vector<float> D((size_t)M * N);
@@ -175,7 +222,7 @@ int main() {
           e_max = std::max(e_max, e / dmax);
           e_mag = std::max(e_mag, e / mag[t]);
         }
-        printf("  passes %d chunk %5d: max err %.2e of max|D|, %.2e of sum|ab|\n", passes, KC, e_max, e_mag);
+        printf("  passes %d headroom %2d chunk %5d: max err %.2e of max|D|, %.2e of sum|ab|\n", passes, headroom, KC, e_max, e_mag);
       }
     cudaFree(dA);
     cudaFree(dB);

@@ -164,7 +164,7 @@ TEST_CASE("a train_step loop over a World is the Trainer's trajectory bit for bi
     const StepMetrics t = trainer.step();
     CHECK(a.loss == t.loss);
     CHECK(world.workers[0].params.bitwise_equal(trainer.params()));
-    CHECK(world.workers[0].scales.size() == 4);
+    CHECK(world.workers[0].scales.size() == 4);   // no tcgen05 layer: no fp16 operand scales
   }
   // and the World-level migrate_state carries the scales through a resize
   InMemoryTransport tr;

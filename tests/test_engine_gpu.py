@@ -388,8 +388,10 @@ def test_collective_sequence_is_rank_independent(port, monkeypatch):
     matches them by order): a process with all nodes, one with none (it
     reduces zeros), and one whose nodes need three passes all log the same
     sequence — sharded update: per layer L-1..0 reduce-scatter (overlapped with
-    the backward), the tail all-reduce, the max|g| all-reduce; from the second
-    step on, first the weight all-gathers of layers 0..L-1."""
+    the backward), the tail all-reduce, the max all-reduce of the split-fp16
+    operand maxima (2L+3 words, the update's range check), the max|g|
+    all-reduce; from the second step on, first the weight all-gathers of
+    layers 0..L-1."""
     monkeypatch.setenv("VNT_FORCE_COMM", "1")
     w = [128, 256, 256, 10]
     sizes, _ = vnt().uniform_mapping(256, 8, 1)
@@ -412,7 +414,8 @@ def test_collective_sequence_is_rank_independent(port, monkeypatch):
     rs = [("reduce_scatter", o, c) for o, c in reversed(offs)]
     first, second = logs[0]
     assert first[:L] == rs
-    assert [op for op, _, _ in first[L:]] == ["allreduce", "max"]
+    assert [op for op, _, _ in first[L:]] == ["allreduce", "max", "max"]
+    assert first[L + 1][2] == 2 * L + 3
     assert second == [("allgather", o, c) for o, c in offs] + first
     assert logs[1] == logs[0] and logs[2] == logs[0]
 
@@ -458,13 +461,13 @@ def test_single_layer_identity_least_squares_known_answer():
     e.close()
 
 
-@pytest.mark.parametrize("mode", ["ffma", "3xtf32"])
+@pytest.mark.parametrize("mode", ["ffma", "3xf16"])
 def test_union_gradient_is_size_weighted_mean_of_parts(port, mode):
     """test_model.cpp:148-163: the gradient of a union is the size-weighted mean
     of the parts' gradients.  On the engine the 5:3 split as two virtual nodes
     is compared with the two parts run alone (1e-12, the reference's bound: the
     int64 node sums add exactly; only the fp64 divisions by 8, 5, 3 round)."""
-    w = [64, 96, 80, 3] if mode == "3xtf32" else [4, 6, 3]
+    w = [64, 96, 80, 3] if mode == "3xf16" else [4, 6, 3]
     p0 = port.init_params(w, 33)
     x, y = port.synth_batch(99, 64, w[0], w[-1], 0, 8)
 

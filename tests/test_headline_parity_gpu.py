@@ -3,10 +3,12 @@
 oracle (model.cpp:238-360 restated as vo_forward_backward_wide, pinned to the
 exactly rounded oracle in tests/test_oracle.py).
 
-The dense layers run as 3xTF32 tcgen05 GEMMs with K = 4096 (forward,
-bwd-data; accumulated in TMEM in K chunks of 512 then 128 columns, added in
-fp32 registers) and per-node dW K-chains of 8 (cfg3-like) or 256 rows
-(cfg4-like) read as MN-major operands straight from the row-major activations.
+The dense layers run as split-fp16 tcgen05 GEMMs (x 2^s = hi + lo in fp16,
+hi*hi + hi*lo + lo*hi on kind::f16) with K = 4096 (forward, bwd-data;
+accumulated in TMEM in K chunks of 512 then 256 columns, added in fp32
+registers) and per-node dW K-chains of 8 (cfg3-like, padded to 16 rows) or
+256 rows (cfg4-like) read as MN-major operands straight from the row-major
+activation twins.
 
 Stated tolerances (fp32-grade arithmetic against fp64):
   * mean gradient: max |g - g_ref| <= 2e-5 * max |g_ref|, per tensor

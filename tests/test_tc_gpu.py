@@ -90,27 +90,28 @@ def test_tc_trajectory_vs_reference(port):
 
 
 @pytest.mark.parametrize("sizes", [[64, 64, 64, 64], [24, 40, 7, 57, 128], [700, 3, 301]])
-def test_3xtf32_gradient_is_fp32_grade(port, sizes):
-    """3xTF32 (hi*hi + hi*lo + lo*hi): the tensor-core path meets the fp32 tier."""
+def test_3xf16_gradient_is_fp32_grade(port, sizes):
+    """Split-fp16 (x 2^s = hi + lo, hi*hi + hi*lo + lo*hi on kind::f16): the
+    tensor-core path meets the fp32 tier."""
     w = [256, 512, 384, 10]
     B = sum(sizes)
     x, y = port.synth_batch(3, 4096, w[0], w[-1], 0, B)
     p0 = port.init_params(w, 1)
     want, want_loss = port.forward_backward(w, "relu", "softmax-cross-entropy", p0, x, y)
-    e = engine(w, "relu", "softmax-cross-entropy", port, gemm_mode="3xtf32")
+    e = engine(w, "relu", "softmax-cross-entropy", port, gemm_mode="3xf16")
     g, loss = synced_grad(e, x, y, sizes)
     err = np.abs(g - want).max() / np.abs(want).max()
-    print(f"3xtf32 sizes {sizes}: rel grad err {err:.2e}, loss {loss:.9f} vs {want_loss:.9f}")
+    print(f"3xf16 sizes {sizes}: rel grad err {err:.2e}, loss {loss:.9f} vs {want_loss:.9f}")
     assert err < 2e-5
     assert abs(loss - want_loss) < 2e-6 * abs(want_loss)
 
 
 @pytest.mark.parametrize("act,loss", [("tanh", "mse"), ("identity", "softmax-cross-entropy"),
                                       ("tanh", "softmax-cross-entropy"), ("relu", "mse")])
-def test_3xtf32_activations_and_losses(port, act, loss):
+def test_3xf16_activations_and_losses(port, act, loss):
     """Every activation/loss pair of the reference (model.cpp:289-338) through the
-    tcgen05 epilogues (tanh keeps the fp32 activation for its derivative, relu and
-    identity read the hi twin): fp32-grade gradients and loss against the fp64
+    tcgen05 epilogues (tanh and identity keep the fp32 activation for the
+    derivative, relu takes it from the forward's mask bits): fp32-grade gradients and loss against the fp64
     oracle."""
     w = [128, 192, 160, 8]
     sizes = [32, 17, 47, 32]
@@ -118,22 +119,22 @@ def test_3xtf32_activations_and_losses(port, act, loss):
     x, y = port.synth_batch(5, 4096, w[0], w[-1], 0, B)
     p0 = port.init_params(w, 3)
     want, want_loss = port.forward_backward(w, act, loss, p0, x, y)
-    e = engine(w, act, loss, port, seed=3, gemm_mode="3xtf32")
+    e = engine(w, act, loss, port, seed=3, gemm_mode="3xf16")
     g, lo = synced_grad(e, x, y, sizes)
     err = np.abs(g - want).max() / np.abs(want).max()
-    print(f"3xtf32 {act}/{loss}: rel grad err {err:.2e}, loss {lo:.9f} vs {want_loss:.9f}")
+    print(f"3xf16 {act}/{loss}: rel grad err {err:.2e}, loss {lo:.9f} vs {want_loss:.9f}")
     assert err < 2e-5
     # the loss is formed from fp32 logits; an MSE of small residuals magnifies
     # their ~1e-7 relative error, hence 1e-5 here (2e-6 for the CE cases above)
     assert abs(lo - want_loss) < 1e-5 * abs(want_loss)
 
 
-def test_3xtf32_trajectory_and_bitwise(port):
+def test_3xf16_trajectory_and_bitwise(port):
     z = np.load(GOLDEN / "ref_wide_small.npz")
     c = json.loads(str(z["config"]))
     finals = []
     for rr, G in ((0, 1), (192, 2), (64, 3)):
-        e = engine(c["widths"], c["act"], c["loss"], port, seed=c["seed"], gemm_mode="3xtf32",
+        e = engine(c["widths"], c["act"], c["loss"], port, seed=c["seed"], gemm_mode="3xf16",
                    n_devices=G, resident_rows=rr)
         sizes, dev = vnt().uniform_mapping(c["B"], c["V"], G)
         losses = []
@@ -144,18 +145,18 @@ def test_3xtf32_trajectory_and_bitwise(port):
         finals.append((e.get_params(), np.array(losses)))
     rel = np.abs(finals[0][1] - z["losses"]) / np.abs(z["losses"])
     dw = np.abs(finals[0][0] - z["params"]).max()
-    print(f"3xtf32 wide_small: max rel loss dev {rel.max():.2e}, max |dw| {dw:.2e}")
+    print(f"3xf16 wide_small: max rel loss dev {rel.max():.2e}, max |dw| {dw:.2e}")
     assert rel.max() < 2e-5
     assert dw < 2e-5
     for p, l in finals[1:]:
         assert np.array_equal(p, finals[0][0]) and np.array_equal(l, finals[0][1])
 
 
-@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("mode", ["3xf16", "tf32"])
 def test_padding_columns_across_uneven_passes(port, mode):
     """Passes with different node layouts: columns that are one pass's node rows
     are the next pass's padding.  The per-node dW must not see the stale values
-    (plain or 3xTF32 twin operands), so any grouping is bit-identical."""
+    (plain or split-fp16 twin operands), so any grouping is bit-identical."""
     w = [128, 256, 256, 10]
     sizes = [40, 24, 64, 7, 57, 64]
     B = sum(sizes)
@@ -195,7 +196,7 @@ p0 = port.init_params(w, 1)
 want, _ = port.forward_backward(w, "relu", "softmax-cross-entropy", p0, x, y)
 out = []
 for rr in (0, 64):
-    e = vnt.Engine(w, "relu", "softmax-cross-entropy", gemm_mode="3xtf32", resident_rows=rr)
+    e = vnt.Engine(w, "relu", "softmax-cross-entropy", gemm_mode="3xf16", resident_rows=rr)
     e.add_device(1 << 20)
     e.set_params(p0)
     e.device_step(0, x, y, sizes)
@@ -240,7 +241,7 @@ for s in range(3):
     losses.append(e.train_step(x, y, sizes, node_dev, 0.01)[0])
 np.save(sys.argv[1], np.concatenate([np.array(losses), e.get_params()]))
 '''
-    for mode in ("3xtf32", "tf32"):
+    for mode in ("3xf16", "tf32"):
         outs = []
         for k, env_kv in enumerate(({}, {"VNT_TC_DW_PAIR": "0"}, {"VNT_TC_PAIR": "0"})):
             path = str(tmp_path / f"v{mode}{k}.npy")
@@ -268,7 +269,7 @@ w = [512, 768, 640, 10]
 sizes = [128] * 8
 B = sum(sizes)
 p0 = port.init_params(w, 1)
-e = vnt.Engine(w, "relu", "softmax-cross-entropy", gemm_mode="3xtf32")
+e = vnt.Engine(w, "relu", "softmax-cross-entropy", gemm_mode="3xf16")
 e.add_device(1 << 20)
 e.set_params(p0)
 node_dev = np.zeros(len(sizes), dtype=np.int32)
@@ -318,7 +319,7 @@ def test_rescale_retry_on_tcgen05_graph_path(port):
 def test_momentum_on_tcgen05_layers(port):
     """Momentum (no reference oracle: model.cpp:364-374 is plain SGD) on the
     tcgen05 path and its fused SGD tiles: v <- mu v + g; w <- w - lr v against
-    the CPU restatement on oracle gradients, within the 3xTF32 tolerance."""
+    the CPU restatement on oracle gradients, within the split-fp16 tolerance."""
     w = [128, 256, 192, 10]
     mu, lr = 0.9, 0.05
     e = engine(w, "relu", "softmax-cross-entropy", port, seed=2, gemm_mode="auto", momentum=mu)
