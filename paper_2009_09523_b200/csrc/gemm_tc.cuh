@@ -122,8 +122,10 @@ struct EpiArgs {
   uint32_t* mask_out;
   const uint32_t* mask_in;
   int ldm;
-  // split-fp16 twins of out for the next tcgen05 consumer (tw.hi nullptr: none)
+  // split-fp16 twins of out for the next tcgen05 consumer (tw.hi nullptr: none);
+  // tma_out: written by TMA stores (CTA-pair kernel, no plain out)
   Twin16 tw;
+  int tma_out;
   // split-fp16 operands: 2^-sigma of A and B (nullptr: fp32 operands)
   const float* inv_a;
   const float* inv_b;
@@ -806,6 +808,21 @@ inline CUtensorMap make_map(const void* base, uint64_t rows, uint64_t K, uint64_
   return m;
 }
 
+// Split-fp16 output twin [rows][cols] (leading dimension ld) for the
+// epilogue's TMA stores: boxes of 32 columns (64 B) x 32 rows, 64-B swizzle.
+inline CUtensorMap make_map_store16(const __half* base, uint64_t rows, uint64_t cols, uint64_t ld) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)base, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw EngineError(9, "cuTensorMapEncodeTiled (store) failed: " + std::to_string(r));
+  return m;
+}
+
 // MN-major dW operand [rows][F] (features contiguous, F a multiple of the
 // group width gw = 128 B / eb) as a 3-D tensor {gw features, rows, F / gw
 // groups}: a box {gw, gw rows, box_groups} puts the groups kGroupBytes apart
@@ -868,6 +885,12 @@ bool tc_use_pair() {
 // 3-D TMA maps for the MN-major dW operands (VNT_TC_MN3=0: one 2-D box per group).
 bool tc_mn3() {
   static const bool on = !(getenv("VNT_TC_MN3") && getenv("VNT_TC_MN3")[0] == '0');
+  return on;
+}
+
+// TMA stores of the split-fp16 epilogue outputs (VNT_TC_TMA_OUT=0: per-lane stores).
+bool tc_tma_out() {
+  static const bool on = !(getenv("VNT_TC_TMA_OUT") && getenv("VNT_TC_TMA_OUT")[0] == '0');
   return on;
 }
 
@@ -951,6 +974,14 @@ template <int EPI>
 void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M, int N, int K,
                int nseg, const int* seg_k0, const int* seg_rows, vntb::tc::EpiArgs ep) {
   using namespace vntb::tc;
+  // split-fp16 twins as the only output of a pair fwd / bwd: TMA stores
+  OpMaps o = a;
+  ep.tma_out = 0;
+  if (EPI != kTcDw && pair && e->split && ep.tw.hi && !ep.out && tc_tma_out()) {
+    o.hi = make_map_store16(ep.tw.hi, (uint64_t)M, (uint64_t)N, (uint64_t)ep.ldo);
+    o.lo = make_map_store16(ep.tw.lo, (uint64_t)M, (uint64_t)N, (uint64_t)ep.ldo);
+    ep.tma_out = 1;
+  }
   ep.kchunk = EPI == kTcDw ? 0 : tc_kchunk(e);
   ep.kfirst = tc_kfirst(e);
   // The backward GEMMs share the GPU with the per-layer gradient reductions,
@@ -961,10 +992,10 @@ void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M
   // CTA-pair kernels for all three GEMMs in both modes
   if (pair) {
     if (e->split)
-      launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
+      launch_gemm_pair<EPI, 3>(a.hi, b.hi, a.lo, b.lo, o.hi, o.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
                                sms, e->stream);
     else
-      launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
+      launch_gemm_pair<EPI, 1>(a.hi, b.hi, a.lo, b.lo, o.hi, o.lo, M, N, K, nseg, seg_k0, seg_rows, ep,
                                sms, e->stream);
     e->launches++;
     return;

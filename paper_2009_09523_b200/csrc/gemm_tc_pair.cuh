@@ -4,8 +4,10 @@
 // [n0 + r BN/2, +BN/2) in its own smem; the leader (r = 0) issues
 // tcgen05.mma.cta_group::2 on the pair's operands and each CTA receives its
 // 128 accumulator rows in its own TMEM.  Per SM each CTA stages only half of
-// B.  The fwd/bwd epilogue writes the row-major outputs through
-// a per-warp smem transpose tile (kEpiStageBytes) so stores are 128 B rows.
+// B.  The fwd/bwd epilogue writes the split-fp16 twins of its
+// output with TMA stores (a per-warp 32x32 box per twin staged in smem,
+// 64-B swizzle), and a plain fp32 output, when one is needed, through a
+// per-warp smem transpose tile so stores are 128 B rows (kEpiStageBytes).
 #pragma once
 
 namespace vntb {
@@ -24,7 +26,9 @@ struct PairCfg {
   static constexpr int kTmemCols = 2 * BN;
   // fwd / bwd epilogue: a 32x33 fp32 transpose tile per epilogue warp
   static constexpr int kEpiStageBytes = EPI == kTcDw ? 0 : 8 * 32 * 33 * 4;
-  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256 + kEpiStageBytes;
+  // barriers in the first 256 B of a 1024-B block after the stages; the
+  // epilogue staging (1024-B aligned for the swizzled TMA boxes) after it
+  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 1024 + kEpiStageBytes;
   static_assert(kSmemBytes <= 232448, "exceeds the opt-in shared memory per block");
 };
 
@@ -93,6 +97,18 @@ __device__ __forceinline__ void mma_f16_pair(uint32_t d, uint64_t a, uint64_t b,
       : "memory");
 }
 
+// TMA store of a 2-D box from this CTA's smem (bulk async group of the thread).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   (uint64_t)tm),
+               "r"(su32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // Whole-warp callers, one elected lane issues (see mma_tf32).
 __device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                               uint32_t accumulate) {
@@ -125,7 +141,8 @@ template <int EPI, int SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmAl,
-                   const __grid_constant__ CUtensorMap tmBl, int K, int nseg,
+                   const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmOh,
+                   const __grid_constant__ CUtensorMap tmOl, int K, int nseg,
                    const int* __restrict__ seg_k0, const int* __restrict__ seg_rows, EpiArgs ep) {
   using C = PairCfg<EPI, SPLIT>;
   using F = Fmt<SPLIT>;
@@ -141,7 +158,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  float* stile = (float*)(smem + STAGES * C::kStageBytes + 256);
+  float* stile = (float*)(smem + STAGES * C::kStageBytes + 1024);
+  uint8_t* tstage = smem + STAGES * C::kStageBytes + 1024;   // TMA-store boxes (same region)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -301,7 +319,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const float unscale = ep.inv_a ? *ep.inv_a * *ep.inv_b : 1.f;   // split-fp16: 2^-(sigma_A + sigma_B)
     const float dscale = EPI == kTcDw ? *ep.scale_p * unscale : 1.f;   // dW: 2^s of the tensor
     const float tmul = ep.tw.hi ? *ep.tw.mul : 1.f;
-    float tmax = 0.f;   // max |x| of the twins written
+    // TMA-stored twins: the epilogue works at the twins' scale 2^sigma_out
+    // from the start (v = acc 2^-(sA+sB) 2^sigma_out, bias x 2^sigma_out):
+    // power-of-two scaling commutes with the rounding, relu and the f' masks,
+    // so the split sees the same bits (tmax is divided back at the end)
+    const bool tscaled = SPLIT == 3 && ep.tma_out;
+    const float vscale = tscaled ? unscale * tmul : unscale;
+    const float bscale = tscaled ? tmul : 1.f;
+    float tmax = 0.f;   // max |x| of the twins written (x 2^sigma_out when tscaled)
     uint32_t it = 0;
     float amax = 0.f;   // NaN-propagating max |x|: NaN/inf partials end up in it
     TC_PROBE_DECL;
@@ -332,11 +357,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int nb = n0 + col;
         if constexpr (SPLIT == 3) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= unscale;
+          for (int j = 0; j < 32; ++j) v[j] *= vscale;
         }
         if constexpr (EPI == kTcFwd) {
           // bias: one coalesced load per warp, broadcast by shuffles
-          const float bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) : 0.f;
+          const float bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) * bscale : 0.f;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float bj = __shfl_sync(0xffffffffu, bl, j);
@@ -375,10 +400,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
+        if constexpr (SPLIT == 3) if (ep.tma_out) {
+          // split-fp16 twins only: this lane's row of the warp's 32x32 box,
+          // hi and lo as 4 x 16 B each into the 64-B-swizzled staging boxes
+          // (16-B chunk c of row r at chunk c ^ ((r >> 1) & 3): conflict-free),
+          // then one TMA store per twin; rows / columns past the tensor are
+          // clipped by the TMA unit
+          uint8_t* box = tstage + (warp - kEpiWarp0) * 4096;
+          if (lane == 0) tma_store_wait_read();   // the previous boxes were read out
+          __syncwarp();
+          // v is at the twins' scale already (tscaled); columns past N are
+          // zero (zero-filled B rows, zero bias), rows past M are excluded
+          if (r < ep.M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tmax = fmax_nan(tmax, fabsf(v[j]));
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float x0 = v[8 * c + 2 * j], x1 = v[8 * c + 2 * j + 1];
+              const __half2 hh = __floats2half2_rn(x0, x1);
+              const float2 hf = __half22float2(hh);
+              const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+              h[j] = *reinterpret_cast<const uint32_t*>(&hh);
+              l[j] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+            const uint32_t off = (uint32_t)lane * 64 + (uint32_t)((c ^ ((lane >> 1) & 3)) * 16);
+            *reinterpret_cast<uint4*>(box + off) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(box + 2048 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmOh, box, nb, m0 + q * 32);
+            tma_store_2d(&tmOl, box + 2048, nb, m0 + q * 32);
+            tma_store_commit();
+          }
+          return;
+        }
         // row-major copies: transpose the warp's 32x32 block through smem so
         // every store writes 128 contiguous bytes of one row (a per-thread
         // float4 row store touches 32 lines per instruction)
+#ifdef VNT_DIAG_NO_STORE
+        if (false) {
+#else
         if (ep.out || ep.tw.hi) {
+#endif
           float* st = stile + (warp - kEpiWarp0) * (32 * 33);
 #pragma unroll
           for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
@@ -476,7 +545,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #ifdef VNT_TC_PROBE
     if (warp == kEpiWarp0 && lane == 0 && rank == 0) TC_PROBE_DONE(EPI + 3, 4);
 #endif
-    if (EPI != kTcDw && ep.tw.hi) twin_flush(ep.tw, tmax, tmul);
+    if (EPI != kTcDw && ep.tw.hi) twin_flush(ep.tw, tscaled ? tmax * (1.f / tmul) : tmax, tmul);
+    if (EPI != kTcDw && ep.tma_out && lane == 0) tma_store_wait_read();   // smem outlives the stores' reads
     if (EPI == kTcDw) {
       if (!(amax <= 3.402823466e38f))   // NaN or inf: some partial was non-finite
         atomicAdd(reinterpret_cast<unsigned long long*>(&ep.tail[kTailNonfinite]), 1ull);
@@ -498,9 +568,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 template <int EPI, int SPLIT>
 inline void launch_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& al,
-                             const CUtensorMap& bl, int M, int N, int K, int nseg,
-                             const int* seg_k0, const int* seg_rows, const EpiArgs& ep, int sms,
-                             cudaStream_t s) {
+                             const CUtensorMap& bl, const CUtensorMap& oh, const CUtensorMap& ol, int M,
+                             int N, int K, int nseg, const int* seg_k0, const int* seg_rows,
+                             const EpiArgs& ep, int sms, cudaStream_t s) {
   using C = PairCfg<EPI, SPLIT>;
   static bool attr = false;
   if (!attr) {
@@ -510,7 +580,7 @@ inline void launch_gemm_pair(const CUtensorMap& a, const CUtensorMap& b, const C
   }
   const int tiles = (int)(ceil_div(M, 2 * BM) * ceil_div(N, C::BN));
   const int pairs = std::max(1, std::min(tiles, sms / 2));
-  k_gemm_tc_pair<EPI, SPLIT><<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a, b, al, bl, K, nseg,
+  k_gemm_tc_pair<EPI, SPLIT><<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a, b, al, bl, oh, ol, K, nseg,
                                                                         seg_k0, seg_rows, ep);
   VNT_LAUNCH_CHECK();
 }

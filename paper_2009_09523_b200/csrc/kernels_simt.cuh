@@ -56,7 +56,9 @@ __device__ __forceinline__ void twin_flush(const Twin16& t, float m, float mul) 
   unsigned lane;
   asm("mov.u32 %0, %%laneid;" : "=r"(lane));
   if (b != 0u && lane == (unsigned)(__ffs(mask) - 1)) {
-    atomicMax(t.amax, (unsigned long long)b);
+    // filter on a (possibly stale, never larger) cached copy of the max: most
+    // warps skip the same-address atomic, which serialises in L2
+    if ((unsigned long long)b > *t.amax) atomicMax(t.amax, (unsigned long long)b);
     if (!(__uint_as_float(b) * mul < kH16Lim)) atomicAdd(reinterpret_cast<unsigned long long*>(t.flag), 1ull);
   }
 }

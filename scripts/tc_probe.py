@@ -51,9 +51,14 @@ for s in range(2):
     e.train_step_ptr(x.data_ptr(), y.data_ptr(), B, sizes, dev, 0.01, resident=True)
 torch.cuda.synchronize()
 probe(buf)
+t0 = torch.cuda.Event(enable_timing=True)
+t1 = torch.cuda.Event(enable_timing=True)
+t0.record()
 for s in range(steps):
     e.train_step_ptr(x.data_ptr(), y.data_ptr(), B, sizes, dev, 0.01, resident=True)
+t1.record()
 torch.cuda.synchronize()
+print(f"ms/step (probe build) {t0.elapsed_time(t1) / steps:.3f}")
 probe(buf)
 a = np.array(buf, dtype=np.float64).reshape(6, 8)
 names = ["fwd", "bwd", "dW", "pair fwd", "pair bwd", "pair dW"]
