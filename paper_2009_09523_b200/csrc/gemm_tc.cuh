@@ -70,7 +70,7 @@ enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
 // Diagnostics build only (-DVNT_TC_PROBE, scripts/tc_probe.py): cycles each
 // role spends waiting on its barriers, per kernel kind (EPI + 3 * pair).
 #ifdef VNT_TC_PROBE
-__device__ unsigned long long g_tc_probe[6][8];
+__device__ unsigned long long g_tc_probe[6][12];   // 8..11: final-epilogue / promote cycles and counts
 #define TC_PROBE_DECL long long _pw = 0, _pt = clock64()
 #define TC_PROBE_WAIT(stmt)          \
   do {                               \
@@ -123,7 +123,8 @@ struct EpiArgs {
   const uint32_t* mask_in;
   int ldm;
   // split-fp16 twins of out for the next tcgen05 consumer (tw.hi nullptr: none);
-  // tma_out: written by TMA stores (CTA-pair kernel, no plain out)
+  // tma_out (CTA-pair fwd / bwd): 1 = the twins are the only output, 2 = the
+  // plain fp32 out is (no twins); written by TMA stores from smem boxes
   Twin16 tw;
   int tma_out;
   // split-fp16 operands: 2^-sigma of A and B (nullptr: fp32 operands)
@@ -823,6 +824,21 @@ inline CUtensorMap make_map_store16(const __half* base, uint64_t rows, uint64_t 
   return m;
 }
 
+// Plain fp32 output [rows][cols] for the epilogue's TMA stores: boxes of 32
+// columns (128 B) x 32 rows, 128-B swizzle.
+inline CUtensorMap make_map_store32(const float* base, uint64_t rows, uint64_t cols, uint64_t ld) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 4};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw EngineError(9, "cuTensorMapEncodeTiled (store32) failed: " + std::to_string(r));
+  return m;
+}
+
 // MN-major dW operand [rows][F] (features contiguous, F a multiple of the
 // group width gw = 128 B / eb) as a 3-D tensor {gw features, rows, F / gw
 // groups}: a box {gw, gw rows, box_groups} puts the groups kGroupBytes apart
@@ -974,15 +990,24 @@ template <int EPI>
 void tc_launch(vnt_engine* e, bool pair, const OpMaps& a, const OpMaps& b, int M, int N, int K,
                int nseg, const int* seg_k0, const int* seg_rows, vntb::tc::EpiArgs ep) {
   using namespace vntb::tc;
-  // split-fp16 twins as the only output of a pair fwd / bwd: TMA stores
+  // a pair fwd / bwd with one kind of output (the split-fp16 twins, or the
+  // plain fp32 tensor): TMA stores
   OpMaps o = a;
   ep.tma_out = 0;
-  if (EPI != kTcDw && pair && e->split && ep.tw.hi && !ep.out && tc_tma_out()) {
-    o.hi = make_map_store16(ep.tw.hi, (uint64_t)M, (uint64_t)N, (uint64_t)ep.ldo);
-    o.lo = make_map_store16(ep.tw.lo, (uint64_t)M, (uint64_t)N, (uint64_t)ep.ldo);
-    ep.tma_out = 1;
+  if (EPI != kTcDw && pair && tc_tma_out()) {
+    if (e->split && ep.tw.hi && !ep.out) {
+      o.hi = make_map_store16(ep.tw.hi, (uint64_t)M, (uint64_t)N, (uint64_t)ep.ldo);
+      o.lo = make_map_store16(ep.tw.lo, (uint64_t)M, (uint64_t)N, (uint64_t)ep.ldo);
+      ep.tma_out = 1;
+    } else if (ep.out && !ep.tw.hi && ep.ldo % 4 == 0) {
+      o.hi = make_map_store32(ep.out, (uint64_t)M, (uint64_t)N, (uint64_t)ep.ldo);
+      o.lo = o.hi;
+      ep.tma_out = 2;
+    }
   }
-  ep.kchunk = EPI == kTcDw ? 0 : tc_kchunk(e);
+  // K <= 1024 (the 784-wide first layer) runs as one TMEM chain: its error
+  // is within the promoted 4096 chains' (profiles/r02_tf32_precision_probe.txt)
+  ep.kchunk = (EPI == kTcDw || K <= 1024) ? 0 : tc_kchunk(e);
   ep.kfirst = tc_kfirst(e);
   // The backward GEMMs share the GPU with the per-layer gradient reductions,
   // and with a sharded update the forward ones with the weight all-gathers:

@@ -23,7 +23,13 @@ struct PairCfg {
   static constexpr int kBytesB = BNH * 128;
   static constexpr int kStageBytes = (SPLIT == 3 ? 2 : 1) * (kBytesA + kBytesB);
   static constexpr int STAGES = (192 * 1024 / kStageBytes) < 6 ? (192 * 1024 / kStageBytes) : 6;
-  static constexpr int kTmemCols = 2 * BN;
+  // TMEM accumulator buffers: fwd / bwd 2 x 256 columns; dW 4 x 128, so the
+  // MMAs run up to three virtual nodes ahead of the per-node int64 epilogue
+#ifndef VNT_DW_NBUF
+#define VNT_DW_NBUF 4
+#endif
+  static constexpr int NBUF = EPI == kTcDw ? VNT_DW_NBUF : 2;
+  static constexpr int kTmemCols = NBUF * BN;
   // fwd / bwd epilogue: a 32x33 fp32 transpose tile per epilogue warp
   static constexpr int kEpiStageBytes = EPI == kTcDw ? 0 : 8 * 32 * 33 * 4;
   // barriers in the first 256 B of a 1024-B block after the stages; the
@@ -156,8 +162,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* full = (uint64_t*)(smem + STAGES * C::kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* tempty = tfull + C::NBUF;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + C::NBUF);
   float* stile = (float*)(smem + STAGES * C::kStageBytes + 1024);
   uint8_t* tstage = smem + STAGES * C::kStageBytes + 1024;   // TMA-store boxes (same region)
 
@@ -175,7 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::NBUF; ++b) {
       mbar_init(&tfull[b], 1);
       // dW: one arrival per CTA after its 8 epilogue warps meet on a named
       // barrier (per virtual node); fwd/bwd: every epilogue warp of both CTAs
@@ -269,8 +275,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       TC_PROBE_DECL;
       for (int tile = pair; tile < tiles; tile += npairs)
       for (int sg = 0; sg < segs; ++sg, ++it) {
-        const int b = it & 1;
-        TC_PROBE_WAIT(mbar_wait_cluster(&tempty[b], ((it >> 1) & 1) ^ 1));
+        const int b = (int)(it % C::NBUF);
+        TC_PROBE_WAIT(mbar_wait_cluster(&tempty[b], ((it / C::NBUF) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * BN);
         int kb, kl;
@@ -323,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // from the start (v = acc 2^-(sA+sB) 2^sigma_out, bias x 2^sigma_out):
     // power-of-two scaling commutes with the rounding, relu and the f' masks,
     // so the split sees the same bits (tmax is divided back at the end)
-    const bool tscaled = SPLIT == 3 && ep.tma_out;
+    const bool tscaled = SPLIT == 3 && ep.tma_out == 1;
     const float vscale = tscaled ? unscale * tmul : unscale;
     const float bscale = tscaled ? tmul : 1.f;
     float tmax = 0.f;   // max |x| of the twins written (x 2^sigma_out when tscaled)
@@ -361,7 +367,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if constexpr (EPI == kTcFwd) {
           // bias: one coalesced load per warp, broadcast by shuffles
+#ifdef VNT_DIAG_NO_BIAS
+          const float bl = 0.f;
+#else
           const float bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) * bscale : 0.f;
+#endif
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float bj = __shfl_sync(0xffffffffu, bl, j);
@@ -369,7 +379,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         if constexpr (EPI == kTcFwd) {
+#ifdef VNT_DIAG_NO_MASKOUT
+          if (false) {
+#else
           if (ep.mask_out && r < ep.M) {
+#endif
             uint32_t m = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) m |= (nb + j < ep.N && v[j] > 0.f ? 1u : 0u) << j;
@@ -400,7 +414,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if constexpr (SPLIT == 3) if (ep.tma_out) {
+        if (ep.tma_out == 2) {
+          // plain fp32 output only: this lane's row (128 B) into the warp's
+          // 128-B-swizzled 32x32 box (chunk c of row r at c ^ (r & 7)), one
+          // TMA store
+          uint8_t* box = tstage + (warp - kEpiWarp0) * 4096;
+          if (lane == 0) tma_store_wait_read();
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t off = (uint32_t)lane * 128 + (uint32_t)((c ^ (lane & 7)) * 16);
+            *reinterpret_cast<float4*>(box + off) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmOh, box, nb, m0 + q * 32);
+            tma_store_commit();
+          }
+          return;
+        }
+        if constexpr (SPLIT == 3) if (ep.tma_out == 1) {
           // split-fp16 twins only: this lane's row of the warp's 32x32 box,
           // hi and lo as 4 x 16 B each into the 64-B-swizzled staging boxes
           // (16-B chunk c of row r at chunk c ^ ((r >> 1) & 3): conflict-free),
@@ -474,11 +508,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float pacc[COLS / 32][32];
         const uint32_t lane_col = ((uint32_t)(q * 32) << 16) + (uint32_t)(h * COLS);
         for (int sg = 0; sg < segs; ++sg, ++it) {
-          const int b = it & 1;
-          TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
+          const int b = (int)(it % C::NBUF);
+          TC_PROBE_WAIT(mbar_wait(&tfull[b], (it / C::NBUF) & 1));
           tc_fence_after();
           const bool last = sg + 1 == segs;
+#ifdef VNT_TC_PROBE
+          const long long _p0 = clock64();
+#endif
           promote_chunk<COLS / 32>(tmem + lane_col + (uint32_t)(b * BN), pacc, sg == 0, last);
+#ifdef VNT_TC_PROBE
+          if (lane == 0 && warp == kEpiWarp0 && rank == 0) {
+            atomicAdd(&g_tc_probe[EPI + 3][10], (unsigned long long)(clock64() - _p0));
+            atomicAdd(&g_tc_probe[EPI + 3][11], 1ull);
+          }
+#endif
           if (last) break;
           tc_fence_before();
           __syncwarp();
@@ -487,20 +530,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         sg0 = segs - 1;
       }
       for (int sg = sg0; sg < segs; ++sg, ++it) {
-      const int b = it & 1;
-      TC_PROBE_WAIT(mbar_wait(&tfull[b], (it >> 1) & 1));
+      const int b = (int)(it % C::NBUF);
+      TC_PROBE_WAIT(mbar_wait(&tfull[b], (it / C::NBUF) & 1));
       tc_fence_after();
+#ifdef VNT_TC_PROBE
+      const long long _f0 = clock64();
+#endif
       if constexpr (EPI == kTcDw) {
         // per-node quantisation, as k_gemm_tc's dW epilogue
 #pragma unroll
         for (int c = 0; c < COLS / 16; ++c) {
           float v[16];
+#ifdef VNT_DIAG_DW_NOLD
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = (float)(c + j);
+#else
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
+#endif
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const float x = v[j] * dscale;   // exact: power of two
             amax = fmax_nan(amax, fabsf(x));
+#ifdef VNT_DIAG_DW_NOCVT
+            acc[c * 16 + j] += (long long)__float_as_int(x);
+#else
             acc[c * 16 + j] += __float2ll_rn(x);
+#endif
           }
         }
       } else {
@@ -515,6 +570,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
+#ifdef VNT_TC_PROBE
+      if (lane == 0 && warp == kEpiWarp0 && rank == 0) {
+        atomicAdd(&g_tc_probe[EPI + 3][8], (unsigned long long)(clock64() - _f0));
+        atomicAdd(&g_tc_probe[EPI + 3][9], 1ull);
+      }
+#endif
       if (EPI == kTcDw) {
         asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 epilogue warps of this CTA
         if (warp == kEpiWarp0 && lane == 0) mbar_arrive_leader(&tempty[b]);

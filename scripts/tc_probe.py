@@ -36,7 +36,7 @@ B, V = 8192, 64
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 lib = vnt.load_engine()
 probe = lib.vnt_debug_tc_probe
-buf = (C.c_ulonglong * 48)()
+buf = (C.c_ulonglong * 72)()
 
 r = np.random.default_rng(1)
 params = np.concatenate([np.concatenate([r.standard_normal(WIDE[i] * WIDE[i + 1]) / np.sqrt(WIDE[i]),
@@ -60,7 +60,7 @@ t1.record()
 torch.cuda.synchronize()
 print(f"ms/step (probe build) {t0.elapsed_time(t1) / steps:.3f}")
 probe(buf)
-a = np.array(buf, dtype=np.float64).reshape(6, 8)
+a = np.array(buf, dtype=np.float64).reshape(6, 12)
 names = ["fwd", "bwd", "dW", "pair fwd", "pair bwd", "pair dW"]
 for k in range(6):
     if a[k, 1] == 0:
@@ -68,4 +68,7 @@ for k in range(6):
     print(f"{names[k]:9s} producer wait {a[k, 0] / a[k, 1]:.3f} | MMA tempty wait {a[k, 2] / a[k, 3]:.3f}"
           f" full wait {a[k, 6] / a[k, 3]:.3f} | epilogue tfull wait {a[k, 4] / max(a[k, 5], 1):.3f}"
           f" | MMA-thread cycles/launch-CTA {a[k, 3]:.3e}")
+    if a[k, 9]:
+        print(f"{'':9s} final epilogue {a[k, 8] / a[k, 9]:.0f} cyc x {a[k, 9]:.0f}"
+              + (f" | promote {a[k, 10] / a[k, 11]:.0f} cyc x {a[k, 11]:.0f}" if a[k, 11] else ""))
 e.close()
