@@ -3051,7 +3051,7 @@ int vnt_engine_memcpy_h2d(vnt_engine* e, void* dst, const void* src, uint64_t by
 int vnt_debug_tc_probe(unsigned long long* out) {
   if (cudaMemcpyFromSymbol(out, vntb::tc::g_tc_probe, sizeof(vntb::tc::g_tc_probe)) != cudaSuccess)
     return 1;
-  static const unsigned long long zero[6 * 12] = {};
+  static const unsigned long long zero[6 * 16] = {};
   return cudaMemcpyToSymbol(vntb::tc::g_tc_probe, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
 }
 #endif

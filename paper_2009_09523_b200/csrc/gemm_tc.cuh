@@ -70,7 +70,7 @@ enum : int { kTcFwd = 0, kTcBwd = 1, kTcDw = 2 };
 // Diagnostics build only (-DVNT_TC_PROBE, scripts/tc_probe.py): cycles each
 // role spends waiting on its barriers, per kernel kind (EPI + 3 * pair).
 #ifdef VNT_TC_PROBE
-__device__ unsigned long long g_tc_probe[6][12];   // 8..11: final-epilogue / promote cycles and counts
+__device__ unsigned long long g_tc_probe[6][16];   // 8..11: final-epilogue / promote cycles and counts; 12..15: finish phases
 #define TC_PROBE_DECL long long _pw = 0, _pt = clock64()
 #define TC_PROBE_WAIT(stmt)          \
   do {                               \

@@ -349,6 +349,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // bwd-data with a relu mask: this thread's 128 mask bits, loaded before
       // the K chunks so the final epilogue never waits on memory
       unsigned long long mk01 = 0, mk23 = 0;
+      // fwd: this lane's bias of each 32-column chunk, loaded with the tile
+      float bias_c[EPI == kTcFwd ? COLS / 32 : 1];
+      if constexpr (EPI == kTcFwd) {
+#pragma unroll
+        for (int c = 0; c < COLS / 32; ++c) {
+          const int n = n0 + h * COLS + 32 * c + lane;
+          bias_c[c] = n < ep.N ? __ldg(ep.bias + n) * bscale : 0.f;
+        }
+      }
       if constexpr (EPI == kTcBwd) {
         if (ep.mask_in && r < ep.M) {
           const uint4 w = __ldg(reinterpret_cast<const uint4*>(ep.mask_in + (size_t)r * ep.ldm + (n0 + h * COLS) / 32));
@@ -361,23 +370,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // through the per-warp smem transpose tile.
       auto finish32 = [&](float (&v)[32], int col) {
         const int nb = n0 + col;
+#ifdef VNT_TC_PROBE
+#ifndef VNT_PROBE_K
+#define VNT_PROBE_K 0
+#endif
+        const bool _rec = lane == 0 && warp == kEpiWarp0 && rank == 0 && (VNT_PROBE_K == 0 || K == VNT_PROBE_K);
+        long long _t0 = clock64();
+#define FIN_MARK(slot)                                                          \
+  do {                                                                          \
+    const long long _t1 = clock64();                                            \
+    if (_rec) atomicAdd(&g_tc_probe[EPI + 3][slot], (unsigned long long)(_t1 - _t0)); \
+    _t0 = _t1;                                                                  \
+  } while (0)
+#else
+#define FIN_MARK(slot)
+#endif
         if constexpr (SPLIT == 3) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= vscale;
         }
         if constexpr (EPI == kTcFwd) {
           // bias: one coalesced load per warp, broadcast by shuffles
-#ifdef VNT_DIAG_NO_BIAS
-          const float bl = 0.f;
-#else
-          const float bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) * bscale : 0.f;
-#endif
+          // bias_c[] indexed by a select chain (a runtime index would move it to local memory)
+          const int cc = (col - h * COLS) >> 5;
+          float bl = bias_c[0];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float bj = __shfl_sync(0xffffffffu, bl, j);
-            if (nb + j < ep.N) v[j] = act_fwd(ep.act, v[j] + bj);
+          for (int c = 1; c < COLS / 32; ++c) bl = cc == c ? bias_c[c] : bl;
+#ifdef VNT_DIAG_BIAS_LATE
+          bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) * bscale : 0.f;
+#endif
+          // the activation switch outside the element loop: a per-element
+          // act_fwd inlined 32 tanh bodies into the relu path (I-cache bound)
+          if (ep.act == 0 && nb + 32 <= ep.N) {
+            // relu, full chunk: the 32 biases as 8 broadcast 16-B loads (L1 hits)
+            const float4* bp = reinterpret_cast<const float4*>(ep.bias + nb);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b4 = __ldg(bp + j / 4);
+              v[j] = fmaxf(fmaf(b4.x, bscale, v[j]), 0.f);   // relu (model.cpp:216)
+              v[j + 1] = fmaxf(fmaf(b4.y, bscale, v[j + 1]), 0.f);
+              v[j + 2] = fmaxf(fmaf(b4.z, bscale, v[j + 2]), 0.f);
+              v[j + 3] = fmaxf(fmaf(b4.w, bscale, v[j + 3]), 0.f);
+            }
+          } else if (ep.act == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float bj = __shfl_sync(0xffffffffu, bl, j);
+              if (nb + j < ep.N) v[j] = fmaxf(v[j] + bj, 0.f);
+            }
+          } else {
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+              const float bj = __shfl_sync(0xffffffffu, bl, j);
+              if (nb + j < ep.N) v[j] = act_fwd(ep.act, v[j] + bj);
+            }
           }
         }
+        FIN_MARK(12);
         if constexpr (EPI == kTcFwd) {
 #ifdef VNT_DIAG_NO_MASKOUT
           if (false) {
@@ -390,6 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ep.mask_out[(size_t)r * ep.ldm + nb / 32] = m;
           }
         }
+        FIN_MARK(13);
         if (r < ep.M) {
           if (EPI == kTcBwd && ep.mask_in) {
             const int c = (col - h * COLS) >> 5;
@@ -443,6 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* box = tstage + (warp - kEpiWarp0) * 4096;
           if (lane == 0) tma_store_wait_read();   // the previous boxes were read out
           __syncwarp();
+          FIN_MARK(14);
           // v is at the twins' scale already (tscaled); columns past N are
           // zero (zero-filled B rows, zero bias), rows past M are excluded
           if (r < ep.M) {
@@ -472,6 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_store_2d(&tmOl, box + 2048, nb, m0 + q * 32);
             tma_store_commit();
           }
+          FIN_MARK(15);
           return;
         }
         // row-major copies: transpose the warp's 32x32 block through smem so
@@ -571,7 +623,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
 #ifdef VNT_TC_PROBE
-      if (lane == 0 && warp == kEpiWarp0 && rank == 0) {
+      if (lane == 0 && warp == kEpiWarp0 && rank == 0 && (VNT_PROBE_K == 0 || K == VNT_PROBE_K)) {
         atomicAdd(&g_tc_probe[EPI + 3][8], (unsigned long long)(clock64() - _f0));
         atomicAdd(&g_tc_probe[EPI + 3][9], 1ull);
       }

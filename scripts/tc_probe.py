@@ -36,7 +36,7 @@ B, V = 8192, 64
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 lib = vnt.load_engine()
 probe = lib.vnt_debug_tc_probe
-buf = (C.c_ulonglong * 72)()
+buf = (C.c_ulonglong * 96)()
 
 r = np.random.default_rng(1)
 params = np.concatenate([np.concatenate([r.standard_normal(WIDE[i] * WIDE[i + 1]) / np.sqrt(WIDE[i]),
@@ -60,7 +60,7 @@ t1.record()
 torch.cuda.synchronize()
 print(f"ms/step (probe build) {t0.elapsed_time(t1) / steps:.3f}")
 probe(buf)
-a = np.array(buf, dtype=np.float64).reshape(6, 12)
+a = np.array(buf, dtype=np.float64).reshape(6, 16)
 names = ["fwd", "bwd", "dW", "pair fwd", "pair bwd", "pair dW"]
 for k in range(6):
     if a[k, 1] == 0:
@@ -71,4 +71,8 @@ for k in range(6):
     if a[k, 9]:
         print(f"{'':9s} final epilogue {a[k, 8] / a[k, 9]:.0f} cyc x {a[k, 9]:.0f}"
               + (f" | promote {a[k, 10] / a[k, 11]:.0f} cyc x {a[k, 11]:.0f}" if a[k, 11] else ""))
+    if a[k, 12] + a[k, 13] + a[k, 14] + a[k, 15]:
+        n = max(a[k, 9], 1) * 4
+        print(f"{'':9s} per 32-col finish: bias/act {a[k, 12] / n:.0f} | mask {a[k, 13] / n:.0f} | store wait "
+              f"{a[k, 14] / n:.0f} | convert+stage {a[k, 15] / n:.0f} cyc")
 e.close()
