@@ -661,9 +661,14 @@ struct BackSkinny {
                   const int* row0, const int* nrows, int nn, float* Dout, vntb::Twin16 twins,
                   const float* scale_w, long long* Gw, int tw, const float* scale_b, long long* Gb, int tb,
                   float lim, long long* tail) {
-    dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
-    k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, twins, scale_w, Gw,
-                                               tw, scale_b, Gb, tb, lim, tail);
+    // nodes per block (their quantised partials added in registers, one int64
+    // atomic per element): 1 measured fastest at cfg3 (4 per block: 120 ->
+    // 153 us, fewer blocks in flight)
+    const int bx = (int)ceil_div(in, 128);
+    const int npb = 1;
+    dim3 grid((unsigned)bx, (unsigned)ceil_div(nn, npb));
+    k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, nn, npb, Dout, twins, scale_w,
+                                               Gw, tw, scale_b, Gb, tb, lim, tail);
   }
 };
 template <int NO>
@@ -1111,13 +1116,19 @@ void run_pass(vnt_engine* e, const Pass& p, const std::vector<StatsLaunch>* stat
     }
     prof_end(e, 2.0 * rows * (double)in_l * out_l);
     if (db_done != l) {
-      dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
       // a tcgen05 bwd-data leaves D only as its split-fp16 twins
       const bool twins_only = l + 1 < L && e->tc_layer[l + 1] && e->Dh[l + 1];
-      k_db<<<grid, 128, 0, s>>>(e->D[l + 1], twins_only ? e->Dh[l + 1] : nullptr,
-                                twins_only ? e->Dl[l + 1] : nullptr,
-                                twins_only ? h16_inv(e, h16_op_d(e, l + 1)) : nullptr,
-                                out_l, row0, nrows, sp_scale(e, tb), lim, e->G + e->boff[l], e->tail, tb);
+      if (twins_only && out_l % 2 == 0) {
+        dim3 grid((unsigned)ceil_div(out_l, 256), (unsigned)nn);
+        k_db2<<<grid, 128, 0, s>>>(e->Dh[l + 1], e->Dl[l + 1], h16_inv(e, h16_op_d(e, l + 1)), out_l, row0,
+                                   nrows, sp_scale(e, tb), lim, e->G + e->boff[l], e->tail, tb);
+      } else {
+        dim3 grid((unsigned)ceil_div(out_l, 128), (unsigned)nn);
+        k_db<<<grid, 128, 0, s>>>(e->D[l + 1], twins_only ? e->Dh[l + 1] : nullptr,
+                                  twins_only ? e->Dl[l + 1] : nullptr,
+                                  twins_only ? h16_inv(e, h16_op_d(e, l + 1)) : nullptr,
+                                  out_l, row0, nrows, sp_scale(e, tb), lim, e->G + e->boff[l], e->tail, tb);
+      }
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
@@ -1609,7 +1620,11 @@ void launch_sgd(vnt_engine* e, bool reduce_h16 = true) {
         static const int tr = getenv("VNT_SGD_TR") ? atoi(getenv("VNT_SGD_TR")) : 32;
         const int TR = (tr == 64 || tr == 128) ? tr : 32;
         dim3 grid((unsigned)ceil_div(a.cols, 32), (unsigned)ceil_div(a.rows, TR)), block(32, 8);
-        if (a.v64) k_sgd_weight<true><<<grid, block, 0, s>>>(a);
+        if (twins_only && a.rows % 2 == 0 && a.cols % 2 == 0) {
+          dim3 g2((unsigned)ceil_div(a.cols, 64), (unsigned)ceil_div(a.rows, 64));
+          if (a.v64) k_sgd_twins<true><<<g2, block, 0, s>>>(a);
+          else k_sgd_twins<false><<<g2, block, 0, s>>>(a);
+        } else if (a.v64) k_sgd_weight<true><<<grid, block, 0, s>>>(a);
         else if (TR == 32) k_sgd_weight<false, 32><<<grid, block, 0, s>>>(a);
         else if (TR == 128) k_sgd_weight<false, 128><<<grid, block, 0, s>>>(a);
         else k_sgd_weight<false><<<grid, block, 0, s>>>(a);

@@ -593,6 +593,49 @@ __global__ void k_db(const float* __restrict__ D, const __half* __restrict__ Dh,
   if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&G[o]), (unsigned long long)q);
 }
 
+// k_db on the split-fp16 twins, two columns per thread (__half2 loads: 128 B
+// per warp and row): the same per-column row order as k_db, so the same bits.
+__global__ void k_db2(const __half* __restrict__ Dh, const __half* __restrict__ Dl,
+                      const float* __restrict__ inv_p, int out, const int* __restrict__ vn_row0,
+                      const int* __restrict__ vn_rows, const float* __restrict__ scale_p, float lim,
+                      long long* __restrict__ G, long long* __restrict__ tail, int tensor) {
+  const int o = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int v = blockIdx.y;
+  if (o >= out) return;
+  const int r0 = vn_row0[v], n = vn_rows[v];
+  const float scale = *scale_p, inv = *inv_p;
+  const __half2* dh = reinterpret_cast<const __half2*>(Dh + (size_t)r0 * out + o);
+  const __half2* dl = reinterpret_cast<const __half2*>(Dl + (size_t)r0 * out + o);
+  const size_t ld = (size_t)out / 2;
+  float g0 = 0.f, g1 = 0.f;
+  int r = 0;
+  for (; r + 8 <= n; r += 8) {   // 8 rows in flight, adds in row order per column
+    float t0[8], t1[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float2 h = __half22float2(dh[(size_t)(r + j) * ld]);
+      const float2 l = __half22float2(dl[(size_t)(r + j) * ld]);
+      t0[j] = (h.x + l.x) * inv;
+      t1[j] = (h.y + l.y) * inv;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      g0 += t0[j];
+      g1 += t1[j];
+    }
+  }
+  for (; r < n; ++r) {
+    const float2 h = __half22float2(dh[(size_t)r * ld]);
+    const float2 l = __half22float2(dl[(size_t)r * ld]);
+    g0 += (h.x + l.x) * inv;
+    g1 += (h.y + l.y) * inv;
+  }
+  const long long q0 = quantise(g0, scale, lim, tail, tensor);
+  const long long q1 = quantise(g1, scale, lim, tail, tensor);
+  if (q0) atomicAdd(reinterpret_cast<unsigned long long*>(&G[o]), (unsigned long long)q0);
+  if (q1) atomicAdd(reinterpret_cast<unsigned long long*>(&G[o + 1]), (unsigned long long)q1);
+}
+
 // ---------------------------------------------- skinny layers (out <= 32)
 template <int NO>   // rows per warp in k_fwd_skinny (R*NO accumulators per lane)
 __host__ __device__ constexpr int skinny_rows() { return NO > 16 ? 2 : 4; }
@@ -870,89 +913,98 @@ __global__ void __launch_bounds__(512) k_fwd_skinny_res(const float* __restrict_
 template <int NO>
 __global__ void __launch_bounds__(128) k_skinny_backward(
     const float* __restrict__ X, const float* __restrict__ Dn, const float* __restrict__ W, int in, int no,
-    int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, float* __restrict__ Dout,
-    Twin16 twd, const float* __restrict__ scale_w, long long* __restrict__ Gw,
+    int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, int nn, int npb,
+    float* __restrict__ Dout, Twin16 twd, const float* __restrict__ scale_w, long long* __restrict__ Gw,
     int tw, const float* __restrict__ scale_b, long long* __restrict__ Gb, int tb, float lim,
     long long* __restrict__ tail) {
   static_assert(NO % 4 == 0, "dn rows are read as float4");
   __shared__ __align__(16) float dn[64][NO];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y;
-  const int r0 = vn_row0[v], n = vn_rows[v];
   const bool data = Gb != nullptr;
   const float mul = twd.hi ? *twd.mul : 1.f;
+  const float sw = *scale_w, sb = data ? *scale_b : 0.f;
   float m = 0.f;
-  float w[NO], g[NO];
+  float w[NO];
 #pragma unroll
-  for (int o = 0; o < NO; ++o) {
-    w[o] = (data && i < in && o < no) ? __ldg(W + (size_t)i * no + o) : 0.f;
-    g[o] = 0.f;
-  }
-  float db = 0.f;
-  for (int c = 0; c < n; c += 64) {
-    const int cn = min(64, n - c);
-    __syncthreads();
-    for (int k = threadIdx.x; k < cn * NO; k += blockDim.x)
-      dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
-    __syncthreads();
-    if (i >= in) continue;
-    const float* xp = X + (size_t)(r0 + c) * in + i;
-    for (int rr = 0; rr < cn; rr += 8) {
-      float a[8];
+  for (int o = 0; o < NO; ++o) w[o] = (data && i < in && o < no) ? __ldg(W + (size_t)i * no + o) : 0.f;
+  // the block's npb nodes: each node's partials quantised, their int64 sum
+  // kept in registers, one atomic per element at the end (not one per node)
+  long long qg[NO], qdb = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) a[j] = rr + j < cn ? __ldg(xp + (size_t)(rr + j) * in) : 0.f;
+  for (int o = 0; o < NO; ++o) qg[o] = 0;
+  const int v_end = min(nn, (int)(blockIdx.y + 1) * npb);
+  for (int v = blockIdx.y * npb; v < v_end; ++v) {
+    const int r0 = vn_row0[v], n = vn_rows[v];
+    float g[NO];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (rr + j >= cn) break;
-        const float4* d4 = reinterpret_cast<const float4*>(&dn[rr + j][0]);
-        float acc = 0.f;
+    for (int o = 0; o < NO; ++o) g[o] = 0.f;
+    float db = 0.f;
+    for (int c = 0; c < n; c += 64) {
+      const int cn = min(64, n - c);
+      __syncthreads();
+      for (int k = threadIdx.x; k < cn * NO; k += blockDim.x)
+        dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
+      __syncthreads();
+      if (i >= in) continue;
+      const float* xp = X + (size_t)(r0 + c) * in + i;
+      for (int rr = 0; rr < cn; rr += 8) {
+        float a[8];
 #pragma unroll
-        for (int o = 0; o < NO; o += 4) {
-          const float4 d = d4[o / 4];
-          g[o] = fmaf(a[j], d.x, g[o]);
-          g[o + 1] = fmaf(a[j], d.y, g[o + 1]);
-          g[o + 2] = fmaf(a[j], d.z, g[o + 2]);
-          g[o + 3] = fmaf(a[j], d.w, g[o + 3]);
-          acc = fmaf(d.x, w[o], acc);
-          acc = fmaf(d.y, w[o + 1], acc);
-          acc = fmaf(d.z, w[o + 2], acc);
-          acc = fmaf(d.w, w[o + 3], acc);
-        }
-        if (data) {
-          const float dv = acc * act_grad_from_out(act, a[j]);
-          const size_t idx = (size_t)(r0 + c + rr + j) * in + i;
-          if (Dout) Dout[idx] = dv;
-          if (twd.hi) {
-            put16(twd.hi, twd.lo, idx, dv, mul);
-            m = fmax_nan(m, fabsf(dv));
+        for (int j = 0; j < 8; ++j) a[j] = rr + j < cn ? __ldg(xp + (size_t)(rr + j) * in) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (rr + j >= cn) break;
+          const float4* d4 = reinterpret_cast<const float4*>(&dn[rr + j][0]);
+          float acc = 0.f;
+#pragma unroll
+          for (int o = 0; o < NO; o += 4) {
+            const float4 d = d4[o / 4];
+            g[o] = fmaf(a[j], d.x, g[o]);
+            g[o + 1] = fmaf(a[j], d.y, g[o + 1]);
+            g[o + 2] = fmaf(a[j], d.z, g[o + 2]);
+            g[o + 3] = fmaf(a[j], d.w, g[o + 3]);
+            acc = fmaf(d.x, w[o], acc);
+            acc = fmaf(d.y, w[o + 1], acc);
+            acc = fmaf(d.z, w[o + 2], acc);
+            acc = fmaf(d.w, w[o + 3], acc);
           }
-          db += dv;
+          if (data) {
+            const float dv = acc * act_grad_from_out(act, a[j]);
+            const size_t idx = (size_t)(r0 + c + rr + j) * in + i;
+            if (Dout) Dout[idx] = dv;
+            if (twd.hi) {
+              put16(twd.hi, twd.lo, idx, dv, mul);
+              m = fmax_nan(m, fabsf(dv));
+            }
+            db += dv;
+          }
         }
       }
+    }
+    if (i < in) {
+      if (data)   // the node's pad rows (up to kNodeRowPad) carry zero deltas
+        for (int r = n; r < (int)round_up(n, kNodeRowPad); ++r) {
+          const size_t idx = (size_t)(r0 + r) * in + i;
+          if (Dout) Dout[idx] = 0.f;
+          if (twd.hi) {
+            twd.hi[idx] = __float2half_rn(0.f);
+            twd.lo[idx] = __float2half_rn(0.f);
+          }
+        }
+#pragma unroll
+      for (int o = 0; o < NO; ++o)
+        if (o < no) qg[o] += quantise(g[o], sw, lim, tail, tw);
+      if (data) qdb += quantise(db, sb, lim, tail, tb);
     }
   }
   if (twd.hi) twin_flush(twd, m, mul);
   if (i >= in) return;
-  if (data)   // the node's pad rows (up to kNodeRowPad) carry zero deltas
-    for (int r = n; r < (int)round_up(n, kNodeRowPad); ++r) {
-      const size_t idx = (size_t)(r0 + r) * in + i;
-      if (Dout) Dout[idx] = 0.f;
-      if (twd.hi) {
-        twd.hi[idx] = __float2half_rn(0.f);
-        twd.lo[idx] = __float2half_rn(0.f);
-      }
-    }
-  const float sw = *scale_w;
 #pragma unroll
   for (int o = 0; o < NO; ++o) {
     if (o >= no) break;
-    const long long q = quantise(g[o], sw, lim, tail, tw);
-    if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&Gw[(size_t)i * no + o]), (unsigned long long)q);
+    if (qg[o]) atomicAdd(reinterpret_cast<unsigned long long*>(&Gw[(size_t)i * no + o]), (unsigned long long)qg[o]);
   }
-  if (data) {
-    const long long q = quantise(db, *scale_b, lim, tail, tb);
-    if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&Gb[i]), (unsigned long long)q);
-  }
+  if (data && qdb) atomicAdd(reinterpret_cast<unsigned long long*>(&Gb[i]), (unsigned long long)qdb);
 }
 
 // -------------------------------------------------------------------- SGD
@@ -1109,6 +1161,83 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
         if (a.wt32h) put16(a.wt32h, a.wt32l, o, v, wmul);
       }
     }
+  }
+}
+
+// Weight tensor of a tcgen05 layer (only its split-fp16 twins are consumed):
+// 64x64 tiles, 32x8 threads, each thread two adjacent columns x 8 rows (16-B
+// loads of S and w), the row-major twins as half2 and the transposed twins
+// through an smem tile as half2 pairs of rows (128 B per warp store).  Same
+// per-element arithmetic as k_sgd_weight (same bits).  rows, cols even.
+template <bool MOM>
+__global__ void __launch_bounds__(256, MOM ? 2 : 3) k_sgd_twins(SgdArgs a) {
+  constexpr int TR = 64, TC = 64, PER = TR / 8;
+  __shared__ float tile[TR][TC + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
+  const int c = c0 + 2 * tx;
+  longlong2 S[PER];
+  double2 w[PER], v[MOM ? PER : 1];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {   // loads first: the poison check overlaps them
+    const int r = r0 + ty + 8 * k;
+    const bool ok = r < a.rows && c < a.cols;
+    const size_t idx = (size_t)r * a.cols + c;
+    S[k] = ok ? __ldg(reinterpret_cast<const longlong2*>(a.G + idx)) : make_longlong2(0, 0);
+    w[k] = ok ? *reinterpret_cast<const double2*>(a.w64 + idx) : make_double2(0.0, 0.0);
+    if constexpr (MOM) v[k] = ok ? *reinterpret_cast<const double2*>(a.v64 + idx) : make_double2(0.0, 0.0);
+  }
+  if (block_poisoned(a.tail, a.ntail_flags, a.sp, a.h16max, a.h16n)) return;
+  const double inv_scale = a.sp->inv_scale[a.tensor], inv_b = a.sp->inv_b;
+  const double lr = a.sp->lr, mu = a.sp->mu;
+  const float wmul = *a.wtw.mul;
+  float wm = 0.f;
+  double mx = 0.0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int r = r0 + ty + 8 * k;
+    const bool ok = r < a.rows && c < a.cols;
+    const double g0 = __dmul_rn(__ll2double_rn(S[k].x) * inv_scale, inv_b);
+    const double g1 = __dmul_rn(__ll2double_rn(S[k].y) * inv_scale, inv_b);
+    double u0 = g0, u1 = g1;
+    if constexpr (MOM) {
+      u0 = __dadd_rn(__dmul_rn(mu, v[k].x), g0);
+      u1 = __dadd_rn(__dmul_rn(mu, v[k].y), g1);
+    }
+    const double n0 = __dsub_rn(w[k].x, __dmul_rn(lr, u0));
+    const double n1 = __dsub_rn(w[k].y, __dmul_rn(lr, u1));
+    const float f0 = __double2float_rn(n0), f1 = __double2float_rn(n1);
+    tile[ty + 8 * k][2 * tx] = ok ? f0 : 0.f;
+    tile[ty + 8 * k][2 * tx + 1] = ok ? f1 : 0.f;
+    if (ok) {
+      const size_t idx = (size_t)r * a.cols + c;
+      *reinterpret_cast<double2*>(a.w64 + idx) = make_double2(n0, n1);
+      if constexpr (MOM) *reinterpret_cast<double2*>(a.v64 + idx) = make_double2(u0, u1);
+      const float s0 = f0 * wmul, s1 = f1 * wmul;
+      const __half2 hh = __floats2half2_rn(s0, s1);
+      const float2 hf = __half22float2(hh);
+      *reinterpret_cast<__half2*>(a.w32h + idx) = hh;
+      *reinterpret_cast<__half2*>(a.w32l + idx) = __floats2half2_rn(s0 - hf.x, s1 - hf.y);
+      if (a.gout) *reinterpret_cast<double2*>(a.gout + idx) = make_double2(g0, g1);
+      wm = fmax_nan(wm, fmax_nan(fabsf(f0), fabsf(f1)));
+      mx = fmax(mx, fmax(fabs(g0), fabs(g1)));
+    }
+  }
+  twin_flush(a.wtw, wm, wmul);
+  block_max_to(a.gmax, mx);
+  __syncthreads();
+  // transposed twins WT[col][row]: warp ty takes columns ty, ty + 8, ...; lane
+  // tx the row pair (2 tx, 2 tx + 1)
+#pragma unroll
+  for (int k = 0; k < TC / 8; ++k) {
+    const int cc = ty + 8 * k, col = c0 + cc, r = r0 + 2 * tx;
+    if (col >= a.cols || r >= a.rows) continue;
+    const float s0 = tile[2 * tx][cc] * wmul, s1 = tile[2 * tx + 1][cc] * wmul;
+    const __half2 hh = __floats2half2_rn(s0, s1);
+    const float2 hf = __half22float2(hh);
+    const size_t o = (size_t)col * a.rows + r;
+    *reinterpret_cast<__half2*>(a.wt32h + o) = hh;
+    *reinterpret_cast<__half2*>(a.wt32l + o) = __floats2half2_rn(s0 - hf.x, s1 - hf.y);
   }
 }
 
