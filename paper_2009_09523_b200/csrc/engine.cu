@@ -1707,24 +1707,49 @@ struct H16Review {
 H16Review h16_retune(vnt_engine* e) {
   H16Review r;
   if (!e->split) return r;
-  bool resplit = false;
-  for (int op = 0; op < h16_nops(e); ++op) {
+  auto max_of = [&](int op) {
     const uint32_t b = (uint32_t)e->h_h16max[op];
-    if (b == 0) continue;
     float m;
     std::memcpy(&m, &b, sizeof m);
-    if (!std::isfinite(m)) {
-      r.finite = false;
-      continue;
-    }
+    return m;
+  };
+  // one operand's band rule; returns false past an fp16 overflow
+  auto retune = [&](int op) {
+    const float m = max_of(op);
     const double x = std::ldexp((double)m, e->h16_sig[op]);
     // the device-side test of block_poisoned (StepParams mul < 2^100)
     if (h16_reduced(e) && x < vntb::kH16Under && e->h16_sig[op] < vntb::kH16SigMax) r.under = true;
-    if (x >= 1024.0 && x < 16384.0) continue;
-    e->h16_sig[op] = std::min(h16_sigma_for(m), vntb::kH16SigMax);
-    if (op == h16_op_w(e)) resplit = !e->shard;
+    if (!(x >= 1024.0 && x < 16384.0)) e->h16_sig[op] = std::min(h16_sigma_for(m), vntb::kH16SigMax);
+    return x < (double)vntb::kH16Lim;
+  };
+  // Activations and deltas in dataflow order (X0 .. X_L, then D_L .. D_1): an
+  // operand that overflowed fp16 poisons everything computed from it, so the
+  // scan stops there (the redo measures the rest); a non-finite maximum before
+  // any overflow is a genuine non-finite value.
+  std::vector<int> order;
+  for (int l = 0; l <= e->L; ++l) order.push_back(h16_op_x(e, l));
+  for (int l = e->L; l >= 1; --l) order.push_back(h16_op_d(e, l));
+  for (int op : order) {
+    const float m = max_of(op);
+    if (m == 0.f) continue;
+    if (!std::isfinite(m)) {
+      r.finite = false;
+      break;
+    }
+    if (!retune(op)) break;
   }
-  if (resplit && r.finite) refresh_from_master(e);
+  // the weights (their twins for the next step when unsharded)
+  const int w = h16_op_w(e);
+  const float mw = max_of(w);
+  if (mw != 0.f) {
+    if (!std::isfinite(mw)) {
+      r.finite = false;
+    } else {
+      const int before = e->h16_sig[w];
+      retune(w);
+      if (e->h16_sig[w] != before && !e->shard) refresh_from_master(e);
+    }
+  }
   return r;
 }
 

@@ -96,3 +96,41 @@ def test_scale_state_continues_trajectory_bitwise(port):
     assert np.array_equal(a.scales(full=True), b.scales(full=True))
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("force_comm", ["0", "1"])
+def test_weight_scale_follows_a_jump(port, monkeypatch, force_comm):
+    """Hidden weights that grow ~100x in one update leave their split-fp16
+    band: the twins are re-split (unsharded: from the fp64 master at the new
+    sigma; sharded one-rank NCCL group: the next expansion reads the new sigma),
+    so the next gradient is still fp32-grade against the oracle at the new
+    weights."""
+    monkeypatch.setenv("VNT_FORCE_COMM", force_comm)
+    sizes = np.array([48, 16, 32, 32], np.uint64)
+    dev = np.zeros(len(sizes), np.int32)
+    x, y = port.synth_batch(6, 2048, W[0], W[-1], 0, 128)
+    e = engine(port)
+    p0 = port.init_params(W, 1)
+    hidden = slice(0, W[0] * W[1] + W[1] + W[1] * W[2])   # the tcgen05 layers' weights (+ bias 0)
+    sig0 = e.scales(full=True)[-1]
+    e.train_step(x, y, sizes, dev, 3000.0)   # a huge step: the hidden weights grow
+    p1 = e.get_params()
+    growth = np.abs(p1[hidden]).max() / np.abs(p0[hidden]).max()
+    e.train_step(x, y, sizes, dev, 1e-9)     # runs on the re-split twins
+    sig1 = e.scales(full=True)[-1]
+    x2, y2 = port.synth_batch(6, 2048, W[0], W[-1], 128, 128)
+    p2 = e.get_params()
+    want, want_loss = port.forward_backward(W, "relu", "softmax-cross-entropy", p2, x2, y2)
+    for attempt in range(8):   # RESCALE: the caller redoes the step (virtual_exec.cpp)
+        e.device_step(0, x2, y2, sizes)
+        try:
+            g, loss_sum, ex = e.sync()
+            break
+        except vnt().VntError as err2:
+            assert err2.code == 12
+    err = np.abs(g - want).max() / np.abs(want).max()
+    print(f"force_comm {force_comm}: hidden weights x{growth:.0f}, sigma_W {sig0} -> {sig1}, rel grad err {err:.2e}")
+    assert growth > 16 and sig1 <= sig0 - 4
+    assert err < 2e-5
+    assert abs(loss_sum / ex - want_loss) < 2e-6 * abs(want_loss)
+    e.close()
