@@ -396,9 +396,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           float bl = bias_c[0];
 #pragma unroll
           for (int c = 1; c < COLS / 32; ++c) bl = cc == c ? bias_c[c] : bl;
-#ifdef VNT_DIAG_BIAS_LATE
-          bl = nb + lane < ep.N ? __ldg(ep.bias + nb + lane) * bscale : 0.f;
-#endif
           // the activation switch outside the element loop: a per-element
           // act_fwd inlined 32 tanh bodies into the relu path (I-cache bound)
           if (ep.act == 0 && nb + 32 <= ep.N) {
@@ -428,11 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         FIN_MARK(12);
         if constexpr (EPI == kTcFwd) {
-#ifdef VNT_DIAG_NO_MASKOUT
-          if (false) {
-#else
           if (ep.mask_out && r < ep.M) {
-#endif
             uint32_t m = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) m |= (nb + j < ep.N && v[j] > 0.f ? 1u : 0u) << j;
@@ -529,11 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // row-major copies: transpose the warp's 32x32 block through smem so
         // every store writes 128 contiguous bytes of one row (a per-thread
         // float4 row store touches 32 lines per instruction)
-#ifdef VNT_DIAG_NO_STORE
-        if (false) {
-#else
         if (ep.out || ep.tw.hi) {
-#endif
           float* st = stile + (warp - kEpiWarp0) * (32 * 33);
 #pragma unroll
           for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
@@ -593,21 +582,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < COLS / 16; ++c) {
           float v[16];
-#ifdef VNT_DIAG_DW_NOLD
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = (float)(c + j);
-#else
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + h * COLS + c * 16), v);
-#endif
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const float x = v[j] * dscale;   // exact: power of two
             amax = fmax_nan(amax, fabsf(x));
-#ifdef VNT_DIAG_DW_NOCVT
-            acc[c * 16 + j] += (long long)__float_as_int(x);
-#else
             acc[c * 16 + j] += __float2ll_rn(x);
-#endif
           }
         }
       } else {
