@@ -218,8 +218,8 @@ print(json.dumps({"err": err, "bitwise": bool(np.array_equal(out[0], out[1]))}))
 def test_kernel_variants_are_bit_identical(port, tmp_path):
     """CTA-pair and single-CTA tcgen05 kernels run the same per-element K-chains
     (same k order, same three MMAs per k-step): a few training steps give
-    bit-identical losses and parameters with VNT_TC_PAIR=0, VNT_TC_DW_PAIR=0
-    and the defaults."""
+    bit-identical losses and parameters with VNT_TC_PAIR=0, VNT_TC_DW_PAIR=0,
+    VNT_TC_TMA_OUT=0 (per-lane epilogue stores) and the defaults."""
     import os
     import subprocess
     import sys
@@ -243,14 +243,15 @@ np.save(sys.argv[1], np.concatenate([np.array(losses), e.get_params()]))
 '''
     for mode in ("3xf16", "tf32"):
         outs = []
-        for k, env_kv in enumerate(({}, {"VNT_TC_DW_PAIR": "0"}, {"VNT_TC_PAIR": "0"})):
+        for k, env_kv in enumerate(({}, {"VNT_TC_DW_PAIR": "0"}, {"VNT_TC_PAIR": "0"},
+                                    {"VNT_TC_TMA_OUT": "0"})):
             path = str(tmp_path / f"v{mode}{k}.npy")
             r = subprocess.run([sys.executable, "-c", code, path, mode], capture_output=True,
                                text=True, env=dict(os.environ, **env_kv),
                                cwd=str(GOLDEN.parents[1]), timeout=300)
             assert r.returncode == 0, r.stderr[-2000:]
             outs.append(np.load(path))
-        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), mode
+        assert all(np.array_equal(outs[0], o) for o in outs[1:]), mode
 
 
 def test_tile_raster_does_not_change_bits(port, tmp_path):
