@@ -910,8 +910,11 @@ __global__ void __launch_bounds__(512) k_fwd_skinny_res(const float* __restrict_
 // partials are quantised and added into G with int64 atomics (exact).  D[l]
 // is written as the split-fp16 twins and/or plain (each nullable); Gb == nullptr
 // (l == 0): no bwd-data / db.
+#ifndef VNT_SKB_MINB
+#define VNT_SKB_MINB 1
+#endif
 template <int NO>
-__global__ void __launch_bounds__(128) k_skinny_backward(
+__global__ void __launch_bounds__(128, VNT_SKB_MINB) k_skinny_backward(
     const float* __restrict__ X, const float* __restrict__ Dn, const float* __restrict__ W, int in, int no,
     int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, int nn, int npb,
     float* __restrict__ Dout, Twin16 twd, const float* __restrict__ scale_w, long long* __restrict__ Gw,
@@ -947,10 +950,16 @@ __global__ void __launch_bounds__(128) k_skinny_backward(
       __syncthreads();
       if (i >= in) continue;
       const float* xp = X + (size_t)(r0 + c) * in + i;
+      // the next 8 rows are loaded while these 8 are folded (16 loads in flight)
+      float an[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) an[j] = j < cn ? __ldg(xp + (size_t)j * in) : 0.f;
       for (int rr = 0; rr < cn; rr += 8) {
         float a[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = rr + j < cn ? __ldg(xp + (size_t)(rr + j) * in) : 0.f;
+        for (int j = 0; j < 8; ++j) a[j] = an[j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) an[j] = rr + 8 + j < cn ? __ldg(xp + (size_t)(rr + 8 + j) * in) : 0.f;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (rr + j >= cn) break;
