@@ -143,6 +143,8 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+__device__ __noinline__ float act_fwd_call(int act, float z) { return act_fwd(act, z); }
+
 template <int EPI, int SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -416,10 +418,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (nb + j < ep.N) v[j] = fmaxf(v[j] + bj, 0.f);
             }
           } else {
-#pragma unroll 4
+            // tanh / identity: out of line (a partially unrolled loop here would
+            // move v[] to local memory for the whole epilogue)
+#pragma unroll
             for (int j = 0; j < 32; ++j) {
               const float bj = __shfl_sync(0xffffffffu, bl, j);
-              if (nb + j < ep.N) v[j] = act_fwd(ep.act, v[j] + bj);
+              if (nb + j < ep.N) v[j] = act_fwd_call(ep.act, v[j] + bj);
             }
           }
         }
