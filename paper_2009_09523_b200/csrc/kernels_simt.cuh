@@ -1179,7 +1179,7 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
 // through an smem tile as half2 pairs of rows (128 B per warp store).  Same
 // per-element arithmetic as k_sgd_weight (same bits).  rows, cols even.
 template <bool MOM>
-__global__ void __launch_bounds__(256, MOM ? 2 : 3) k_sgd_twins(SgdArgs a) {
+__global__ void __launch_bounds__(256, 2) k_sgd_twins(SgdArgs a) {
   constexpr int TR = 64, TC = 64, PER = TR / 8;
   __shared__ float tile[TR][TC + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
