@@ -609,19 +609,18 @@ __global__ void k_db2(const __half* __restrict__ Dh, const __half* __restrict__ 
   const size_t ld = (size_t)out / 2;
   float g0 = 0.f, g1 = 0.f;
   int r = 0;
-  for (; r + 8 <= n; r += 8) {   // 8 rows in flight, adds in row order per column
-    float t0[8], t1[8];
+  for (; r + 16 <= n; r += 16) {   // 16 rows in flight, adds in row order per column
+    __half2 hh[16], ll[16];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float2 h = __half22float2(dh[(size_t)(r + j) * ld]);
-      const float2 l = __half22float2(dl[(size_t)(r + j) * ld]);
-      t0[j] = (h.x + l.x) * inv;
-      t1[j] = (h.y + l.y) * inv;
+    for (int j = 0; j < 16; ++j) {
+      hh[j] = dh[(size_t)(r + j) * ld];
+      ll[j] = dl[(size_t)(r + j) * ld];
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      g0 += t0[j];
-      g1 += t1[j];
+    for (int j = 0; j < 16; ++j) {
+      const float2 h = __half22float2(hh[j]), l = __half22float2(ll[j]);
+      g0 += (h.x + l.x) * inv;
+      g1 += (h.y + l.y) * inv;
     }
   }
   for (; r < n; ++r) {

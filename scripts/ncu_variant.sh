@@ -16,6 +16,6 @@ PY
   printf "%s: " "$D"
   ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:$K" -c "$C" --csv \
       python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-extra 2>/dev/null \
-    | grep -v "^==" | tail -n +2 | awk -F'","' '{gsub(/"/,"",$NF); s+=$NF; n++} END {printf "%.1f us mean over %d\n", s/n/1000, n}'
+    | grep -v "^==" | tail -n +2 | awk -F'","' '{gsub(/"/,"",$NF); k=substr($5,1,40); s[k]+=$NF; n[k]++} END {for (k in s) printf "\n  %-40s %.1f us x %d", k, s[k]/n[k]/1000, n[k]; printf "\n"}'
 done
 cp /tmp/vnt_default.so paper_2009_09523_b200/libvnt_engine.so
