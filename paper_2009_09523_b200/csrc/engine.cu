@@ -661,14 +661,9 @@ struct BackSkinny {
                   const int* row0, const int* nrows, int nn, float* Dout, vntb::Twin16 twins,
                   const float* scale_w, long long* Gw, int tw, const float* scale_b, long long* Gb, int tb,
                   float lim, long long* tail) {
-    // nodes per block (their quantised partials added in registers, one int64
-    // atomic per element): 1 measured fastest at cfg3 (4 per block: 120 ->
-    // 153 us, fewer blocks in flight)
-    const int bx = (int)ceil_div(in, 128);
-    const int npb = 1;
-    dim3 grid((unsigned)bx, (unsigned)ceil_div(nn, npb));
-    k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, nn, npb, Dout, twins, scale_w,
-                                               Gw, tw, scale_b, Gb, tb, lim, tail);
+    dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
+    k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, twins, scale_w, Gw,
+                                               tw, scale_b, Gb, tb, lim, tail);
   }
 };
 template <int NO>

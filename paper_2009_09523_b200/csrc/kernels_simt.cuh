@@ -909,110 +909,98 @@ __global__ void __launch_bounds__(512) k_fwd_skinny_res(const float* __restrict_
 // partials are quantised and added into G with int64 atomics (exact).  D[l]
 // is written as the split-fp16 twins and/or plain (each nullable); Gb == nullptr
 // (l == 0): no bwd-data / db.
-#ifndef VNT_SKB_MINB
-#define VNT_SKB_MINB 1
-#endif
 template <int NO>
-__global__ void __launch_bounds__(128, VNT_SKB_MINB) k_skinny_backward(
+__global__ void __launch_bounds__(128) k_skinny_backward(
     const float* __restrict__ X, const float* __restrict__ Dn, const float* __restrict__ W, int in, int no,
-    int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, int nn, int npb,
-    float* __restrict__ Dout, Twin16 twd, const float* __restrict__ scale_w, long long* __restrict__ Gw,
-    int tw, const float* __restrict__ scale_b, long long* __restrict__ Gb, int tb, float lim,
+    int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, float* __restrict__ Dout,
+    Twin16 twd, const float* __restrict__ scale_w, long long* __restrict__ Gw, int tw,
+    const float* __restrict__ scale_b, long long* __restrict__ Gb, int tb, float lim,
     long long* __restrict__ tail) {
   static_assert(NO % 4 == 0, "dn rows are read as float4");
   __shared__ __align__(16) float dn[64][NO];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  const int r0 = vn_row0[v], n = vn_rows[v];
   const bool data = Gb != nullptr;
   const float mul = twd.hi ? *twd.mul : 1.f;
-  const float sw = *scale_w, sb = data ? *scale_b : 0.f;
   float m = 0.f;
-  float w[NO];
+  float w[NO], g[NO];
 #pragma unroll
-  for (int o = 0; o < NO; ++o) w[o] = (data && i < in && o < no) ? __ldg(W + (size_t)i * no + o) : 0.f;
-  // the block's npb nodes: each node's partials quantised, their int64 sum
-  // kept in registers, one atomic per element at the end (not one per node)
-  long long qg[NO], qdb = 0;
+  for (int o = 0; o < NO; ++o) {
+    w[o] = (data && i < in && o < no) ? __ldg(W + (size_t)i * no + o) : 0.f;
+    g[o] = 0.f;
+  }
+  float db = 0.f;
+  for (int c = 0; c < n; c += 64) {
+    const int cn = min(64, n - c);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cn * NO; k += blockDim.x)
+      dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
+    __syncthreads();
+    if (i >= in) continue;
+    const float* xp = X + (size_t)(r0 + c) * in + i;
+    // the next 8 rows are loaded while these 8 are folded (16 loads in flight)
+    float an[8];
 #pragma unroll
-  for (int o = 0; o < NO; ++o) qg[o] = 0;
-  const int v_end = min(nn, (int)(blockIdx.y + 1) * npb);
-  for (int v = blockIdx.y * npb; v < v_end; ++v) {
-    const int r0 = vn_row0[v], n = vn_rows[v];
-    float g[NO];
+    for (int j = 0; j < 8; ++j) an[j] = j < cn ? __ldg(xp + (size_t)j * in) : 0.f;
+    for (int rr = 0; rr < cn; rr += 8) {
+      float a[8];
 #pragma unroll
-    for (int o = 0; o < NO; ++o) g[o] = 0.f;
-    float db = 0.f;
-    for (int c = 0; c < n; c += 64) {
-      const int cn = min(64, n - c);
-      __syncthreads();
-      for (int k = threadIdx.x; k < cn * NO; k += blockDim.x)
-        dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
-      __syncthreads();
-      if (i >= in) continue;
-      const float* xp = X + (size_t)(r0 + c) * in + i;
-      // the next 8 rows are loaded while these 8 are folded (16 loads in flight)
-      float an[8];
+      for (int j = 0; j < 8; ++j) a[j] = an[j];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) an[j] = j < cn ? __ldg(xp + (size_t)j * in) : 0.f;
-      for (int rr = 0; rr < cn; rr += 8) {
-        float a[8];
+      for (int j = 0; j < 8; ++j) an[j] = rr + 8 + j < cn ? __ldg(xp + (size_t)(rr + 8 + j) * in) : 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = an[j];
+      for (int j = 0; j < 8; ++j) {
+        if (rr + j >= cn) break;
+        const float4* d4 = reinterpret_cast<const float4*>(&dn[rr + j][0]);
+        float acc = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) an[j] = rr + 8 + j < cn ? __ldg(xp + (size_t)(rr + 8 + j) * in) : 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (rr + j >= cn) break;
-          const float4* d4 = reinterpret_cast<const float4*>(&dn[rr + j][0]);
-          float acc = 0.f;
-#pragma unroll
-          for (int o = 0; o < NO; o += 4) {
-            const float4 d = d4[o / 4];
-            g[o] = fmaf(a[j], d.x, g[o]);
-            g[o + 1] = fmaf(a[j], d.y, g[o + 1]);
-            g[o + 2] = fmaf(a[j], d.z, g[o + 2]);
-            g[o + 3] = fmaf(a[j], d.w, g[o + 3]);
-            acc = fmaf(d.x, w[o], acc);
-            acc = fmaf(d.y, w[o + 1], acc);
-            acc = fmaf(d.z, w[o + 2], acc);
-            acc = fmaf(d.w, w[o + 3], acc);
+        for (int o = 0; o < NO; o += 4) {
+          const float4 d = d4[o / 4];
+          g[o] = fmaf(a[j], d.x, g[o]);
+          g[o + 1] = fmaf(a[j], d.y, g[o + 1]);
+          g[o + 2] = fmaf(a[j], d.z, g[o + 2]);
+          g[o + 3] = fmaf(a[j], d.w, g[o + 3]);
+          acc = fmaf(d.x, w[o], acc);
+          acc = fmaf(d.y, w[o + 1], acc);
+          acc = fmaf(d.z, w[o + 2], acc);
+          acc = fmaf(d.w, w[o + 3], acc);
+        }
+        if (data) {
+          const float dv = acc * act_grad_from_out(act, a[j]);
+          const size_t idx = (size_t)(r0 + c + rr + j) * in + i;
+          if (Dout) Dout[idx] = dv;
+          if (twd.hi) {
+            put16(twd.hi, twd.lo, idx, dv, mul);
+            m = fmax_nan(m, fabsf(dv));
           }
-          if (data) {
-            const float dv = acc * act_grad_from_out(act, a[j]);
-            const size_t idx = (size_t)(r0 + c + rr + j) * in + i;
-            if (Dout) Dout[idx] = dv;
-            if (twd.hi) {
-              put16(twd.hi, twd.lo, idx, dv, mul);
-              m = fmax_nan(m, fabsf(dv));
-            }
-            db += dv;
-          }
+          db += dv;
         }
       }
-    }
-    if (i < in) {
-      if (data)   // the node's pad rows (up to kNodeRowPad) carry zero deltas
-        for (int r = n; r < (int)round_up(n, kNodeRowPad); ++r) {
-          const size_t idx = (size_t)(r0 + r) * in + i;
-          if (Dout) Dout[idx] = 0.f;
-          if (twd.hi) {
-            twd.hi[idx] = __float2half_rn(0.f);
-            twd.lo[idx] = __float2half_rn(0.f);
-          }
-        }
-#pragma unroll
-      for (int o = 0; o < NO; ++o)
-        if (o < no) qg[o] += quantise(g[o], sw, lim, tail, tw);
-      if (data) qdb += quantise(db, sb, lim, tail, tb);
     }
   }
   if (twd.hi) twin_flush(twd, m, mul);
   if (i >= in) return;
+  if (data)   // the node's pad rows (up to kNodeRowPad) carry zero deltas
+    for (int r = n; r < (int)round_up(n, kNodeRowPad); ++r) {
+      const size_t idx = (size_t)(r0 + r) * in + i;
+      if (Dout) Dout[idx] = 0.f;
+      if (twd.hi) {
+        twd.hi[idx] = __float2half_rn(0.f);
+        twd.lo[idx] = __float2half_rn(0.f);
+      }
+    }
+  const float sw = *scale_w;
 #pragma unroll
   for (int o = 0; o < NO; ++o) {
     if (o >= no) break;
-    if (qg[o]) atomicAdd(reinterpret_cast<unsigned long long*>(&Gw[(size_t)i * no + o]), (unsigned long long)qg[o]);
+    const long long q = quantise(g[o], sw, lim, tail, tw);
+    if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&Gw[(size_t)i * no + o]), (unsigned long long)q);
   }
-  if (data && qdb) atomicAdd(reinterpret_cast<unsigned long long*>(&Gb[i]), (unsigned long long)qdb);
+  if (data) {
+    const long long q = quantise(db, *scale_b, lim, tail, tb);
+    if (q) atomicAdd(reinterpret_cast<unsigned long long*>(&Gb[i]), (unsigned long long)q);
+  }
 }
 
 // -------------------------------------------------------------------- SGD
