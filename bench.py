@@ -456,6 +456,11 @@ def run_ours(args, work):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "arithmetic": {"auto": "dense GEMMs: fp32 emulated by split-fp16 operands (x 2^s = hi + lo) on tcgen05 "
+                               "kind::f16, three MMAs per k16 step, fp32 accumulation; per-node gradients "
+                               "int64 fixed point; update fp64",
+                       "3xf16": "as auto", "3xtf32": "as auto", "tf32": "dense GEMMs: 1-pass tcgen05 kind::tf32",
+                       "ffma": "fp32 FMA everywhere"}[args.gemm_mode],
         "config": run_config(args, work, world),
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "prefetch": not args.no_prefetch,
