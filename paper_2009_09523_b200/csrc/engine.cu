@@ -162,7 +162,7 @@ struct vnt_engine {
     bool valid = false;
   } pf_next;
   std::vector<float*> X, D;
-  // 3xTF32 operand twins (hi = rna_tf32(x), lo = x - hi), only when split.
+  // split-fp16 operand twins (x 2^sigma = hi + lo, kernels_simt.cuh), only when split.
   bool split = false;
   // whole-node kernel for small all-FFMA models (kernels_node.cuh)
   bool node_path = false;

@@ -147,7 +147,7 @@ struct EpiArgs {
   // (multiple of Fmt::BKE; 0 = all of K at once) and the chunk sums are added in
   // fp32 registers in chunk order ("promotion").  tcgen05's TMEM accumulation
   // loses precision over long K chains (scripts/ubench_tf32_precision.cu:
-  // 3xTF32 at K = 4096 is 3e-5 of max|D| in one chain, 1.2e-6 in 128-column
+  // split-fp16 at K = 4096 is 1.5e-5 of max|D| in one chain, 6.3e-7 in 128-column
   // chunks vs 2.3e-6 for an fp32 FMA chain).  The first chunk of a tile is
   // kfirst long: while it runs, the epilogue of the previous tile (its
   // output stores, bursty across all SMs) still holds the other buffer.
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) m |= (nb + j < ep.N && v[j] > 0.f ? 1u : 0u) << j;
           ep.mask_out[(size_t)r * ep.ldm + nb / 32] = m;
         }
-        if (ep.out) {   // null: only the 3xTF32 twins are consumed
+        if (ep.out) {   // null: only the split-fp16 twins are consumed
           float* orow = ep.out + (size_t)r * ep.ldo + nb;
           if (nb + 32 <= ep.N) {
 #pragma unroll

@@ -33,6 +33,6 @@ struct GpuModel {
   int ndev = 0;
 };
 
-int engine_gemm_mode();  // VNT_GEMM_MODE env: auto|ffma|tf32|3xtf32
+int engine_gemm_mode();  // VNT_GEMM_MODE env: auto|ffma|tf32|3xf16 (3xtf32: old name)
 
 }  // namespace vnt::detail

@@ -3,7 +3,7 @@
 // vnt::Trainer.  Same config keys (unknown keys rejected), same outputs
 // (StepMetrics JSONL, params JSON {"layout","values"}), same --compare-against
 // semantics and exit codes (0 ok, 2 config/shape, 3 capacity, 4 divergence, 1
-// other).  Extension keys: "gemm_mode" (auto|ffma|tf32|3xtf32), "momentum".
+// other).  Extension keys: "gemm_mode" (auto|ffma|tf32|3xf16; 3xtf32 = 3xf16), "momentum".
 // The reference's `profile` / `solve` commands drive the cluster planner,
 // which is out of scope here.
 //
@@ -114,7 +114,7 @@ int gemm_mode_of(const std::string& s) {
   if (s == "auto") return VNT_GEMM_AUTO;
   if (s == "ffma") return VNT_GEMM_FFMA;
   if (s == "tf32") return VNT_GEMM_TF32;
-  if (s == "3xtf32") return VNT_GEMM_3XTF32;
+  if (s == "3xf16" || s == "3xtf32") return VNT_GEMM_3XF16;
   throw vnt::ConfigError("unknown gemm_mode: " + s);
 }
 
