@@ -1580,6 +1580,20 @@ void launch_sgd(vnt_engine* e, bool reduce_h16 = true) {
     e->launches++;
     return;
   }
+  // bias vectors: k_sgd_multi, one grid row per tensor (the same per-element
+  // update as k_sgd_vec), instead of a launch per layer
+  SgdMulti biases{};
+  int nb = 0;
+  uint64_t maxb = 1;
+  auto flush_biases = [&] {
+    if (!nb) return;
+    dim3 grid((unsigned)std::min<uint64_t>(ceil_div(maxb, 256), 64), (unsigned)nb);
+    k_sgd_multi<<<grid, 256, 0, s>>>(biases);
+    VNT_LAUNCH_CHECK();
+    e->launches++;
+    nb = 0;
+    maxb = 1;
+  };
   for (int l = 0; l < e->L; ++l) {
     for (int part = 0; part < 2; ++part) {
       const int t = 2 * l + part;
@@ -1624,14 +1638,19 @@ void launch_sgd(vnt_engine* e, bool reduce_h16 = true) {
         else if (TR == 128) k_sgd_weight<false, 128><<<grid, block, 0, s>>>(a);
         else k_sgd_weight<false><<<grid, block, 0, s>>>(a);
       } else {
+        // the biases of up to 2 kNodeMaxLayers layers in one launch (below)
         a.rows = 1;
         a.cols = (int)e->widths[l + 1];
-        k_sgd_vec<<<(unsigned)std::min<uint64_t>(ceil_div(a.cols, 256), 1024), 256, 0, s>>>(a);
+        biases.t[nb++] = a;
+        maxb = std::max<uint64_t>(maxb, (uint64_t)a.cols);
+        if (nb == 2 * kNodeMaxLayers || l == e->L - 1) flush_biases();
+        continue;
       }
       VNT_LAUNCH_CHECK();
       e->launches++;
     }
   }
+  flush_biases();
 }
 
 struct Readback {

@@ -389,7 +389,7 @@ struct SgdMulti {
 
 __global__ void __launch_bounds__(256) k_sgd_multi(const __grid_constant__ SgdMulti m) {
   const SgdArgs& a = m.t[blockIdx.y];
-  if (block_poisoned(a.tail, a.ntail_flags)) return;
+  if (block_poisoned(a.tail, a.ntail_flags, a.sp, a.h16max, a.h16n)) return;
   const size_t n = (size_t)a.rows * a.cols;
   double mx = 0.0;
   for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
