@@ -1581,7 +1581,7 @@ void launch_sgd(vnt_engine* e, bool reduce_h16 = true) {
     return;
   }
   // bias vectors: k_sgd_multi, one grid row per tensor (the same per-element
-  // update as k_sgd_vec), instead of a launch per layer
+  // update, sgd_one), instead of a launch per layer
   SgdMulti biases{};
   int nb = 0;
   uint64_t maxb = 1;

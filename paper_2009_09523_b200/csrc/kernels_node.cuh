@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kNodeThreads) k_node_step(NodeArgs a) {
 }
 
 // SGD of every tensor of a small model in one launch (blockIdx.y = tensor):
-// k_sgd_vec's arithmetic on each flat tensor, plus the padded weight image the
+// sgd_one's arithmetic on each flat tensor (the layered path's bias vectors too), plus the padded weight image the
 // whole-node kernel stages (no transposed copy is kept).
 struct SgdMulti {
   SgdArgs t[2 * kNodeMaxLayers];

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_sgd_shard(ShardSgdArgs a) {
   for (long long i = a.lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.hi; i += stride) {
     const long long k = i - a.lo;
     const bool bias = i >= a.nw;
-    // same operation order as k_sgd_weight / k_sgd_vec (bitwise identical update)
+    // same operation order as k_sgd_weight / k_sgd_twins / sgd_one (bitwise identical update)
     const double g = __dmul_rn(__ll2double_rn(a.Gs[k]) * (bias ? isb : isw), inv_b);
     double u = g;
     if constexpr (MOM) {

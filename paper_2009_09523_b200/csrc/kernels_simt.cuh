@@ -1237,19 +1237,6 @@ __global__ void __launch_bounds__(256, 2) k_sgd_twins(SgdArgs a) {
   }
 }
 
-__global__ void k_sgd_vec(SgdArgs a) {
-  if (block_poisoned(a.tail, a.ntail_flags, a.sp, a.h16max, a.h16n)) return;
-  const size_t n = (size_t)a.rows * a.cols;
-  double mx = 0.0;
-  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
-       k += (size_t)gridDim.x * blockDim.x) {
-    float w32;
-    mx = fmax(mx, sgd_one(a, k, w32));
-    a.w32[k] = w32;
-  }
-  block_max_to(a.gmax, mx);
-}
-
 // fp64 master -> fp32 working copies (set_params / resize seeding).
 __global__ void k_refresh_weight(const double* __restrict__ w64, float* __restrict__ w32,
                                  float* __restrict__ wt32, int rows, int cols) {
