@@ -618,8 +618,6 @@ void resplit_weight_twins(vnt_engine* e) {
     if (!e->tc_layer[l]) continue;
     const size_t n = e->widths[l] * e->widths[l + 1];
     split_into(e, e->w32 + e->woff[l], e->w32h + e->woff[l], e->w32l + e->woff[l], n, op, vntb::kTailH16W);
-    split_into(e, e->wt32 + e->wtoff[l], e->wt32h + e->wtoff[l], e->wt32l + e->wtoff[l], n, op,
-               vntb::kTailH16W);
   }
 }
 
@@ -1447,8 +1445,7 @@ void await_layer_weights(vnt_engine* e, int l) {
   // the twins feed this step: their range flag is the redo slot kTailH16
   const vntb::Twin16 tw = twins_only ? twin_of(e, e->w32h + wo, e->w32l + wo, h16_op_w(e)) : vntb::Twin16{};
   k_expand_weight<<<grid, block, 0, s>>>(src, rows, cols, twins_only ? nullptr : e->w32 + wo,
-                                         twins_only ? nullptr : e->wt32 + to, tw,
-                                         twins_only ? e->wt32h + to : nullptr, twins_only ? e->wt32l + to : nullptr);
+                                         e->tc_layer[l] ? nullptr : e->wt32 + to, tw, nullptr, nullptr);
   VNT_LAUNCH_CHECK();
   k_expand_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, s>>>(src + (size_t)rows * cols, cols, e->w32 + bo);
   VNT_LAUNCH_CHECK();
@@ -1604,14 +1601,13 @@ void launch_sgd(vnt_engine* e, bool reduce_h16 = true) {
       a.G = e->G + off;
       // a split-fp16 layer's weight GEMMs read only the twins (written for
       // the next step: their range flag is kTailH16W, not a redo of this one)
+      // Wᵀ (fp32) only for a non-tcgen05 layer (the skinny / FFMA forward)
       const bool twins_only = part == 0 && e->split && e->tc_layer[l];
       a.w32 = twins_only ? nullptr : e->w32 + off;
-      a.wt32 = (part || twins_only) ? nullptr : e->wt32 + e->wtoff[l];
+      a.wt32 = (part || e->tc_layer[l]) ? nullptr : e->wt32 + e->wtoff[l];
       if (twins_only) {
         a.w32h = e->w32h + off;
         a.w32l = e->w32l + off;
-        a.wt32h = e->wt32h + e->wtoff[l];
-        a.wt32l = e->wt32l + e->wtoff[l];
         a.wtw = twin_of(e, a.w32h, a.w32l, h16_op_w(e), vntb::kTailH16W);
       }
       a.gout = e->gout ? e->gout + off : nullptr;
@@ -2210,8 +2206,7 @@ int vnt_engine_create(const vnt_model_desc* model, const vnt_engine_options* opt
     if (e->split) {
       e->w32h = (__half*)dalloc(e->P * sizeof(__half));
       e->w32l = (__half*)dalloc(e->P * sizeof(__half));
-      e->wt32h = (__half*)dalloc(toff * sizeof(__half));
-      e->wt32l = (__half*)dalloc(toff * sizeof(__half));
+      // no Wᵀ twins: the forward reads W [in][out] as an MN-major operand
     }
     // split-fp16 scales before any history: activations |x| < 2^7, deltas
     // |d| < 2^5 (larger values flag kTailH16 and the step is redone at the

@@ -250,8 +250,8 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 // Instruction descriptor: kind::tf32, D fp32, A/B tf32, K-major (fwd /
 // bwd-data) or MN-major (dW: bits 15/16; both operands are the row-major
 // activations / deltas themselves, K = rows).
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool mn_major = false) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (mn_major ? (3u << 15) : 0u) |
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn = false, bool b_mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
@@ -269,8 +269,9 @@ __device__ __forceinline__ uint64_t sdesc_sw128_mn16(uint32_t saddr) {
 }
 
 // Instruction descriptor: kind::f16, D fp32, A/B fp16.
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool mn_major = false) {
-  return (1u << 4) | (mn_major ? (3u << 15) : 0u) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool a_mn = false, bool b_mn = false) {
+  return (1u << 4) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 
 // MN-major tf32 operand: the only smem layout tcgen05 takes for it is the
@@ -326,8 +327,8 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr) {
 }
 
 template <int SPLIT>
-__host__ __device__ constexpr uint32_t idesc_of(int M, int N, bool mn_major) {
-  return SPLIT == 3 ? idesc_f16(M, N, mn_major) : idesc_tf32(M, N, mn_major);
+__host__ __device__ constexpr uint32_t idesc_of(int M, int N, bool a_mn, bool b_mn) {
+  return SPLIT == 3 ? idesc_f16(M, N, a_mn, b_mn) : idesc_tf32(M, N, a_mn, b_mn);
 }
 
 // Epilogue side of the split-fp16 outputs: this thread's max |x| (and the
@@ -490,11 +491,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kl; k += BKE) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             mbar_expect_tx(&full[stage], C::kStageBytes);
+            // A: MN-major for the dW (BKE rows of the row-major X per stage,
+            // GW-feature 128-B groups F::kGroupBytes apart: one 3-D box when the
+            // width allows, ep.mn3 bit 0, else a 2-D box per group), K-major
+            // otherwise; B: MN-major for the dW (D) and the forward (W [in][out]
+            // itself: no transposed copy), K-major for the bwd-data.
             if constexpr (EPI == kTcDw) {
-              // MN-major: BKE rows of the row-major X / D per stage, GW-feature
-              // (128-B) groups F::kGroupBytes apart — one 3-D box per operand
-              // when the width is a multiple of GW (ep.mn3 bit 0: A, bit 1:
-              // B), else one 2-D box per group (zero fill past the width)
               if (ep.mn3 & 1) {
                 tma_load_3d(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / GW);
                 if (SPLIT == 3) tma_load_3d(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / GW);
@@ -507,6 +509,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 kb + k);
                 }
               }
+            } else {
+              tma_load_2d(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
+              if (SPLIT == 3) tma_load_2d(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
+            }
+            if constexpr (EPI != kTcBwd) {
               if (ep.mn3 & 2) {
                 tma_load_3d(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / GW);
                 if (SPLIT == 3) tma_load_3d(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / GW);
@@ -520,12 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             } else {
-              tma_load_2d(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
               tma_load_2d(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
-              if (SPLIT == 3) {
-                tma_load_2d(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
-                tma_load_2d(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
-              }
+              if (SPLIT == 3) tma_load_2d(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -539,7 +542,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     regs_dec();
     {
-      constexpr uint32_t idesc = idesc_of<SPLIT>(BM, BN, EPI == kTcDw);
+      constexpr bool a_mn = EPI == kTcDw, b_mn = EPI != kTcBwd;   // operand majors (producer above)
+      constexpr uint32_t idesc = idesc_of<SPLIT>(BM, BN, a_mn, b_mn);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;  // global (tile, segment) counter
@@ -560,24 +564,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full[stage], phase);
 #endif
             tc_fence_after();
-            constexpr bool mn = EPI == kTcDw;
-            const uint64_t ad = mn ? sdesc_mn<SPLIT>(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
-            const uint64_t bd = mn ? sdesc_mn<SPLIT>(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
-            const uint64_t ald = mn ? sdesc_mn<SPLIT>(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
-            const uint64_t bld = mn ? sdesc_mn<SPLIT>(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
+            const uint64_t ad = a_mn ? sdesc_mn<SPLIT>(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
+            const uint64_t bd = b_mn ? sdesc_mn<SPLIT>(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
+            const uint64_t ald = a_mn ? sdesc_mn<SPLIT>(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
+            const uint64_t bld = b_mn ? sdesc_mn<SPLIT>(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
             // dW: a node's K-chain is its rows rounded up to kNodeRowPad (K
             // steps past that are rows of the next node: skipped); a K step
             // is KSTEP 128-B rows (MN-major), 32 B inside the row (K-major)
             constexpr int KS = F::KSTEP;
-            const int ksteps = mn ? min(BKE, kl - k) / KS : BKE / KS;
+            const int ksteps = EPI == kTcDw ? min(BKE, kl - k) / KS : BKE / KS;
 #pragma unroll
             for (int kk = 0; kk < BKE / KS; ++kk) {
               if (kk >= ksteps) break;
-              const uint64_t o = (uint64_t)(mn ? kk * KS * 8 : kk * 2);
-              mma_op<SPLIT>(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+              const uint64_t oa = (uint64_t)(a_mn ? kk * KS * 8 : kk * 2);
+              const uint64_t ob = (uint64_t)(b_mn ? kk * KS * 8 : kk * 2);
+              mma_op<SPLIT>(d, ad + oa, bd + ob, idesc, (k > 0 || kk > 0) ? 1u : 0u);
               if (SPLIT == 3) {
-                mma_op<SPLIT>(d, ad + o, bld + o, idesc, 1u);
-                mma_op<SPLIT>(d, ald + o, bd + o, idesc, 1u);
+                mma_op<SPLIT>(d, ad + oa, bld + ob, idesc, 1u);
+                mma_op<SPLIT>(d, ald + oa, bd + ob, idesc, 1u);
               }
             }
             mma_commit(&empty[stage]);
@@ -1042,10 +1046,15 @@ void tc_forward(vnt_engine* e, int l, int rows, bool last) {
   const uint32_t bn = pair ? PairCfg<kTcFwd>::BNH : TileCfg<kTcFwd>::BN;
   const uint64_t lda = l == 0 ? e->ld0 : (uint64_t)K;
   const OpMaps a = op_maps(e, e->X[l], e->Xh[l], e->Xl[l], rows, K, lda, BM);
-  const uint64_t wo = e->wtoff[l];
-  const OpMaps b = op_maps(e, e->wt32 + wo, e->split ? e->wt32h + wo : nullptr,
-                           e->split ? e->wt32l + wo : nullptr, N, K, K, bn);
+  // B = W [in][out] itself as an MN-major operand (K = in rows, out features
+  // contiguous): the forward needs no transposed copy of the weights
+  const uint64_t wo = e->woff[l];
+  const uint32_t gw = (uint32_t)tc_bke(e);
+  const bool b3 = N % gw == 0 && tc_mn3();
+  const OpMaps b = op_maps(e, e->w32 + wo, e->split ? e->w32h + wo : nullptr, e->split ? e->w32l + wo : nullptr,
+                           (uint64_t)K, (uint64_t)N, (uint64_t)N, gw, true, b3 ? bn / gw : 0);
   EpiArgs ep{};
+  ep.mn3 = b3 ? 2 : 0;
   ep.M = rows;
   ep.N = N;
   ep.bias = e->w32 + e->boff[l];

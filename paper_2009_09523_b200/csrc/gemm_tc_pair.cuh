@@ -222,41 +222,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kl; k += BKE) {
             TC_PROBE_WAIT(mbar_wait(&empty[stage], phase ^ 1));
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+            // A: MN-major for the dW (BKE rows of the row-major X per stage,
+            // GW-feature 128-B groups F::kGroupBytes apart: one 3-D box when the
+            // width allows, ep.mn3 bit 0, else a 2-D box per group), K-major
+            // otherwise; B: MN-major for the dW (D) and the forward (W [in][out]
+            // itself: no transposed copy), K-major for the bwd-data.
             if constexpr (EPI == kTcDw) {
-              // MN-major: BKE rows of the row-major X / D per stage (see k_gemm_tc)
               if (ep.mn3 & 1) {
                 tma_load_3d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], 0, kb + k, m0 / GW);
                 if (SPLIT == 3) tma_load_3d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], 0, kb + k, m0 / GW);
               } else {
 #pragma unroll
                 for (int g = 0; g < BM / GW; ++g) {
-                  tma_load_2d_pair(sA + stage * C::kBytesA + g * F::kGroupBytes, &tmA, &full[stage], m0 + GW * g,
-                                   kb + k);
+                  tma_load_2d_pair(sA + stage * C::kBytesA + g * F::kGroupBytes, &tmA, &full[stage], m0 + GW * g, kb + k);
                   if (SPLIT == 3)
-                    tma_load_2d_pair(sAl + stage * C::kBytesA + g * F::kGroupBytes, &tmAl, &full[stage],
-                                     m0 + GW * g, kb + k);
+                    tma_load_2d_pair(sAl + stage * C::kBytesA + g * F::kGroupBytes, &tmAl, &full[stage], m0 + GW * g,
+                                kb + k);
                 }
               }
+            } else {
+              tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
+              if (SPLIT == 3) tma_load_2d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
+            }
+            if constexpr (EPI != kTcBwd) {
               if (ep.mn3 & 2) {
                 tma_load_3d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], 0, kb + k, n0 / GW);
                 if (SPLIT == 3) tma_load_3d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], 0, kb + k, n0 / GW);
               } else {
 #pragma unroll
                 for (int g = 0; g < BNH / GW; ++g) {
-                  tma_load_2d_pair(sB + stage * C::kBytesB + g * F::kGroupBytes, &tmB, &full[stage], n0 + GW * g,
-                                   kb + k);
+                  tma_load_2d_pair(sB + stage * C::kBytesB + g * F::kGroupBytes, &tmB, &full[stage], n0 + GW * g, kb + k);
                   if (SPLIT == 3)
-                    tma_load_2d_pair(sBl + stage * C::kBytesB + g * F::kGroupBytes, &tmBl, &full[stage],
-                                     n0 + GW * g, kb + k);
+                    tma_load_2d_pair(sBl + stage * C::kBytesB + g * F::kGroupBytes, &tmBl, &full[stage], n0 + GW * g,
+                                kb + k);
                 }
               }
             } else {
-              tma_load_2d_pair(sA + stage * C::kBytesA, &tmA, &full[stage], kb + k, m0);
               tma_load_2d_pair(sB + stage * C::kBytesB, &tmB, &full[stage], kb + k, n0);
-              if (SPLIT == 3) {
-                tma_load_2d_pair(sAl + stage * C::kBytesA, &tmAl, &full[stage], kb + k, m0);
-                tma_load_2d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
-              }
+              if (SPLIT == 3) tma_load_2d_pair(sBl + stage * C::kBytesB, &tmBl, &full[stage], kb + k, n0);
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -270,7 +273,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     regs_dec();
     if (rank == 0) {
-      constexpr uint32_t idesc = idesc_of<SPLIT>(PM, BN, EPI == kTcDw);
+      constexpr bool a_mn = EPI == kTcDw, b_mn = EPI != kTcBwd;   // operand majors (producer above)
+      constexpr uint32_t idesc = idesc_of<SPLIT>(PM, BN, a_mn, b_mn);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;
@@ -291,21 +295,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], phase);
 #endif
           tc_fence_after();
-          constexpr bool mn = EPI == kTcDw;
-          const uint64_t ad = mn ? sdesc_mn<SPLIT>(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
-          const uint64_t bd = mn ? sdesc_mn<SPLIT>(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
-          const uint64_t ald = mn ? sdesc_mn<SPLIT>(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
-          const uint64_t bld = mn ? sdesc_mn<SPLIT>(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
+          const uint64_t ad = a_mn ? sdesc_mn<SPLIT>(su32(sA + stage * C::kBytesA)) : sdesc_sw128(su32(sA + stage * C::kBytesA));
+          const uint64_t bd = b_mn ? sdesc_mn<SPLIT>(su32(sB + stage * C::kBytesB)) : sdesc_sw128(su32(sB + stage * C::kBytesB));
+          const uint64_t ald = a_mn ? sdesc_mn<SPLIT>(su32(sAl + stage * C::kBytesA)) : sdesc_sw128(su32(sAl + stage * C::kBytesA));
+          const uint64_t bld = b_mn ? sdesc_mn<SPLIT>(su32(sBl + stage * C::kBytesB)) : sdesc_sw128(su32(sBl + stage * C::kBytesB));
           constexpr int KS = F::KSTEP;
-          const int ksteps = mn ? min(BKE, kl - k) / KS : BKE / KS;   // dW: node rows rounded to kNodeRowPad
+          // dW: node rows rounded to kNodeRowPad (K steps past them are the next node's rows)
+          const int ksteps = EPI == kTcDw ? min(BKE, kl - k) / KS : BKE / KS;
 #pragma unroll
           for (int kk = 0; kk < BKE / KS; ++kk) {
             if (kk >= ksteps) break;
-            const uint64_t o = (uint64_t)(mn ? kk * KS * 8 : kk * 2);
-            mma_op_pair<SPLIT>(d, ad + o, bd + o, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            // a K step: KS 128-B rows (MN-major), 32 B inside the row (K-major)
+            const uint64_t oa = (uint64_t)(a_mn ? kk * KS * 8 : kk * 2);
+            const uint64_t ob = (uint64_t)(b_mn ? kk * KS * 8 : kk * 2);
+            mma_op_pair<SPLIT>(d, ad + oa, bd + ob, idesc, (k > 0 || kk > 0) ? 1u : 0u);
             if (SPLIT == 3) {
-              mma_op_pair<SPLIT>(d, ad + o, bld + o, idesc, 1u);
-              mma_op_pair<SPLIT>(d, ald + o, bd + o, idesc, 1u);
+              mma_op_pair<SPLIT>(d, ad + oa, bld + ob, idesc, 1u);
+              mma_op_pair<SPLIT>(d, ald + oa, bd + ob, idesc, 1u);
             }
           }
           mma_commit_pair(&empty[stage]);

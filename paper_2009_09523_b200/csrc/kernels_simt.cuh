@@ -1016,7 +1016,7 @@ struct SgdArgs {
   float* w32;
   float* wt32;          // transposed copy (weights only) or nullptr
   __half *w32h, *w32l;   // split-fp16 twins of w32 (or nullptr)
-  __half *wt32h, *wt32l; // split-fp16 twins of wt32 (or nullptr)
+  __half *wt32h, *wt32l; // split-fp16 twins of wt32 (unused: the forward reads W MN-major)
   Twin16 wtw;            // the weights' scale, max and range slot (kTailH16W)
   double* gout;         // optional mean-gradient export
   unsigned long long* gmax;  // max |g| of this tensor (bit pattern of a positive double)
@@ -1160,15 +1160,14 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
   }
 }
 
-// Weight tensor of a tcgen05 layer (only its split-fp16 twins are consumed):
-// 64x64 tiles, 32x8 threads, each thread two adjacent columns x 8 rows (16-B
-// loads of S and w), the row-major twins as half2 and the transposed twins
-// through an smem tile as half2 pairs of rows (128 B per warp store).  Same
+// Weight tensor of a tcgen05 layer (only its split-fp16 twins are consumed,
+// by the forward as an MN-major operand and by the bwd-data K-major: no
+// transposed copy): 64x64 tiles, 32x8 threads, each thread two adjacent
+// columns x 8 rows (16-B loads of S and w), the twins as half2.  Same
 // per-element arithmetic as k_sgd_weight (same bits).  rows, cols even.
 template <bool MOM>
 __global__ void __launch_bounds__(256, 2) k_sgd_twins(SgdArgs a) {
   constexpr int TR = 64, TC = 64, PER = TR / 8;
-  __shared__ float tile[TR][TC + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int c = c0 + 2 * tx;
@@ -1203,8 +1202,6 @@ __global__ void __launch_bounds__(256, 2) k_sgd_twins(SgdArgs a) {
     const double n0 = __dsub_rn(w[k].x, __dmul_rn(lr, u0));
     const double n1 = __dsub_rn(w[k].y, __dmul_rn(lr, u1));
     const float f0 = __double2float_rn(n0), f1 = __double2float_rn(n1);
-    tile[ty + 8 * k][2 * tx] = ok ? f0 : 0.f;
-    tile[ty + 8 * k][2 * tx + 1] = ok ? f1 : 0.f;
     if (ok) {
       const size_t idx = (size_t)r * a.cols + c;
       *reinterpret_cast<double2*>(a.w64 + idx) = make_double2(n0, n1);
@@ -1221,20 +1218,6 @@ __global__ void __launch_bounds__(256, 2) k_sgd_twins(SgdArgs a) {
   }
   twin_flush(a.wtw, wm, wmul);
   block_max_to(a.gmax, mx);
-  __syncthreads();
-  // transposed twins WT[col][row]: warp ty takes columns ty, ty + 8, ...; lane
-  // tx the row pair (2 tx, 2 tx + 1)
-#pragma unroll
-  for (int k = 0; k < TC / 8; ++k) {
-    const int cc = ty + 8 * k, col = c0 + cc, r = r0 + 2 * tx;
-    if (col >= a.cols || r >= a.rows) continue;
-    const float s0 = tile[2 * tx][cc] * wmul, s1 = tile[2 * tx + 1][cc] * wmul;
-    const __half2 hh = __floats2half2_rn(s0, s1);
-    const float2 hf = __half22float2(hh);
-    const size_t o = (size_t)col * a.rows + r;
-    *reinterpret_cast<__half2*>(a.wt32h + o) = hh;
-    *reinterpret_cast<__half2*>(a.wt32l + o) = __floats2half2_rn(s0 - hf.x, s1 - hf.y);
-  }
 }
 
 // fp64 master -> fp32 working copies (set_params / resize seeding).
