@@ -182,7 +182,7 @@ struct vnt_engine {
   // relu' of X[l] as bits [rows][mask_ld(l)] when both the producing forward
   // and the consuming bwd-data of X[l] run on tcgen05 (relu_mask(l))
   std::vector<uint32_t*> Mk;
-  __half *w32h = nullptr, *w32l = nullptr, *wt32h = nullptr, *wt32l = nullptr;
+  __half *w32h = nullptr, *w32l = nullptr;
   // split-fp16 operand scales: sigma per operand tensor (X[l] at l, D[l] at
   // L+1+l, all weights at 2L+2), chosen from the previous step's global max|x|
   // (h16max: one word per operand after gmax, max-reduced across ranks)
@@ -1445,7 +1445,7 @@ void await_layer_weights(vnt_engine* e, int l) {
   // the twins feed this step: their range flag is the redo slot kTailH16
   const vntb::Twin16 tw = twins_only ? twin_of(e, e->w32h + wo, e->w32l + wo, h16_op_w(e)) : vntb::Twin16{};
   k_expand_weight<<<grid, block, 0, s>>>(src, rows, cols, twins_only ? nullptr : e->w32 + wo,
-                                         e->tc_layer[l] ? nullptr : e->wt32 + to, tw, nullptr, nullptr);
+                                         e->tc_layer[l] ? nullptr : e->wt32 + to, tw);
   VNT_LAUNCH_CHECK();
   k_expand_vec<<<(unsigned)ceil_div(cols, 256), 256, 0, s>>>(src + (size_t)rows * cols, cols, e->w32 + bo);
   VNT_LAUNCH_CHECK();
@@ -2293,7 +2293,7 @@ void vnt_engine_destroy(vnt_engine* e) {
   for (auto& kv : e->plans)
     for (auto& p : kv.second) cudaFree(p.d_meta);
   for (auto* p : e->scratch) cudaFree(p);
-  for (void* p : {(void*)e->w32h, (void*)e->w32l, (void*)e->wt32h, (void*)e->wt32l})
+  for (void* p : {(void*)e->w32h, (void*)e->w32l})
     if (p) cudaFree(p);
   for (auto* v : {&e->Xh, &e->Xl, &e->Dh, &e->Dl})
     for (auto* p : *v)

@@ -67,11 +67,10 @@ __global__ void k_f64_to_f32(const double* __restrict__ src, float* __restrict__
 }
 
 // Gathered fp32 weight [rows][cols] -> row-major copy and split-fp16 twins,
-// transposed copy and twins (each output nullable), 32x32 tiles through smem.
+// transposed fp32 copy (each output nullable), 32x32 tiles through smem.
 // The twins' range flag is tw.flag (kTailH16: these twins feed this step).
 __global__ void k_expand_weight(const float* __restrict__ src, int rows, int cols,
-                                float* __restrict__ w32, float* __restrict__ wt32, Twin16 tw,
-                                __half* __restrict__ wt32h, __half* __restrict__ wt32l) {
+                                float* __restrict__ w32, float* __restrict__ wt32, Twin16 tw) {
   __shared__ float tile[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
@@ -93,7 +92,7 @@ __global__ void k_expand_weight(const float* __restrict__ src, int rows, int col
     tile[ty + 8 * k][tx] = v;
   }
   if (tw.hi) twin_flush(tw, m, mul);
-  if (!wt32 && !wt32h) return;
+  if (!wt32) return;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -101,8 +100,7 @@ __global__ void k_expand_weight(const float* __restrict__ src, int rows, int col
     if (r < rows && c < cols) {
       const float v = tile[tx][ty + 8 * k];
       const size_t o = (size_t)c * rows + r;
-      if (wt32) wt32[o] = v;
-      if (wt32h) put16(wt32h, wt32l, o, v, mul);
+      wt32[o] = v;
     }
   }
 }

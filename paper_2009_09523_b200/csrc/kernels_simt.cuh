@@ -1016,7 +1016,6 @@ struct SgdArgs {
   float* w32;
   float* wt32;          // transposed copy (weights only) or nullptr
   __half *w32h, *w32l;   // split-fp16 twins of w32 (or nullptr)
-  __half *wt32h, *wt32l; // split-fp16 twins of wt32 (unused: the forward reads W MN-major)
   Twin16 wtw;            // the weights' scale, max and range slot (kTailH16W)
   double* gout;         // optional mean-gradient export
   unsigned long long* gmax;  // max |g| of this tensor (bit pattern of a positive double)
@@ -1139,7 +1138,7 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
   }
   if (a.w32h) twin_flush(a.wtw, wm, wmul);
   block_max_to(a.gmax, mx);
-  if (!a.wt32 && !a.wt32h) return;
+  if (!a.wt32) return;
   __syncthreads();
   // transposed: WT[c][r], 32 columns x TR rows -> each warp row writes TR contiguous rows
 #pragma unroll
@@ -1153,8 +1152,7 @@ __global__ void __launch_bounds__(256, MOM ? 2 : (TR <= 32 ? 4 : 3)) k_sgd_weigh
       if (r < a.rows) {
         const float v = tile[h * 32 + tx][cc];
         const size_t o = (size_t)col * a.rows + r;
-        if (a.wt32) a.wt32[o] = v;
-        if (a.wt32h) put16(a.wt32h, a.wt32l, o, v, wmul);
+        a.wt32[o] = v;
       }
     }
   }
