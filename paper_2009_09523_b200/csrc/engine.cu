@@ -100,7 +100,7 @@ struct vnt_engine {
   // Sharded update (comm && layered path): layer l's gradient
   // slice is reduce-scattered into Gs, this rank updates its 1/G of the
   // parameters, and the new fp32 weights are all-gathered (deferred to the
-  // next step's forward, layer by layer) and expanded into W / Wᵀ / twins.
+  // next step's forward, layer by layer) and expanded into W's twins (or W / Wᵀ).
   bool shard = false;
   std::vector<uint64_t> sh_c, sh_lo, sh_hi, sh_soff, sh_aoff;   // per layer
   long long* Gs = nullptr;        // reduced chunks, sum_l c_l

@@ -7,7 +7,8 @@
 //   k_sgd_shard    exact mean (double(S) 2^-s / B), SGD / momentum on the fp64
 //                  master, the new fp32 weights into the all-gather send chunk;
 //   k_expand_*     after the all-gather of those chunks: the fp32 copies the
-//                  GEMMs read (W, Wᵀ or their split-fp16 hi/lo twins, bias),
+//                  GEMMs read (a tcgen05 layer: W's split-fp16 hi/lo twins;
+//                  other layers: W and Wᵀ; the bias),
 //                  the same bits the unsharded k_sgd_weight writes.
 #pragma once
 
