@@ -628,7 +628,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) v[j] *= unscale;
         }
         if (EPI == kTcBwd && ep.mask_in) {
-          const uint32_t m = __ldg(ep.mask_in + (size_t)r * ep.ldm + nb / 32);
+          // (a chunk past the width has no mask word: the row holds ldm words)
+          const uint32_t m = nb < ep.N ? __ldg(ep.mask_in + (size_t)r * ep.ldm + nb / 32) : 0u;
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= ((m >> j) & 1u) ? 1.f : 0.f;   // relu' (model.cpp:336)
         } else if (EPI == kTcBwd && nb + 32 <= ep.N) {
@@ -653,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (EPI == kTcFwd && ep.mask_out) {
+        if (EPI == kTcFwd && ep.mask_out && nb < ep.N) {   // the row's ldm words cover [0, N) only
           uint32_t m = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) m |= (nb + j < ep.N && v[j] > 0.f ? 1u : 0u) << j;

@@ -367,7 +367,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       if constexpr (EPI == kTcBwd) {
-        if (ep.mask_in && r < ep.M) {
+        // (a column half past the width has no mask words: the row holds ldm
+        // = round_up(ceil(N / 32), 4) words)
+        if (ep.mask_in && r < ep.M && n0 + h * COLS < ep.N) {
           const uint4 w = __ldg(reinterpret_cast<const uint4*>(ep.mask_in + (size_t)r * ep.ldm + (n0 + h * COLS) / 32));
           mk01 = (unsigned long long)w.x | ((unsigned long long)w.y << 32);
           mk23 = (unsigned long long)w.z | ((unsigned long long)w.w << 32);
@@ -435,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         FIN_MARK(12);
         if constexpr (EPI == kTcFwd) {
-          if (ep.mask_out && r < ep.M) {
+          if (ep.mask_out && r < ep.M && nb < ep.N) {   // the row's ldm words cover [0, N) only
             uint32_t m = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) m |= (nb + j < ep.N && v[j] > 0.f ? 1u : 0u) << j;

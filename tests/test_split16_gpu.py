@@ -134,3 +134,35 @@ def test_weight_scale_follows_a_jump(port, monkeypatch, force_comm):
     assert err < 2e-5
     assert abs(loss_sum / ex - want_loss) < 2e-6 * abs(want_loss)
     e.close()
+
+
+def test_many_layers_bias_batches(port):
+    """19 tcgen05 layers: the bias vectors are updated in batches of 16 per
+    k_sgd_multi launch; a step's update equals lr x the fp64 oracle's gradient
+    (fp32 tier) for every tensor, biases included.  (A first step calibrates
+    the fixed-point scales: the deep relu stack's early gradients are far
+    below the step-0 estimate max|g| = 1.)"""
+    w = [64] * 19 + [10]
+    sizes = np.array([32, 32, 16, 48], np.uint64)
+    dev = np.zeros(len(sizes), np.int32)
+    B = int(sizes.sum())
+    x, y = port.synth_batch(8, 2048, w[0], w[-1], 0, B)
+    e = engine(port, widths=w, seed=5)
+    lr = 1e-6
+    e.train_step(x, y, sizes, dev, lr)
+    p1 = e.get_params()
+    want, want_loss = port.forward_backward(w, "relu", "softmax-cross-entropy", p1, x, y)
+    loss, _ = e.train_step(x, y, sizes, dev, lr)
+    g = (p1 - e.get_params()) / lr
+    off = 0
+    worst = 0.0
+    for l in range(len(w) - 1):
+        for n in (w[l] * w[l + 1], w[l + 1]):
+            m = np.abs(want[off:off + n]).max()
+            if m > 0:
+                worst = max(worst, float(np.abs(g[off:off + n] - want[off:off + n]).max() / m))
+            off += n
+    print(f"19 layers: worst per-tensor rel grad err {worst:.2e}, loss {loss:.9f} vs {want_loss:.9f}")
+    assert worst < 2e-5
+    assert abs(loss - want_loss) < 2e-6 * abs(want_loss)
+    e.close()
