@@ -166,3 +166,22 @@ def test_many_layers_bias_batches(port):
     assert worst < 2e-5
     assert abs(loss - want_loss) < 2e-6 * abs(want_loss)
     e.close()
+
+
+@pytest.mark.parametrize("w", [[72, 136, 88, 10], [64, 96, 64, 72, 10]])
+def test_ragged_widths(port, w):
+    """Hidden widths that are multiples of 8 but not of the 64-feature TMA
+    group or the 256-column tile (2-D operand boxes, partial relu-mask words,
+    clipped epilogue stores): fp32-tier gradient against the oracle."""
+    sizes = np.array([40, 24, 48, 16], np.uint64)
+    x, y = port.synth_batch(11, 2048, w[0], w[-1], 0, 128)
+    p0 = port.init_params(w, 2)
+    want, want_loss = port.forward_backward(w, "relu", "softmax-cross-entropy", p0, x, y)
+    e = engine(port, widths=w, seed=2)
+    e.device_step(0, x, y, sizes)
+    g, loss_sum, ex = e.sync()
+    err = np.abs(g - want).max() / np.abs(want).max()
+    print(f"widths {w}: rel grad err {err:.2e}")
+    assert err < 2e-5
+    assert abs(loss_sum / ex - want_loss) < 2e-6 * abs(want_loss)
+    e.close()
