@@ -659,6 +659,12 @@ struct BackSkinny {
                   const int* row0, const int* nrows, int nn, float* Dout, vntb::Twin16 twins,
                   const float* scale_w, long long* Gw, int tw, const float* scale_b, long long* Gb, int tb,
                   float lim, long long* tail) {
+    if (in % 2 == 0) {   // two features per thread (same bits)
+      dim3 grid((unsigned)ceil_div(in, 256), (unsigned)nn);
+      k_skinny_backward2<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, twins, scale_w, Gw,
+                                                  tw, scale_b, Gb, tb, lim, tail);
+      return;
+    }
     dim3 grid((unsigned)ceil_div(in, 128), (unsigned)nn);
     k_skinny_backward<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, twins, scale_w, Gw,
                                                tw, scale_b, Gb, tb, lim, tail);

@@ -1003,6 +1003,125 @@ __global__ void __launch_bounds__(128) k_skinny_backward(
   }
 }
 
+// k_skinny_backward with two adjacent input features per thread (in even):
+// float2 loads of X, the D twins as half2, the dn rows read once for both —
+// the same per-feature operation order, so the same bits.
+template <int NO>
+__global__ void __launch_bounds__(128) k_skinny_backward2(
+    const float* __restrict__ X, const float* __restrict__ Dn, const float* __restrict__ W, int in, int no,
+    int act, const int* __restrict__ vn_row0, const int* __restrict__ vn_rows, float* __restrict__ Dout,
+    Twin16 twd, const float* __restrict__ scale_w, long long* __restrict__ Gw, int tw,
+    const float* __restrict__ scale_b, long long* __restrict__ Gb, int tb, float lim,
+    long long* __restrict__ tail) {
+  static_assert(NO % 4 == 0, "dn rows are read as float4");
+  __shared__ __align__(16) float dn[64][NO];
+  const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int v = blockIdx.y;
+  const int r0 = vn_row0[v], n = vn_rows[v];
+  const bool data = Gb != nullptr;
+  const float mul = twd.hi ? *twd.mul : 1.f;
+  float m = 0.f;
+  float w0[NO], w1[NO], g0[NO], g1[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    const bool ok = data && i < in && o < no;
+    w0[o] = ok ? __ldg(W + (size_t)i * no + o) : 0.f;
+    w1[o] = ok ? __ldg(W + (size_t)(i + 1) * no + o) : 0.f;
+    g0[o] = g1[o] = 0.f;
+  }
+  float db0 = 0.f, db1 = 0.f;
+  for (int c = 0; c < n; c += 64) {
+    const int cn = min(64, n - c);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cn * NO; k += blockDim.x)
+      dn[k / NO][k % NO] = (k % NO < no) ? Dn[(size_t)(r0 + c + k / NO) * no + k % NO] : 0.f;
+    __syncthreads();
+    if (i >= in) continue;
+    const float2* xp = reinterpret_cast<const float2*>(X + (size_t)(r0 + c) * in + i);
+    const size_t ld2 = (size_t)in / 2;
+    float2 an[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) an[j] = j < cn ? __ldg(xp + (size_t)j * ld2) : make_float2(0.f, 0.f);
+    for (int rr = 0; rr < cn; rr += 8) {
+      float2 a[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = an[j];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        an[j] = rr + 8 + j < cn ? __ldg(xp + (size_t)(rr + 8 + j) * ld2) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (rr + j >= cn) break;
+        const float4* d4 = reinterpret_cast<const float4*>(&dn[rr + j][0]);
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int o = 0; o < NO; o += 4) {
+          const float4 d = d4[o / 4];
+          g0[o] = fmaf(a[j].x, d.x, g0[o]);
+          g0[o + 1] = fmaf(a[j].x, d.y, g0[o + 1]);
+          g0[o + 2] = fmaf(a[j].x, d.z, g0[o + 2]);
+          g0[o + 3] = fmaf(a[j].x, d.w, g0[o + 3]);
+          g1[o] = fmaf(a[j].y, d.x, g1[o]);
+          g1[o + 1] = fmaf(a[j].y, d.y, g1[o + 1]);
+          g1[o + 2] = fmaf(a[j].y, d.z, g1[o + 2]);
+          g1[o + 3] = fmaf(a[j].y, d.w, g1[o + 3]);
+          acc0 = fmaf(d.x, w0[o], acc0);
+          acc0 = fmaf(d.y, w0[o + 1], acc0);
+          acc0 = fmaf(d.z, w0[o + 2], acc0);
+          acc0 = fmaf(d.w, w0[o + 3], acc0);
+          acc1 = fmaf(d.x, w1[o], acc1);
+          acc1 = fmaf(d.y, w1[o + 1], acc1);
+          acc1 = fmaf(d.z, w1[o + 2], acc1);
+          acc1 = fmaf(d.w, w1[o + 3], acc1);
+        }
+        if (data) {
+          const float dv0 = acc0 * act_grad_from_out(act, a[j].x);
+          const float dv1 = acc1 * act_grad_from_out(act, a[j].y);
+          const size_t idx = (size_t)(r0 + c + rr + j) * in + i;
+          if (Dout) *reinterpret_cast<float2*>(Dout + idx) = make_float2(dv0, dv1);
+          if (twd.hi) {
+            const float s0 = dv0 * mul, s1 = dv1 * mul;
+            const __half2 hh = __floats2half2_rn(s0, s1);
+            const float2 hf = __half22float2(hh);
+            *reinterpret_cast<__half2*>(twd.hi + idx) = hh;
+            *reinterpret_cast<__half2*>(twd.lo + idx) = __floats2half2_rn(s0 - hf.x, s1 - hf.y);
+            m = fmax_nan(m, fmax_nan(fabsf(dv0), fabsf(dv1)));
+          }
+          db0 += dv0;
+          db1 += dv1;
+        }
+      }
+    }
+  }
+  if (twd.hi) twin_flush(twd, m, mul);
+  if (i >= in) return;
+  if (data)   // the node's pad rows (up to kNodeRowPad) carry zero deltas
+    for (int r = n; r < (int)round_up(n, kNodeRowPad); ++r) {
+      const size_t idx = (size_t)(r0 + r) * in + i;
+      if (Dout) *reinterpret_cast<float2*>(Dout + idx) = make_float2(0.f, 0.f);
+      if (twd.hi) {
+        *reinterpret_cast<__half2*>(twd.hi + idx) = __floats2half2_rn(0.f, 0.f);
+        *reinterpret_cast<__half2*>(twd.lo + idx) = __floats2half2_rn(0.f, 0.f);
+      }
+    }
+  const float sw = *scale_w;
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    if (o >= no) break;
+    const long long q0 = quantise(g0[o], sw, lim, tail, tw);
+    const long long q1 = quantise(g1[o], sw, lim, tail, tw);
+    if (q0) atomicAdd(reinterpret_cast<unsigned long long*>(&Gw[(size_t)i * no + o]), (unsigned long long)q0);
+    if (q1) atomicAdd(reinterpret_cast<unsigned long long*>(&Gw[(size_t)(i + 1) * no + o]), (unsigned long long)q1);
+  }
+  if (data) {
+    const float sb = *scale_b;
+    const long long q0 = quantise(db0, sb, lim, tail, tb);
+    const long long q1 = quantise(db1, sb, lim, tail, tb);
+    if (q0) atomicAdd(reinterpret_cast<unsigned long long*>(&Gb[i]), (unsigned long long)q0);
+    if (q1) atomicAdd(reinterpret_cast<unsigned long long*>(&Gb[i + 1]), (unsigned long long)q1);
+  }
+}
+
 // -------------------------------------------------------------------- SGD
 // sync_gradients' rounding + x(1/B) (virtual_exec.cpp:169-174) and
 // sgd_apply (model.cpp:364-374) fused: g = double(S) * 2^-s * (1/B);
