@@ -286,6 +286,7 @@ vntb::Twin16 twin_of(vnt_engine* e, __half* hi, __half* lo, int op, int flag = v
 }
 
 #include "gemm_tc.cuh"
+#include "kernels_stream.cuh"
 
 namespace {
 
@@ -659,6 +660,12 @@ struct BackSkinny {
                   const int* row0, const int* nrows, int nn, float* Dout, vntb::Twin16 twins,
                   const float* scale_w, long long* Gw, int tw, const float* scale_b, long long* Gb, int tb,
                   float lim, long long* tail) {
+    static const bool bulk = !(getenv("VNT_SKINNY_BULK") && getenv("VNT_SKINNY_BULK")[0] == '0');
+    if (bulk && in % 4 == 0) {   // X rows streamed through smem by bulk copies (same bits)
+      vntb::launch_skinny_backward_bulk<NO>(s, X, Dn, W, in, no, act, row0, nrows, nn, Dout, twins, scale_w, Gw,
+                                            tw, scale_b, Gb, tb, lim, tail);
+      return;
+    }
     if (in % 2 == 0) {   // two features per thread (same bits)
       dim3 grid((unsigned)ceil_div(in, 256), (unsigned)nn);
       k_skinny_backward2<NO><<<grid, 128, 0, s>>>(X, Dn, W, in, no, act, row0, nrows, Dout, twins, scale_w, Gw,
