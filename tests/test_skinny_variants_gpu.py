@@ -48,7 +48,9 @@ print(json.dumps({"params": hashlib.sha256(np.ascontiguousarray(p).tobytes()).he
 
 
 def _run(bulk, **kw):
-    env = dict(os.environ, VNT_SKINNY_BULK=str(bulk))
+    # VNT_NODE_KERNEL=0: small models take the per-layer kernels (not the
+    # whole-node kernel), so the skinny backward runs
+    env = dict(os.environ, VNT_SKINNY_BULK=str(bulk), VNT_NODE_KERNEL="0")
     out = subprocess.run([sys.executable, "-c", SCRIPT % dict(root=ROOT, **kw)], env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -68,4 +70,17 @@ def test_bulk_backward_partial_slab():
     # features (176-B rows), odd node sizes
     sizes = [97, 64, 33, 150]
     kw = dict(widths=[784, 300, 10], B=sum(sizes), act="relu", sizes=sizes)
+    assert _run(1, **kw) == _run(0, **kw)
+
+
+@pytest.mark.parametrize("widths,act", [
+    ([784, 10], "relu"),                 # layer 0 skinny: dW only (no bwd-data / db)
+    ([784, 256, 4], "identity"),         # NO = 4
+    ([784, 512, 8], "tanh"),             # NO = 8
+    ([784, 256, 16], "relu"),            # NO = 16
+    ([784, 128, 32], "identity"),        # NO = 32
+])
+def test_bulk_backward_instantiations(widths, act):
+    sizes = [40, 88, 19, 61]
+    kw = dict(widths=widths, B=sum(sizes), act=act, sizes=sizes)
     assert _run(1, **kw) == _run(0, **kw)
