@@ -150,6 +150,14 @@ class ClockSampler:
 
     def __init__(self, index=0):
         self.index = index
+        # NVML and nvidia-smi number GPUs physically; CUDA_VISIBLE_DEVICES may
+        # renumber them: address the GPU by its UUID
+        self.uuid = None
+        try:
+            import torch
+            self.uuid = "GPU-" + str(torch.cuda.get_device_properties(index).uuid)
+        except Exception:
+            pass
         self.proc = None
         self.nvml = None
         self.stop = threading.Event()
@@ -160,7 +168,8 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            h = (pynvml.nvmlDeviceGetHandleByUUID(self.uuid) if self.uuid
+                 else pynvml.nvmlDeviceGetHandleByIndex(self.index))
             bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
                     "hw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
                     "sw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
@@ -184,7 +193,7 @@ class ClockSampler:
             self.nvml = None
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
+                ["nvidia-smi", "-i", self.uuid or str(self.index),
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
@@ -238,7 +247,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi",
+                "gpu": self.uuid or self.index}
 
 
 # ------------------------------------------------------------------ reference arm
